@@ -1,0 +1,187 @@
+"""CPU oracle for the Echo learner hot path (arXiv 2508.05387) -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / ``--impl reference``
+legs may import this package.  The product package ``paper_2508_05387_b200`` never imports it and the
+two share no code.  The arithmetic lives in ``echo_oracle.c`` (plain fp64 C loops, one function per
+step of the path, each citing the PAPER.md / SPEC.md passage it follows); this module only builds that
+file with gcc and marshals numpy arrays into it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "echo_oracle.c")
+_LIB = os.path.join(_HERE, "libecho_oracle.so")
+
+DATA_OK, DATA_FUTURE_VERSION, DATA_MIXED_GROUP_VERSION, DATA_BAD_LENGTH, DATA_BAD_ACTION, DATA_CAPACITY = range(6)
+F32, BF16 = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile echo_oracle.c (gcc, -O2, OpenMP, no FMA contraction, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+                               "-fno-fast-math", "-Wall", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _PackResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("first_bad_rollout", ctypes.c_int32),
+                ("n_groups_kept", ctypes.c_int32), ("n_rollouts_kept", ctypes.c_int32),
+                ("n_tokens", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        i32, i64, f32, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double
+        _lib.echo_ref_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, i64,
+                                             P, P, P, P, P, P, ctypes.POINTER(_PackResult)]
+        _lib.echo_ref_pack_batch.restype = ctypes.c_int
+        _lib.echo_ref_group_advantage.argtypes = [i32, i32, f32, P, P, i64, P, P, P]
+        _lib.echo_ref_group_advantage.restype = ctypes.c_int
+        _lib.echo_ref_policy_loss.argtypes = [i64, i32, i64, i32, P, P, P, P, P, P, f64, f32, f32, f32, f32,
+                                              P, P, P, P, P, P]
+        _lib.echo_ref_policy_loss.restype = ctypes.c_int
+        _lib.echo_ref_scaled_loss.argtypes = [i64, i32, i64, P, P, P, P, P, P, f64, f32, f32, f32, f32]
+        _lib.echo_ref_scaled_loss.restype = f64
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dtype):
+    return None if a is None else np.ascontiguousarray(a, dtype=dtype)
+
+
+@dataclass
+class PackOut:
+    status: int
+    first_bad_rollout: int
+    n_groups_kept: int
+    n_rollouts_kept: int
+    n_tokens: int
+    kept_rollout: np.ndarray
+    kept_offset: np.ndarray
+    tok_slot: np.ndarray
+    tok_action: np.ndarray
+    tok_old: np.ndarray
+    tok_ref: np.ndarray | None
+
+
+def pack_batch(version, resp_len, action, old_logp, ref_logp, *, group_size, max_len, vocab, t_train, max_lag,
+               rollout_base=0, token_capacity=None) -> PackOut:
+    """(1) lag filter + pack.  ``action``/``old_logp``/``ref_logp`` are padded ``[R, S]``."""
+    version = _c(version, np.int64)
+    resp_len = _c(resp_len, np.int32)
+    R = int(version.shape[0])
+    action = _c(action, np.int32).reshape(-1)
+    old_logp = _c(old_logp, np.float32).reshape(-1)
+    ref_logp = None if ref_logp is None else _c(ref_logp, np.float32).reshape(-1)
+    cap = R * max_len if token_capacity is None else int(token_capacity)
+    kept_rollout = np.full(R, -1, np.int32)
+    kept_offset = np.zeros(R + 1, np.int64)
+    n_alloc = max(cap, 1)
+    tok_slot = np.zeros(n_alloc, np.int32)
+    tok_action = np.zeros(n_alloc, np.int32)
+    tok_old = np.zeros(n_alloc, np.float32)
+    tok_ref = np.zeros(n_alloc, np.float32) if ref_logp is not None else None
+    res = _PackResult()
+    rc = lib().echo_ref_pack_batch(R, group_size, max_len, vocab, t_train, max_lag, rollout_base,
+                                   _p(version), _p(resp_len), _p(action), _p(old_logp), _p(ref_logp), cap,
+                                   _p(kept_rollout), _p(kept_offset), _p(tok_slot), _p(tok_action), _p(tok_old),
+                                   _p(tok_ref), ctypes.byref(res))
+    if rc != 0:
+        raise ValueError(f"echo_ref_pack_batch: invalid argument (rc={rc})")
+    n = int(res.n_tokens) if res.n_tokens <= cap else 0
+    nk = int(res.n_rollouts_kept)
+    return PackOut(int(res.status), int(res.first_bad_rollout), int(res.n_groups_kept), nk, int(res.n_tokens),
+                   kept_rollout[:nk].copy(), kept_offset[:nk + 1].copy(), tok_slot[:n].copy(), tok_action[:n].copy(),
+                   tok_old[:n].copy(), None if tok_ref is None else tok_ref[:n].copy())
+
+
+def group_advantage(reward, kept_rollout, *, group_size, eps=1e-8, rollout_base=0, want_f64=False):
+    """(2) GRPO advantage per kept rollout slot (fp32) and the 6 advantage statistics (fp64).
+
+    With ``want_f64`` also returns the advantages before their fp32 rounding."""
+    reward = _c(reward, np.float32)
+    kept_rollout = _c(kept_rollout, np.int32)
+    n = int(kept_rollout.shape[0])
+    adv = np.zeros(max(n, 1), np.float32)
+    adv64 = np.zeros(max(n, 1), np.float64)
+    stats = np.zeros(6, np.float64)
+    rc = lib().echo_ref_group_advantage(n, group_size, eps, _p(reward), _p(kept_rollout), rollout_base,
+                                        _p(adv), _p(adv64), _p(stats))
+    if rc != 0:
+        raise ValueError("echo_ref_group_advantage: invalid argument")
+    if want_f64:
+        return adv[:n].copy(), stats, adv64[:n].copy()
+    return adv[:n].copy(), stats
+
+
+@dataclass
+class LossOut:
+    logp: np.ndarray
+    loss: np.ndarray
+    flags: np.ndarray
+    coef: np.ndarray
+    dlogits: np.ndarray | None
+    stats: np.ndarray
+
+
+def policy_loss(logits, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, vocab=None, dtype=None,
+                clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0, want_dlogits=True) -> LossOut:
+    """(3)-(5) for every row of ``logits``.
+
+    ``logits`` is a 2-D numpy array: float32 (dtype F32) or uint16 bf16 bit patterns (dtype BF16).
+    Returns fp64 per-token logp / loss / gradient coefficient, flags, and optional fp64 dlogits.
+    """
+    if dtype is None:
+        dtype = F32 if logits.dtype == np.float32 else BF16
+    logits = np.ascontiguousarray(logits)
+    assert logits.dtype == (np.float32 if dtype == F32 else np.uint16)
+    n, ld = logits.shape
+    V = ld if vocab is None else int(vocab)
+    tok_action = _c(tok_action, np.int32)
+    tok_old = _c(tok_old, np.float32)
+    tok_ref = _c(tok_ref, np.float32)
+    tok_slot = _c(tok_slot, np.int32)
+    adv_slot = _c(adv_slot, np.float32)
+    logp = np.zeros(n, np.float64)
+    loss = np.zeros(n, np.float64)
+    coef = np.zeros(n, np.float64)
+    flags = np.zeros(n, np.uint8)
+    d = np.zeros((n, V), np.float64) if want_dlogits else None
+    stats = np.zeros(10, np.float64)
+    rc = lib().echo_ref_policy_loss(n, V, ld, dtype, _p(logits), _p(tok_action), _p(tok_old), _p(tok_ref),
+                                    _p(tok_slot), _p(adv_slot), float(n_global), clip_low, clip_high, kl_coef,
+                                    grad_scale, _p(logp), _p(loss), _p(flags), _p(coef), _p(d), _p(stats))
+    if rc != 0:
+        raise ValueError("echo_ref_policy_loss: invalid argument")
+    return LossOut(logp, loss, flags, coef, d, stats)
+
+
+def scaled_loss(logits_f64, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, clip_low=0.2,
+                clip_high=0.2, kl_coef=0.0, grad_scale=1.0) -> float:
+    """grad_scale * sum_t l_t / N_global as a function of fp64 logits (for finite differences)."""
+    z = np.ascontiguousarray(logits_f64, dtype=np.float64)
+    n, V = z.shape
+    return float(lib().echo_ref_scaled_loss(n, V, V, _p(z), _p(_c(tok_action, np.int32)), _p(_c(tok_old, np.float32)),
+                                            _p(_c(tok_ref, np.float32)), _p(_c(tok_slot, np.int32)),
+                                            _p(_c(adv_slot, np.float32)), float(n_global), clip_low, clip_high,
+                                            kl_coef, grad_scale))

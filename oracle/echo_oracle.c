@@ -1,0 +1,363 @@
+/*
+ * echo_oracle.c -- plain, slow, obviously-correct CPU oracle for the Echo learner hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` legs may load this library.  The product path (paper_2508_05387_b200/) never
+ * links, imports or calls it, and shares no code, header or constant with it.
+ *
+ * What it computes: one learner step of Echo's training swarm (arXiv 2508.05387, §2.4
+ * :254-282, "consumes trajectory batches, applies a chosen RL algorithm ... step() interface
+ * consuming mini-batches drawn from the shared buffer"), with the GRPO recipe of PAPER.md §3.1
+ * :374-382, written out as its plain definition in fp64:
+ *
+ *   (1) version-lag filter + pack      PAPER.md :192 (param_version tag), :224 (strict
+ *                                      t_train - t_infer > Delta_max), :201 ("lag one or more
+ *                                      updates"); SPEC.md :344/:354 (min_version filter)
+ *   (2) GRPO group-relative advantage  PAPER.md :374 (GRPO named); SPEC.md :206-214 formula
+ *   (3) log pi(a|s) = z_a - logsumexp  PAPER.md :170-171 ("log pi_theta(a|s)" field)
+ *   (4) clipped surrogate + KL         PAPER.md :278 ("PPO, KL-constrained PPO, GRPO");
+ *                                      SPEC.md :219 (clipped ratio objective), :243 (eps = 0.2);
+ *                                      KL coefficient PAPER.md :376-382
+ *   (5) dL/dlogits                     PAPER.md :254-256 ("performs gradient updates")
+ *
+ * Readings of silent / ambiguous points (DESIGN.md "Readings" R1-R17 list them all):
+ *   R1  keep a group iff t_train - v <= max_lag (drop iff strictly greater, PAPER.md :224)
+ *   R3  version tags must be uniform inside a group; the drop is group-granular
+ *   R4  survivors are compacted in ascending order, tokens rollout-major
+ *   R5  KL term is the k3 estimator against pi_ref: exp(ref-logp) - (ref-logp) - 1
+ *   R6  loss = sum_t l_t / N_global (token mean over all ranks' kept tokens)
+ *   R7  population std, A = (r - mean)/(std + eps), eps = 1e-8 (SPEC.md :209, :213)
+ *   R10 "clipped" uses strict inequalities; at equality the gradient flows
+ *
+ * Conventions: every float input is widened exactly to double; all arithmetic is IEEE double with
+ * no FMA contraction (-ffp-contract=off); libm exp/log/sqrt.  The only fp32 rounding the oracle
+ * performs is where the ABI fixes an fp32 output (the advantage table, R13).
+ *
+ * Parity pins (tests/test_oracle_*.py): brute-force pack over all 3^4 lag patterns; SPEC.md :212-214
+ * worked advantage examples; logp = -ln V on uniform rows; spike closed form; old == new => rho = 1;
+ * clip saturation => zero gradient row; central finite differences of the loss vs dlogits.
+ * Nothing here is "parity unpinned".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <float.h>
+#include <string.h>
+
+/* ---- status codes (the oracle's own copies; kept independent of include/echo.h) ---- */
+enum { REF_OK = 0, REF_ERR_INVALID_ARGUMENT = 1 };
+enum {
+  REF_DATA_OK = 0,
+  REF_DATA_FUTURE_VERSION = 1,   /* v > t_train: a rollout from a policy the learner never had */
+  REF_DATA_MIXED_GROUP_VERSION = 2,
+  REF_DATA_BAD_LENGTH = 3,       /* L not in [1, S] (SPEC.md :39, sequences have length >= 1) */
+  REF_DATA_BAD_ACTION = 4,       /* action not in [0, V) */
+  REF_DATA_CAPACITY = 5          /* packed tokens exceed the caller's capacity */
+};
+
+typedef struct {
+  int32_t status;
+  int32_t first_bad_rollout;
+  int32_t n_groups_kept;
+  int32_t n_rollouts_kept;
+  int64_t n_tokens;
+} echo_ref_pack_result;
+
+static double widen_bf16(uint16_t b) {
+  uint32_t u = ((uint32_t)b) << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+
+static double logit_at(const void* logits, int dtype, int64_t ld, int64_t row, int64_t v) {
+  if (dtype == 0) return (double)((const float*)logits)[row * ld + v];
+  return widen_bf16(((const uint16_t*)logits)[row * ld + v]);
+}
+
+/* ======================================================================================
+ * (1) Version-lag filter + pack.
+ *   PAPER.md :192  each rollout is annotated with a param_version tag.
+ *   PAPER.md :224  the coordinator acts when t_train - t_infer > Delta_max (strict), bounding the
+ *                  lag at Delta_max; a rollout with lag == max_lag is therefore still admissible.
+ *   SPEC.md :344   pull returns trajectories with param_version >= min_version
+ *                  (== t_train - max_lag here).
+ *   SPEC.md :44-49 a RolloutBatch is prompt-major: prompt p owns rollouts [p*G, (p+1)*G).
+ * Errors are reported as (rollout, check) lexicographic minimum: checks for rollout i in the
+ * order FUTURE(1) < MIXED(2) < BAD_LENGTH(3) < BAD_ACTION(4); CAPACITY(5) only when nothing
+ * else failed.  On any data error only status / first_bad_rollout are specified.
+ * ====================================================================================== */
+int echo_ref_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len, int32_t vocab,
+                        int64_t t_train, int32_t max_lag, int64_t rollout_base,
+                        const int64_t* version, const int32_t* resp_len,
+                        const int32_t* action, const float* old_logp, const float* ref_logp,
+                        int64_t token_capacity,
+                        int32_t* kept_rollout, int64_t* kept_offset,
+                        int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
+                        echo_ref_pack_result* result) {
+  if (n_rollouts < 0 || group_size < 2 || max_len < 1 || vocab < 1 || max_lag < 0) return REF_ERR_INVALID_ARGUMENT;
+  if (n_rollouts % group_size != 0) return REF_ERR_INVALID_ARGUMENT;
+  const int64_t R = n_rollouts, G = group_size, S = max_len;
+
+  int64_t best_key = INT64_MAX; /* key = rollout * 8 + check */
+  int32_t n_groups_kept = 0, n_rollouts_kept = 0;
+  int64_t n_tokens = 0;
+
+  /* validation of every rollout, ascending */
+  for (int64_t i = 0; i < R; ++i) {
+    int64_t first = (i / G) * G;
+    int64_t key = INT64_MAX;
+    if (version[i] > t_train) key = i * 8 + REF_DATA_FUTURE_VERSION;
+    else if (version[i] != version[first]) key = i * 8 + REF_DATA_MIXED_GROUP_VERSION;
+    else if (resp_len[i] < 1 || resp_len[i] > max_len) key = i * 8 + REF_DATA_BAD_LENGTH;
+    if (key < best_key) best_key = key;
+  }
+
+  /* filter: one decision per group, from its (uniform) version */
+  for (int64_t g = 0; g < R / G; ++g) {
+    int64_t lag = t_train - version[g * G];
+    int keep = (lag <= (int64_t)max_lag);
+    if (!keep) continue;
+    for (int64_t i = g * G; i < (g + 1) * G; ++i) {
+      kept_rollout[n_rollouts_kept] = (int32_t)(rollout_base + i);
+      kept_offset[n_rollouts_kept] = n_tokens;
+      int64_t L = resp_len[i];
+      if (L < 0) L = 0;
+      if (L > S) L = S;
+      n_tokens += L;
+      n_rollouts_kept += 1;
+    }
+    n_groups_kept += 1;
+  }
+  kept_offset[n_rollouts_kept] = n_tokens;
+
+  /* actions of kept rollouts, ascending rollout then position */
+  for (int32_t k = 0; k < n_rollouts_kept; ++k) {
+    int64_t i = (int64_t)kept_rollout[k] - rollout_base;
+    int64_t L = kept_offset[k + 1] - kept_offset[k];
+    for (int64_t j = 0; j < L; ++j) {
+      int32_t a = action[i * S + j];
+      if (a < 0 || a >= vocab) {
+        int64_t key = i * 8 + REF_DATA_BAD_ACTION;
+        if (key < best_key) best_key = key;
+        break;
+      }
+    }
+  }
+
+  /* gather (only when it fits) */
+  if (n_tokens <= token_capacity) {
+    for (int32_t k = 0; k < n_rollouts_kept; ++k) {
+      int64_t i = (int64_t)kept_rollout[k] - rollout_base;
+      for (int64_t t = kept_offset[k]; t < kept_offset[k + 1]; ++t) {
+        int64_t j = t - kept_offset[k];
+        tok_slot[t] = k;
+        tok_action[t] = action[i * S + j];
+        tok_old[t] = old_logp[i * S + j];
+        if (ref_logp && tok_ref) tok_ref[t] = ref_logp[i * S + j];
+      }
+    }
+  }
+
+  result->n_groups_kept = n_groups_kept;
+  result->n_rollouts_kept = n_rollouts_kept;
+  result->n_tokens = n_tokens;
+  if (best_key != INT64_MAX) {
+    result->status = (int32_t)(best_key % 8);
+    result->first_bad_rollout = (int32_t)(rollout_base + best_key / 8);
+  } else if (n_tokens > token_capacity) {
+    result->status = REF_DATA_CAPACITY;
+    result->first_bad_rollout = -1;
+  } else {
+    result->status = REF_DATA_OK;
+    result->first_bad_rollout = -1;
+  }
+  return REF_OK;
+}
+
+/* ======================================================================================
+ * (2) GRPO group-relative advantage, SPEC.md :206-214 (the paper names GRPO at PAPER.md :374
+ * without a formula; SPEC.md :243, :255 record the reconstruction):
+ *     mean = (sum_i r_i) / G            (sequential fp64 sum, index order)
+ *     std  = sqrt((sum_i (r_i - mean)^2) / G)   (population std, SPEC.md :213 worked example)
+ *     A_i  = (r_i - mean) / (std + eps),  eps = 1e-8   -> rounded to fp32 (ABI output type)
+ * adv_f64 (nullable) receives A before the fp32 rounding.
+ * Stats: per group {sum A, sum A^2, sum r, sum r^2} (A as the fp32 value), then summed over groups
+ * in ascending order; adv_stats = {sum A, sum A^2, sum r, sum r^2, n_zero_std_groups, n_rollouts}.
+ * ====================================================================================== */
+int echo_ref_group_advantage(int32_t n_rollouts_kept, int32_t group_size, float eps,
+                             const float* reward, const int32_t* kept_rollout, int64_t rollout_base,
+                             float* adv_slot, double* adv_f64, double* adv_stats) {
+  if (group_size < 2 || n_rollouts_kept < 0 || n_rollouts_kept % group_size != 0) return REF_ERR_INVALID_ARGUMENT;
+  const int64_t G = group_size;
+  double tot[4] = {0, 0, 0, 0};
+  double n_zero_std = 0;
+  for (int64_t g0 = 0; g0 < n_rollouts_kept; g0 += G) {
+    double sum = 0.0;
+    for (int64_t k = g0; k < g0 + G; ++k) sum = sum + (double)reward[kept_rollout[k] - rollout_base];
+    double mean = sum / (double)G;
+    double ss = 0.0;
+    for (int64_t k = g0; k < g0 + G; ++k) {
+      double d = (double)reward[kept_rollout[k] - rollout_base] - mean;
+      ss = ss + d * d;
+    }
+    double std = sqrt(ss / (double)G);
+    if (std == 0.0) n_zero_std += 1.0;
+    double part[4] = {0, 0, 0, 0};
+    for (int64_t k = g0; k < g0 + G; ++k) {
+      double r = (double)reward[kept_rollout[k] - rollout_base];
+      double a64 = (r - mean) / (std + (double)eps);
+      float a = (float)a64;
+      adv_slot[k] = a;
+      if (adv_f64) adv_f64[k] = a64;
+      part[0] = part[0] + (double)a;
+      part[1] = part[1] + (double)a * (double)a;
+      part[2] = part[2] + r;
+      part[3] = part[3] + r * r;
+    }
+    for (int q = 0; q < 4; ++q) tot[q] = tot[q] + part[q];
+  }
+  adv_stats[0] = tot[0];
+  adv_stats[1] = tot[1];
+  adv_stats[2] = tot[2];
+  adv_stats[3] = tot[3];
+  adv_stats[4] = n_zero_std;
+  adv_stats[5] = (double)n_rollouts_kept;
+  return REF_OK;
+}
+
+/* ======================================================================================
+ * (3)-(5) per packed token t (one row of the [tokens x vocab] logits):
+ *   (3) m = max_v z_v;  lse = m + log sum_v exp(z_v - m);  logp = z_a - lse      PAPER.md :170
+ *   (4) rho  = exp(logp - old)                                                    SPEC.md :219
+ *       clipped = (A > 0 and rho > 1+eps_hi) or (A < 0 and rho < 1-eps_lo)        (R10)
+ *       pg   = max(-A rho, -A clip(rho, 1-eps_lo, 1+eps_hi))                      SPEC.md :219
+ *       kl   = exp(ref - logp) - (ref - logp) - 1     (only when beta > 0)        (R5)
+ *       l_t  = pg + beta kl;   L = sum_t l_t / N_global                           (R6)
+ *   (5) dl/dlogp = [not clipped](-A rho) + beta (1 - exp(ref - logp))
+ *       c_t = grad_scale * dl/dlogp / N_global
+ *       d[t,v] = c_t (delta_{v,a} - exp(z_v - lse))                               PAPER.md :254
+ * flags: bit0 = clipped; bit1 = non-finite (lse, logp, rho, l_t or c_t not a finite value that an
+ * fp32 output can hold -- R11).
+ * stats (nullable, sequential fp64 over rows): {sum l, sum (logp-old), sum kl_k3 (if ref),
+ *   n_clipped, n_nonfinite, rho_min, rho_max, sum logp, n_rows, sum rho}, rho stats over
+ *   finite rows only.
+ * dlogits (nullable) is [n_rows x vocab] doubles.
+ * ====================================================================================== */
+static int fits_f32(double x) { return isfinite(x) && fabs(x) <= (double)FLT_MAX; }
+
+int echo_ref_policy_loss(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtype, const void* logits,
+                         const int32_t* tok_action, const float* tok_old, const float* tok_ref,
+                         const int32_t* tok_slot, const float* adv_slot, double n_global,
+                         float clip_low, float clip_high, float kl_coef, float grad_scale,
+                         double* tok_logp, double* tok_loss, uint8_t* tok_flags, double* tok_coef,
+                         double* dlogits, double* stats) {
+  if (n_rows < 0 || vocab < 1 || ld < vocab || (dtype != 0 && dtype != 1)) return REF_ERR_INVALID_ARGUMENT;
+  if (kl_coef > 0.0f && tok_ref == NULL) return REF_ERR_INVALID_ARGUMENT;
+  const double lo = 1.0 - (double)clip_low, hi = 1.0 + (double)clip_high;
+  const double beta = (double)kl_coef;
+
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < n_rows; ++t) {
+    /* (3) log-softmax at the sampled action */
+    double m = -INFINITY;
+    int has_nan = 0;
+    for (int64_t v = 0; v < vocab; ++v) {
+      double z = logit_at(logits, dtype, ld, t, v);
+      if (isnan(z)) has_nan = 1;
+      if (z > m) m = z;
+    }
+    double s = 0.0;
+    for (int64_t v = 0; v < vocab; ++v) s = s + exp(logit_at(logits, dtype, ld, t, v) - m);
+    double lse = (has_nan || !isfinite(m)) ? NAN : m + log(s);
+    int32_t a = tok_action[t];
+    double logp = logit_at(logits, dtype, ld, t, a) - lse;
+
+    /* (4) clipped importance-ratio surrogate + optional KL to the reference policy */
+    double A = (double)adv_slot[tok_slot[t]];
+    double rho = exp(logp - (double)tok_old[t]);
+    int clipped = (A > 0.0 && rho > hi) || (A < 0.0 && rho < lo);
+    double rho_c = rho < lo ? lo : (rho > hi ? hi : rho);
+    double un = -A * rho, cl = -A * rho_c;
+    double pg = un > cl ? un : cl;
+    double kl = 0.0, dkl = 0.0;
+    if (beta > 0.0) {
+      double x = (double)tok_ref[t] - logp;
+      kl = exp(x) - x - 1.0;
+      dkl = 1.0 - exp(x);
+    }
+    double loss = pg + beta * kl;
+    double dl_dlogp = (clipped ? 0.0 : -A * rho) + beta * dkl;
+    double c = (double)grad_scale * dl_dlogp / n_global;
+    int nonfinite = !(fits_f32(lse) && fits_f32(logp) && fits_f32(rho) && fits_f32(loss) && fits_f32(c));
+
+    tok_logp[t] = logp;
+    tok_loss[t] = loss;
+    tok_flags[t] = (uint8_t)((clipped ? 1 : 0) | (nonfinite ? 2 : 0));
+    if (tok_coef) tok_coef[t] = c;
+
+    /* (5) gradient of the loss with respect to every logit of the row */
+    if (dlogits) {
+      for (int64_t v = 0; v < vocab; ++v) {
+        double p = exp(logit_at(logits, dtype, ld, t, v) - lse);
+        dlogits[t * (int64_t)vocab + v] = c * ((v == a ? 1.0 : 0.0) - p);
+      }
+    }
+  }
+
+  if (stats) {
+    double acc[10] = {0, 0, 0, 0, 0, INFINITY, -INFINITY, 0, 0, 0};
+    for (int64_t t = 0; t < n_rows; ++t) {
+      double logp = tok_logp[t];
+      acc[0] = acc[0] + tok_loss[t];
+      acc[1] = acc[1] + (logp - (double)tok_old[t]);
+      if (tok_ref) {
+        double x = (double)tok_ref[t] - logp;
+        acc[2] = acc[2] + (exp(x) - x - 1.0);
+      }
+      acc[3] = acc[3] + (double)(tok_flags[t] & 1);
+      acc[4] = acc[4] + (double)((tok_flags[t] >> 1) & 1);
+      if (!(tok_flags[t] & 2)) {
+        double rho = exp(logp - (double)tok_old[t]);
+        if (rho < acc[5]) acc[5] = rho;
+        if (rho > acc[6]) acc[6] = rho;
+        acc[9] = acc[9] + rho;
+      }
+      acc[7] = acc[7] + logp;
+      acc[8] = acc[8] + 1.0;
+    }
+    for (int q = 0; q < 10; ++q) stats[q] = acc[q];
+  }
+  return REF_OK;
+}
+
+/* Scalar loss of a set of rows as a function of the logits, for finite-difference pins of (5):
+ * returns (1/N_global) * sum_t l_t * grad_scale, i.e. the quantity whose gradient dlogits is. */
+double echo_ref_scaled_loss(int64_t n_rows, int32_t vocab, int64_t ld, const double* logits,
+                            const int32_t* tok_action, const float* tok_old, const float* tok_ref,
+                            const int32_t* tok_slot, const float* adv_slot, double n_global,
+                            float clip_low, float clip_high, float kl_coef, float grad_scale) {
+  const double lo = 1.0 - (double)clip_low, hi = 1.0 + (double)clip_high;
+  const double beta = (double)kl_coef;
+  double total = 0.0;
+  for (int64_t t = 0; t < n_rows; ++t) {
+    const double* z = logits + t * ld;
+    double m = -INFINITY;
+    for (int64_t v = 0; v < vocab; ++v) if (z[v] > m) m = z[v];
+    double s = 0.0;
+    for (int64_t v = 0; v < vocab; ++v) s = s + exp(z[v] - m);
+    double logp = z[tok_action[t]] - (m + log(s));
+    double A = (double)adv_slot[tok_slot[t]];
+    double rho = exp(logp - (double)tok_old[t]);
+    double rho_c = rho < lo ? lo : (rho > hi ? hi : rho);
+    double un = -A * rho, cl = -A * rho_c;
+    double pg = un > cl ? un : cl;
+    double kl = 0.0;
+    if (beta > 0.0) {
+      double x = (double)tok_ref[t] - logp;
+      kl = exp(x) - x - 1.0;
+    }
+    total = total + (pg + beta * kl);
+  }
+  return (double)grad_scale * total / n_global;
+}
