@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of one Echo learner step (BASELINE.json metric: policy-loss fwd+bwd tokens/s and % of HBM roofline).
+
+A step = the whole hot path over one batch of the workload on every rank: H2D of the rank's rollouts (e2e only),
+(1) pack + the one 32-byte D2H that sizes the logits, (2) GRPO advantage, all-reduce of counts, then for each
+micro-batch of M packed rows the fused (3)-(5) kernel over [M x V] bf16 logits in place, the statistics
+reduction and its all-reduce, and the D2H of the step statistics.  The logits of each micro-batch are written
+by the synthetic generator (the stand-in for the model's LM-head forward, which in a trainer produces them on
+the device) OUTSIDE the timed segments, followed by a 256 MB write that flushes L2, so each kernel starts cold.
+
+value      = kept tokens of all ranks / max-over-ranks device time of the path (inputs resident in HBM)
+e2e.value  = the same through the public step API with pinned host inputs copied H2D and the statistics read
+             back inside the timed region (generator time subtracted, it is not part of the method)
+
+  python bench.py [--gpus N --steps K --warmup W] [--config qwen3-4b] [--algo auto|row_l2|cluster_smem]
+  python bench.py --impl reference ...      # the CPU oracle arm (rank 0 only)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "policy-loss fwd+bwd tokens/sec and % HBM roofline at 1/2/4/8 B200"
+DEFAULT_CONFIG = "qwen3-4b"      # BASELINE.json configs[1]: the single-GPU configuration the metric is quoted on
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="echo", choices=["echo", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "cluster_smem"])
+    ap.add_argument("--micro-batch", type=int, default=32768)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-oracle sample duration")
+    return ap.parse_args()
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, D2D copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def bytes_per_token(V, esize, kl):
+    """Algorithmic HBM bytes per packed token of the fused kernel: read the logits row once,
+    write the gradient row once, plus per-token metadata (action 4, old 4, slot 4, [ref 4], logp 4, loss 4,
+    flags 1).  The adv_slot table is a few KB and stays in cache."""
+    return 2 * V * esize + 21 + (4 if kl else 0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ================================================================================= the CPU oracle (baseline arm)
+def oracle_rate(cfg, rank_batch, n_tokens_total, target_s, threads=None):
+    """Time the oracle (as it stands) on a bounded sample of the workload on this host's cores: the full pack +
+    advantage of the batch, and the fused loss on a row sample sized to ~target_s.  Returns a dict."""
+    import oracle
+    import synth
+    if threads:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+    cores = len(os.sched_getaffinity(0))
+    b = rank_batch
+    t0 = time.perf_counter()
+    pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,
+                           vocab=cfg.V, t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
+    adv, _ = oracle.group_advantage(b.reward, pk.kept_rollout, group_size=cfg.G)
+    t_meta = time.perf_counter() - t0
+    keys = (pk.kept_rollout[pk.tok_slot].astype(np.int64) * cfg.S
+            + (np.arange(pk.n_tokens, dtype=np.int64) - pk.kept_offset[pk.tok_slot]))
+
+    # a pool of sampled rows (numpy twin of the GPU generator; generation is not timed), evaluated repeatedly
+    # until ~target_s of oracle time: the oracle's cost per row does not depend on the values
+    rng = np.random.default_rng(0)
+    pool = rng.integers(0, pk.n_tokens, 32)
+    z = synth.logits_rows(keys[pool], pk.tok_action[pool], cfg.V, cfg.seed, "bf16" if cfg.dtype == "bf16" else "f32")
+    tr = None if pk.tok_ref is None else pk.tok_ref[pool]
+    t_loss, rows = 0.0, 0
+    while t_loss < target_s or rows == 0:
+        t = time.perf_counter()
+        oracle.policy_loss(z, pk.tok_action[pool], pk.tok_old[pool], tr, pk.tok_slot[pool], adv,
+                           n_global=pk.n_tokens, kl_coef=cfg.kl_coef)
+        t_loss += time.perf_counter() - t
+        rows += len(pool)
+    per_row = t_loss / rows
+    step_s = t_meta + per_row * n_tokens_total
+    return {"tokens_per_s": n_tokens_total / step_s, "rows": rows, "t_loss": t_loss, "t_meta": t_meta,
+            "cores": cores, "per_row_s": per_row, "step_s": step_s}
+
+
+def reference_arm(args):
+    """--impl reference: the CPU oracle on the box's host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    b = synth.make_batch(cfg)
+    budget = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    results = []
+    for i in range(args.warmup + args.steps):
+        r = oracle_rate(cfg, b, _kept_tokens(cfg, b), budget)
+        if i >= args.warmup:
+            results.append(r)
+    v = statistics.median([r["tokens_per_s"] for r in results])
+    r = results[-1]
+    sample = (f"pack+advantage of the full {cfg.name} batch ({cfg.R} rollouts) + fused loss on {r['rows']} sampled rows "
+              f"(V={cfg.V}; a pool of 32 generated rows evaluated repeatedly); whole-step time extrapolated as t_meta + N * t_row")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(
+                [x["step_s"] for x in results]), "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "prompts": cfg.P, "group_size": cfg.G, "seq_len": cfg.S,
+                       "vocab": cfg.V, "max_lag": cfg.max_lag, "kl_coef": cfg.kl_coef},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _kept_tokens(cfg, b):
+    import synth
+    keep = (synth.T_TRAIN - b.version) <= cfg.max_lag
+    return int(b.resp_len[keep].sum())
+
+
+# ================================================================================= the B200 arm
+def main_echo(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_05387_b200 import abi
+    from paper_2508_05387_b200.parallel import init_from_env, shard_groups
+    from paper_2508_05387_b200.step import LearnerStep
+    import synth
+    import synth.gpu as sgpu
+
+    rank, world = init_from_env("nccl")
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    base = synth.CONFIGS[args.config]
+    if args.scaling == "weak" and world > 1:
+        cfg = synth.Config(base.name, base.P * world, base.G, base.S, base.V, base.dtype, base.max_lag, base.kl_coef,
+                           base.lag_mode, base.index, base.stale_groups * world, base.fixed_lags, base.lengths)
+    else:
+        cfg = base
+    g0, g1 = shard_groups(cfg.P, world, rank)
+    r0, r1 = g0 * cfg.G, g1 * cfg.G
+    b = synth.make_batch(cfg, r0, r1)
+    kl = cfg.kl_coef > 0
+    host = {k: torch.from_numpy(np.ascontiguousarray(getattr(b, k))).pin_memory()
+            for k in ("version", "resp_len", "reward", "action", "old_logp", "ref_logp")}
+    st = LearnerStep(n_rollouts=r1 - r0, group_size=cfg.G, max_len=cfg.S, vocab=cfg.V, dtype=cfg.dtype,
+                     has_ref=True, device=dev)
+    M = args.micro_batch
+    ld = (cfg.V + 7) // 8 * 8
+    logits = torch.empty(M, ld, dtype=torch.bfloat16 if cfg.dtype == "bf16" else torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    algo = {"auto": None, "row_l2": abi.ECHO_ALGO_ROW_L2, "cluster_smem": abi.ECHO_ALGO_CLUSTER_SMEM}[args.algo]
+    stream = torch.cuda.current_stream()
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def one_step(record):
+        t0 = ev()
+        h2d = st.h2d(host["version"], host["resp_len"], host["reward"], host["action"], host["old_logp"],
+                     host["ref_logp"])
+        t1 = ev()
+        info = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag, rollout_base=r0)
+        assert info.status == 0, info
+        st.advantage()
+        st.reduce_counts()
+        t2 = ev()
+        gens, kers = [], []
+        N = info.n_tokens
+        for row0 in range(0, N, M):
+            m = min(M, N - row0)
+            ga = ev()
+            sgpu.fill_logits(logits[:m], dtype=cfg.dtype, vocab=cfg.V, row0=row0, tok_slot=st.tok_slot,
+                             tok_action=st.tok_action, kept_rollout=st.kept_rollout, kept_offset=st.kept_offset,
+                             max_len=cfg.S, seed=cfg.seed)
+            flush.fill_(float(row0))
+            gb = ev()
+            st.loss(logits[:m], row0, kl_coef=cfg.kl_coef, grad_scale=1.0, algo=algo)
+            kb = ev()
+            gens.append((ga, gb))
+            kers.append((gb, kb))
+        t3 = ev()
+        st.finish(read_back=False)
+        t4 = ev()
+        st.stats_host[:9].copy_(st.stats1, non_blocking=True)
+        st.stats_host[9:].copy_(st.loss_stats, non_blocking=True)
+        t5 = ev()
+        torch.cuda.synchronize()
+        if not record:
+            return None
+        el = lambda a, b_: a.elapsed_time(b_)
+        gen_ms = sum(el(a, b_) for a, b_ in gens)
+        ker = [el(a, b_) for a, b_ in kers]
+        return {"e2e_ms": el(t0, t5) - gen_ms, "dev_ms": el(t1, t2) + sum(ker) + el(t3, t4), "kernel_ms": ker,
+                "n_tokens": N, "h2d": h2d, "d2h": abi.PACK_RESULT_BYTES + st.stats_host.numel() * 8,
+                "nonfinite": float(st.stats_host[9 + 4]), "loss": float(st.stats_host[9]) / max(N, 1)}
+
+    for _ in range(args.warmup):
+        one_step(False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = st.launches
+    recs = [one_step(True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = st.launches - launches0
+
+    dev_ms = sum(r["dev_ms"] for r in recs)
+    e2e_ms = sum(r["e2e_ms"] for r in recs)
+    toks = sum(r["n_tokens"] for r in recs)
+    kern = [k for r in recs for k in r["kernel_ms"]]
+    full = [k for r in recs for k, n in zip(r["kernel_ms"], _mb_sizes(r["n_tokens"], M)) if n == M]
+    agg = torch.tensor([dev_ms, e2e_ms, float(toks), float(sum(r["nonfinite"] for r in recs))], dtype=torch.float64,
+                       device=dev)
+    if world > 1:
+        mx = agg[:2].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = agg[2:].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        agg = torch.cat([mx, sm])
+    dev_ms, e2e_ms, toks_all, nonfinite = agg.tolist()
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+        return
+    peak, peak_src = measured_peak()
+    esize = 2 if cfg.dtype == "bf16" else 4
+    bpt = bytes_per_token(cfg.V, esize, kl)
+    avg_full = statistics.mean(full) if full else statistics.mean(kern)
+    achieved = bpt * M / (avg_full * 1e-3) / 1e9
+    traffic = _ncu_traffic(args)
+    line = {
+        "metric": METRIC, "value": toks_all / (dev_ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+        "config": {"workload": cfg.name, "prompts": cfg.P, "group_size": cfg.G, "seq_len": cfg.S, "vocab": cfg.V,
+                   "max_lag": cfg.max_lag, "kl_coef": cfg.kl_coef, "tokens_per_step": int(toks_all / args.steps),
+                   "micro_batch_rows": M, "algo": args.algo, "parallelism": f"dp{world}",
+                   "l2": "inputs >> L2 (10 GB micro-batches) + 256 MB L2 flush after each generator launch"},
+        "clocks": clk,
+        "e2e": {"value": toks_all / (e2e_ms * 1e-3), "unit": "tokens/s",
+                "h2d_bytes_per_step": recs[0]["h2d"], "d2h_bytes_per_step": recs[0]["d2h"]},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "bytes_per_token": bpt,
+                     "kernel": "echo_policy_loss_fwd_bwd", "kernel_ms_avg": avg_full,
+                     "kernel_share_of_step": sum(kern) / sum(r["dev_ms"] for r in recs),
+                     "frac_of_8TBps_nominal": achieved / 8000.0},
+        "nonfinite_tokens": nonfinite,
+        "loss": recs[-1]["loss"],
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        r = oracle_rate(cfg, b, toks_all / args.steps, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "oracle",
+            "sample": f"pack+advantage of the full batch + fused loss on {r['rows']} rows (a pool of 32 sampled rows, repeated) "
+                      f"({r['t_loss']:.1f} s); step extrapolated as t_meta + N * t_row"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+
+
+def _mb_sizes(N, M):
+    return [min(M, N - r) for r in range(0, N, M)]
+
+
+def _ncu_traffic(args):
+    """dram bytes per launch from the committed ncu --set full capture of this workload, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(f"{args.config}/{args.algo}") or d.get(args.config)
+        return None if e is None else e.get("bytes_per_launch_at_M32768")
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    import __graft_entry__
+    __graft_entry__.build()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    main_echo(args)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+if __name__ == "__main__":
+    main()

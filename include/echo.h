@@ -1,0 +1,187 @@
+/*
+ * echo.h -- C ABI of the B200-native learner hot path of Echo (arXiv 2508.05387).
+ *
+ * One learner step of the training swarm (§2.4 :254-282: the trainer's step() "consuming
+ * mini-batches drawn from the shared buffer") over version-tagged rollouts (PAPER.md :192) runs:
+ *
+ *   echo_pack_batch           (1) version-lag filter + pack        PAPER.md :192, :201, :224
+ *   echo_group_advantage      (2) GRPO group-relative advantage    PAPER.md :374; SPEC.md :206-214
+ *   echo_policy_loss_fwd_bwd  (3) log-softmax gather  (4) clipped surrogate + KL  (5) dL/dlogits in place
+ *                                                                  PAPER.md :170-171, :278, :376-382
+ *   echo_loss_stats           fixed-order fp64 reduction of the per-token outputs (statistics)
+ *
+ * Conventions shared by every entry point
+ *   - All array pointers are DEVICE pointers owned by the caller (e.g. torch allocations).  The library
+ *     never allocates, frees, synchronises or calls NCCL; every kernel goes on `stream` (a cudaStream_t,
+ *     NULL = the legacy default stream).  Calls are reentrant across streams; no global mutable state.
+ *   - The returned echo_status covers ARGUMENTS only (null pointers, sizes, alignment, device is not
+ *     sm_100) and launch failures (cudaGetLastError -> ECHO_ERR_CUDA).  Data-dependent errors are
+ *     reported on the device (echo_pack_result.status, the non-finite counter of echo_loss_stats) so
+ *     that no call hides a host synchronisation.
+ *   - Results are deterministic: no floating-point atomics; every reduction has a fixed order that
+ *     depends only on the sizes (vocab, n_tokens), never on grid size, micro-batch split or rank.
+ *   - Requires an sm_100 (B200) device; there is no fallback path.
+ */
+#ifndef ECHO_H
+#define ECHO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ECHO_API __attribute__((visibility("default")))
+#else
+#define ECHO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ECHO_OK = 0,
+  ECHO_ERR_INVALID_ARGUMENT = 1,
+  ECHO_ERR_UNSUPPORTED = 2, /* no sm_100 device / shape outside the kernels' range */
+  ECHO_ERR_CUDA = 3         /* a CUDA runtime call or kernel launch failed */
+} echo_status;
+
+typedef enum { ECHO_F32 = 0, ECHO_BF16 = 1 } echo_dtype;
+
+/* Data-dependent errors, written by echo_pack_batch into echo_pack_result.status. */
+enum {
+  ECHO_DATA_OK = 0,
+  ECHO_DATA_FUTURE_VERSION = 1,      /* param_version > t_train (SPEC.md :388 t_infer <= t_train)     */
+  ECHO_DATA_MIXED_GROUP_VERSION = 2, /* versions differ inside one prompt group (SPEC.md :48)          */
+  ECHO_DATA_BAD_LENGTH = 3,          /* resp_len not in [1, max_len] (SPEC.md :39: length >= 1)        */
+  ECHO_DATA_BAD_ACTION = 4,          /* a kept token's action not in [0, vocab)                        */
+  ECHO_DATA_CAPACITY = 5             /* n_tokens > token_capacity: token arrays were not written       */
+};
+
+/* Per-token flag bits (tok_flags). */
+enum { ECHO_FLAG_CLIPPED = 1, ECHO_FLAG_NONFINITE = 2 };
+
+/* Algorithm selector for echo_policy_loss_fwd_bwd_ex (tests / benchmarks). */
+enum {
+  ECHO_ALGO_AUTO = 0,
+  ECHO_ALGO_ROW_L2 = 1,      /* one CTA per row, two streaming passes; the second pass re-reads from L2 */
+  ECHO_ALGO_CLUSTER_SMEM = 2 /* CTA pair per row, each half-row resident in a TMA-fed shared-memory ring:
+                                exactly one HBM read + one HBM write per logit (bf16, vocab <= 196608) */
+};
+
+/* Device-resident result of echo_pack_batch (32 bytes). */
+typedef struct {
+  int32_t status;            /* ECHO_DATA_*                                                        */
+  int32_t first_bad_rollout; /* global rollout id of the first error, -1 if none / CAPACITY          */
+  int32_t n_groups_kept;
+  int32_t n_rollouts_kept;   /* = n_groups_kept * group_size                                       */
+  int64_t n_tokens;          /* packed (kept) tokens N_local = sum of kept resp_len                 */
+  int64_t internal;          /* library scratch; do not read or write                              */
+} echo_pack_result;
+
+/*
+ * (1) Version-lag filter + pack.
+ * Cites: rollouts carry a param_version tag (PAPER.md :192); the coordinator bounds the policy lag by
+ * the strict trigger t_train - t_infer > Delta_max (PAPER.md :224), so a rollout group is KEPT iff
+ * t_train - version <= max_lag and dropped iff the lag is strictly greater -- the same predicate as the
+ * buffer's param_version >= min_version (SPEC.md :344) with min_version = t_train - max_lag.
+ *
+ * Input layout (this rank's shard of the step's batch; group-major, SPEC.md :44-49):
+ *   n_rollouts R (multiple of group_size), group_size G >= 2, max_len S >= 1, vocab V >= 1.
+ *   version[R] int64, resp_len[R] int32; action / old_logp / ref_logp are padded row-major [R x S]
+ *   (position j of rollout i at i*S + j; positions >= resp_len[i] are never read).  ref_logp may be
+ *   NULL (then tok_ref must be NULL too).  rollout_base = global id of local rollout 0.
+ * Outputs (ascending, stable compaction; tokens rollout-major):
+ *   kept_rollout[R]   global ids of kept rollouts (first n_rollouts_kept entries written)
+ *   kept_offset[R+1]  CSR offsets into the token arrays (first n_rollouts_kept + 1 entries written)
+ *   tok_slot / tok_action / tok_old / tok_ref [token_capacity]: per packed token its kept-rollout
+ *   slot, action, old log-prob (the rollout's "logprobs" field, PAPER.md :162) and reference log-prob.
+ *   *result (device): see echo_pack_result.  On a data error only status and first_bad_rollout are
+ *   specified; the first error is the (rollout, check) lexicographic minimum with checks ordered
+ *   FUTURE < MIXED < BAD_LENGTH < BAD_ACTION; CAPACITY only when no other error occurred.
+ * Launches: 3 kernels.  Integer / bit-copy work only: results are bit-exact.
+ */
+ECHO_API echo_status echo_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len, int32_t vocab,
+                            int64_t t_train, int32_t max_lag, int64_t rollout_base,
+                            const int64_t* version, const int32_t* resp_len,
+                            const int32_t* action, const float* old_logp, const float* ref_logp,
+                            int64_t token_capacity,
+                            int32_t* kept_rollout, int64_t* kept_offset,
+                            int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
+                            echo_pack_result* result, void* stream);
+
+/*
+ * (2) GRPO group-relative advantage (PAPER.md :374 names GRPO; formula SPEC.md :209-213):
+ *   for each kept group of G rollouts, in fp64 with round-to-nearest and no FMA contraction:
+ *   mean = (sum r)/G, std = sqrt(sum (r - mean)^2 / G) (population), A = (r - mean)/(std + eps),
+ *   rounded to fp32.  Every token of rollout i receives A_i through tok_slot (SPEC.md :209).
+ * reward[R]: per-rollout return (sum of its per-step rewards, PAPER.md :164), indexed by local id.
+ * kept_rollout / pack: outputs of echo_pack_batch on the same shard.
+ * Outputs: adv_slot[R] (first n_rollouts_kept written), adv_stats[6] fp64 partial sums
+ *   {sum A, sum A^2, sum r, sum r^2, n_zero_std_groups, n_rollouts_kept} (A as fp32 values; per-group
+ *   partials summed in ascending group order).  Bit-identical to a sequential fp64 evaluation.
+ * Launches: 1 kernel.
+ */
+ECHO_API echo_status echo_group_advantage(int32_t n_rollouts, int32_t group_size, float eps,
+                                 const float* reward, const int32_t* kept_rollout, int64_t rollout_base,
+                                 const echo_pack_result* pack, float* adv_slot, double* adv_stats,
+                                 void* stream);
+
+/*
+ * (3)+(4)+(5) fused: one streaming pass per logits row.
+ *   (3) logp_t = z[t,a_t] - logsumexp_v z[t,v]   (the log pi_theta(a|s) field, PAPER.md :170)
+ *   (4) rho = exp(logp - old); pg = max(-A rho, -A clip(rho, 1-clip_low, 1+clip_high)) (SPEC.md :219,
+ *       eps 0.2 :243); if kl_coef > 0: kl = exp(ref-logp) - (ref-logp) - 1 (k3 to pi_ref);
+ *       l_t = pg + kl_coef * kl;  the step loss is sum_t l_t / N_global.
+ *   (5) c_t = grad_scale/N_global * ([not clipped](-A rho) + kl_coef (1 - exp(ref - logp)));
+ *       logits[t, v] <- c_t (delta_{v,a_t} - softmax(z[t,:])_v)  for v < vocab (IN PLACE; columns
+ *       vocab..ld-1 untouched).  "clipped" = (A > 0 and rho > 1+clip_high) or (A < 0 and rho < 1-clip_low).
+ * logits: [n_rows x ld] row-major, dtype ECHO_BF16 or ECHO_F32, base and ld*sizeof(dtype) 16-byte
+ *   aligned; row t is packed token t of this micro-batch.  Per-token inputs (tok_action, tok_old,
+ *   tok_ref, tok_slot) are offset by the caller to the micro-batch's first row; tok_ref may be NULL iff
+ *   kl_coef == 0.  adv_slot: echo_group_advantage output.  n_global: DEVICE pointer to one double,
+ *   the all-reduced kept-token count (fed on device: no host sync).
+ * Outputs per row: tok_logp, tok_loss (l_t, fp32), tok_flags (ECHO_FLAG_*).  A row whose lse, logp, rho,
+ *   l_t or c_t is not finite gets ECHO_FLAG_NONFINITE; its gradient row is unspecified.
+ * Arithmetic: fp32 accumulation over the bf16/fp32 logits, gradient stored with round-to-nearest-even.
+ * Launches: 1 kernel (0 when n_rows == 0).
+ */
+ECHO_API echo_status echo_policy_loss_fwd_bwd(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
+                                     const int32_t* tok_action, const float* tok_old, const float* tok_ref,
+                                     const int32_t* tok_slot, const float* adv_slot, const double* n_global,
+                                     float clip_low, float clip_high, float kl_coef, float grad_scale,
+                                     float* tok_logp, float* tok_loss, uint8_t* tok_flags, void* stream);
+
+/* Same, with an explicit ECHO_ALGO_* choice (ECHO_ERR_UNSUPPORTED if that kernel cannot take the shape). */
+ECHO_API echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
+                                        const int32_t* tok_action, const float* tok_old, const float* tok_ref,
+                                        const int32_t* tok_slot, const float* adv_slot, const double* n_global,
+                                        float clip_low, float clip_high, float kl_coef, float grad_scale,
+                                        float* tok_logp, float* tok_loss, uint8_t* tok_flags, int32_t algo,
+                                        void* stream);
+
+/*
+ * Statistics of the per-token outputs over n_tokens packed tokens (all micro-batches of the step):
+ *   loss_stats[10] = {sum l_t, sum (logp - old), sum k3(ref, logp) (0 if tok_ref NULL), n_clipped,
+ *                     n_nonfinite, rho_min, rho_max, sum logp, n_tokens, sum rho}
+ *   evaluated in fp64 from the fp32 per-token values (rho = exp(logp - old), k3 = e^x - x - 1 with
+ *   x = ref - logp); rho statistics over rows without ECHO_FLAG_NONFINITE (rho_min = +inf, rho_max = -inf
+ *   when there are none).  Fixed-order fp64 reduction: bitwise reproducible for a given n_tokens.
+ * workspace: device buffer of echo_loss_stats_workspace_bytes() bytes (no initialisation needed).
+ * Launches: 2 kernels.
+ */
+ECHO_API size_t echo_loss_stats_workspace_bytes(void);
+ECHO_API echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp, const float* tok_old,
+                            const float* tok_ref, const uint8_t* tok_flags, double* workspace, double* loss_stats,
+                            void* stream);
+
+/* Human-readable name of a status code (static storage). */
+ECHO_API const char* echo_status_string(echo_status status);
+
+/* ABI version: bumped on any signature change. */
+ECHO_API int32_t echo_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ECHO_H */

@@ -1,0 +1,139 @@
+"""ctypes binding of libecho.so -- the C ABI of include/echo.h, same names, argument marshalling only.
+
+Every entry point takes torch tensors (or None for nullable pointers) and forwards their device pointers,
+plus the caller's CUDA stream (default: torch's current stream).  No arithmetic of the method happens here:
+every step of the path runs in the kernels of libecho.so.  If the library is missing this module raises
+at import time -- there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import struct
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libecho.so")
+
+ECHO_OK, ECHO_ERR_INVALID_ARGUMENT, ECHO_ERR_UNSUPPORTED, ECHO_ERR_CUDA = range(4)
+ECHO_F32, ECHO_BF16 = 0, 1
+(ECHO_DATA_OK, ECHO_DATA_FUTURE_VERSION, ECHO_DATA_MIXED_GROUP_VERSION, ECHO_DATA_BAD_LENGTH, ECHO_DATA_BAD_ACTION,
+ ECHO_DATA_CAPACITY) = range(6)
+ECHO_FLAG_CLIPPED, ECHO_FLAG_NONFINITE = 1, 2
+ECHO_ALGO_AUTO, ECHO_ALGO_ROW_L2, ECHO_ALGO_CLUSTER_SMEM = 0, 1, 2
+PACK_RESULT_BYTES = 32
+
+# kernels launched per call (for the bench's gpu_launches count)
+LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2}
+
+EXPORTS = ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
+           "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_status_string", "echo_abi_version")
+
+
+class EchoError(RuntimeError):
+    def __init__(self, fn, status):
+        self.status = status
+        super().__init__(f"{fn} -> {_lib.echo_status_string(status).decode()}")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    i32, i64, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+    lib.echo_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, i64, P, P, P, P, P, P, P, P]
+    lib.echo_group_advantage.argtypes = [i32, i32, f32, P, P, i64, P, P, P, P]
+    lib.echo_policy_loss_fwd_bwd.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P, P, f32, f32, f32, f32, P, P, P, P]
+    lib.echo_policy_loss_fwd_bwd_ex.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P, P, f32, f32, f32, f32, P, P, P,
+                                                i32, P]
+    lib.echo_loss_stats.argtypes = [i64, P, P, P, P, P, P, P, P]
+    lib.echo_loss_stats_workspace_bytes.argtypes = []
+    lib.echo_loss_stats_workspace_bytes.restype = ctypes.c_size_t
+    lib.echo_status_string.argtypes = [ctypes.c_int]
+    lib.echo_status_string.restype = ctypes.c_char_p
+    lib.echo_abi_version.restype = i32
+    for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
+               "echo_loss_stats"):
+        getattr(lib, fn).restype = ctypes.c_int
+    return lib
+
+
+_lib = _load()
+
+
+def _p(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _s(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _check(fn, st):
+    if st != ECHO_OK:
+        raise EchoError(fn, st)
+
+
+def echo_abi_version() -> int:
+    return _lib.echo_abi_version()
+
+
+def echo_status_string(status: int) -> str:
+    return _lib.echo_status_string(status).decode()
+
+
+def echo_pack_batch(n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, version, resp_len, action,
+                    old_logp, ref_logp, token_capacity, kept_rollout, kept_offset, tok_slot, tok_action, tok_old,
+                    tok_ref, result, stream=None):
+    _check("echo_pack_batch", _lib.echo_pack_batch(
+        n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, _p(version), _p(resp_len), _p(action),
+        _p(old_logp), _p(ref_logp), token_capacity, _p(kept_rollout), _p(kept_offset), _p(tok_slot), _p(tok_action),
+        _p(tok_old), _p(tok_ref), _p(result), _s(stream)))
+
+
+def echo_group_advantage(n_rollouts, group_size, eps, reward, kept_rollout, rollout_base, pack, adv_slot, adv_stats,
+                         stream=None):
+    _check("echo_group_advantage", _lib.echo_group_advantage(
+        n_rollouts, group_size, eps, _p(reward), _p(kept_rollout), rollout_base, _p(pack), _p(adv_slot),
+        _p(adv_stats), _s(stream)))
+
+
+def echo_policy_loss_fwd_bwd(logits, dtype, n_rows, vocab, ld, tok_action, tok_old, tok_ref, tok_slot, adv_slot,
+                             n_global, clip_low, clip_high, kl_coef, grad_scale, tok_logp, tok_loss, tok_flags,
+                             stream=None, algo=None):
+    if algo is None:
+        _check("echo_policy_loss_fwd_bwd", _lib.echo_policy_loss_fwd_bwd(
+            _p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot),
+            _p(adv_slot), _p(n_global), clip_low, clip_high, kl_coef, grad_scale, _p(tok_logp), _p(tok_loss),
+            _p(tok_flags), _s(stream)))
+    else:
+        _check("echo_policy_loss_fwd_bwd_ex", _lib.echo_policy_loss_fwd_bwd_ex(
+            _p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot),
+            _p(adv_slot), _p(n_global), clip_low, clip_high, kl_coef, grad_scale, _p(tok_logp), _p(tok_loss),
+            _p(tok_flags), algo, _s(stream)))
+
+
+def echo_loss_stats_workspace_bytes() -> int:
+    return int(_lib.echo_loss_stats_workspace_bytes())
+
+
+def echo_loss_stats(n_tokens, tok_loss, tok_logp, tok_old, tok_ref, tok_flags, workspace, loss_stats, stream=None):
+    _check("echo_loss_stats", _lib.echo_loss_stats(
+        n_tokens, _p(tok_loss), _p(tok_logp), _p(tok_old), _p(tok_ref), _p(tok_flags), _p(workspace), _p(loss_stats),
+        _s(stream)))
+
+
+def parse_pack_result(raw: bytes) -> dict:
+    """Decode the 32-byte echo_pack_result read back from the device."""
+    status, first_bad, n_groups, n_rollouts, n_tokens, _ = struct.unpack("<iiiiqq", raw)
+    return {"status": status, "first_bad_rollout": first_bad, "n_groups_kept": n_groups,
+            "n_rollouts_kept": n_rollouts, "n_tokens": n_tokens}

@@ -1,0 +1,149 @@
+// abi.cu -- the extern "C" entry points of libecho (include/echo.h): argument validation + launches.
+#include <cuda_bf16.h>
+
+#include "echo_internal.h"
+
+namespace {
+
+// sm_100 check + SM count of the current device (queried per call: no global mutable state).
+echo_status device_sms(int* num_sms) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return ECHO_ERR_CUDA;
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return ECHO_ERR_CUDA;
+  if (cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) return ECHO_ERR_CUDA;
+  if (major != 10 || minor != 0) return ECHO_ERR_UNSUPPORTED;
+  if (cudaDeviceGetAttribute(num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return ECHO_ERR_CUDA;
+  return ECHO_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+echo_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ECHO_OK : ECHO_ERR_CUDA; }
+
+}  // namespace
+
+extern "C" {
+
+int32_t echo_abi_version(void) { return 1; }
+
+const char* echo_status_string(echo_status s) {
+  switch (s) {
+    case ECHO_OK: return "ECHO_OK";
+    case ECHO_ERR_INVALID_ARGUMENT: return "ECHO_ERR_INVALID_ARGUMENT";
+    case ECHO_ERR_UNSUPPORTED: return "ECHO_ERR_UNSUPPORTED";
+    case ECHO_ERR_CUDA: return "ECHO_ERR_CUDA";
+  }
+  return "ECHO_ERR_UNKNOWN";
+}
+
+echo_status echo_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len, int32_t vocab, int64_t t_train,
+                            int32_t max_lag, int64_t rollout_base, const int64_t* version, const int32_t* resp_len,
+                            const int32_t* action, const float* old_logp, const float* ref_logp,
+                            int64_t token_capacity, int32_t* kept_rollout, int64_t* kept_offset, int32_t* tok_slot,
+                            int32_t* tok_action, float* tok_old, float* tok_ref, echo_pack_result* result,
+                            void* stream) {
+  if (n_rollouts < 0 || group_size < 2 || max_len < 1 || vocab < 1 || max_lag < 0 || token_capacity < 0)
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rollouts % group_size != 0) return ECHO_ERR_INVALID_ARGUMENT;
+  if (rollout_base < 0 || rollout_base + (int64_t)n_rollouts > INT32_MAX) return ECHO_ERR_INVALID_ARGUMENT;
+  if (!result || !kept_offset || (n_rollouts > 0 && (!version || !resp_len || !action || !old_logp || !kept_rollout)))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (token_capacity > 0 && (!tok_slot || !tok_action || !tok_old)) return ECHO_ERR_INVALID_ARGUMENT;
+  if ((ref_logp == nullptr) != (tok_ref == nullptr)) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  return from_cuda(echo::launch_pack(n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, version,
+                                     resp_len, action, old_logp, ref_logp, token_capacity, kept_rollout, kept_offset,
+                                     tok_slot, tok_action, tok_old, tok_ref, result,
+                                     static_cast<cudaStream_t>(stream), sms));
+}
+
+echo_status echo_group_advantage(int32_t n_rollouts, int32_t group_size, float eps, const float* reward,
+                                 const int32_t* kept_rollout, int64_t rollout_base, const echo_pack_result* pack,
+                                 float* adv_slot, double* adv_stats, void* stream) {
+  if (n_rollouts < 0 || group_size < 2 || n_rollouts % group_size != 0 || !(eps >= 0.0f))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (!pack || !adv_stats || (n_rollouts > 0 && (!reward || !kept_rollout || !adv_slot)))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  return from_cuda(echo::launch_group_advantage(group_size, eps, rollout_base, reward, kept_rollout, pack, adv_slot,
+                                                adv_stats, static_cast<cudaStream_t>(stream)));
+}
+
+echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
+                                        const int32_t* tok_action, const float* tok_old, const float* tok_ref,
+                                        const int32_t* tok_slot, const float* adv_slot, const double* n_global,
+                                        float clip_low, float clip_high, float kl_coef, float grad_scale,
+                                        float* tok_logp, float* tok_loss, uint8_t* tok_flags, int32_t algo,
+                                        void* stream) {
+  if (dtype != ECHO_F32 && dtype != ECHO_BF16) return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows < 0 || vocab < 1 || ld < vocab) return ECHO_ERR_INVALID_ARGUMENT;
+  const int64_t esize = dtype == ECHO_BF16 ? 2 : 4;
+  if ((ld * esize) % 16 != 0) return ECHO_ERR_INVALID_ARGUMENT;
+  if (!(clip_low >= 0.0f && clip_low < 1.0f && clip_high >= 0.0f) || !(kl_coef >= 0.0f)) return ECHO_ERR_INVALID_ARGUMENT;
+  if (!n_global) return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows > 0) {
+    if (!logits || !aligned16(logits) || !tok_action || !tok_old || !tok_slot || !adv_slot || !tok_logp ||
+        !tok_loss || !tok_flags)
+      return ECHO_ERR_INVALID_ARGUMENT;
+    if (kl_coef > 0.0f && !tok_ref) return ECHO_ERR_INVALID_ARGUMENT;
+  }
+  if (algo != ECHO_ALGO_AUTO && algo != ECHO_ALGO_ROW_L2 && algo != ECHO_ALGO_CLUSTER_SMEM)
+    return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  if (n_rows == 0) return ECHO_OK;
+  const bool cluster_ok = echo::cluster_algo_supports(dtype, vocab);
+  if (algo == ECHO_ALGO_AUTO) algo = (cluster_ok && vocab >= 16384) ? ECHO_ALGO_CLUSTER_SMEM : ECHO_ALGO_ROW_L2;
+  if (algo == ECHO_ALGO_CLUSTER_SMEM && !cluster_ok) return ECHO_ERR_UNSUPPORTED;
+  echo::LossParams p;
+  p.logits = static_cast<uint8_t*>(logits);
+  p.n_rows = n_rows;
+  p.V = vocab;
+  p.ld_bytes = ld * esize;
+  p.tok_action = tok_action;
+  p.tok_old = tok_old;
+  p.tok_ref = tok_ref;
+  p.tok_slot = tok_slot;
+  p.adv_slot = adv_slot;
+  p.n_global = n_global;
+  p.clip_low = clip_low;
+  p.clip_high = clip_high;
+  p.kl_coef = kl_coef;
+  p.grad_scale = grad_scale;
+  p.tok_logp = tok_logp;
+  p.tok_loss = tok_loss;
+  p.tok_flags = tok_flags;
+  return from_cuda(echo::launch_policy_loss(p, dtype, algo, static_cast<cudaStream_t>(stream), sms));
+}
+
+echo_status echo_policy_loss_fwd_bwd(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
+                                     const int32_t* tok_action, const float* tok_old, const float* tok_ref,
+                                     const int32_t* tok_slot, const float* adv_slot, const double* n_global,
+                                     float clip_low, float clip_high, float kl_coef, float grad_scale, float* tok_logp,
+                                     float* tok_loss, uint8_t* tok_flags, void* stream) {
+  return echo_policy_loss_fwd_bwd_ex(logits, dtype, n_rows, vocab, ld, tok_action, tok_old, tok_ref, tok_slot,
+                                     adv_slot, n_global, clip_low, clip_high, kl_coef, grad_scale, tok_logp, tok_loss,
+                                     tok_flags, ECHO_ALGO_AUTO, stream);
+}
+
+size_t echo_loss_stats_workspace_bytes(void) { return echo::loss_stats_workspace_bytes(); }
+
+echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp, const float* tok_old,
+                            const float* tok_ref, const uint8_t* tok_flags, double* workspace, double* loss_stats,
+                            void* stream) {
+  if (n_tokens < 0 || !workspace || !loss_stats) return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_tokens > 0 && (!tok_loss || !tok_logp || !tok_old || !tok_flags)) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  return from_cuda(echo::launch_loss_stats(n_tokens, tok_loss, tok_logp, tok_old, tok_ref, tok_flags, workspace,
+                                           loss_stats, static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

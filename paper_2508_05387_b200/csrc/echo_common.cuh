@@ -1,0 +1,212 @@
+// echo_common.cuh -- sm_100a device helpers shared by the libecho kernels (inline PTX).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "echo.h"
+
+#define ECHO_DEVINL __device__ __forceinline__
+
+namespace echo {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ---------------------------------------------------------------- bf16 <-> fp32 (bit level)
+ECHO_DEVINL float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+ECHO_DEVINL float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+// Two fp32 -> packed bf16x2, round-to-nearest-even (F2FP.BF16.F32.PACK_AB).  `lo` lands in bits 0..15.
+ECHO_DEVINL uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+ECHO_DEVINL float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ---------------------------------------------------------------- L2 cache policies
+ECHO_DEVINL uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+ECHO_DEVINL uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+ECHO_DEVINL uint4 ldg_v4_hint(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+ECHO_DEVINL void stg_v4_hint(void* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
+// ---------------------------------------------------------------- shared-memory addressing
+ECHO_DEVINL uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+ECHO_DEVINL uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// ---------------------------------------------------------------- mbarrier
+ECHO_DEVINL void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+ECHO_DEVINL void fence_mbar_init_cluster() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+ECHO_DEVINL void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar) : "memory");
+}
+ECHO_DEVINL void mbar_arrive_expect_tx(uint32_t bar, uint32_t tx) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
+               "r"(tx)
+               : "memory");
+}
+ECHO_DEVINL bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+ECHO_DEVINL void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// Acquire at cluster scope: for data written into this CTA's smem by the peer CTA (st.async).
+ECHO_DEVINL bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+ECHO_DEVINL void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait_cluster(bar, parity)) {
+  }
+}
+
+// ---------------------------------------------------------------- bulk async copy (TMA, 1-D)
+// global -> this CTA's shared memory, completion signalled on `bar` (complete_tx::bytes).
+ECHO_DEVINL void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+// ---------------------------------------------------------------- clusters / DSMEM
+ECHO_DEVINL uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+ECHO_DEVINL uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+ECHO_DEVINL uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+ECHO_DEVINL uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+ECHO_DEVINL void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 16-byte remote store into the peer CTA's smem that completes 16 tx-bytes on the peer's mbarrier.
+ECHO_DEVINL void st_async_v4(uint32_t remote_addr, uint4 v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(
+                   remote_addr),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(remote_bar)
+               : "memory");
+}
+
+// ---------------------------------------------------------------- named barriers
+ECHO_DEVINL void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------- online (max, sum-exp) pair
+// Merge is symmetric bit-for-bit (IEEE add/mul commute), so butterfly reductions give every lane the
+// same value; the order of a tree depends only on thread layout.
+struct MaxSum {
+  float m;  // running max (-inf when empty)
+  float s;  // sum of exp(x - m)
+};
+ECHO_DEVINL MaxSum maxsum_merge(MaxSum a, MaxSum b) {
+  float m = fmaxf(a.m, b.m);
+  if (m == -INFINITY) return MaxSum{m, a.s + b.s};
+  float sa = a.s * ex2((a.m - m) * kLog2e);
+  float sb = b.s * ex2((b.m - m) * kLog2e);
+  return MaxSum{m, sa + sb};
+}
+ECHO_DEVINL MaxSum warp_maxsum(MaxSum v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    MaxSum w{__shfl_xor_sync(0xffffffffu, v.m, o), __shfl_xor_sync(0xffffffffu, v.s, o)};
+    v = maxsum_merge(v, w);
+  }
+  return v;
+}
+
+// ---------------------------------------------------------------- the per-row scalar epilogue (4)
+struct RowScalars {
+  float logp, loss, coef;  // coef = c_t: dl/dlogp * grad_scale / N_global
+  uint8_t flags;
+};
+// lse: log-sum-exp of the row; za: logit at the action.
+ECHO_DEVINL RowScalars row_epilogue(float lse, float za, float old, float ref, float adv, float clip_low,
+                                    float clip_high, float kl_coef, float grad_scale, double n_global) {
+  RowScalars r;
+  float logp = za - lse;
+  float rho = expf(logp - old);
+  float lo = 1.0f - clip_low, hi = 1.0f + clip_high;
+  bool clipped = (adv > 0.0f && rho > hi) || (adv < 0.0f && rho < lo);
+  float rho_c = fminf(fmaxf(rho, lo), hi);
+  float pg = fmaxf(-adv * rho, -adv * rho_c);
+  float kl = 0.0f, dkl = 0.0f;
+  if (kl_coef > 0.0f) {
+    float x = ref - logp;
+    float ex = expf(x);
+    kl = ex - x - 1.0f;
+    dkl = 1.0f - ex;
+  }
+  float loss = pg + kl_coef * kl;
+  float dl = (clipped ? 0.0f : -adv * rho) + kl_coef * dkl;
+  float coef = (float)((double)grad_scale * (double)dl / n_global);
+  bool finite = isfinite(lse) && isfinite(logp) && isfinite(rho) && isfinite(loss) && isfinite(coef);
+  r.logp = logp;
+  r.loss = loss;
+  r.coef = coef;
+  r.flags = (uint8_t)((clipped ? ECHO_FLAG_CLIPPED : 0) | (finite ? 0 : ECHO_FLAG_NONFINITE));
+  return r;
+}
+
+}  // namespace echo

@@ -1,0 +1,47 @@
+// echo_internal.h -- host-side launcher declarations shared by the libecho translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "echo.h"
+
+namespace echo {
+
+// Parameter block of the fused policy-loss kernels (passed by value as a kernel argument).
+struct LossParams {
+  uint8_t* logits;
+  int64_t n_rows;
+  int32_t V;
+  int64_t ld_bytes;
+  const int32_t* __restrict__ tok_action;
+  const float* __restrict__ tok_old;
+  const float* __restrict__ tok_ref;
+  const int32_t* __restrict__ tok_slot;
+  const float* __restrict__ adv_slot;
+  const double* __restrict__ n_global;
+  float clip_low, clip_high, kl_coef, grad_scale;
+  float* __restrict__ tok_logp;
+  float* __restrict__ tok_loss;
+  uint8_t* __restrict__ tok_flags;
+};
+
+cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_train, int32_t max_lag,
+                        int64_t rollout_base, const int64_t* version, const int32_t* resp_len, const int32_t* action,
+                        const float* old_logp, const float* ref_logp, int64_t cap, int32_t* kept_rollout,
+                        int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
+                        echo_pack_result* res, cudaStream_t stream, int num_sms);
+
+cudaError_t launch_group_advantage(int32_t G, float eps, int64_t rollout_base, const float* reward,
+                                   const int32_t* kept_rollout, const echo_pack_result* pack, float* adv_slot,
+                                   double* adv_stats, cudaStream_t stream);
+
+bool cluster_algo_supports(int32_t dtype, int32_t V);
+cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms);
+
+size_t loss_stats_workspace_bytes();
+cudaError_t launch_loss_stats(int64_t n, const float* tok_loss, const float* tok_logp, const float* tok_old,
+                              const float* tok_ref, const uint8_t* tok_flags, double* ws, double* out,
+                              cudaStream_t stream);
+
+}  // namespace echo

@@ -1,0 +1,172 @@
+// pack.cu -- (1) version-lag filter + pack (PAPER.md :192, :201, :224; SPEC.md :44-49, :344).
+//
+// Three launches, integer work only (bit-exact):
+//   pack_scan_kernel     1 CTA x 1024 threads: validate every rollout, decide keep per group from its
+//                        version (keep iff t_train - v <= max_lag), exclusive-scan kept rollouts and
+//                        their lengths into kept_rollout / kept_offset, min-reduce the error key.
+//   pack_gather_kernel   grid-stride over kept slots: copy each kept rollout's first L tokens
+//                        (action, old, ref) into the packed arrays, tag tok_slot, check action range.
+//   pack_finalize_kernel 1 thread: decode the error key into status / first_bad_rollout.
+// The error key is rollout * 8 + check (checks ordered FUTURE < MIXED < BAD_LENGTH < BAD_ACTION), so the
+// reported error is the (rollout, check) lexicographic minimum -- independent of thread scheduling.
+#include "echo_common.cuh"
+#include "echo_internal.h"
+
+namespace echo {
+
+constexpr int kScanThreads = 1024;
+constexpr unsigned long long kNoError = 0xFFFFFFFFFFFFFFFFull;
+
+__global__ void __launch_bounds__(kScanThreads) pack_scan_kernel(
+    int32_t R, int32_t G, int32_t S, int64_t t_train, int32_t max_lag, int64_t rollout_base,
+    const int64_t* __restrict__ version, const int32_t* __restrict__ resp_len, int32_t* __restrict__ kept_rollout,
+    int64_t* __restrict__ kept_offset, echo_pack_result* __restrict__ res) {
+  __shared__ unsigned long long s_err;
+  __shared__ int32_t s_wkeep[32];
+  __shared__ int64_t s_wtok[32];
+  __shared__ int32_t s_carry_keep;
+  __shared__ int64_t s_carry_tok;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    s_err = kNoError;
+    s_carry_keep = 0;
+    s_carry_tok = 0;
+  }
+  __syncthreads();
+
+  for (int32_t base = 0; base < R; base += kScanThreads) {
+    const int32_t i = base + tid;
+    int32_t keep = 0;
+    int64_t len = 0;
+    if (i < R) {
+      const int64_t v = version[i];
+      const int64_t v0 = version[(i / G) * G];
+      const int32_t L = resp_len[i];
+      unsigned long long key = kNoError;
+      if (v > t_train)
+        key = (unsigned long long)i * 8 + ECHO_DATA_FUTURE_VERSION;
+      else if (v != v0)
+        key = (unsigned long long)i * 8 + ECHO_DATA_MIXED_GROUP_VERSION;
+      else if (L < 1 || L > S)
+        key = (unsigned long long)i * 8 + ECHO_DATA_BAD_LENGTH;
+      if (key != kNoError) atomicMin(&s_err, key);
+      keep = (t_train - v0) <= (int64_t)max_lag ? 1 : 0;
+      len = keep ? (int64_t)min(max(L, 0), S) : 0;
+    }
+    // block-wide exclusive scan of (keep, len): warp inclusive scan, then warp totals
+    int32_t ik = keep;
+    int64_t it = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t k2 = __shfl_up_sync(0xffffffffu, ik, o);
+      int64_t t2 = __shfl_up_sync(0xffffffffu, it, o);
+      if (lane >= o) {
+        ik += k2;
+        it += t2;
+      }
+    }
+    if (lane == 31) {
+      s_wkeep[warp] = ik;
+      s_wtok[warp] = it;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int32_t wk = s_wkeep[lane];
+      int64_t wt = s_wtok[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int32_t k2 = __shfl_up_sync(0xffffffffu, wk, o);
+        int64_t t2 = __shfl_up_sync(0xffffffffu, wt, o);
+        if (lane >= o) {
+          wk += k2;
+          wt += t2;
+        }
+      }
+      s_wkeep[lane] = wk;  // inclusive over warps
+      s_wtok[lane] = wt;
+    }
+    __syncthreads();
+    const int32_t excl_k = s_carry_keep + (warp ? s_wkeep[warp - 1] : 0) + ik - keep;
+    const int64_t excl_t = s_carry_tok + (warp ? s_wtok[warp - 1] : 0) + it - len;
+    if (keep) {
+      kept_rollout[excl_k] = (int32_t)(rollout_base + i);
+      kept_offset[excl_k] = excl_t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_carry_keep += s_wkeep[31];
+      s_carry_tok += s_wtok[31];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    kept_offset[s_carry_keep] = s_carry_tok;
+    res->n_rollouts_kept = s_carry_keep;
+    res->n_groups_kept = s_carry_keep / G;
+    res->n_tokens = s_carry_tok;
+    res->internal = (int64_t)s_err;
+    res->status = ECHO_DATA_OK;
+    res->first_bad_rollout = -1;
+  }
+}
+
+__global__ void __launch_bounds__(256) pack_gather_kernel(
+    int32_t S, int32_t V, int64_t rollout_base, int64_t cap, const int32_t* __restrict__ action,
+    const float* __restrict__ old_logp, const float* __restrict__ ref_logp, const int32_t* __restrict__ kept_rollout,
+    const int64_t* __restrict__ kept_offset, int32_t* __restrict__ tok_slot, int32_t* __restrict__ tok_action,
+    float* __restrict__ tok_old, float* __restrict__ tok_ref, echo_pack_result* __restrict__ res) {
+  __shared__ unsigned long long s_bad;
+  const int32_t n_kept = res->n_rollouts_kept;
+  const bool write = res->n_tokens <= cap;
+  for (int32_t k = blockIdx.x; k < n_kept; k += gridDim.x) {
+    if (threadIdx.x == 0) s_bad = kNoError;
+    __syncthreads();
+    const int64_t i = (int64_t)kept_rollout[k] - rollout_base;
+    const int64_t off = kept_offset[k];
+    const int32_t L = (int32_t)(kept_offset[k + 1] - off);
+    const int64_t src = i * S;
+    for (int32_t j = threadIdx.x; j < L; j += blockDim.x) {
+      const int32_t a = action[src + j];
+      if (a < 0 || a >= V) s_bad = (unsigned long long)i * 8 + ECHO_DATA_BAD_ACTION;  // same value from all
+      if (write) {
+        tok_slot[off + j] = k;
+        tok_action[off + j] = a;
+        tok_old[off + j] = old_logp[src + j];
+        if (tok_ref) tok_ref[off + j] = ref_logp[src + j];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_bad != kNoError)
+      atomicMin(reinterpret_cast<unsigned long long*>(&res->internal), s_bad);
+  }
+}
+
+__global__ void pack_finalize_kernel(int64_t rollout_base, int64_t cap, echo_pack_result* res) {
+  const unsigned long long key = (unsigned long long)res->internal;
+  if (key != kNoError) {
+    res->status = (int32_t)(key % 8);
+    res->first_bad_rollout = (int32_t)(rollout_base + (int64_t)(key / 8));
+  } else if (res->n_tokens > cap) {
+    res->status = ECHO_DATA_CAPACITY;
+    res->first_bad_rollout = -1;
+  } else {
+    res->status = ECHO_DATA_OK;
+    res->first_bad_rollout = -1;
+  }
+}
+
+cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_train, int32_t max_lag,
+                        int64_t rollout_base, const int64_t* version, const int32_t* resp_len, const int32_t* action,
+                        const float* old_logp, const float* ref_logp, int64_t cap, int32_t* kept_rollout,
+                        int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
+                        echo_pack_result* res, cudaStream_t stream, int num_sms) {
+  pack_scan_kernel<<<1, kScanThreads, 0, stream>>>(R, G, S, t_train, max_lag, rollout_base, version, resp_len,
+                                                   kept_rollout, kept_offset, res);
+  int grid = R < num_sms * 8 ? (R > 0 ? R : 1) : num_sms * 8;
+  pack_gather_kernel<<<grid, 256, 0, stream>>>(S, V, rollout_base, cap, action, old_logp, ref_logp, kept_rollout,
+                                               kept_offset, tok_slot, tok_action, tok_old, tok_ref, res);
+  pack_finalize_kernel<<<1, 1, 0, stream>>>(rollout_base, cap, res);
+  return cudaGetLastError();
+}
+
+}  // namespace echo

@@ -1,0 +1,155 @@
+"""One learner step on one rank, driven through the C ABI (the public API a trainer's ``step()`` calls).
+
+    h2d        rollouts of this rank's shard, host (pinned) -> device
+    pack       echo_pack_batch                 (1) lag filter + pack; one 32-byte D2H read sizes the logits
+    advantage  echo_group_advantage            (2) GRPO advantage
+    stats1     all-reduce {N, advantage/reward sums, group counts} -> N_global stays on the device
+    loss       echo_policy_loss_fwd_bwd        (3)-(5) once per micro-batch of logits rows (in place)
+    finish     echo_loss_stats + all-reduce    statistics of the step, read back for logging
+
+torch is used for device memory, pinned host staging, streams and process groups only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import abi
+from .parallel import allreduce_sum_, reduce_loss_stats_, LOSS_STATS, STATS1
+
+
+@dataclass
+class PackInfo:
+    status: int
+    first_bad_rollout: int
+    n_groups_kept: int
+    n_rollouts_kept: int
+    n_tokens: int
+
+
+class LearnerStep:
+    def __init__(self, *, n_rollouts: int, group_size: int, max_len: int, vocab: int, dtype: str = "bf16",
+                 has_ref: bool = True, device=None, group=None, eps: float = 1e-8):
+        self.R, self.G, self.S, self.V = n_rollouts, group_size, max_len, vocab
+        self.dtype = dtype
+        self.edtype = abi.ECHO_BF16 if dtype == "bf16" else abi.ECHO_F32
+        self.has_ref = has_ref
+        self.eps = eps
+        self.group = group
+        self.launches = 0
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        self.device = dev
+        R, S = n_rollouts, max_len
+        cap = max(R * S, 1)
+        e = dict(device=dev)
+        # inputs
+        self.version = torch.empty(R, dtype=torch.int64, **e)
+        self.resp_len = torch.empty(R, dtype=torch.int32, **e)
+        self.reward = torch.empty(R, dtype=torch.float32, **e)
+        self.action = torch.empty(R * S, dtype=torch.int32, **e)
+        self.old_logp = torch.empty(R * S, dtype=torch.float32, **e)
+        self.ref_logp = torch.empty(R * S, dtype=torch.float32, **e) if has_ref else None
+        # packed state
+        self.cap = cap
+        self.kept_rollout = torch.empty(max(R, 1), dtype=torch.int32, **e)
+        self.kept_offset = torch.empty(R + 1, dtype=torch.int64, **e)
+        self.tok_slot = torch.empty(cap, dtype=torch.int32, **e)
+        self.tok_action = torch.empty(cap, dtype=torch.int32, **e)
+        self.tok_old = torch.empty(cap, dtype=torch.float32, **e)
+        self.tok_ref = torch.empty(cap, dtype=torch.float32, **e) if has_ref else None
+        self.pack_result = torch.zeros(abi.PACK_RESULT_BYTES, dtype=torch.uint8, **e)
+        self.adv_slot = torch.empty(max(R, 1), dtype=torch.float32, **e)
+        self.adv_stats = torch.empty(6, dtype=torch.float64, **e)
+        self.stats1 = torch.zeros(len(STATS1), dtype=torch.float64, **e)
+        # per-token outputs
+        self.tok_logp = torch.empty(cap, dtype=torch.float32, **e)
+        self.tok_loss = torch.empty(cap, dtype=torch.float32, **e)
+        self.tok_flags = torch.empty(cap, dtype=torch.uint8, **e)
+        self.ws = torch.empty(abi.echo_loss_stats_workspace_bytes() // 8, dtype=torch.float64, **e)
+        self.loss_stats = torch.empty(len(LOSS_STATS), dtype=torch.float64, **e)
+        # pinned host staging for the two reads of a step
+        self.pack_host = torch.empty(abi.PACK_RESULT_BYTES, dtype=torch.uint8, pin_memory=True)
+        self.stats_host = torch.empty(len(STATS1) + len(LOSS_STATS), dtype=torch.float64, pin_memory=True)
+        self.pack_info: PackInfo | None = None
+
+    # ------------------------------------------------------------------ inputs
+    def h2d(self, version, resp_len, reward, action, old_logp, ref_logp=None) -> int:
+        """Copy this step's rollouts (host tensors, ideally pinned) to the device; returns bytes moved."""
+        n = 0
+        for dst, src in ((self.version, version), (self.resp_len, resp_len), (self.reward, reward),
+                         (self.action, action), (self.old_logp, old_logp), (self.ref_logp, ref_logp)):
+            if dst is None or src is None:
+                continue
+            src = src.reshape(-1)
+            dst[: src.numel()].copy_(src, non_blocking=True)
+            n += src.numel() * src.element_size()
+        return n
+
+    # ------------------------------------------------------------------ (1) + (2)
+    def pack(self, *, t_train: int, max_lag: int, rollout_base: int = 0, n_rollouts: int | None = None,
+             read_back: bool = True) -> PackInfo | None:
+        R = self.R if n_rollouts is None else n_rollouts
+        abi.echo_pack_batch(R, self.G, self.S, self.V, t_train, max_lag, rollout_base, self.version, self.resp_len,
+                            self.action, self.old_logp, self.ref_logp, self.cap, self.kept_rollout, self.kept_offset,
+                            self.tok_slot, self.tok_action, self.tok_old, self.tok_ref, self.pack_result)
+        self.launches += abi.LAUNCHES["echo_pack_batch"]
+        self._R_step, self._base = R, rollout_base
+        if not read_back:
+            return None
+        self.pack_host.copy_(self.pack_result, non_blocking=True)
+        torch.cuda.current_stream().synchronize()          # the step's one host sync: sizes the logits
+        self.pack_info = PackInfo(**abi.parse_pack_result(bytes(self.pack_host.numpy().tobytes())))
+        return self.pack_info
+
+    def advantage(self):
+        abi.echo_group_advantage(self._R_step, self.G, self.eps, self.reward, self.kept_rollout, self._base,
+                                 self.pack_result, self.adv_slot, self.adv_stats)
+        self.launches += abi.LAUNCHES["echo_group_advantage"]
+
+    def reduce_counts(self) -> torch.Tensor:
+        """stats1 = {N, sum A, sum A^2, sum r, sum r^2, n_zero_std, n_rollouts_kept, n_groups_kept, n_dropped},
+        all-reduced; returns the device view holding N_global (fed to the loss kernel without a host sync)."""
+        info = self.pack_info
+        n_groups = self._R_step // self.G
+        self.stats1[0] = float(info.n_tokens)
+        self.stats1[1:7].copy_(self.adv_stats)
+        self.stats1[7] = float(info.n_groups_kept)
+        self.stats1[8] = float(n_groups - info.n_groups_kept)
+        allreduce_sum_(self.stats1, self.group)
+        return self.stats1[0:1]
+
+    # ------------------------------------------------------------------ (3)-(5)
+    def loss(self, logits: torch.Tensor, row0: int, *, clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0,
+             algo=None, stream=None):
+        """Fused loss fwd+bwd over packed rows [row0, row0 + logits.shape[0]); logits become dlogits."""
+        n_rows, ld = logits.shape
+        sl = slice(row0, row0 + n_rows)
+        abi.echo_policy_loss_fwd_bwd(logits, self.edtype, n_rows, self.V, ld, self.tok_action[sl], self.tok_old[sl],
+                                     self.tok_ref[sl] if (self.tok_ref is not None and kl_coef > 0) else None,
+                                     self.tok_slot[sl], self.adv_slot, self.stats1[0:1], clip_low, clip_high, kl_coef,
+                                     grad_scale, self.tok_logp[sl], self.tok_loss[sl], self.tok_flags[sl],
+                                     stream=stream, algo=algo)
+        self.launches += abi.LAUNCHES["echo_policy_loss_fwd_bwd"] if n_rows > 0 else 0
+
+    # ------------------------------------------------------------------ statistics
+    def finish(self, read_back: bool = True) -> dict | None:
+        n = self.pack_info.n_tokens
+        abi.echo_loss_stats(n, self.tok_loss, self.tok_logp, self.tok_old,
+                            self.tok_ref if self.tok_ref is not None else None, self.tok_flags, self.ws,
+                            self.loss_stats)
+        self.launches += abi.LAUNCHES["echo_loss_stats"]
+        reduce_loss_stats_(self.loss_stats, self.group)
+        if not read_back:
+            return None
+        self.stats_host[: len(STATS1)].copy_(self.stats1, non_blocking=True)
+        self.stats_host[len(STATS1):].copy_(self.loss_stats, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        v = self.stats_host.tolist()
+        out = dict(zip(STATS1, v[: len(STATS1)]))
+        out.update({"loss/" + k: x for k, x in zip(LOSS_STATS, v[len(STATS1):])})
+        out["loss"] = out["loss/sum_loss"] / out["n_tokens"] if out["n_tokens"] else 0.0
+        return out
+
+    def d2h_bytes(self) -> int:
+        return abi.PACK_RESULT_BYTES + self.stats_host.numel() * 8

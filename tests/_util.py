@@ -1,0 +1,77 @@
+"""Shared helpers for the parity tests (CUDA path via the C ABI vs. the CPU oracle on the same seeded inputs)."""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+import oracle
+import synth
+
+
+def bf16_ulp(x):
+    """ulp of bf16 values (8 significant bits)."""
+    x = np.abs(np.asarray(x, np.float64))
+    e = np.floor(np.log2(np.maximum(x, 2.0 ** -126)))
+    return 2.0 ** (e - 7)
+
+
+def pow2_scale_for(max_abs_d_at_unit_scale: float) -> float:
+    """Power-of-two grad_scale s with max|d| in [0.25, 0.5) (makes the 2e-3 bar meaningful)."""
+    if max_abs_d_at_unit_scale == 0:
+        return 1.0
+    return 2.0 ** (math.floor(math.log2(0.5 / max_abs_d_at_unit_scale)))
+
+
+@dataclass
+class OracleStep:
+    pk: oracle.PackOut
+    adv: np.ndarray
+    adv_stats: np.ndarray
+    keys: np.ndarray          # global token key per packed token
+
+
+def oracle_step(cfg: synth.Config, b: synth.Batch, rollout_base=0) -> OracleStep:
+    pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,
+                           vocab=cfg.V, t_train=synth.T_TRAIN, max_lag=cfg.max_lag, rollout_base=rollout_base)
+    adv, st = oracle.group_advantage(b.reward, pk.kept_rollout, group_size=cfg.G, rollout_base=rollout_base)
+    keys = (pk.kept_rollout[pk.tok_slot].astype(np.int64) * cfg.S
+            + (np.arange(pk.n_tokens, dtype=np.int64) - pk.kept_offset[pk.tok_slot]))
+    return OracleStep(pk, adv, st, keys)
+
+
+def host_rows(cfg: synth.Config, keys, actions):
+    """Logits rows from the numpy twin of the GPU generator: uint16 bf16 bits or float32."""
+    return synth.logits_rows(keys, actions, cfg.V, cfg.seed, "bf16" if cfg.dtype == "bf16" else "f32")
+
+
+def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dtype: str, clip=(0.2, 0.2),
+               old=None):
+    """Element-wise parity of a set of rows; returns number of gradient rows compared.
+
+    logp: |d| <= 1e-5 + 1e-6 |logp|; l_t: rtol 1e-5 (+1e-6 abs); dlogits (bf16): |d| <= 2^-8 |d_ref| + 4e-6 |c_t|
+    (faithful bf16 rounding + fp32 slack) and the north_star bar max|d| <= 2e-3; (fp32): |d| <= 1e-5 |c_t|.
+    Rows whose reference ratio sits within 1e-5 of a clip boundary decide "clipped" in different precisions
+    (fp64 vs fp32): only logp is compared there.
+    """
+    logp_gpu = np.asarray(logp_gpu, np.float64)
+    assert np.all(np.abs(logp_gpu - ref.logp) <= 1e-5 + 1e-6 * np.abs(ref.logp)), \
+        f"logp max err {np.max(np.abs(logp_gpu - ref.logp))}"
+    rho = np.exp(ref.logp - np.asarray(old, np.float64))
+    near = (np.abs(rho - (1 - clip[0])) < 1e-5) | (np.abs(rho - (1 + clip[1])) < 1e-5)
+    ok = ~near & ((ref.flags & 2) == 0)
+    np.testing.assert_array_equal(np.asarray(flags_gpu)[ok], ref.flags[ok])
+    loss_gpu = np.asarray(loss_gpu, np.float64)
+    assert np.all(np.abs(loss_gpu - ref.loss)[ok] <= 1e-5 * np.abs(ref.loss[ok]) + 1e-6)
+    d = np.asarray(d_gpu, np.float64)[ok]
+    dr = ref.dlogits[ok]
+    c = np.abs(ref.coef[ok])[:, None]
+    if dtype == "bf16":
+        tol = 2.0 ** -8 * np.abs(dr) + 4e-6 * c
+    else:
+        tol = 1e-5 * c
+    err = np.abs(d - dr)
+    bad = err > tol + 1e-30
+    assert not bad.any(), f"dlogits: {bad.sum()} elements out of tolerance; worst {err[bad].max()} at tol {tol[bad].min()}"
+    return int(ok.sum()), float(err.max()) if err.size else 0.0

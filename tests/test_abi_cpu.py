@@ -1,0 +1,90 @@
+"""CPU-side checks of the boundary: libecho.so builds for sm_100a, loads, exports every symbol include/echo.h
+declares; the product package never touches the oracle and fails loudly without its native library."""
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2508_05387_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "echo.h")).read()
+    return sorted(set(re.findall(r"ECHO_API\s+[\w\s\*]+?\b(echo_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd"):
+        assert s in syms
+    assert len(syms) >= 8
+
+
+def test_library_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(PKG, "libecho.so")], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(\w+)$", out, re.M))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    import paper_2508_05387_b200.abi as abi
+    assert set(abi.EXPORTS) == set(declared_symbols())
+    assert abi.echo_abi_version() == 1
+    assert abi.echo_status_string(abi.ECHO_ERR_UNSUPPORTED) == "ECHO_ERR_UNSUPPORTED"
+    assert abi.echo_loss_stats_workspace_bytes() > 0
+
+
+def test_library_is_sm100a_code():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", os.path.join(PKG, "libecho.so")],
+                         capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_cluster_kernel_uses_tma_bulk_copies_and_dsmem():
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", os.path.join(PKG, "libecho.so")],
+                          capture_output=True, text=True, check=True).stdout
+    blocks = re.split(r"\n\s*Function : ", sass)
+    cluster = [b for b in blocks if b.startswith("_ZN4echo26policy_loss_cluster_kernel")]
+    assert len(cluster) == 1
+    body = cluster[0]
+    assert "UBLKCP.S.G" in body      # cp.async.bulk global->shared (TMA engine)
+    assert "SYNCS" in body           # mbarrier phase / tx tracking
+    assert "STAS" in body            # st.async into the peer CTA's shared memory (DSMEM)
+    assert "UCGABAR" in body         # cluster barrier (setup / teardown only)
+    assert "STG.E.NA.128" in body    # 16-byte gradient stores
+    assert "HMMA" not in body and "UTCHMMA" not in body   # no tensor cores: a stream, not a contraction
+
+
+def test_calls_without_gpu_report_an_error_not_a_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    import paper_2508_05387_b200.abi as abi
+    with pytest.raises(abi.EchoError):
+        abi.echo_loss_stats(0, None, None, None, None, None, 8, 8, stream=0)
+
+
+def test_product_never_imports_the_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
+                assert "echo_ref_" not in txt and "echo_oracle" not in txt, f
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    dst = tmp_path / "paper_2508_05387_b200"
+    shutil.copytree(PKG, dst, ignore=shutil.ignore_patterns("*.so", "__pycache__"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2508_05387_b200"], cwd=tmp_path, capture_output=True,
+                       text=True)
+    assert r.returncode != 0 and "not built" in r.stderr

@@ -1,0 +1,381 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star, made scale-aware in tests/_util.check_rows): packing and indices bit-exact;
+advantages bit-exact; per-token logp |err| <= 1e-5; step loss within 1e-5 relative (of max(|L|, mean|l|));
+dlogits within 2e-3 absolute for bf16 at a grad_scale putting max|d| in [0.25, 0.5), and faithful per element.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from _util import check_rows, host_rows, oracle_step, pow2_scale_for
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = {"row_l2": 1, "cluster_smem": 2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def device_step(cfg, b, rollout_base=0, has_ref=True):
+    from paper_2508_05387_b200.step import LearnerStep
+    R = b.version.shape[0]
+    st = LearnerStep(n_rollouts=R, group_size=cfg.G, max_len=cfg.S, vocab=cfg.V, dtype=cfg.dtype, has_ref=has_ref)
+    t = [torch.from_numpy(np.ascontiguousarray(x)) for x in (b.version, b.resp_len, b.reward, b.action, b.old_logp)]
+    st.h2d(*t, torch.from_numpy(np.ascontiguousarray(b.ref_logp)) if has_ref else None)
+    info = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag, rollout_base=rollout_base)
+    st.advantage()
+    st.reduce_counts()
+    return st, info
+
+
+def fill(st, cfg, row0, n_rows, ld=None):
+    import synth.gpu as sgpu
+    ld = cfg.V if ld is None else ld
+    dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    logits = torch.zeros(n_rows, ld, dtype=dt, device="cuda")
+    sgpu.fill_logits(logits, dtype=cfg.dtype, vocab=cfg.V, row0=row0, tok_slot=st.tok_slot, tok_action=st.tok_action,
+                     kept_rollout=st.kept_rollout, kept_offset=st.kept_offset, max_len=cfg.S, seed=cfg.seed)
+    return logits
+
+
+def as_oracle_rows(t):
+    t = t.cpu()
+    return t.view(torch.int16).numpy().view(np.uint16) if t.dtype == torch.bfloat16 else t.numpy()
+
+
+# ---------------------------------------------------------------------------------------------- generator
+def test_gpu_generator_matches_host_twin():
+    for name in ("tiny", "qwen2.5-7b"):
+        cfg = synth.CONFIGS[name]
+        b = synth.make_batch(cfg, 0, 2 * cfg.G)
+        st, info = device_step(cfg, b)
+        o = oracle_step(cfg, b)
+        rows = np.array([0, 1, 7, info.n_tokens - 1])
+        logits = fill(st, cfg, 0, info.n_tokens)
+        got = as_oracle_rows(logits[torch.from_numpy(rows).cuda()])
+        np.testing.assert_array_equal(got, host_rows(cfg, o.keys[rows], o.pk.tok_action[rows]))
+
+
+# ---------------------------------------------------------------------------------------------- (1) pack
+@pytest.mark.parametrize("name,lengths", [("tiny", "full"), ("tiny", "ragged"), ("qwen2.5-7b", "ragged"),
+                                          ("qwen3-4b", "full")])
+def test_pack_bit_exact(name, lengths):
+    cfg = synth.CONFIGS[name]
+    b = synth.make_batch(cfg, lengths=lengths)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    pk = o.pk
+    assert (info.status, info.first_bad_rollout, info.n_groups_kept, info.n_rollouts_kept, info.n_tokens) == \
+        (pk.status, pk.first_bad_rollout, pk.n_groups_kept, pk.n_rollouts_kept, pk.n_tokens)
+    n, k = pk.n_tokens, pk.n_rollouts_kept
+    np.testing.assert_array_equal(st.kept_rollout[:k].cpu().numpy(), pk.kept_rollout)
+    np.testing.assert_array_equal(st.kept_offset[:k + 1].cpu().numpy(), pk.kept_offset)
+    for gpu, ref in ((st.tok_slot, pk.tok_slot), (st.tok_action, pk.tok_action), (st.tok_old, pk.tok_old),
+                     (st.tok_ref, pk.tok_ref)):
+        assert gpu[:n].cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_pack_exhaustive_lags_and_shards():
+    import itertools
+    cfg = synth.CONFIGS["tiny"]
+    base = synth.make_batch(cfg, lengths="ragged")
+    for lags in itertools.product([0, 1, 2], repeat=4):
+        b = synth.make_batch(cfg, lengths="ragged")
+        b.version = (synth.T_TRAIN - np.repeat(np.array(lags), cfg.G)).astype(np.int64)
+        st, info = device_step(cfg, b)
+        pk = oracle_step(cfg, b).pk
+        assert info.n_tokens == pk.n_tokens and info.n_groups_kept == pk.n_groups_kept
+        np.testing.assert_array_equal(st.tok_action[:pk.n_tokens].cpu().numpy(), pk.tok_action)
+    # shards with rollout_base give global ids
+    for r0, r1 in ((0, 8), (8, 16), (4, 12)):
+        b = synth.make_batch(cfg, r0, r1, lengths="ragged")
+        st, info = device_step(cfg, b, rollout_base=r0)
+        pk = oracle_step(cfg, b, rollout_base=r0).pk
+        np.testing.assert_array_equal(st.kept_rollout[:pk.n_rollouts_kept].cpu().numpy(), pk.kept_rollout)
+    assert base is not None
+
+
+def test_pack_errors_and_capacity():
+    cfg = synth.CONFIGS["tiny"]
+    cases = []
+    b = synth.make_batch(cfg); b.version = b.version.copy(); b.version[5] = synth.T_TRAIN + 1; cases.append(b)
+    b = synth.make_batch(cfg); b.version = b.version.copy(); b.version[6] -= 1; cases.append(b)
+    b = synth.make_batch(cfg); b.resp_len = b.resp_len.copy(); b.resp_len[9] = 0; cases.append(b)
+    b = synth.make_batch(cfg); b.action = b.action.copy(); b.action[7, 3] = cfg.V; b.action[13, 0] = -1; cases.append(b)
+    b = synth.make_batch(cfg); b.action = b.action.copy(); b.action[8, 1] = cfg.V; cases.append(b)   # dropped: unread
+    b = synth.make_batch(cfg); b.version = b.version.copy(); b.version[12] = synth.T_TRAIN + 5
+    b.action = b.action.copy(); b.action[1, 0] = -7; cases.append(b)
+    for b in cases:
+        st, info = device_step(cfg, b)
+        pk = oracle_step(cfg, b).pk
+        assert (info.status, info.first_bad_rollout) == (pk.status, pk.first_bad_rollout)
+    # capacity
+    from paper_2508_05387_b200 import abi
+    b = synth.make_batch(cfg)
+    st, _ = device_step(cfg, b)
+    st.cap = 767
+    info = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
+    assert info.status == abi.ECHO_DATA_CAPACITY and info.n_tokens == 768
+
+
+# ---------------------------------------------------------------------------------------------- (2) advantage
+@pytest.mark.parametrize("name", ["tiny", "qwen2.5-7b", "qwen3-30b-a3b"])
+def test_advantage_bit_exact(name):
+    cfg = synth.CONFIGS[name]
+    b = synth.make_batch(cfg, want_tokens=False)
+    S = 4                                            # metadata-only shape: lengths do not affect (2)
+    b.action = np.zeros((cfg.R, S), np.int32)
+    b.old_logp = np.zeros((cfg.R, S), np.float32)
+    b.ref_logp = np.zeros((cfg.R, S), np.float32)
+    b.resp_len = np.full(cfg.R, S, np.int32)
+    small = synth.Config(cfg.name, cfg.P, cfg.G, S, cfg.V, cfg.dtype, cfg.max_lag, cfg.kl_coef, cfg.lag_mode,
+                         cfg.index, cfg.stale_groups, cfg.fixed_lags)
+    st, info = device_step(small, b)
+    o = oracle_step(small, b)
+    assert st.adv_slot[:len(o.adv)].cpu().numpy().tobytes() == o.adv.tobytes()
+    assert st.adv_stats.cpu().numpy().tobytes() == o.adv_stats.tobytes()
+    # continuous (Sokoban-style) returns, PAPER.md :344 reward structure
+    rng = np.random.default_rng(1)
+    b.reward = (rng.integers(-2, 3, cfg.R) + 10.0 * (rng.random(cfg.R) < 0.2) - 0.1 * rng.integers(1, 40, cfg.R)
+                ).astype(np.float32)
+    st, info = device_step(small, b)
+    o = oracle_step(small, b)
+    assert st.adv_slot[:len(o.adv)].cpu().numpy().tobytes() == o.adv.tobytes()
+    assert st.adv_stats.cpu().numpy().tobytes() == o.adv_stats.tobytes()
+
+
+# ---------------------------------------------------------------------------------------------- (3)-(5)
+@pytest.mark.parametrize("kl_coef", [0.0, 0.001, 0.5])
+def test_tiny_full_step(kl_coef):
+    """configs[0] end to end: every output element vs the oracle (fp32 logits, ROW_L2 kernel)."""
+    cfg = synth.CONFIGS["tiny"]
+    b = synth.make_batch(cfg)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    n = info.n_tokens
+    logits = fill(st, cfg, 0, n)
+    z = as_oracle_rows(logits)
+    probe = oracle.policy_loss(z, o.pk.tok_action, o.pk.tok_old, o.pk.tok_ref, o.pk.tok_slot, o.adv, n_global=n,
+                               kl_coef=kl_coef)
+    s = pow2_scale_for(np.abs(probe.dlogits).max())
+    ref = oracle.policy_loss(z, o.pk.tok_action, o.pk.tok_old, o.pk.tok_ref, o.pk.tok_slot, o.adv, n_global=n,
+                             kl_coef=kl_coef, grad_scale=s)
+    st.loss(logits, 0, kl_coef=kl_coef, grad_scale=s)
+    out = st.finish()
+    check_rows(d_gpu=logits.cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
+               loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
+               dtype="f32", old=o.pk.tok_old)
+    L_ref = ref.loss.sum() / n
+    assert abs(out["loss"] - L_ref) <= 1e-5 * max(abs(L_ref), np.abs(ref.loss).mean())
+    for k, i in (("loss/n_clipped", 3), ("loss/n_nonfinite", 4), ("loss/n_tokens", 8)):
+        assert out[k] == ref.stats[i]
+    for k, i in (("loss/sum_logp_minus_old", 1), ("loss/sum_kl_k3", 2), ("loss/sum_logp", 7), ("loss/sum_rho", 9),
+                 ("loss/rho_min", 5), ("loss/rho_max", 6)):
+        assert abs(out[k] - ref.stats[i]) <= 1e-5 * max(1.0, abs(ref.stats[i])), k
+    assert out["n_tokens"] == n and out["n_groups_kept"] == 3 and out["n_groups_dropped"] == 1
+
+
+def _uniform_case(V, dtype, algo):
+    from paper_2508_05387_b200 import abi
+    n = 6
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    logits = torch.zeros(n, V, dtype=dt, device="cuda")
+    logits[1] += 3.5
+    logits[2] -= 17.25
+    act = torch.tensor([0, 1, V - 1, V // 2, 7, 123], dtype=torch.int32, device="cuda")
+    old = torch.zeros(n, dtype=torch.float32, device="cuda")
+    slot = torch.zeros(n, dtype=torch.int32, device="cuda")
+    adv = torch.ones(1, dtype=torch.float32, device="cuda")
+    ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
+    logp, loss = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    abi.echo_policy_loss_fwd_bwd(logits, abi.ECHO_BF16 if dtype == "bf16" else abi.ECHO_F32, n, V, V, act, old, None,
+                                 slot, adv, ng, 0.2, 0.2, 0.0, 1.0, logp, loss, flags, algo=algo)
+    return logits, logp.cpu().numpy()
+
+
+@pytest.mark.parametrize("V,dtype,algo", [(1024, "f32", 1), (151936, "bf16", 1), (151936, "bf16", 2),
+                                          (152064, "bf16", 2)])
+def test_uniform_rows_give_minus_log_v(V, dtype, algo):
+    """Closed form (SPEC.md :202): uniform logits give logp = -ln V; the GPU is within 2 fp32 ulp."""
+    _, logp = _uniform_case(V, dtype, algo)
+    target = np.float32(-math.log(V))
+    ulp = np.spacing(np.abs(target))
+    assert np.all(np.abs(logp - target) <= 2 * ulp), (logp, target)
+
+
+@pytest.mark.parametrize("algo", [1, 2])
+def test_clip_saturation_and_two_call_ratio(algo):
+    """old == new (two-call protocol) gives rho = 1 exactly and c = -A s/N; clip saturation zeroes whole rows."""
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, 2 * cfg.G)
+    st, info = device_step(cfg, b)
+    n = 512
+    base = fill(st, cfg, 0, n)
+    work = base.clone()
+    st.loss(work, 0, kl_coef=0.0, algo=algo)
+    logp1 = st.tok_logp[:n].clone()
+    # call 2: old = logp of call 1
+    st.tok_old[:n] = logp1
+    work = base.clone()
+    st.loss(work, 0, kl_coef=0.0, algo=algo)
+    assert torch.equal(st.tok_logp[:n], logp1)                       # deterministic
+    adv = st.adv_slot[st.tok_slot[:n].long()]
+    assert torch.equal(st.tok_loss[:n], -adv)                        # rho == 1 exactly -> pg = -A
+    assert not torch.any(st.tok_flags[:n])
+    # clip saturation: A > 0 rows with rho = e^0.5 > 1.2, A < 0 rows with rho = e^-0.5 < 0.8
+    sign = torch.sign(adv)
+    st.tok_old[:n] = logp1 - 0.5 * sign
+    work = base.clone()
+    st.loss(work, 0, kl_coef=0.0, algo=algo)
+    nz = adv != 0
+    assert torch.all(st.tok_flags[:n][nz] == 1)
+    assert torch.count_nonzero(work[nz]) == 0
+
+
+@pytest.mark.parametrize("algo", [1, 2])
+def test_determinism_and_microbatch_invariance(algo):
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, 2 * cfg.G)
+    st, info = device_step(cfg, b)
+    n = 700
+    base = fill(st, cfg, 0, n)
+    a = base.clone()
+    st.loss(a, 0, kl_coef=cfg.kl_coef, algo=algo)
+    la = st.tok_logp[:n].clone()
+    b2 = base.clone()
+    st.loss(b2[:333], 0, kl_coef=cfg.kl_coef, algo=algo)             # odd split
+    st.loss(b2[333:], 333, kl_coef=cfg.kl_coef, algo=algo)
+    assert torch.equal(a.view(torch.int16), b2.view(torch.int16))
+    assert torch.equal(la, st.tok_logp[:n])
+
+
+@pytest.mark.parametrize("name", ["qwen3-4b", "qwen2.5-7b", "qwen3-32b", "qwen3-30b-a3b"])
+@pytest.mark.parametrize("algo_name", ["cluster_smem", "row_l2"])
+def test_full_config_sampled_rows(name, algo_name):
+    """BASELINE.json full sizes, the bench's micro-batch (32768 rows) and launch configuration: sampled rows
+    of the first and the last micro-batch against the oracle, plus the row-sum invariant on every row."""
+    cfg = synth.CONFIGS[name]
+    algo = ALGOS[algo_name]
+    b = synth.make_batch(cfg)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    N = info.n_tokens
+    assert N == o.pk.n_tokens
+    M = 32768
+    rng = np.random.default_rng(7)
+    for row0 in (0, ((N - 1) // M) * M):
+        m = min(M, N - row0)
+        logits = fill(st, cfg, row0, m)
+        sample = np.unique(np.concatenate([[0, m - 1], rng.integers(0, m, 30)]))
+        gl = row0 + sample
+        z = host_rows(cfg, o.keys[gl], o.pk.tok_action[gl])
+        tr = None if o.pk.tok_ref is None else o.pk.tok_ref[gl]
+        probe = oracle.policy_loss(z, o.pk.tok_action[gl], o.pk.tok_old[gl], tr, o.pk.tok_slot[gl], o.adv,
+                                   n_global=N, kl_coef=cfg.kl_coef)
+        s = pow2_scale_for(np.abs(probe.dlogits).max())
+        ref = oracle.policy_loss(z, o.pk.tok_action[gl], o.pk.tok_old[gl], tr, o.pk.tok_slot[gl], o.adv, n_global=N,
+                                 kl_coef=cfg.kl_coef, grad_scale=s)
+        st.loss(logits, row0, kl_coef=cfg.kl_coef, grad_scale=s, algo=algo)
+        idx = torch.from_numpy(sample).cuda()
+        d = logits[idx].float().cpu().numpy()
+        check_rows(d_gpu=d, logp_gpu=st.tok_logp[gl].cpu().numpy(), loss_gpu=st.tok_loss[gl].cpu().numpy(),
+                   flags_gpu=st.tok_flags[gl].cpu().numpy(), ref=ref, dtype=cfg.dtype, old=o.pk.tok_old[gl])
+        assert np.max(np.abs(d - ref.dlogits)) <= 2e-3                 # the north_star bar
+        # every row of the micro-batch: |sum_v d| <= 2^-8 |c| (bf16 RNE) + fp32 slack
+        rows_sum = logits.float().sum(dim=1).abs()
+        logp = st.tok_logp[row0:row0 + m].double()
+        rho = torch.exp(logp - st.tok_old[row0:row0 + m].double())
+        A = st.adv_slot[st.tok_slot[row0:row0 + m].long()].double()
+        kl_term = 0.0
+        if cfg.kl_coef > 0:
+            kl_term = cfg.kl_coef * (1 - torch.exp(st.tok_ref[row0:row0 + m].double() - logp)).abs()
+        cbound = (A.abs() * rho + kl_term) * s / N
+        assert torch.all(rows_sum.double() <= 2.0 ** -7 * cbound + 1e-6)
+        del logits
+    torch.cuda.empty_cache()
+
+
+def test_nonfinite_rows_flagged():
+    from paper_2508_05387_b200 import abi
+    V = 4096
+    for dtype, algo in (("bf16", 1), ("bf16", 2), ("f32", 1)):
+        dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        z = torch.zeros(6, V, dtype=dt, device="cuda")
+        z[0, 3] = float("nan")
+        z[1, :] = float("-inf")
+        z[2, 5] = float("inf")
+        z[3, :10] = float("-inf")
+        z[4, 20] = float("-inf")
+        act = torch.tensor([0, 0, 0, 30, 20, 1], dtype=torch.int32, device="cuda")
+        old = torch.tensor([0, 0, 0, 0, 0, -100.0], device="cuda")
+        slot = torch.zeros(6, dtype=torch.int32, device="cuda")
+        adv = torch.ones(1, device="cuda")
+        ng = torch.tensor([6.0], dtype=torch.float64, device="cuda")
+        logp, loss = torch.empty(6, device="cuda"), torch.empty(6, device="cuda")
+        flags = torch.empty(6, dtype=torch.uint8, device="cuda")
+        abi.echo_policy_loss_fwd_bwd(z, abi.ECHO_BF16 if dtype == "bf16" else abi.ECHO_F32, 6, V, V, act, old, None,
+                                     slot, adv, ng, 0.2, 0.2, 0.0, 1.0, logp, loss, flags, algo=algo)
+        np.testing.assert_array_equal((flags.cpu().numpy() >> 1) & 1, [1, 1, 1, 0, 1, 1])
+        assert abs(logp[3].item() + math.log(V - 10)) < 1e-5
+
+
+@pytest.mark.parametrize("V,ld,algo", [(1000, 1008, 1), (1001, 1008, 1), (151935, 151936, 2), (151935, 151936, 1),
+                                       (40001, 40008, 2)])
+def test_ragged_vocab_and_padding_untouched(V, ld, algo):
+    """V not a multiple of the 8-element vector: tail handling; columns V..ld-1 are never written."""
+    from paper_2508_05387_b200 import abi
+    n = 37
+    rng = np.random.default_rng(V)
+    zf = (rng.normal(size=(n, ld)) * 2).astype(np.float32)
+    zb = torch.from_numpy(zf).to(torch.bfloat16)
+    raw = zb.view(torch.int16).numpy().view(np.uint16)
+    act = rng.integers(0, V, n).astype(np.int32)
+    act[0] = V - 1
+    old = (rng.normal(size=n) * 0.3 - 10).astype(np.float32)
+    slot = (np.arange(n) % 4).astype(np.int32)
+    adv = np.array([1.0, -0.5, 0.25, -2.0], np.float32)
+    ref = oracle.policy_loss(raw[:, :V].copy(), act, old, None, slot, adv, n_global=n, vocab=V, grad_scale=float(n))
+    logits = zb.cuda()
+    c = lambda x: torch.from_numpy(x).cuda()
+    ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
+    logp, loss = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    abi.echo_policy_loss_fwd_bwd(logits, abi.ECHO_BF16, n, V, ld, c(act), c(old), None, c(slot), c(adv), ng, 0.2, 0.2,
+                                 0.0, float(n), logp, loss, flags, algo=algo)
+    out = logits.cpu()
+    assert torch.equal(out[:, V:].view(torch.int16), zb[:, V:].view(torch.int16))
+    check_rows(d_gpu=out[:, :V].float().numpy(), logp_gpu=logp.cpu().numpy(), loss_gpu=loss.cpu().numpy(),
+               flags_gpu=flags.cpu().numpy(), ref=ref, dtype="bf16", old=old)
+
+
+def test_abi_argument_errors():
+    from paper_2508_05387_b200 import abi
+    z = torch.zeros(2, 1000, dtype=torch.bfloat16, device="cuda")
+    i = torch.zeros(2, dtype=torch.int32, device="cuda")
+    f = torch.zeros(2, device="cuda")
+    ng = torch.ones(1, dtype=torch.float64, device="cuda")
+    args = lambda **kw: dict(dict(logits=z, dtype=abi.ECHO_BF16, n_rows=2, vocab=1000, ld=1000, tok_action=i,
+                                  tok_old=f, tok_ref=None, tok_slot=i, adv_slot=f, n_global=ng, clip_low=0.2,
+                                  clip_high=0.2, kl_coef=0.0, grad_scale=1.0, tok_logp=f, tok_loss=f,
+                                  tok_flags=torch.zeros(2, dtype=torch.uint8, device="cuda")), **kw)
+    with pytest.raises(abi.EchoError):
+        abi.echo_policy_loss_fwd_bwd(**args(ld=1001))                 # ld * 2 not a multiple of 16
+    with pytest.raises(abi.EchoError):
+        abi.echo_policy_loss_fwd_bwd(**args(kl_coef=0.1))             # KL needs tok_ref
+    with pytest.raises(abi.EchoError):
+        abi.echo_policy_loss_fwd_bwd(**args(dtype=7))
+    with pytest.raises(abi.EchoError) as e:
+        abi.echo_policy_loss_fwd_bwd(**args(dtype=abi.ECHO_F32, ld=1000), algo=abi.ECHO_ALGO_CLUSTER_SMEM)
+    assert e.value.status == abi.ECHO_ERR_UNSUPPORTED
+    abi.echo_policy_loss_fwd_bwd(**args(n_rows=0))                    # empty micro-batch: no launch, OK
