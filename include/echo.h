@@ -64,8 +64,12 @@ enum { ECHO_FLAG_CLIPPED = 1, ECHO_FLAG_NONFINITE = 2 };
 enum {
   ECHO_ALGO_AUTO = 0,
   ECHO_ALGO_ROW_L2 = 1,      /* one CTA per row, two streaming passes; the second pass re-reads from L2 */
-  ECHO_ALGO_CLUSTER_SMEM = 2 /* CTA pair per row, each half-row resident in a TMA-fed shared-memory ring:
-                                exactly one HBM read + one HBM write per logit (bf16, vocab <= 196608) */
+  ECHO_ALGO_CLUSTER_SMEM = 2, /* CTA pair per row, each half-row resident in a TMA-fed shared-memory ring:
+                                 exactly one HBM read + one HBM write per logit (bf16, vocab <= 196608) */
+  ECHO_ALGO_CLUSTER_REG = 3,  /* CTA pair per row, half-row held in registers, the TMA ring only stages the
+                                 next rows; exp(z - m) kept as fp16 between the passes (bf16, vocab <= 155648) */
+  ECHO_ALGO_CLUSTER_REG_EXACT = 4 /* as CLUSTER_REG, but the write-back recomputes exp from the bf16 logits
+                                     (fp32 end to end; two exponentials per logit) */
 };
 
 /* Device-resident result of echo_pack_batch (32 bytes). */
@@ -158,6 +162,11 @@ ECHO_API echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, in
                                         float clip_low, float clip_high, float kl_coef, float grad_scale,
                                         float* tok_logp, float* tok_loss, uint8_t* tok_flags, int32_t algo,
                                         void* stream);
+
+/* Launch shape echo_policy_loss_fwd_bwd_ex would use on the current device (no launch):
+ * shape[5] = {resolved algo, grid CTAs, CTAs per cluster, threads per CTA, dynamic smem bytes}. */
+ECHO_API echo_status echo_policy_loss_launch_shape(int32_t dtype, int64_t n_rows, int32_t vocab, int32_t algo,
+                                                   int32_t* shape);
 
 /*
  * Statistics of the per-token outputs over n_tokens packed tokens (all micro-batches of the step):

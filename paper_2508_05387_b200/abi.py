@@ -19,13 +19,14 @@ ECHO_F32, ECHO_BF16 = 0, 1
 (ECHO_DATA_OK, ECHO_DATA_FUTURE_VERSION, ECHO_DATA_MIXED_GROUP_VERSION, ECHO_DATA_BAD_LENGTH, ECHO_DATA_BAD_ACTION,
  ECHO_DATA_CAPACITY) = range(6)
 ECHO_FLAG_CLIPPED, ECHO_FLAG_NONFINITE = 1, 2
-ECHO_ALGO_AUTO, ECHO_ALGO_ROW_L2, ECHO_ALGO_CLUSTER_SMEM = 0, 1, 2
+ECHO_ALGO_AUTO, ECHO_ALGO_ROW_L2, ECHO_ALGO_CLUSTER_SMEM, ECHO_ALGO_CLUSTER_REG, ECHO_ALGO_CLUSTER_REG_EXACT = range(5)
 PACK_RESULT_BYTES = 32
 
 # kernels launched per call (for the bench's gpu_launches count)
 LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2}
 
 EXPORTS = ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
+           "echo_policy_loss_launch_shape",
            "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_status_string", "echo_abi_version")
 
 
@@ -47,6 +48,8 @@ def _load():
     lib.echo_policy_loss_fwd_bwd_ex.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P, P, f32, f32, f32, f32, P, P, P,
                                                 i32, P]
     lib.echo_loss_stats.argtypes = [i64, P, P, P, P, P, P, P, P]
+    lib.echo_policy_loss_launch_shape.argtypes = [i32, i64, i32, i32, P]
+    lib.echo_policy_loss_launch_shape.restype = ctypes.c_int
     lib.echo_loss_stats_workspace_bytes.argtypes = []
     lib.echo_loss_stats_workspace_bytes.restype = ctypes.c_size_t
     lib.echo_status_string.argtypes = [ctypes.c_int]
@@ -120,6 +123,13 @@ def echo_policy_loss_fwd_bwd(logits, dtype, n_rows, vocab, ld, tok_action, tok_o
             _p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot),
             _p(adv_slot), _p(n_global), clip_low, clip_high, kl_coef, grad_scale, _p(tok_logp), _p(tok_loss),
             _p(tok_flags), algo, _s(stream)))
+
+
+def echo_policy_loss_launch_shape(dtype, n_rows, vocab, algo=ECHO_ALGO_AUTO) -> dict:
+    buf = (ctypes.c_int32 * 5)()
+    _check("echo_policy_loss_launch_shape",
+           _lib.echo_policy_loss_launch_shape(dtype, n_rows, vocab, algo, ctypes.cast(buf, ctypes.c_void_p)))
+    return dict(zip(("algo", "grid_ctas", "cluster_ctas", "threads", "smem_bytes"), list(buf)))
 
 
 def echo_loss_stats_workspace_bytes() -> int:

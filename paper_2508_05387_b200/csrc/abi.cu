@@ -21,6 +21,25 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 echo_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ECHO_OK : ECHO_ERR_CUDA; }
 
+// ECHO_ALGO_AUTO -> the register-resident CTA-pair kernel for bf16 vocabularies up to 153600 (Qwen's),
+// the SMEM-resident one up to 196608, the row kernel otherwise; explicit choices are checked for support.
+echo_status resolve_algo(int32_t dtype, int32_t vocab, int32_t* algo) {
+  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_CLUSTER_REG_EXACT) return ECHO_ERR_INVALID_ARGUMENT;
+  const bool cluster_ok = echo::cluster_algo_supports(dtype, vocab);
+  const bool reg_ok = echo::cluster_reg_supports(dtype, vocab);
+  if (*algo == ECHO_ALGO_AUTO) {
+    if (reg_ok && vocab >= 16384)
+      *algo = ECHO_ALGO_CLUSTER_REG_EXACT;
+    else if (cluster_ok && vocab >= 16384)
+      *algo = ECHO_ALGO_CLUSTER_SMEM;
+    else
+      *algo = ECHO_ALGO_ROW_L2;
+  }
+  if (*algo == ECHO_ALGO_CLUSTER_SMEM && !cluster_ok) return ECHO_ERR_UNSUPPORTED;
+  if ((*algo == ECHO_ALGO_CLUSTER_REG || *algo == ECHO_ALGO_CLUSTER_REG_EXACT) && !reg_ok) return ECHO_ERR_UNSUPPORTED;
+  return ECHO_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -92,15 +111,12 @@ echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_r
       return ECHO_ERR_INVALID_ARGUMENT;
     if (kl_coef > 0.0f && !tok_ref) return ECHO_ERR_INVALID_ARGUMENT;
   }
-  if (algo != ECHO_ALGO_AUTO && algo != ECHO_ALGO_ROW_L2 && algo != ECHO_ALGO_CLUSTER_SMEM)
-    return ECHO_ERR_INVALID_ARGUMENT;
   int sms = 0;
   echo_status st = device_sms(&sms);
   if (st != ECHO_OK) return st;
   if (n_rows == 0) return ECHO_OK;
-  const bool cluster_ok = echo::cluster_algo_supports(dtype, vocab);
-  if (algo == ECHO_ALGO_AUTO) algo = (cluster_ok && vocab >= 16384) ? ECHO_ALGO_CLUSTER_SMEM : ECHO_ALGO_ROW_L2;
-  if (algo == ECHO_ALGO_CLUSTER_SMEM && !cluster_ok) return ECHO_ERR_UNSUPPORTED;
+  st = resolve_algo(dtype, vocab, &algo);
+  if (st != ECHO_OK) return st;
   echo::LossParams p;
   p.logits = static_cast<uint8_t*>(logits);
   p.n_rows = n_rows;
@@ -130,6 +146,28 @@ echo_status echo_policy_loss_fwd_bwd(void* logits, int32_t dtype, int64_t n_rows
   return echo_policy_loss_fwd_bwd_ex(logits, dtype, n_rows, vocab, ld, tok_action, tok_old, tok_ref, tok_slot,
                                      adv_slot, n_global, clip_low, clip_high, kl_coef, grad_scale, tok_logp, tok_loss,
                                      tok_flags, ECHO_ALGO_AUTO, stream);
+}
+
+echo_status echo_policy_loss_launch_shape(int32_t dtype, int64_t n_rows, int32_t vocab, int32_t algo,
+                                          int32_t* shape) {
+  if ((dtype != ECHO_F32 && dtype != ECHO_BF16) || n_rows < 1 || vocab < 1 || !shape) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  st = resolve_algo(dtype, vocab, &algo);
+  if (st != ECHO_OK) return st;
+  echo::LossParams p{};
+  p.n_rows = n_rows;
+  p.V = vocab;
+  echo::LaunchShape s{};
+  st = from_cuda(echo::launch_policy_loss(p, dtype, algo, nullptr, sms, &s));
+  if (st != ECHO_OK) return st;
+  shape[0] = algo;
+  shape[1] = s.grid_ctas;
+  shape[2] = s.cluster_ctas;
+  shape[3] = s.threads;
+  shape[4] = s.smem_bytes;
+  return ECHO_OK;
 }
 
 size_t echo_loss_stats_workspace_bytes(void) { return echo::loss_stats_workspace_bytes(); }

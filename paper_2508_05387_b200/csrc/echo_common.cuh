@@ -22,6 +22,56 @@ ECHO_DEVINL uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
+// Two fp32 -> packed f16x2 (RNE); `lo` lands in bits 0..15.  And back.
+ECHO_DEVINL uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+ECHO_DEVINL float f16lo(uint32_t w) {
+  float f;
+  asm("{\n\t.reg .f16 h;\n\tmov.b32 {h, _}, %1;\n\tcvt.f32.f16 %0, h;\n\t}" : "=f"(f) : "r"(w));
+  return f;
+}
+ECHO_DEVINL float f16hi(uint32_t w) {
+  float f;
+  asm("{\n\t.reg .f16 h;\n\tmov.b32 {_, h}, %1;\n\tcvt.f32.f16 %0, h;\n\t}" : "=f"(f) : "r"(w));
+  return f;
+}
+
+// ---------------------------------------------------------------- packed helpers (Blackwell f32x2 pipes)
+// A pair of fp32 lives in one 64-bit register pair; fma/add/mul.rn.f32x2 issue as one FFMA2/FADD2/FMUL2.
+ECHO_DEVINL uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+ECHO_DEVINL void f2split(uint64_t v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+ECHO_DEVINL uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+ECHO_DEVINL uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+ECHO_DEVINL uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// bf16x2 word -> fp32 pair (exact)
+ECHO_DEVINL uint64_t bf2_to_f2(uint32_t w) { return f2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)); }
+// max of two bf16x2 words (exact; a NaN operand yields the other operand)
+ECHO_DEVINL uint32_t bmax2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+constexpr uint32_t kBf16NegInf2 = 0xFF80FF80u;
+
 ECHO_DEVINL float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

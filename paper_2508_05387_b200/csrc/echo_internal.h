@@ -37,7 +37,15 @@ cudaError_t launch_group_advantage(int32_t G, float eps, int64_t rollout_base, c
                                    double* adv_stats, cudaStream_t stream);
 
 bool cluster_algo_supports(int32_t dtype, int32_t V);
-cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms);
+bool cluster_reg_supports(int32_t dtype, int32_t V);
+
+// Launch shape a policy-loss call uses (reported by echo_policy_loss_launch_shape).
+struct LaunchShape {
+  int32_t grid_ctas, cluster_ctas, threads, smem_bytes;
+};
+// With shape != nullptr: fill in the launch shape and launch nothing.
+cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms,
+                               LaunchShape* shape = nullptr);
 
 size_t loss_stats_workspace_bytes();
 cudaError_t launch_loss_stats(int64_t n, const float* tok_loss, const float* tok_logp, const float* tok_old,

@@ -46,14 +46,26 @@ def host_rows(cfg: synth.Config, keys, actions):
     return synth.logits_rows(keys, actions, cfg.V, cfg.seed, "bf16" if cfg.dtype == "bf16" else "f32")
 
 
+def coef_slack(ref: oracle.LossOut, old, tok_ref, adv_tok, kl_coef, grad_scale, n_global):
+    """Bound on |c_gpu - c_ref| from the fp32 log-prob alone: dc/dlogp = s/N (-A rho [unclipped] - beta e^x),
+    x = ref - logp, times |d logp| <= 1e-6 (1 + |logp|) (fp32 log-sum-exp over the row), plus fp32 rounding."""
+    rho = np.exp(ref.logp - np.asarray(old, np.float64))
+    sens = np.abs(np.asarray(adv_tok, np.float64)) * rho
+    if kl_coef > 0:
+        sens = sens + kl_coef * np.exp(np.asarray(tok_ref, np.float64) - ref.logp)
+    return grad_scale / n_global * sens * 1e-6 * (1 + np.abs(ref.logp)) + 1e-6 * np.abs(ref.coef)
+
+
 def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dtype: str, clip=(0.2, 0.2),
-               old=None):
+               old=None, cslack=None):
     """Element-wise parity of a set of rows; returns number of gradient rows compared.
 
-    logp: |d| <= 1e-5 + 1e-6 |logp|; l_t: rtol 1e-5 (+1e-6 abs); dlogits (bf16): |d| <= 2^-8 |d_ref| + 4e-6 |c_t|
-    (faithful bf16 rounding + fp32 slack) and the north_star bar max|d| <= 2e-3; (fp32): |d| <= 1e-5 |c_t|.
-    Rows whose reference ratio sits within 1e-5 of a clip boundary decide "clipped" in different precisions
-    (fp64 vs fp32): only logp is compared there.
+    logp: |d| <= 1e-5 + 1e-6 |logp|; l_t: rtol 1e-5 (+1e-6 abs); dlogits (bf16): |d| <= ulp_bf16(d_ref) + 4e-6 |c_t|
+    + slack_t (faithful rounding: one of the two bf16 neighbours of the exact value) and the
+    north_star bar max|d| <= 2e-3 (checked by the callers at max|d_ref| in [0.25, 0.5));
+    (fp32): |d| <= 1e-5 |d_ref| + 4e-6 |c_t| + slack_t, where slack_t (coef_slack) bounds the error the fp32
+    log-prob propagates into c_t.  Rows whose reference ratio sits within 1e-5 of a clip boundary decide
+    "clipped" in different precisions (fp64 vs fp32): only logp is compared there.
     """
     logp_gpu = np.asarray(logp_gpu, np.float64)
     assert np.all(np.abs(logp_gpu - ref.logp) <= 1e-5 + 1e-6 * np.abs(ref.logp)), \
@@ -67,11 +79,14 @@ def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dty
     d = np.asarray(d_gpu, np.float64)[ok]
     dr = ref.dlogits[ok]
     c = np.abs(ref.coef[ok])[:, None]
-    if dtype == "bf16":
-        tol = 2.0 ** -8 * np.abs(dr) + 4e-6 * c
-    else:
-        tol = 1e-5 * c
+    slack = 0.0 if cslack is None else np.asarray(cslack)[ok][:, None]
+    base = bf16_ulp(dr) if dtype == "bf16" else 1e-5 * np.abs(dr)      # faithful bf16 rounding: within 1 ulp
+    tol = np.broadcast_to(base + 4e-6 * c + slack, d.shape)
     err = np.abs(d - dr)
     bad = err > tol + 1e-30
-    assert not bad.any(), f"dlogits: {bad.sum()} elements out of tolerance; worst {err[bad].max()} at tol {tol[bad].min()}"
+    if bad.any():
+        r, v = np.nonzero(bad)
+        i = np.argmax(err[bad] / tol[bad])
+        raise AssertionError(f"dlogits: {bad.sum()} elements out of tolerance; worst row {r[i]} col {v[i]}: "
+                             f"gpu {d[r[i], v[i]]!r} ref {dr[r[i], v[i]]!r} c {c[r[i], 0]!r} tol {tol[r[i], v[i]]!r}")
     return int(ok.sum()), float(err.max()) if err.size else 0.0

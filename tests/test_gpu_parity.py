@@ -12,11 +12,11 @@ import torch
 
 import oracle
 import synth
-from _util import check_rows, host_rows, oracle_step, pow2_scale_for
+from _util import check_rows, coef_slack, host_rows, oracle_step, pow2_scale_for
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = {"row_l2": 1, "cluster_smem": 2}
+ALGOS = {"row_l2": 1, "cluster_smem": 2, "cluster_reg": 3, "cluster_reg_exact": 4}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -174,7 +174,8 @@ def test_tiny_full_step(kl_coef):
     out = st.finish()
     check_rows(d_gpu=logits.cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
                loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
-               dtype="f32", old=o.pk.tok_old)
+               dtype="f32", old=o.pk.tok_old,
+               cslack=coef_slack(ref, o.pk.tok_old, o.pk.tok_ref, o.adv[o.pk.tok_slot], kl_coef, s, n))
     L_ref = ref.loss.sum() / n
     assert abs(out["loss"] - L_ref) <= 1e-5 * max(abs(L_ref), np.abs(ref.loss).mean())
     for k, i in (("loss/n_clipped", 3), ("loss/n_nonfinite", 4), ("loss/n_tokens", 8)):
@@ -205,7 +206,7 @@ def _uniform_case(V, dtype, algo):
 
 
 @pytest.mark.parametrize("V,dtype,algo", [(1024, "f32", 1), (151936, "bf16", 1), (151936, "bf16", 2),
-                                          (152064, "bf16", 2)])
+                                          (152064, "bf16", 2), (151936, "bf16", 3), (152064, "bf16", 4)])
 def test_uniform_rows_give_minus_log_v(V, dtype, algo):
     """Closed form (SPEC.md :202): uniform logits give logp = -ln V; the GPU is within 2 fp32 ulp."""
     _, logp = _uniform_case(V, dtype, algo)
@@ -214,7 +215,7 @@ def test_uniform_rows_give_minus_log_v(V, dtype, algo):
     assert np.all(np.abs(logp - target) <= 2 * ulp), (logp, target)
 
 
-@pytest.mark.parametrize("algo", [1, 2])
+@pytest.mark.parametrize("algo", [1, 2, 3, 4])
 def test_clip_saturation_and_two_call_ratio(algo):
     """old == new (two-call protocol) gives rho = 1 exactly and c = -A s/N; clip saturation zeroes whole rows."""
     cfg = synth.CONFIGS["qwen3-4b"]
@@ -243,7 +244,7 @@ def test_clip_saturation_and_two_call_ratio(algo):
     assert torch.count_nonzero(work[nz]) == 0
 
 
-@pytest.mark.parametrize("algo", [1, 2])
+@pytest.mark.parametrize("algo", [1, 2, 3, 4])
 def test_determinism_and_microbatch_invariance(algo):
     cfg = synth.CONFIGS["qwen3-4b"]
     b = synth.make_batch(cfg, 0, 2 * cfg.G)
@@ -261,7 +262,7 @@ def test_determinism_and_microbatch_invariance(algo):
 
 
 @pytest.mark.parametrize("name", ["qwen3-4b", "qwen2.5-7b", "qwen3-32b", "qwen3-30b-a3b"])
-@pytest.mark.parametrize("algo_name", ["cluster_smem", "row_l2"])
+@pytest.mark.parametrize("algo_name", ["cluster_reg", "cluster_reg_exact", "cluster_smem", "row_l2"])
 def test_full_config_sampled_rows(name, algo_name):
     """BASELINE.json full sizes, the bench's micro-batch (32768 rows) and launch configuration: sampled rows
     of the first and the last micro-batch against the oracle, plus the row-sum invariant on every row."""
@@ -290,7 +291,8 @@ def test_full_config_sampled_rows(name, algo_name):
         idx = torch.from_numpy(sample).cuda()
         d = logits[idx].float().cpu().numpy()
         check_rows(d_gpu=d, logp_gpu=st.tok_logp[gl].cpu().numpy(), loss_gpu=st.tok_loss[gl].cpu().numpy(),
-                   flags_gpu=st.tok_flags[gl].cpu().numpy(), ref=ref, dtype=cfg.dtype, old=o.pk.tok_old[gl])
+                   flags_gpu=st.tok_flags[gl].cpu().numpy(), ref=ref, dtype=cfg.dtype, old=o.pk.tok_old[gl],
+                   cslack=coef_slack(ref, o.pk.tok_old[gl], tr, o.adv[o.pk.tok_slot[gl]], cfg.kl_coef, s, N))
         assert np.max(np.abs(d - ref.dlogits)) <= 2e-3                 # the north_star bar
         # every row of the micro-batch: |sum_v d| <= 2^-8 |c| (bf16 RNE) + fp32 slack
         rows_sum = logits.float().sum(dim=1).abs()
@@ -309,7 +311,7 @@ def test_full_config_sampled_rows(name, algo_name):
 def test_nonfinite_rows_flagged():
     from paper_2508_05387_b200 import abi
     V = 4096
-    for dtype, algo in (("bf16", 1), ("bf16", 2), ("f32", 1)):
+    for dtype, algo in (("bf16", 1), ("bf16", 2), ("bf16", 3), ("bf16", 4), ("f32", 1)):
         dt = torch.bfloat16 if dtype == "bf16" else torch.float32
         z = torch.zeros(6, V, dtype=dt, device="cuda")
         z[0, 3] = float("nan")
@@ -331,7 +333,7 @@ def test_nonfinite_rows_flagged():
 
 
 @pytest.mark.parametrize("V,ld,algo", [(1000, 1008, 1), (1001, 1008, 1), (151935, 151936, 2), (151935, 151936, 1),
-                                       (40001, 40008, 2)])
+                                       (40001, 40008, 2), (151935, 151936, 3), (40001, 40008, 4), (153600, 153600, 3)])
 def test_ragged_vocab_and_padding_untouched(V, ld, algo):
     """V not a multiple of the 8-element vector: tail handling; columns V..ld-1 are never written."""
     from paper_2508_05387_b200 import abi
@@ -356,7 +358,8 @@ def test_ragged_vocab_and_padding_untouched(V, ld, algo):
     out = logits.cpu()
     assert torch.equal(out[:, V:].view(torch.int16), zb[:, V:].view(torch.int16))
     check_rows(d_gpu=out[:, :V].float().numpy(), logp_gpu=logp.cpu().numpy(), loss_gpu=loss.cpu().numpy(),
-               flags_gpu=flags.cpu().numpy(), ref=ref, dtype="bf16", old=old)
+               flags_gpu=flags.cpu().numpy(), ref=ref, dtype="bf16", old=old,
+               cslack=coef_slack(ref, old, None, adv[slot], 0.0, float(n), n))
 
 
 def test_abi_argument_errors():
