@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="echo", choices=["echo", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "cluster_smem", "cluster_reg", "cluster_reg_exact"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "cluster_smem", "cluster_reg", "cluster_reg_exact", "quad_reg", "quad_reg_exact", "pipe"])
     ap.add_argument("--micro-batch", type=int, default=32768)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -223,8 +223,7 @@ def main_echo(args):
     ld = (cfg.V + 7) // 8 * 8
     logits = torch.empty(M, ld, dtype=torch.bfloat16 if cfg.dtype == "bf16" else torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    algo = {"auto": None, "row_l2": abi.ECHO_ALGO_ROW_L2, "cluster_smem": abi.ECHO_ALGO_CLUSTER_SMEM,
-            "cluster_reg": abi.ECHO_ALGO_CLUSTER_REG, "cluster_reg_exact": abi.ECHO_ALGO_CLUSTER_REG_EXACT}[args.algo]
+    algo = None if args.algo == "auto" else abi.ALGO_NAMES[args.algo]
     stream = torch.cuda.current_stream()
 
     def ev():

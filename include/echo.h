@@ -68,8 +68,13 @@ enum {
                                  exactly one HBM read + one HBM write per logit (bf16, vocab <= 196608) */
   ECHO_ALGO_CLUSTER_REG = 3,  /* CTA pair per row, half-row held in registers, the TMA ring only stages the
                                  next rows; exp(z - m) kept as fp16 between the passes (bf16, vocab <= 155648) */
-  ECHO_ALGO_CLUSTER_REG_EXACT = 4 /* as CLUSTER_REG, but the write-back recomputes exp from the bf16 logits
-                                     (fp32 end to end; two exponentials per logit) */
+  ECHO_ALGO_CLUSTER_REG_EXACT = 4, /* as CLUSTER_REG, but the write-back recomputes exp from the bf16 logits
+                                      (fp32 end to end; two exponentials per logit) */
+  ECHO_ALGO_QUAD_REG = 5,         /* 4-CTA cluster per row, quarter-row in registers, two CTAs (two rows) per
+                                     SM; exp(z - m) kept as fp16 between the passes (bf16, vocab <= 155648) */
+  ECHO_ALGO_QUAD_REG_EXACT = 6,   /* as QUAD_REG, write-back recomputes exp from the bf16 logits (fp32) */
+  ECHO_ALGO_PIPE = 7              /* one SM per row, warp-specialised: TMA producer, reducer warps (pass 1 of
+                                     row k+1), writer warps (pass 2 of row k, second read from L2); bf16, any V */
 };
 
 /* Device-resident result of echo_pack_batch (32 bytes). */

@@ -19,7 +19,10 @@ ECHO_F32, ECHO_BF16 = 0, 1
 (ECHO_DATA_OK, ECHO_DATA_FUTURE_VERSION, ECHO_DATA_MIXED_GROUP_VERSION, ECHO_DATA_BAD_LENGTH, ECHO_DATA_BAD_ACTION,
  ECHO_DATA_CAPACITY) = range(6)
 ECHO_FLAG_CLIPPED, ECHO_FLAG_NONFINITE = 1, 2
-ECHO_ALGO_AUTO, ECHO_ALGO_ROW_L2, ECHO_ALGO_CLUSTER_SMEM, ECHO_ALGO_CLUSTER_REG, ECHO_ALGO_CLUSTER_REG_EXACT = range(5)
+(ECHO_ALGO_AUTO, ECHO_ALGO_ROW_L2, ECHO_ALGO_CLUSTER_SMEM, ECHO_ALGO_CLUSTER_REG, ECHO_ALGO_CLUSTER_REG_EXACT,
+ ECHO_ALGO_QUAD_REG, ECHO_ALGO_QUAD_REG_EXACT, ECHO_ALGO_PIPE) = range(8)
+ALGO_NAMES = {"auto": 0, "row_l2": 1, "cluster_smem": 2, "cluster_reg": 3, "cluster_reg_exact": 4, "quad_reg": 5,
+              "quad_reg_exact": 6, "pipe": 7}
 PACK_RESULT_BYTES = 32
 
 # kernels launched per call (for the bench's gpu_launches count)
@@ -36,10 +39,10 @@ class EchoError(RuntimeError):
         super().__init__(f"{fn} -> {_lib.echo_status_string(status).decode()}")
 
 
-def _load():
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
-    lib = ctypes.CDLL(LIB_PATH)
+def _load(path=LIB_PATH):
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
     P = ctypes.c_void_p
     i32, i64, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float
     lib.echo_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, i64, P, P, P, P, P, P, P, P]

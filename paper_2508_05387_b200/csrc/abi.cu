@@ -24,11 +24,14 @@ echo_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ECHO_OK : ECHO_
 // ECHO_ALGO_AUTO -> the register-resident CTA-pair kernel for bf16 vocabularies up to 153600 (Qwen's),
 // the SMEM-resident one up to 196608, the row kernel otherwise; explicit choices are checked for support.
 echo_status resolve_algo(int32_t dtype, int32_t vocab, int32_t* algo) {
-  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_CLUSTER_REG_EXACT) return ECHO_ERR_INVALID_ARGUMENT;
+  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_PIPE) return ECHO_ERR_INVALID_ARGUMENT;
   const bool cluster_ok = echo::cluster_algo_supports(dtype, vocab);
   const bool reg_ok = echo::cluster_reg_supports(dtype, vocab);
+  const bool quad_ok = echo::quad_supports(dtype, vocab);
   if (*algo == ECHO_ALGO_AUTO) {
-    if (reg_ok && vocab >= 16384)
+    if (quad_ok && vocab >= 16384)
+      *algo = ECHO_ALGO_QUAD_REG_EXACT;
+    else if (reg_ok && vocab >= 16384)
       *algo = ECHO_ALGO_CLUSTER_REG_EXACT;
     else if (cluster_ok && vocab >= 16384)
       *algo = ECHO_ALGO_CLUSTER_SMEM;
@@ -37,10 +40,22 @@ echo_status resolve_algo(int32_t dtype, int32_t vocab, int32_t* algo) {
   }
   if (*algo == ECHO_ALGO_CLUSTER_SMEM && !cluster_ok) return ECHO_ERR_UNSUPPORTED;
   if ((*algo == ECHO_ALGO_CLUSTER_REG || *algo == ECHO_ALGO_CLUSTER_REG_EXACT) && !reg_ok) return ECHO_ERR_UNSUPPORTED;
+  if ((*algo == ECHO_ALGO_QUAD_REG || *algo == ECHO_ALGO_QUAD_REG_EXACT) && !quad_ok) return ECHO_ERR_UNSUPPORTED;
+  if (*algo == ECHO_ALGO_PIPE && dtype != ECHO_BF16) return ECHO_ERR_UNSUPPORTED;
   return ECHO_OK;
 }
 
 }  // namespace
+
+#ifdef ECHO_TRACE
+// Diagnostic build only (libecho_trace.so, tools/trace_kernel.py): per-CTA phase timestamps of the next calls.
+static unsigned long long* g_trace = nullptr;
+static int32_t g_trace_rows = 0;
+extern "C" ECHO_API void echo_trace_set(unsigned long long* buf, int32_t rows) {
+  g_trace = buf;
+  g_trace_rows = rows;
+}
+#endif
 
 extern "C" {
 
@@ -135,6 +150,12 @@ echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_r
   p.tok_logp = tok_logp;
   p.tok_loss = tok_loss;
   p.tok_flags = tok_flags;
+  p.trace = nullptr;
+  p.trace_rows = 0;
+#ifdef ECHO_TRACE
+  p.trace = g_trace;
+  p.trace_rows = g_trace_rows;
+#endif
   return from_cuda(echo::launch_policy_loss(p, dtype, algo, static_cast<cudaStream_t>(stream), sms));
 }
 

@@ -259,4 +259,32 @@ ECHO_DEVINL RowScalars row_epilogue(float lse, float za, float old, float ref, f
   return r;
 }
 
+// Same epilogue with the coefficient scale s / N_global folded into one fp32 factor (per-kernel constant).
+ECHO_DEVINL RowScalars row_epilogue_f(float lse, float za, float old, float ref, float adv, float clip_low,
+                                      float clip_high, float kl_coef, float gscale) {
+  RowScalars r;
+  const float logp = za - lse;
+  const float rho = expf(logp - old);
+  const float lo = 1.0f - clip_low, hi = 1.0f + clip_high;
+  const bool clipped = (adv > 0.0f && rho > hi) || (adv < 0.0f && rho < lo);
+  const float rho_c = fminf(fmaxf(rho, lo), hi);
+  const float pg = fmaxf(-adv * rho, -adv * rho_c);
+  float kl = 0.0f, dkl = 0.0f;
+  if (kl_coef > 0.0f) {
+    const float x = ref - logp;
+    const float ex = expf(x);
+    kl = ex - x - 1.0f;
+    dkl = 1.0f - ex;
+  }
+  const float loss = pg + kl_coef * kl;
+  const float dl = (clipped ? 0.0f : -adv * rho) + kl_coef * dkl;
+  const float coef = dl * gscale;
+  const bool finite = isfinite(lse) && isfinite(logp) && isfinite(rho) && isfinite(loss) && isfinite(coef);
+  r.logp = logp;
+  r.loss = loss;
+  r.coef = coef;
+  r.flags = (uint8_t)((clipped ? ECHO_FLAG_CLIPPED : 0) | (finite ? 0 : ECHO_FLAG_NONFINITE));
+  return r;
+}
+
 }  // namespace echo

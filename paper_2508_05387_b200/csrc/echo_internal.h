@@ -24,6 +24,8 @@ struct LossParams {
   float* __restrict__ tok_logp;
   float* __restrict__ tok_loss;
   uint8_t* __restrict__ tok_flags;
+  unsigned long long* trace;  // ECHO_TRACE builds only: per-CTA phase timestamps (tools/trace_kernel.py)
+  int32_t trace_rows;
 };
 
 cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_train, int32_t max_lag,
@@ -43,7 +45,16 @@ bool cluster_reg_supports(int32_t dtype, int32_t V);
 struct LaunchShape {
   int32_t grid_ctas, cluster_ctas, threads, smem_bytes;
 };
-// With shape != nullptr: fill in the launch shape and launch nothing.
+// Per-kernel launchers (policy_loss_{reg,smem,row}.cu); with shape != nullptr: report the shape, launch nothing.
+cudaError_t launch_cluster_reg(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms,
+                               LaunchShape* shape);
+cudaError_t launch_cluster_smem(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
+cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape);
+int max_active_clusters(const void* fn, int threads, size_t smem, int cluster, int fallback);
+cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape);
+bool quad_supports(int32_t dtype, int32_t V);
+cudaError_t launch_pipe(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
+// Dispatch by algorithm; with shape != nullptr: fill in the launch shape and launch nothing.
 cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms,
                                LaunchShape* shape = nullptr);
 

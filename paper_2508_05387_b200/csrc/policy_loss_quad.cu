@@ -1,0 +1,313 @@
+// policy_loss_quad.cu -- ECHO_ALGO_QUAD_REG / _EXACT: the B200 design of the fused (3)+(4)+(5) kernel.
+//
+// One logits row (V ~ 152k bf16 = 297 KB) is owned by a thread-block cluster of kQCtas = 4 CTAs; CTA r holds
+// the quarter [r q, (r+1) q) of the row (q = ceil(V/4) rounded to 8) in REGISTERS: 8 warps x 32 threads x
+// 19 vectors of 16 B = 76 registers per thread.  Two such CTAs share an SM (registers 2 x 256 x 128 = 64 K,
+// shared memory 2 x 111 KB), so every SM always has two rows in flight: while one CTA waits on its cluster
+// merge or drains its stores, the other keeps the MUFU / FMA pipes busy.  The persistent grid (296 CTAs =
+// 74 clusters) strides over rows; HBM sees exactly one read and one write per logit.
+//
+// Per CTA and row:
+//   stage    1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx, L2 evict_first) stream the quarter-row
+//            through a 27 x 4 KB shared-memory ring; thread 0 refills a slot as soon as all 8 warps have copied
+//            it into registers, so the ring always runs ~1.4 quarter-rows ahead of the compute
+//   pass 1a  ring -> registers, exact bf16x2 running max m_t
+//   pass 1b  e = 2^((z - m_t) log2e) (MUFU), s_t = sum e (FADD2); kStoreExp: registers <- e as fp16
+//   merge    (m_t, s_t) -> warp (xor shuffles) -> CTA (warp 0) -> cluster: each CTA st.async's its
+//            {m, s, z_a} into slot [rank] of every peer's shared memory, completing 16 tx-bytes on the peer's
+//            mbarrier; all CTAs merge the 4 partials in rank order -> identical lse bits everywhere
+//   epilogue lse, logp, rho, clip, KL, c_t (fp32), rank 0 writes the per-token outputs
+//   pass 2   d = e k_t (k_t = -c_t 2^((m_t - lse) log2e), FMUL2)  or, exact, d = -c_t 2^((z - lse) log2e);
+//            bf16 RNE, 16-byte stores in place; the action column gets c_t (1 - p_a) from the fp32 epilogue
+// Determinism: the reduction tree depends only on V and the tile constants, never on the grid or the rank.
+#include <cuda_bf16.h>
+
+#include "echo_common.cuh"
+#include "echo_internal.h"
+#include "policy_loss_common.cuh"
+
+namespace echo {
+
+constexpr int kQCtas = 4;                           // CTAs per row (cluster size)
+constexpr int kQWarps = 8;                          // all warps compute; thread 0 also issues the TMA refills
+constexpr int kQThreads = kQWarps * 32;             // 256
+constexpr int kQChunk = kQThreads * 16;             // 4 KB: one 16-byte vector per thread
+constexpr int kQChunkElems = kQChunk / 2;           // 2048 bf16
+constexpr int kQRing = 27;                          // 108 KB staging ring (two CTAs per SM)
+constexpr int kQRegChunks = 19;                     // 19 x 2048 bf16 per CTA: V <= 155648 (Qwen 151936 / 152064)
+constexpr int kQBar = 1;                            // named barrier id
+
+struct __align__(128) QuadSmem {
+  uint8_t ring[kQRing][kQChunk];
+  uint64_t full[4];      // per row (it % 4): all chunks of the row landed (one complete_tx per chunk)
+  uint64_t consumed[4];  // per row (it % 4): all 8 warps copied the row into registers
+  uint64_t xbar[2];
+  uint4 xbuf[2][kQCtas];  // cluster partials {m, s, z_a, -} per row parity and source rank
+  float red_m[kQWarps];
+  float red_s[kQWarps];
+  float za;
+  float coef;
+  float lse;
+  float da;
+};
+
+struct QuadGeom {
+  int32_t c0, c1;          // this CTA's columns [c0, c1)
+  uint32_t slice_bytes;    // bytes loaded per row (c1 rounded up to 8 columns)
+  int nchunks;             // ring chunks per row
+};
+
+ECHO_DEVINL QuadGeom quad_geom(int32_t V, uint32_t rank) {
+  QuadGeom g;
+  const int32_t q = ((V + kQCtas - 1) / kQCtas + 7) & ~7;
+  // slices start on 8-column boundaries; a rank past the end gets an empty slice [V8, V8)
+  const int32_t v8 = (V + 7) & ~7;
+  g.c0 = min((int32_t)rank * q, v8);
+  g.c1 = max(min((int32_t)(rank + 1) * q, V), g.c0);
+  const int32_t c1r = (g.c1 + 7) & ~7;
+  g.slice_bytes = (uint32_t)(c1r - g.c0) * 2u;
+  g.nchunks = (int)((g.slice_bytes + kQChunk - 1) / kQChunk);
+  return g;
+}
+
+// Issue all chunks of row iteration `it` (one lane per chunk, expect_tx by lane 0 on the row's barrier).
+ECHO_DEVINL void quad_issue_row(const LossParams& p, const QuadGeom& g, uint32_t cid, uint32_t ncl, uint32_t it,
+                                int lane, uint32_t full0, uint32_t ring0, uint64_t pol) {
+  const uint32_t bar = full0 + 8 * (it & 3u);
+  if (lane == 0) mbar_arrive_expect_tx(bar, g.slice_bytes);
+  const int64_t row = (int64_t)cid + (int64_t)it * ncl;
+  const uint8_t* src = p.logits + row * p.ld_bytes + (int64_t)g.c0 * 2;
+  for (int c = lane; c < g.nchunks; c += 32) {
+    const uint32_t slot = (it * (uint32_t)g.nchunks + c) % kQRing;
+    const uint32_t nb = min((uint32_t)kQChunk, g.slice_bytes - (uint32_t)c * kQChunk);
+    bulk_g2s(ring0 + slot * kQChunk, src + (int64_t)c * kQChunk, nb, bar, pol);
+  }
+}
+
+template <bool kStoreExp>
+__global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
+    policy_loss_quad_kernel(const LossParams p) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  QuadSmem& sm = *reinterpret_cast<QuadSmem*>(smem_raw);
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t cid = cluster_id_x(), ncl = nclusters_x();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int32_t V = p.V;
+  const QuadGeom g = quad_geom(V, rank);
+  const int nchunks = g.nchunks;
+  const int32_t c0 = g.c0, c1 = g.c1;
+  const uint32_t full0 = smem_u32(&sm.full[0]), cons0 = smem_u32(&sm.consumed[0]), ring0 = smem_u32(&sm.ring[0][0]);
+  const uint32_t my_rows = p.n_rows > (int64_t)cid ? (uint32_t)((p.n_rows - 1 - cid) / ncl + 1) : 0u;
+
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(cons0 + 8 * i, kQWarps);
+    }
+    mbar_init(smem_u32(&sm.xbar[0]), 1);
+    mbar_init(smem_u32(&sm.xbar[1]), 1);
+    fence_mbar_init_cluster();
+  }
+  cluster_sync_all();
+
+  const uint64_t ld_pol = policy_evict_first();
+  if (warp == 0 && my_rows > 0 && nchunks > 0) quad_issue_row(p, g, cid, ncl, 0, lane, full0, ring0, ld_pol);
+
+  uint32_t xbuf_remote[kQCtas], xbar_remote[kQCtas];
+#pragma unroll
+  for (int r = 0; r < kQCtas; ++r) {
+    xbuf_remote[r] = mapa(smem_u32(&sm.xbuf[0][rank]), r);
+    xbar_remote[r] = mapa(smem_u32(&sm.xbar[0]), r);
+  }
+  const uint64_t st_pol = policy_evict_first();
+  const float gscale = (float)((double)p.grad_scale / *p.n_global);
+  const int32_t col_t = c0 + tid * 8;
+  const bool last_valid = (uint32_t)(nchunks - 1) * kQChunk + (uint32_t)tid * 16u < g.slice_bytes;
+  const bool has_tail = (c1 & 7) && (c1 & ~7) >= col_t && ((c1 & ~7) - col_t) % kQChunkElems == 0;
+  const int nstore = nchunks - (last_valid ? 0 : 1) - (has_tail ? 1 : 0);
+  const uint64_t l2e2 = f2(kLog2e, kLog2e);
+  const uint32_t my_off = (uint32_t)tid * 16u;
+  uint32_t it = 0;
+
+  for (int64_t row = cid; row < p.n_rows; row += ncl, ++it) {
+    const int32_t a = p.tok_action[row];
+    RowMeta meta{0.f, 0.f, 0.f};
+    if (tid == 0) meta = load_meta(p, row);
+
+    ECHO_TRACE_MARK(p, it, 0);
+    // ---- pass 1a: one wait for the whole row, then ring -> registers; each warp marks the row consumed
+    uint4 v[kQRegChunks];
+    if (nchunks > 0) mbar_wait(full0 + 8 * (it & 3u), (it >> 2) & 1u);
+#pragma unroll
+    for (int c = 0; c < kQRegChunks; ++c) {
+      if (c < nchunks) {
+        const uint32_t slot = (it * (uint32_t)nchunks + c) % kQRing;
+        uint4 w = lds_v4(ring0 + slot * kQChunk + my_off);
+        if (c == nchunks - 1) {
+          if (!last_valid) w = make_uint4(kBf16NegInf2, kBf16NegInf2, kBf16NegInf2, kBf16NegInf2);
+          if (has_tail) w = mask_tail(w, c1 & 7);
+        }
+        v[c] = w;
+      } else {
+        v[c] = make_uint4(kBf16NegInf2, kBf16NegInf2, kBf16NegInf2, kBf16NegInf2);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cons0 + 8 * (it & 3u));
+    // warp 0 streams the next row into the slots just released (its chunks only overlap rows <= it)
+    if (warp == 0 && it + 1 < my_rows && nchunks > 0) {
+      if (lane == 0) mbar_wait(cons0 + 8 * (it & 3u), (it >> 2) & 1u);
+      __syncwarp();
+      quad_issue_row(p, g, cid, ncl, it + 1, lane, full0, ring0, ld_pol);
+    }
+    __syncwarp();
+
+    ECHO_TRACE_MARK(p, it, 1);
+    uint32_t mx2 = kBf16NegInf2;
+#pragma unroll
+    for (int c = 0; c < kQRegChunks; ++c) mx2 = bmax2(mx2, bmax2(bmax2(v[c].x, v[c].y), bmax2(v[c].z, v[c].w)));
+    const float mx = fmaxf(__uint_as_float(mx2 << 16), __uint_as_float(mx2 & 0xFFFF0000u));
+    const bool own_a = a >= col_t && a < c1 && ((a - col_t) % kQChunkElems) < 8;
+    if (own_a) {
+      const int ca = (a - col_t) / kQChunkElems, ea = (a - col_t) % kQChunkElems;
+      uint32_t word = 0;
+#pragma unroll
+      for (int c = 0; c < kQRegChunks; ++c)
+        if (c == ca) word = (ea >> 1) == 0 ? v[c].x : (ea >> 1) == 1 ? v[c].y : (ea >> 1) == 2 ? v[c].z : v[c].w;
+      sm.za = (ea & 1) ? __uint_as_float(word & 0xFFFF0000u) : __uint_as_float(word << 16);
+    }
+
+    // ---- pass 1b
+    const float mb = (mx == -INFINITY) ? 0.0f : mx * kLog2e;
+    const uint64_t nmb2 = f2(-mb, -mb);
+    uint64_t s2 = f2(0.0f, 0.0f);
+#pragma unroll
+    for (int c = 0; c < kQRegChunks; ++c) {
+      if (c < nchunks) {
+        uint32_t* w = &v[c].x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float e0, e1;
+          f2split(fma2(bf2_to_f2(w[k]), l2e2, nmb2), e0, e1);
+          e0 = ex2(e0);
+          e1 = ex2(e1);
+          s2 = add2(s2, f2(e0, e1));
+          if (kStoreExp) w[k] = pack_f16x2(e0, e1);
+        }
+      }
+    }
+    float slo, shi;
+    f2split(s2, slo, shi);
+    const MaxSum acc = warp_maxsum(MaxSum{mx, slo + shi});
+    if (lane == 0) {
+      sm.red_m[warp] = acc.m;
+      sm.red_s[warp] = acc.s;
+    }
+    ECHO_TRACE_MARK(p, it, 2);
+    named_bar_sync(kQBar, kQThreads);
+    ECHO_TRACE_MARK(p, it, 3);
+
+    // ---- CTA merge (warp 0), cluster merge (st.async to every peer), epilogue (lane 0)
+    if (warp == 0) {
+      MaxSum mine = lane < kQWarps ? MaxSum{sm.red_m[lane], sm.red_s[lane]} : MaxSum{-INFINITY, 0.0f};
+      mine = warp_maxsum(mine);
+      if (lane == 0) {
+        const uint32_t par = it & 1u;
+        const bool owner = (a >= c0 && a < c1);
+        const uint4 msg = make_uint4(__float_as_uint(mine.m), __float_as_uint(mine.s),
+                                     __float_as_uint(owner ? sm.za : 0.0f), owner ? 1u : 0u);
+        const uint32_t xbar_local = smem_u32(&sm.xbar[par]);
+        mbar_arrive_expect_tx(xbar_local, 16 * kQCtas);
+#pragma unroll
+        for (int r = 0; r < kQCtas; ++r)
+          st_async_v4(xbuf_remote[r] + par * (16u * kQCtas), msg, xbar_remote[r] + par * 8u);
+        mbar_wait_cluster(xbar_local, (it >> 1) & 1u);
+        MaxSum tot{-INFINITY, 0.0f};
+        float za = NAN;
+#pragma unroll
+        for (int r = 0; r < kQCtas; ++r) {
+          const uint4 m = sm.xbuf[par][r];
+          tot = r == 0 ? MaxSum{__uint_as_float(m.x), __uint_as_float(m.y)}
+                       : maxsum_merge(tot, MaxSum{__uint_as_float(m.x), __uint_as_float(m.y)});
+          if (m.w) za = __uint_as_float(m.z);
+        }
+        const float lse = tot.m + logf(tot.s);
+        if (a < 0 || a >= V) za = NAN;
+        const RowScalars r = row_epilogue_f(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high,
+                                            p.kl_coef, gscale);
+        if (rank == 0) {
+          p.tok_logp[row] = r.logp;
+          p.tok_loss[row] = r.loss;
+          p.tok_flags[row] = r.flags;
+        }
+        const float pa = ex2(fmaf(za, kLog2e, -lse * kLog2e));
+        sm.coef = r.coef;
+        sm.lse = lse;
+        sm.da = fmaf(-r.coef, pa, r.coef);
+      }
+    }
+    named_bar_sync(kQBar, kQThreads);
+    ECHO_TRACE_MARK(p, it, 4);
+    const float coef = sm.coef, lse = sm.lse;
+
+    // ---- pass 2
+    const float kt = mx == -INFINITY ? 0.0f : -coef * ex2((mx - lse) * kLog2e);
+    const uint64_t k2 = kStoreExp ? f2(kt, kt) : f2(-coef, -coef);
+    const uint64_t nlse2 = f2(-lse * kLog2e, -lse * kLog2e);
+    uint8_t* const row_base = p.logits + row * p.ld_bytes;
+    uint8_t* const dst = row_base + (int64_t)col_t * 2;
+#pragma unroll
+    for (int c = 0; c < kQRegChunks; ++c) {
+      if (c < nchunks) {
+        uint32_t* w = &v[c].x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float d0, d1;
+          if (kStoreExp) {
+            f2split(mul2(f2(f16lo(w[k]), f16hi(w[k])), k2), d0, d1);
+          } else {
+            float t0, t1;
+            f2split(fma2(bf2_to_f2(w[k]), l2e2, nlse2), t0, t1);
+            f2split(mul2(f2(ex2(t0), ex2(t1)), k2), d0, d1);
+          }
+          w[k] = pack_bf16x2(d0, d1);
+        }
+        if (c < nstore)
+          stg_v4_hint(dst + (int64_t)c * kQChunk, v[c], st_pol);
+        else if (has_tail && c == nchunks - 1)
+          store_partial8(reinterpret_cast<__nv_bfloat16*>(dst + (int64_t)c * kQChunk), v[c], c1 & 7);
+      }
+    }
+    ECHO_TRACE_MARK(p, it, 5);
+    if (own_a) reinterpret_cast<__nv_bfloat16*>(row_base)[a] = __float2bfloat16_rn(sm.da);
+  }
+  cluster_sync_all();
+}
+
+bool quad_supports(int32_t dtype, int32_t V) {
+  if (dtype != ECHO_BF16 || V < 8 * kQCtas) return false;
+  const int32_t q = ((V + kQCtas - 1) / kQCtas + 7) & ~7;
+  return ((int64_t)q * 2 + kQChunk - 1) / kQChunk <= kQRegChunks;
+}
+
+template <bool kStoreExp>
+static cudaError_t launch_quad_t(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  const size_t smem = sizeof(QuadSmem);
+  const void* fn = (const void*)policy_loss_quad_kernel<kStoreExp>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t clusters = max_active_clusters(fn, kQThreads, smem, kQCtas, num_sms * 2 / kQCtas);
+  if (clusters > p.n_rows) clusters = p.n_rows;
+  if (shape) {
+    *shape = LaunchShape{(int32_t)(clusters * kQCtas), kQCtas, kQThreads, (int32_t)smem};
+    return cudaSuccess;
+  }
+  policy_loss_quad_kernel<kStoreExp><<<(unsigned)(clusters * kQCtas), kQThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  return store_exp ? launch_quad_t<true>(p, stream, num_sms, shape) : launch_quad_t<false>(p, stream, num_sms, shape);
+}
+
+}  // namespace echo

@@ -1,0 +1,162 @@
+// policy_loss_row.cu -- ECHO_ALGO_ROW_L2 (see policy_loss.cu for the overview).
+#include <cuda_bf16.h>
+
+#include "echo_common.cuh"
+#include "echo_internal.h"
+#include "policy_loss_common.cuh"
+
+namespace echo {
+
+// ====================================================================== ECHO_ALGO_ROW_L2
+constexpr int kRThreads = 1024;
+constexpr int kRWarps = kRThreads / 32;
+constexpr int kRUnroll = 4;
+
+template <int DT>  // 0 = fp32, 1 = bf16
+struct RowVec;
+template <>
+struct RowVec<1> {
+  static constexpr int N = 8;
+  static ECHO_DEVINL void unpack(const uint4& w, float (&x)[8]) { unpack8(w, x); }
+  static ECHO_DEVINL uint4 pack(const float (&x)[8]) {
+    return make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
+                      pack_bf16x2(x[6], x[7]));
+  }
+  static ECHO_DEVINL float load1(const uint8_t* row, int32_t v) {
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(row)[v]);
+  }
+  static ECHO_DEVINL void store1(uint8_t* row, int32_t v, float x) {
+    reinterpret_cast<__nv_bfloat16*>(row)[v] = __float2bfloat16_rn(x);
+  }
+};
+template <>
+struct RowVec<0> {
+  static constexpr int N = 4;
+  static ECHO_DEVINL void unpack(const uint4& w, float (&x)[4]) {
+    x[0] = __uint_as_float(w.x); x[1] = __uint_as_float(w.y);
+    x[2] = __uint_as_float(w.z); x[3] = __uint_as_float(w.w);
+  }
+  static ECHO_DEVINL uint4 pack(const float (&x)[4]) {
+    return make_uint4(__float_as_uint(x[0]), __float_as_uint(x[1]), __float_as_uint(x[2]), __float_as_uint(x[3]));
+  }
+  static ECHO_DEVINL float load1(const uint8_t* row, int32_t v) { return reinterpret_cast<const float*>(row)[v]; }
+  static ECHO_DEVINL void store1(uint8_t* row, int32_t v, float x) { reinterpret_cast<float*>(row)[v] = x; }
+};
+
+template <int DT>
+__global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const LossParams p) {
+  using RV = RowVec<DT>;
+  constexpr int N = RV::N;
+  __shared__ float s_m[kRWarps], s_s[kRWarps];
+  __shared__ float s_za, s_coef, s_lse_l2e;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t V = p.V;
+  const int32_t nvec = V / N;
+  const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+  const double n_global = *p.n_global;
+
+  for (int64_t row = blockIdx.x; row < p.n_rows; row += gridDim.x) {
+    uint8_t* rowp = p.logits + row * p.ld_bytes;
+    const int32_t a = p.tok_action[row];
+    RowMeta meta{0.f, 0.f, 0.f};
+    if (tid == 0) {
+      meta = load_meta(p, row);
+      s_za = NAN;
+    }
+    __syncthreads();
+
+    // ---- pass 1
+    MaxSum acc{-INFINITY, 0.0f};
+    for (int32_t v0 = tid; v0 < nvec; v0 += kRThreads * kRUnroll) {
+      uint4 w[kRUnroll];
+#pragma unroll
+      for (int u = 0; u < kRUnroll; ++u) {
+        const int32_t v = v0 + u * kRThreads;
+        if (v < nvec) w[u] = ldg_v4_hint(rowp + (int64_t)v * 16, pol_keep);
+      }
+#pragma unroll
+      for (int u = 0; u < kRUnroll; ++u) {
+        const int32_t v = v0 + u * kRThreads;
+        if (v < nvec) {
+          float x[N];
+          RV::unpack(w[u], x);
+          const int32_t col = v * N;
+          if ((uint32_t)(a - col) < (uint32_t)N) {
+#pragma unroll
+            for (int e = 0; e < N; ++e)
+              if (col + e == a) s_za = x[e];
+          }
+          online_update<N>(acc, x);
+        }
+      }
+    }
+    for (int32_t col = nvec * N + tid; col < V; col += kRThreads) {  // ragged tail (V % N)
+      float x[1] = {RV::load1(rowp, col)};
+      if (col == a) s_za = x[0];
+      online_update<1>(acc, x);
+    }
+    acc = warp_maxsum(acc);
+    if (lane == 0) {
+      s_m[warp] = acc.m;
+      s_s[warp] = acc.s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      MaxSum tot{s_m[0], s_s[0]};
+      for (int w = 1; w < kRWarps; ++w) tot = maxsum_merge(tot, MaxSum{s_m[w], s_s[w]});
+      const float lse = tot.m + logf(tot.s);
+      const float za = (a < 0 || a >= V) ? NAN : s_za;
+      const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high, p.kl_coef,
+                                        p.grad_scale, n_global);
+      p.tok_logp[row] = r.logp;
+      p.tok_loss[row] = r.loss;
+      p.tok_flags[row] = r.flags;
+      s_coef = r.coef;
+      s_lse_l2e = lse * kLog2e;
+    }
+    __syncthreads();
+    const float coef = s_coef, lse_l2e = s_lse_l2e;
+
+    // ---- pass 2
+    for (int32_t v0 = tid; v0 < nvec; v0 += kRThreads * kRUnroll) {
+      uint4 w[kRUnroll];
+#pragma unroll
+      for (int u = 0; u < kRUnroll; ++u) {
+        const int32_t v = v0 + u * kRThreads;
+        if (v < nvec) w[u] = ldg_v4_hint(rowp + (int64_t)v * 16, pol_drop);
+      }
+#pragma unroll
+      for (int u = 0; u < kRUnroll; ++u) {
+        const int32_t v = v0 + u * kRThreads;
+        if (v < nvec) {
+          float x[N];
+          RV::unpack(w[u], x);
+          grad_values<N>(x, v * N, a, coef, lse_l2e);
+          stg_v4_hint(rowp + (int64_t)v * 16, RV::pack(x), pol_drop);
+        }
+      }
+    }
+    for (int32_t col = nvec * N + tid; col < V; col += kRThreads) {
+      float x[1] = {RV::load1(rowp, col)};
+      grad_values<1>(x, col, a, coef, lse_l2e);
+      RV::store1(rowp, col, x[0]);
+    }
+    __syncthreads();  // s_* reuse by the next row
+  }
+}
+
+cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  int64_t grid = num_sms;
+  if (grid > p.n_rows) grid = p.n_rows;
+  if (shape) {
+    *shape = LaunchShape{(int32_t)grid, 1, kRThreads, 0};
+    return cudaSuccess;
+  }
+  if (dtype == ECHO_BF16)
+    policy_loss_row_kernel<1><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+  else
+    policy_loss_row_kernel<0><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace echo

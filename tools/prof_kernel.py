@@ -22,7 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="qwen3-4b")
     ap.add_argument("--rows", type=int, default=32768)
-    ap.add_argument("--algos", default="cluster_reg,cluster_reg_exact,cluster_smem,row_l2")
+    ap.add_argument("--algos", default="quad_reg,quad_reg_exact,cluster_reg,cluster_reg_exact,cluster_smem,row_l2")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--streams", action="store_true", help="also time torch in-place / copy streams")
@@ -50,8 +50,7 @@ def main():
     logits = torch.empty(M, ld, dtype=torch.bfloat16, device="cuda")
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     bpt = 2 * cfg.V * 2 + 21 + (4 if cfg.kl_coef > 0 else 0)
-    names = {"row_l2": abi.ECHO_ALGO_ROW_L2, "cluster_smem": abi.ECHO_ALGO_CLUSTER_SMEM,
-             "cluster_reg": abi.ECHO_ALGO_CLUSTER_REG, "cluster_reg_exact": abi.ECHO_ALGO_CLUSTER_REG_EXACT}
+    names = abi.ALGO_NAMES
     out = {"config": cfg.name, "rows": M, "bytes_per_token": bpt, "algos": {}}
 
     def regen():
