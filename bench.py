@@ -12,7 +12,7 @@ value      = kept tokens of all ranks / max-over-ranks device time of the path (
 e2e.value  = the same through the public step API with pinned host inputs copied H2D and the statistics read
              back inside the timed region (generator time subtracted, it is not part of the method)
 
-  python bench.py [--gpus N --steps K --warmup W] [--config qwen3-4b] [--algo auto|row_l2|cluster_smem]
+  python bench.py [--gpus N --steps K --warmup W] [--config qwen3-4b] [--algo auto|quad_reg|quad_reg_exact|row_l2]
   python bench.py --impl reference ...      # the CPU oracle arm (rank 0 only)
 """
 from __future__ import annotations
@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="echo", choices=["echo", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "cluster_smem", "cluster_reg", "cluster_reg_exact", "quad_reg", "quad_reg_exact", "pipe"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "quad_reg", "quad_reg_exact"])
     ap.add_argument("--micro-batch", type=int, default=32768)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

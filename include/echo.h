@@ -62,19 +62,14 @@ enum { ECHO_FLAG_CLIPPED = 1, ECHO_FLAG_NONFINITE = 2 };
 
 /* Algorithm selector for echo_policy_loss_fwd_bwd_ex (tests / benchmarks). */
 enum {
-  ECHO_ALGO_AUTO = 0,
-  ECHO_ALGO_ROW_L2 = 1,      /* one CTA per row, two streaming passes; the second pass re-reads from L2 */
-  ECHO_ALGO_CLUSTER_SMEM = 2, /* CTA pair per row, each half-row resident in a TMA-fed shared-memory ring:
-                                 exactly one HBM read + one HBM write per logit (bf16, vocab <= 196608) */
-  ECHO_ALGO_CLUSTER_REG = 3,  /* CTA pair per row, half-row held in registers, the TMA ring only stages the
-                                 next rows; exp(z - m) kept as fp16 between the passes (bf16, vocab <= 155648) */
-  ECHO_ALGO_CLUSTER_REG_EXACT = 4, /* as CLUSTER_REG, but the write-back recomputes exp from the bf16 logits
-                                      (fp32 end to end; two exponentials per logit) */
-  ECHO_ALGO_QUAD_REG = 5,         /* 4-CTA cluster per row, quarter-row in registers, two CTAs (two rows) per
-                                     SM; exp(z - m) kept as fp16 between the passes (bf16, vocab <= 155648) */
-  ECHO_ALGO_QUAD_REG_EXACT = 6,   /* as QUAD_REG, write-back recomputes exp from the bf16 logits (fp32) */
-  ECHO_ALGO_PIPE = 7              /* one SM per row, warp-specialised: TMA producer, reducer warps (pass 1 of
-                                     row k+1), writer warps (pass 2 of row k, second read from L2); bf16, any V */
+  ECHO_ALGO_AUTO = 0,           /* QUAD_REG for bf16 with 16384 <= vocab <= 155648, ROW_L2 otherwise */
+  ECHO_ALGO_ROW_L2 = 1,         /* one 1024-thread CTA per row, two streaming passes, the second re-reads the row
+                                   from L2; bf16 or fp32, any vocab */
+  ECHO_ALGO_QUAD_REG = 2,       /* 4-CTA cluster per row, each CTA a quarter-row in registers, two CTAs (two rows)
+                                   per SM, TMA-fed ring, DSMEM merge; exp(z - m) kept as fp16 between the passes
+                                   (bf16, vocab <= 155648) -- the B200 design */
+  ECHO_ALGO_QUAD_REG_EXACT = 3  /* as QUAD_REG, but the write-back recomputes exp from the bf16 logits (fp32 end to
+                                   end; two exponentials per logit) */
 };
 
 /* Device-resident result of echo_pack_batch (32 bytes). */

@@ -21,27 +21,13 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 echo_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ECHO_OK : ECHO_ERR_CUDA; }
 
-// ECHO_ALGO_AUTO -> the register-resident CTA-pair kernel for bf16 vocabularies up to 153600 (Qwen's),
-// the SMEM-resident one up to 196608, the row kernel otherwise; explicit choices are checked for support.
+// ECHO_ALGO_AUTO -> the 4-CTA register-resident kernel for bf16 Qwen-size vocabularies, the row kernel otherwise;
+// explicit choices are checked for support.
 echo_status resolve_algo(int32_t dtype, int32_t vocab, int32_t* algo) {
-  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_PIPE) return ECHO_ERR_INVALID_ARGUMENT;
-  const bool cluster_ok = echo::cluster_algo_supports(dtype, vocab);
-  const bool reg_ok = echo::cluster_reg_supports(dtype, vocab);
+  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_QUAD_REG_EXACT) return ECHO_ERR_INVALID_ARGUMENT;
   const bool quad_ok = echo::quad_supports(dtype, vocab);
-  if (*algo == ECHO_ALGO_AUTO) {
-    if (quad_ok && vocab >= 16384)
-      *algo = ECHO_ALGO_QUAD_REG_EXACT;
-    else if (reg_ok && vocab >= 16384)
-      *algo = ECHO_ALGO_CLUSTER_REG_EXACT;
-    else if (cluster_ok && vocab >= 16384)
-      *algo = ECHO_ALGO_CLUSTER_SMEM;
-    else
-      *algo = ECHO_ALGO_ROW_L2;
-  }
-  if (*algo == ECHO_ALGO_CLUSTER_SMEM && !cluster_ok) return ECHO_ERR_UNSUPPORTED;
-  if ((*algo == ECHO_ALGO_CLUSTER_REG || *algo == ECHO_ALGO_CLUSTER_REG_EXACT) && !reg_ok) return ECHO_ERR_UNSUPPORTED;
+  if (*algo == ECHO_ALGO_AUTO) *algo = (quad_ok && vocab >= 16384) ? ECHO_ALGO_QUAD_REG : ECHO_ALGO_ROW_L2;
   if ((*algo == ECHO_ALGO_QUAD_REG || *algo == ECHO_ALGO_QUAD_REG_EXACT) && !quad_ok) return ECHO_ERR_UNSUPPORTED;
-  if (*algo == ECHO_ALGO_PIPE && dtype != ECHO_BF16) return ECHO_ERR_UNSUPPORTED;
   return ECHO_OK;
 }
 

@@ -38,22 +38,16 @@ cudaError_t launch_group_advantage(int32_t G, float eps, int64_t rollout_base, c
                                    const int32_t* kept_rollout, const echo_pack_result* pack, float* adv_slot,
                                    double* adv_stats, cudaStream_t stream);
 
-bool cluster_algo_supports(int32_t dtype, int32_t V);
-bool cluster_reg_supports(int32_t dtype, int32_t V);
 
 // Launch shape a policy-loss call uses (reported by echo_policy_loss_launch_shape).
 struct LaunchShape {
   int32_t grid_ctas, cluster_ctas, threads, smem_bytes;
 };
-// Per-kernel launchers (policy_loss_{reg,smem,row}.cu); with shape != nullptr: report the shape, launch nothing.
-cudaError_t launch_cluster_reg(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms,
-                               LaunchShape* shape);
-cudaError_t launch_cluster_smem(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
+// Per-kernel launchers (policy_loss_{quad,row}.cu); with shape != nullptr: report the shape, launch nothing.
 cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape);
 int max_active_clusters(const void* fn, int threads, size_t smem, int cluster, int fallback);
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape);
 bool quad_supports(int32_t dtype, int32_t V);
-cudaError_t launch_pipe(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
 // Dispatch by algorithm; with shape != nullptr: fill in the launch shape and launch nothing.
 cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms,
                                LaunchShape* shape = nullptr);

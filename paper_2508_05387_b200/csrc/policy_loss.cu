@@ -8,23 +8,18 @@
 // The path is a memory-bound stream (no contraction): the design goal is exactly one HBM read and one HBM
 // write per logit, 128-bit accesses, and nothing else on the memory bus.
 //
-// Two kernels:
-//   ECHO_ALGO_CLUSTER_SMEM (policy_loss_cluster_kernel; bf16, V <= 196608) -- the B200 design.
-//     A thread-block cluster of 2 CTAs (2 SMs) owns one row; each CTA owns half of it.  A producer warp
-//     streams the half-row into a 26 x 8 KB shared-memory ring with 1-D TMA bulk copies
-//     (cp.async.bulk + mbarrier complete_tx, L2 evict_first).  16 consumer warps run pass 1 straight out
-//     of shared memory, reduce (m, s) warp -> CTA, and swap the CTA pair's partials through DSMEM with one
-//     st.async that completes on the peer's mbarrier (no cluster-wide barrier per row, so the producer
-//     never stalls).  Both CTAs merge the two partials in rank order -> identical lse bits.  Pass 2 reads
-//     the half-row again from shared memory (not HBM), writes 16-byte gradient vectors, and frees ring
-//     slots, which the producer immediately refills with the next row.  HBM traffic = 1R + 1W exactly,
-//     independent of L2 behaviour; persistent grid of 74 clusters (148 SMs).
-//   ECHO_ALGO_ROW_L2 (policy_loss_row_kernel; bf16 or fp32, any V) -- one 1024-thread CTA per row,
-//     persistent over rows; pass 1 loads with L2 evict_last, pass 2 re-loads (an L2 hit when the ~45 MB
-//     of rows in flight stay resident) with evict_first and stores in place.
+// Kernels (one dispatch, echo_policy_loss_fwd_bwd_ex):
+//   ECHO_ALGO_QUAD_REG / _EXACT (policy_loss_quad.cu; bf16, V <= 155648) -- the B200 design: a 4-CTA cluster
+//     owns a row, each CTA keeps its quarter-row in registers, two CTAs (two rows) share an SM so that one row's
+//     MUFU-bound reduction overlaps the other's cluster merge and store burst; rows arrive through a TMA-fed
+//     shared-memory ring; the CTA partials are merged through DSMEM (st.async + mbarrier); exactly one HBM read
+//     and one HBM write per logit.
+//   ECHO_ALGO_ROW_L2 (policy_loss_row.cu; bf16 or fp32, any V) -- one 1024-thread CTA per row, persistent over
+//     rows; pass 1 loads with L2 evict_last, pass 2 re-loads (an L2 hit when the ~45 MB of rows in flight stay
+//     resident) with evict_first and stores in place.  Generic path for fp32 and out-of-range vocabularies.
 //
 // Determinism: every row is reduced by the same thread layout (vector j of a row always belongs to the
-// same thread, xor-butterfly warp merges, fixed warp order, rank-0-then-rank-1 pair merge), so results
+// same thread, xor-butterfly warp merges, fixed warp order, rank-ordered cluster merge), so results
 // depend only on (V, tile constants) -- not on the grid, the micro-batch split or the rank.
 #include <cuda_bf16.h>
 
@@ -59,12 +54,8 @@ int max_active_clusters(const void* fn, int threads, size_t smem, int cluster, i
 
 cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms,
                                LaunchShape* shape) {
-  if (algo == ECHO_ALGO_PIPE) return launch_pipe(p, stream, num_sms, shape);
   if (algo == ECHO_ALGO_QUAD_REG) return launch_quad(p, true, stream, num_sms, shape);
   if (algo == ECHO_ALGO_QUAD_REG_EXACT) return launch_quad(p, false, stream, num_sms, shape);
-  if (algo == ECHO_ALGO_CLUSTER_REG) return launch_cluster_reg(p, true, stream, num_sms, shape);
-  if (algo == ECHO_ALGO_CLUSTER_REG_EXACT) return launch_cluster_reg(p, false, stream, num_sms, shape);
-  if (algo == ECHO_ALGO_CLUSTER_SMEM) return launch_cluster_smem(p, stream, num_sms, shape);
   return launch_row(p, dtype, stream, num_sms, shape);
 }
 

@@ -49,17 +49,18 @@ def test_library_is_sm100a_code():
     assert "sm_100a" in out
 
 
-def test_cluster_kernel_uses_tma_bulk_copies_and_dsmem():
+def test_quad_kernel_uses_tma_bulk_copies_and_dsmem():
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", os.path.join(PKG, "libecho.so")],
                           capture_output=True, text=True, check=True).stdout
     blocks = re.split(r"\n\s*Function : ", sass)
-    cluster = [b for b in blocks if b.startswith("_ZN4echo26policy_loss_cluster_kernel")]
-    assert len(cluster) == 1
-    body = cluster[0]
+    quad = [b for b in blocks if "policy_loss_quad_kernel" in b.split("\n", 1)[0]]
+    assert len(quad) == 2                       # fp16-cache and exact variants
+    body = quad[0]
     assert "UBLKCP.S.G" in body      # cp.async.bulk global->shared (TMA engine)
     assert "SYNCS" in body           # mbarrier phase / tx tracking
     assert "STAS" in body            # st.async into the peer CTA's shared memory (DSMEM)
     assert "UCGABAR" in body         # cluster barrier (setup / teardown only)
+    assert "MUFU.EX2" in body and "FFMA2" in body   # one MUFU exp per logit, packed fp32x2 math
     assert "STG.E.NA.128" in body    # 16-byte gradient stores
     assert "HMMA" not in body and "UTCHMMA" not in body   # no tensor cores: a stream, not a contraction
 

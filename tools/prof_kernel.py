@@ -22,7 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="qwen3-4b")
     ap.add_argument("--rows", type=int, default=32768)
-    ap.add_argument("--algos", default="quad_reg,quad_reg_exact,cluster_reg,cluster_reg_exact,cluster_smem,row_l2")
+    ap.add_argument("--algos", default="quad_reg,quad_reg_exact,row_l2")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--streams", action="store_true", help="also time torch in-place / copy streams")

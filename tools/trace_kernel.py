@@ -20,7 +20,7 @@ import torch  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--algos", default="cluster_reg,quad_reg")
+    ap.add_argument("--algos", default="quad_reg,quad_reg_exact")
     ap.add_argument("--rows", type=int, default=32768)
     args = ap.parse_args()
     import _build
