@@ -3,8 +3,8 @@
 //   loss_stats = {sum l, sum (logp-old), sum k3(ref,logp), n_clipped, n_nonfinite, rho_min, rho_max,
 //                 sum logp, n_tokens, sum rho}
 // Launch 1: kStatBlocks (fixed) blocks; block b owns tokens [b*n/B, (b+1)*n/B) and reduces them with a
-// fixed thread-strided loop + fixed shuffle tree into workspace[b].  Launch 2: one warp folds the B
-// partials in ascending order.  The partition depends only on n_tokens, so the result is bitwise
+// fixed thread-strided loop + fixed shuffle tree into workspace[b].  Launch 2: one warp per statistic folds
+// the B partials in a fixed order (contiguous lane ranges, then an xor tree).  The partition depends only on n_tokens, so the result is bitwise
 // reproducible (and the W-rank all-reduce of these vectors only changes the order of B-level sums).
 #include "echo_common.cuh"
 #include "echo_internal.h"
@@ -86,15 +86,22 @@ __global__ void __launch_bounds__(kStatThreads) loss_stats_partial_kernel(
   }
 }
 
-__global__ void loss_stats_final_kernel(const double* __restrict__ ws, double* __restrict__ out) {
-  const int i = threadIdx.x;
-  if (i >= kNStat) return;
-  double v = ws[i];
-  for (int b = 1; b < kStatBlocks; ++b) {
+// One warp per statistic: lane l folds the partials [l B/32, (l+1) B/32) in order, then a fixed xor tree.
+__global__ void __launch_bounds__(32 * kNStat) loss_stats_final_kernel(const double* __restrict__ ws,
+                                                                      double* __restrict__ out) {
+  const int i = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lo = lane * kStatBlocks / 32, hi = (lane + 1) * kStatBlocks / 32;
+  double v = (i == 5) ? INFINITY : (i == 6) ? -INFINITY : 0.0;
+  for (int b = lo; b < hi; ++b) {
     const double x = ws[b * kNStat + i];
     v = (i == 5) ? fmin(v, x) : (i == 6) ? fmax(v, x) : v + x;
   }
-  out[i] = v;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = (i == 5) ? fmin(v, x) : (i == 6) ? fmax(v, x) : v + x;
+  }
+  if (lane == 0) out[i] = v;
 }
 
 size_t loss_stats_workspace_bytes() { return sizeof(double) * kStatBlocks * kNStat; }
@@ -104,7 +111,7 @@ cudaError_t launch_loss_stats(int64_t n, const float* tok_loss, const float* tok
                               cudaStream_t stream) {
   loss_stats_partial_kernel<<<kStatBlocks, kStatThreads, 0, stream>>>(n, tok_loss, tok_logp, tok_old, tok_ref,
                                                                       tok_flags, ws);
-  loss_stats_final_kernel<<<1, 32, 0, stream>>>(ws, out);
+  loss_stats_final_kernel<<<1, 32 * kNStat, 0, stream>>>(ws, out);
   return cudaGetLastError();
 }
 
