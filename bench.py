@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="echo", choices=["echo", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "quad_reg", "quad_reg_exact"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "quad_reg", "quad_reg_exact", "oct_reg"])
     ap.add_argument("--micro-batch", type=int, default=32768)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -121,11 +121,12 @@ class ClockSampler:
 def oracle_rate(cfg, rank_batch, n_tokens_total, target_s, threads=None):
     """Time the oracle (as it stands) on a bounded sample of the workload on this host's cores: the full pack +
     advantage of the batch, and the fused loss on a row sample sized to ~target_s.  Returns a dict."""
+    cores = len(os.sched_getaffinity(0)) if threads is None else int(threads)
+    # torchrun exports OMP_NUM_THREADS=1; the oracle is timed on all of this host's cores (read when the OpenMP
+    # runtime starts, i.e. when the oracle library is first loaded)
+    os.environ["OMP_NUM_THREADS"] = str(cores)
     import oracle
     import synth
-    if threads:
-        os.environ["OMP_NUM_THREADS"] = str(threads)
-    cores = len(os.sched_getaffinity(0))
     b = rank_batch
     t0 = time.perf_counter()
     pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,

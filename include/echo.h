@@ -68,8 +68,9 @@ enum {
   ECHO_ALGO_QUAD_REG = 2,       /* 4-CTA cluster per row, each CTA a quarter-row in registers, two CTAs (two rows)
                                    per SM, TMA-fed ring, DSMEM merge; exp(z - m) kept as fp16 between the passes
                                    (bf16, vocab <= 155648) -- the B200 design */
-  ECHO_ALGO_QUAD_REG_EXACT = 3  /* as QUAD_REG, but the write-back recomputes exp from the bf16 logits (fp32 end to
+  ECHO_ALGO_QUAD_REG_EXACT = 3, /* as QUAD_REG, but the write-back recomputes exp from the bf16 logits (fp32 end to
                                    end; two exponentials per logit) */
+  ECHO_ALGO_OCT_REG = 4         /* as QUAD_REG with an 8-CTA cluster per row and four CTAs (four rows) per SM */
 };
 
 /* Device-resident result of echo_pack_batch (32 bytes). */

@@ -24,10 +24,11 @@ echo_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ECHO_OK : ECHO_
 // ECHO_ALGO_AUTO -> the 4-CTA register-resident kernel for bf16 Qwen-size vocabularies, the row kernel otherwise;
 // explicit choices are checked for support.
 echo_status resolve_algo(int32_t dtype, int32_t vocab, int32_t* algo) {
-  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_QUAD_REG_EXACT) return ECHO_ERR_INVALID_ARGUMENT;
+  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_OCT_REG) return ECHO_ERR_INVALID_ARGUMENT;
   const bool quad_ok = echo::quad_supports(dtype, vocab);
   if (*algo == ECHO_ALGO_AUTO) *algo = (quad_ok && vocab >= 16384) ? ECHO_ALGO_QUAD_REG : ECHO_ALGO_ROW_L2;
   if ((*algo == ECHO_ALGO_QUAD_REG || *algo == ECHO_ALGO_QUAD_REG_EXACT) && !quad_ok) return ECHO_ERR_UNSUPPORTED;
+  if (*algo == ECHO_ALGO_OCT_REG && !echo::oct_supports(dtype, vocab)) return ECHO_ERR_UNSUPPORTED;
   return ECHO_OK;
 }
 

@@ -217,13 +217,17 @@ ECHO_DEVINL MaxSum maxsum_merge(MaxSum a, MaxSum b) {
   float sb = b.s * ex2((b.m - m) * kLog2e);
   return MaxSum{m, sa + sb};
 }
+// Warp merge with ONE exponential per lane on the critical path: butterfly max, rescale, butterfly sum.
+// (A pairwise-merge butterfly would chain 5 dependent MUFU ops, each queued behind the bulk pass-1b exps of
+// the other warps on the SM.)  IEEE add/max commute, so every lane ends with the same bits.
 ECHO_DEVINL MaxSum warp_maxsum(MaxSum v) {
+  float mx = v.m;
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    MaxSum w{__shfl_xor_sync(0xffffffffu, v.m, o), __shfl_xor_sync(0xffffffffu, v.s, o)};
-    v = maxsum_merge(v, w);
-  }
-  return v;
+  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float t = (v.m == -INFINITY) ? 0.0f : v.s * ex2((v.m - mx) * kLog2e);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return MaxSum{mx, t};
 }
 
 // ---------------------------------------------------------------- the per-row scalar epilogue (4)

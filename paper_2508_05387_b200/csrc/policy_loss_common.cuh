@@ -13,7 +13,7 @@ namespace echo {
 #define ECHO_TRACE_MARK(p, it, k)                                                                   \
   do {                                                                                               \
     if (threadIdx.x == 0 && (p).trace && (it) < (uint32_t)(p).trace_rows && blockIdx.x < 64)         \
-      (p).trace[((size_t)blockIdx.x * (p).trace_rows + (it)) * 8 + (k)] = clock64();                \
+      (p).trace[((size_t)blockIdx.x * (p).trace_rows + (it)) * 16 + (k)] = clock64();                \
   } while (0)
 #else
 #define ECHO_TRACE_MARK(p, it, k) \

@@ -1,6 +1,6 @@
 // policy_loss_quad.cu -- ECHO_ALGO_QUAD_REG / _EXACT: the B200 design of the fused (3)+(4)+(5) kernel.
 //
-// One logits row (V ~ 152k bf16 = 297 KB) is owned by a thread-block cluster of kQCtas = 4 CTAs; CTA r holds
+// One logits row (V ~ 152k bf16 = 297 KB) is owned by a thread-block cluster of C::kCtas = 4 CTAs; CTA r holds
 // the quarter [r q, (r+1) q) of the row (q = ceil(V/4) rounded to 8) in REGISTERS: 8 warps x 32 threads x
 // 19 vectors of 16 B = 76 registers per thread.  Two such CTAs share an SM (registers 2 x 256 x 128 = 64 K,
 // shared memory 2 x 111 KB), so every SM always has two rows in flight: while one CTA waits on its cluster
@@ -28,23 +28,32 @@
 
 namespace echo {
 
-constexpr int kQCtas = 4;                           // CTAs per row (cluster size)
-constexpr int kQWarps = 8;                          // all warps compute; thread 0 also issues the TMA refills
-constexpr int kQThreads = kQWarps * 32;             // 256
-constexpr int kQChunk = kQThreads * 16;             // 4 KB: one 16-byte vector per thread
-constexpr int kQChunkElems = kQChunk / 2;           // 2048 bf16
-constexpr int kQRing = 27;                          // 108 KB staging ring (two CTAs per SM)
-constexpr int kQRegChunks = 19;                     // 19 x 2048 bf16 per CTA: V <= 155648 (Qwen 151936 / 152064)
-constexpr int kQBar = 1;                            // named barrier id
+// Tile configurations: a row is split across kCtas CTAs of kWarps warps; 16 warps per SM (4 per SM
+// sub-partition) leaves 128 registers per thread, of which 76 hold the thread's 19 vectors of the row.
+//   QCfg<4, 8>: 4-CTA cluster, 2 CTAs (2 rows) per SM  -- ECHO_ALGO_QUAD_REG
+//   QCfg<8, 4>: 8-CTA cluster, 4 CTAs (4 rows) per SM  -- ECHO_ALGO_OCT_REG
+template <int kCtas_, int kWarps_>
+struct QCfg {
+  static constexpr int kCtas = kCtas_;                  // CTAs per row (cluster size)
+  static constexpr int kWarps = kWarps_;                // all warps compute; warp 0 also issues the TMA loads
+  static constexpr int kThreads = kWarps * 32;
+  static constexpr int kChunk = kThreads * 16;          // one 16-byte vector per thread
+  static constexpr int kChunkElems = kChunk / 2;
+  static constexpr int kCtasPerSm = 16 / kWarps;
+  static constexpr int kRing = 27;                      // staging ring slots (~1.4 slices)
+  static constexpr int kRegChunks = 19;                 // V <= kCtas * 19 * kChunkElems = 155648
+};
+constexpr int kQBar = 1;                                // named barrier id
 
+template <class C>
 struct __align__(128) QuadSmem {
-  uint8_t ring[kQRing][kQChunk];
+  uint8_t ring[C::kRing][C::kChunk];
   uint64_t full[4];      // per row (it % 4): all chunks of the row landed (one complete_tx per chunk)
   uint64_t consumed[4];  // per row (it % 4): all 8 warps copied the row into registers
   uint64_t xbar[2];
-  uint4 xbuf[2][kQCtas];  // cluster partials {m, s, z_a, -} per row parity and source rank
-  float red_m[kQWarps];
-  float red_s[kQWarps];
+  uint4 xbuf[2][C::kCtas];  // cluster partials {m, s, z_a, -} per row parity and source rank
+  float red_m[C::kWarps];
+  float red_s[C::kWarps];
   float za;
   float coef;
   float lse;
@@ -57,20 +66,22 @@ struct QuadGeom {
   int nchunks;             // ring chunks per row
 };
 
+template <class C>
 ECHO_DEVINL QuadGeom quad_geom(int32_t V, uint32_t rank) {
   QuadGeom g;
-  const int32_t q = ((V + kQCtas - 1) / kQCtas + 7) & ~7;
+  const int32_t q = ((V + C::kCtas - 1) / C::kCtas + 7) & ~7;
   // slices start on 8-column boundaries; a rank past the end gets an empty slice [V8, V8)
   const int32_t v8 = (V + 7) & ~7;
   g.c0 = min((int32_t)rank * q, v8);
   g.c1 = max(min((int32_t)(rank + 1) * q, V), g.c0);
   const int32_t c1r = (g.c1 + 7) & ~7;
   g.slice_bytes = (uint32_t)(c1r - g.c0) * 2u;
-  g.nchunks = (int)((g.slice_bytes + kQChunk - 1) / kQChunk);
+  g.nchunks = (int)((g.slice_bytes + C::kChunk - 1) / C::kChunk);
   return g;
 }
 
 // Issue all chunks of row iteration `it` (one lane per chunk, expect_tx by lane 0 on the row's barrier).
+template <class C>
 ECHO_DEVINL void quad_issue_row(const LossParams& p, const QuadGeom& g, uint32_t cid, uint32_t ncl, uint32_t it,
                                 int lane, uint32_t full0, uint32_t ring0, uint64_t pol) {
   const uint32_t bar = full0 + 8 * (it & 3u);
@@ -78,22 +89,22 @@ ECHO_DEVINL void quad_issue_row(const LossParams& p, const QuadGeom& g, uint32_t
   const int64_t row = (int64_t)cid + (int64_t)it * ncl;
   const uint8_t* src = p.logits + row * p.ld_bytes + (int64_t)g.c0 * 2;
   for (int c = lane; c < g.nchunks; c += 32) {
-    const uint32_t slot = (it * (uint32_t)g.nchunks + c) % kQRing;
-    const uint32_t nb = min((uint32_t)kQChunk, g.slice_bytes - (uint32_t)c * kQChunk);
-    bulk_g2s(ring0 + slot * kQChunk, src + (int64_t)c * kQChunk, nb, bar, pol);
+    const uint32_t slot = (it * (uint32_t)g.nchunks + c) % C::kRing;
+    const uint32_t nb = min((uint32_t)C::kChunk, g.slice_bytes - (uint32_t)c * C::kChunk);
+    bulk_g2s(ring0 + slot * C::kChunk, src + (int64_t)c * C::kChunk, nb, bar, pol);
   }
 }
 
-template <bool kStoreExp>
-__global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
+template <class C, bool kStoreExp>
+__global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, C::kCtasPerSm)
     policy_loss_quad_kernel(const LossParams p) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  QuadSmem& sm = *reinterpret_cast<QuadSmem*>(smem_raw);
+  QuadSmem<C>& sm = *reinterpret_cast<QuadSmem<C>*>(smem_raw);
   const uint32_t rank = cluster_ctarank();
   const uint32_t cid = cluster_id_x(), ncl = nclusters_x();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int32_t V = p.V;
-  const QuadGeom g = quad_geom(V, rank);
+  const QuadGeom g = quad_geom<C>(V, rank);
   const int nchunks = g.nchunks;
   const int32_t c0 = g.c0, c1 = g.c1;
   const uint32_t full0 = smem_u32(&sm.full[0]), cons0 = smem_u32(&sm.consumed[0]), ring0 = smem_u32(&sm.ring[0][0]);
@@ -102,7 +113,7 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
   if (tid == 0) {
     for (int i = 0; i < 4; ++i) {
       mbar_init(full0 + 8 * i, 1);
-      mbar_init(cons0 + 8 * i, kQWarps);
+      mbar_init(cons0 + 8 * i, C::kWarps);
     }
     mbar_init(smem_u32(&sm.xbar[0]), 1);
     mbar_init(smem_u32(&sm.xbar[1]), 1);
@@ -111,38 +122,46 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
   cluster_sync_all();
 
   const uint64_t ld_pol = policy_evict_first();
-  if (warp == 0 && my_rows > 0 && nchunks > 0) quad_issue_row(p, g, cid, ncl, 0, lane, full0, ring0, ld_pol);
+  if (warp == 0 && my_rows > 0 && nchunks > 0) quad_issue_row<C>(p, g, cid, ncl, 0, lane, full0, ring0, ld_pol);
 
-  uint32_t xbuf_remote[kQCtas], xbar_remote[kQCtas];
+  uint32_t xbuf_remote[C::kCtas], xbar_remote[C::kCtas];
 #pragma unroll
-  for (int r = 0; r < kQCtas; ++r) {
+  for (int r = 0; r < C::kCtas; ++r) {
     xbuf_remote[r] = mapa(smem_u32(&sm.xbuf[0][rank]), r);
     xbar_remote[r] = mapa(smem_u32(&sm.xbar[0]), r);
   }
   const uint64_t st_pol = policy_evict_first();
   const float gscale = (float)((double)p.grad_scale / *p.n_global);
   const int32_t col_t = c0 + tid * 8;
-  const bool last_valid = (uint32_t)(nchunks - 1) * kQChunk + (uint32_t)tid * 16u < g.slice_bytes;
-  const bool has_tail = (c1 & 7) && (c1 & ~7) >= col_t && ((c1 & ~7) - col_t) % kQChunkElems == 0;
+  const bool last_valid = (uint32_t)(nchunks - 1) * C::kChunk + (uint32_t)tid * 16u < g.slice_bytes;
+  const bool has_tail = (c1 & 7) && (c1 & ~7) >= col_t && ((c1 & ~7) - col_t) % C::kChunkElems == 0;
   const int nstore = nchunks - (last_valid ? 0 : 1) - (has_tail ? 1 : 0);
   const uint64_t l2e2 = f2(kLog2e, kLog2e);
   const uint32_t my_off = (uint32_t)tid * 16u;
   uint32_t it = 0;
 
+  // per-row metadata is loaded one row ahead so its global-load latency never sits on the critical path
+  int32_t a_next = my_rows > 0 ? p.tok_action[cid] : 0;
+  RowMeta meta_next{0.f, 0.f, 0.f};
+  if (tid == 0 && my_rows > 0) meta_next = load_meta(p, cid);
   for (int64_t row = cid; row < p.n_rows; row += ncl, ++it) {
-    const int32_t a = p.tok_action[row];
-    RowMeta meta{0.f, 0.f, 0.f};
-    if (tid == 0) meta = load_meta(p, row);
+    const int32_t a = a_next;
+    const RowMeta meta = meta_next;
+    if (it + 1 < my_rows) {
+      a_next = p.tok_action[row + ncl];
+      if (tid == 0) meta_next = load_meta(p, row + ncl);
+    }
 
     ECHO_TRACE_MARK(p, it, 0);
     // ---- pass 1a: one wait for the whole row, then ring -> registers; each warp marks the row consumed
-    uint4 v[kQRegChunks];
+    uint4 v[C::kRegChunks];
     if (nchunks > 0) mbar_wait(full0 + 8 * (it & 3u), (it >> 2) & 1u);
+    ECHO_TRACE_MARK(p, it, 8);
 #pragma unroll
-    for (int c = 0; c < kQRegChunks; ++c) {
+    for (int c = 0; c < C::kRegChunks; ++c) {
       if (c < nchunks) {
-        const uint32_t slot = (it * (uint32_t)nchunks + c) % kQRing;
-        uint4 w = lds_v4(ring0 + slot * kQChunk + my_off);
+        const uint32_t slot = (it * (uint32_t)nchunks + c) % C::kRing;
+        uint4 w = lds_v4(ring0 + slot * C::kChunk + my_off);
         if (c == nchunks - 1) {
           if (!last_valid) w = make_uint4(kBf16NegInf2, kBf16NegInf2, kBf16NegInf2, kBf16NegInf2);
           if (has_tail) w = mask_tail(w, c1 & 7);
@@ -153,26 +172,28 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
       }
     }
     __syncwarp();
+    ECHO_TRACE_MARK(p, it, 9);
     if (lane == 0) mbar_arrive(cons0 + 8 * (it & 3u));
     // warp 0 streams the next row into the slots just released (its chunks only overlap rows <= it)
     if (warp == 0 && it + 1 < my_rows && nchunks > 0) {
       if (lane == 0) mbar_wait(cons0 + 8 * (it & 3u), (it >> 2) & 1u);
       __syncwarp();
-      quad_issue_row(p, g, cid, ncl, it + 1, lane, full0, ring0, ld_pol);
+      quad_issue_row<C>(p, g, cid, ncl, it + 1, lane, full0, ring0, ld_pol);
     }
+    ECHO_TRACE_MARK(p, it, 10);
     __syncwarp();
 
     ECHO_TRACE_MARK(p, it, 1);
     uint32_t mx2 = kBf16NegInf2;
 #pragma unroll
-    for (int c = 0; c < kQRegChunks; ++c) mx2 = bmax2(mx2, bmax2(bmax2(v[c].x, v[c].y), bmax2(v[c].z, v[c].w)));
+    for (int c = 0; c < C::kRegChunks; ++c) mx2 = bmax2(mx2, bmax2(bmax2(v[c].x, v[c].y), bmax2(v[c].z, v[c].w)));
     const float mx = fmaxf(__uint_as_float(mx2 << 16), __uint_as_float(mx2 & 0xFFFF0000u));
-    const bool own_a = a >= col_t && a < c1 && ((a - col_t) % kQChunkElems) < 8;
+    const bool own_a = a >= col_t && a < c1 && ((a - col_t) % C::kChunkElems) < 8;
     if (own_a) {
-      const int ca = (a - col_t) / kQChunkElems, ea = (a - col_t) % kQChunkElems;
+      const int ca = (a - col_t) / C::kChunkElems, ea = (a - col_t) % C::kChunkElems;
       uint32_t word = 0;
 #pragma unroll
-      for (int c = 0; c < kQRegChunks; ++c)
+      for (int c = 0; c < C::kRegChunks; ++c)
         if (c == ca) word = (ea >> 1) == 0 ? v[c].x : (ea >> 1) == 1 ? v[c].y : (ea >> 1) == 2 ? v[c].z : v[c].w;
       sm.za = (ea & 1) ? __uint_as_float(word & 0xFFFF0000u) : __uint_as_float(word << 16);
     }
@@ -182,7 +203,7 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
     const uint64_t nmb2 = f2(-mb, -mb);
     uint64_t s2 = f2(0.0f, 0.0f);
 #pragma unroll
-    for (int c = 0; c < kQRegChunks; ++c) {
+    for (int c = 0; c < C::kRegChunks; ++c) {
       if (c < nchunks) {
         uint32_t* w = &v[c].x;
 #pragma unroll
@@ -198,40 +219,50 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
     }
     float slo, shi;
     f2split(s2, slo, shi);
+    ECHO_TRACE_MARK(p, it, 11);
     const MaxSum acc = warp_maxsum(MaxSum{mx, slo + shi});
     if (lane == 0) {
       sm.red_m[warp] = acc.m;
       sm.red_s[warp] = acc.s;
     }
     ECHO_TRACE_MARK(p, it, 2);
-    named_bar_sync(kQBar, kQThreads);
+    named_bar_sync(kQBar, C::kThreads);
     ECHO_TRACE_MARK(p, it, 3);
 
     // ---- CTA merge (warp 0), cluster merge (st.async to every peer), epilogue (lane 0)
     if (warp == 0) {
-      MaxSum mine = lane < kQWarps ? MaxSum{sm.red_m[lane], sm.red_s[lane]} : MaxSum{-INFINITY, 0.0f};
+      MaxSum mine = lane < C::kWarps ? MaxSum{sm.red_m[lane], sm.red_s[lane]} : MaxSum{-INFINITY, 0.0f};
       mine = warp_maxsum(mine);
+      ECHO_TRACE_MARK(p, it, 12);
       if (lane == 0) {
         const uint32_t par = it & 1u;
         const bool owner = (a >= c0 && a < c1);
         const uint4 msg = make_uint4(__float_as_uint(mine.m), __float_as_uint(mine.s),
                                      __float_as_uint(owner ? sm.za : 0.0f), owner ? 1u : 0u);
         const uint32_t xbar_local = smem_u32(&sm.xbar[par]);
-        mbar_arrive_expect_tx(xbar_local, 16 * kQCtas);
+        mbar_arrive_expect_tx(xbar_local, 16 * C::kCtas);
 #pragma unroll
-        for (int r = 0; r < kQCtas; ++r)
-          st_async_v4(xbuf_remote[r] + par * (16u * kQCtas), msg, xbar_remote[r] + par * 8u);
+        for (int r = 0; r < C::kCtas; ++r)
+          st_async_v4(xbuf_remote[r] + par * (16u * C::kCtas), msg, xbar_remote[r] + par * 8u);
+        ECHO_TRACE_MARK(p, it, 6);
         mbar_wait_cluster(xbar_local, (it >> 1) & 1u);
-        MaxSum tot{-INFINITY, 0.0f};
-        float za = NAN;
+        ECHO_TRACE_MARK(p, it, 7);
+        // cluster merge in rank order: max first, then the rescaled sum (the exps are independent)
+        float za = NAN, mm = -INFINITY;
+        uint4 msgs[C::kCtas];
 #pragma unroll
-        for (int r = 0; r < kQCtas; ++r) {
-          const uint4 m = sm.xbuf[par][r];
-          tot = r == 0 ? MaxSum{__uint_as_float(m.x), __uint_as_float(m.y)}
-                       : maxsum_merge(tot, MaxSum{__uint_as_float(m.x), __uint_as_float(m.y)});
-          if (m.w) za = __uint_as_float(m.z);
+        for (int r = 0; r < C::kCtas; ++r) {
+          msgs[r] = sm.xbuf[par][r];
+          mm = fmaxf(mm, __uint_as_float(msgs[r].x));
+          if (msgs[r].w) za = __uint_as_float(msgs[r].z);
         }
-        const float lse = tot.m + logf(tot.s);
+        float ss = 0.0f;
+#pragma unroll
+        for (int r = 0; r < C::kCtas; ++r) {
+          const float mr = __uint_as_float(msgs[r].x);
+          ss += (mr == -INFINITY) ? 0.0f : __uint_as_float(msgs[r].y) * ex2((mr - mm) * kLog2e);
+        }
+        const float lse = mm + logf(ss);
         if (a < 0 || a >= V) za = NAN;
         const RowScalars r = row_epilogue_f(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high,
                                             p.kl_coef, gscale);
@@ -246,7 +277,7 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
         sm.da = fmaf(-r.coef, pa, r.coef);
       }
     }
-    named_bar_sync(kQBar, kQThreads);
+    named_bar_sync(kQBar, C::kThreads);
     ECHO_TRACE_MARK(p, it, 4);
     const float coef = sm.coef, lse = sm.lse;
 
@@ -257,7 +288,7 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
     uint8_t* const row_base = p.logits + row * p.ld_bytes;
     uint8_t* const dst = row_base + (int64_t)col_t * 2;
 #pragma unroll
-    for (int c = 0; c < kQRegChunks; ++c) {
+    for (int c = 0; c < C::kRegChunks; ++c) {
       if (c < nchunks) {
         uint32_t* w = &v[c].x;
 #pragma unroll
@@ -273,9 +304,9 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
           w[k] = pack_bf16x2(d0, d1);
         }
         if (c < nstore)
-          stg_v4_hint(dst + (int64_t)c * kQChunk, v[c], st_pol);
+          stg_v4_hint(dst + (int64_t)c * C::kChunk, v[c], st_pol);
         else if (has_tail && c == nchunks - 1)
-          store_partial8(reinterpret_cast<__nv_bfloat16*>(dst + (int64_t)c * kQChunk), v[c], c1 & 7);
+          store_partial8(reinterpret_cast<__nv_bfloat16*>(dst + (int64_t)c * C::kChunk), v[c], c1 & 7);
       }
     }
     ECHO_TRACE_MARK(p, it, 5);
@@ -284,30 +315,40 @@ __global__ void __cluster_dims__(kQCtas, 1, 1) __launch_bounds__(kQThreads, 2)
   cluster_sync_all();
 }
 
-bool quad_supports(int32_t dtype, int32_t V) {
-  if (dtype != ECHO_BF16 || V < 8 * kQCtas) return false;
-  const int32_t q = ((V + kQCtas - 1) / kQCtas + 7) & ~7;
-  return ((int64_t)q * 2 + kQChunk - 1) / kQChunk <= kQRegChunks;
+template <class C>
+static bool supports_t(int32_t dtype, int32_t V) {
+  if (dtype != ECHO_BF16 || V < 8 * C::kCtas) return false;
+  const int32_t q = ((V + C::kCtas - 1) / C::kCtas + 7) & ~7;
+  return ((int64_t)q * 2 + C::kChunk - 1) / C::kChunk <= C::kRegChunks;
 }
 
-template <bool kStoreExp>
-static cudaError_t launch_quad_t(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
-  const size_t smem = sizeof(QuadSmem);
-  const void* fn = (const void*)policy_loss_quad_kernel<kStoreExp>;
+template <class C, bool kStoreExp>
+static cudaError_t launch_t(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  const size_t smem = sizeof(QuadSmem<C>);
+  const void* fn = (const void*)policy_loss_quad_kernel<C, kStoreExp>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  int64_t clusters = max_active_clusters(fn, kQThreads, smem, kQCtas, num_sms * 2 / kQCtas);
+  int64_t clusters = max_active_clusters(fn, C::kThreads, smem, C::kCtas, num_sms * C::kCtasPerSm / C::kCtas);
   if (clusters > p.n_rows) clusters = p.n_rows;
   if (shape) {
-    *shape = LaunchShape{(int32_t)(clusters * kQCtas), kQCtas, kQThreads, (int32_t)smem};
+    *shape = LaunchShape{(int32_t)(clusters * C::kCtas), C::kCtas, C::kThreads, (int32_t)smem};
     return cudaSuccess;
   }
-  policy_loss_quad_kernel<kStoreExp><<<(unsigned)(clusters * kQCtas), kQThreads, smem, stream>>>(p);
+  policy_loss_quad_kernel<C, kStoreExp><<<(unsigned)(clusters * C::kCtas), C::kThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
+using Quad = QCfg<4, 8>;
+using Oct = QCfg<8, 4>;
+
+bool quad_supports(int32_t dtype, int32_t V) { return supports_t<Quad>(dtype, V); }
+bool oct_supports(int32_t dtype, int32_t V) { return supports_t<Oct>(dtype, V); }
+
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape) {
-  return store_exp ? launch_quad_t<true>(p, stream, num_sms, shape) : launch_quad_t<false>(p, stream, num_sms, shape);
+  return store_exp ? launch_t<Quad, true>(p, stream, num_sms, shape) : launch_t<Quad, false>(p, stream, num_sms, shape);
+}
+cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  return launch_t<Oct, true>(p, stream, num_sms, shape);
 }
 
 }  // namespace echo

@@ -101,9 +101,9 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
       s_s[warp] = acc.s;
     }
     __syncthreads();
+    MaxSum tot{-INFINITY, 0.0f};
+    if (warp == 0) tot = warp_maxsum(MaxSum{s_m[lane], s_s[lane]});  // kRWarps == 32: one lane per warp
     if (tid == 0) {
-      MaxSum tot{s_m[0], s_s[0]};
-      for (int w = 1; w < kRWarps; ++w) tot = maxsum_merge(tot, MaxSum{s_m[w], s_s[w]});
       const float lse = tot.m + logf(tot.s);
       const float za = (a < 0 || a >= V) ? NAN : s_za;
       const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high, p.kl_coef,

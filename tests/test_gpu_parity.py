@@ -16,7 +16,7 @@ from _util import check_rows, coef_slack, host_rows, oracle_step, pow2_scale_for
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = {"row_l2": 1, "quad_reg": 2, "quad_reg_exact": 3}
+ALGOS = {"row_l2": 1, "quad_reg": 2, "quad_reg_exact": 3, "oct_reg": 4}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -206,7 +206,8 @@ def _uniform_case(V, dtype, algo):
 
 
 @pytest.mark.parametrize("V,dtype,algo", [(1024, "f32", 1), (151936, "bf16", 1), (151936, "bf16", 2),
-                                          (152064, "bf16", 2), (151936, "bf16", 3), (152064, "bf16", 3)])
+                                          (152064, "bf16", 2), (151936, "bf16", 3), (152064, "bf16", 3),
+                                          (151936, "bf16", 4), (152064, "bf16", 4)])
 def test_uniform_rows_give_minus_log_v(V, dtype, algo):
     """Closed form (SPEC.md :202): uniform logits give logp = -ln V; the GPU is within 2 fp32 ulp."""
     _, logp = _uniform_case(V, dtype, algo)
@@ -215,7 +216,7 @@ def test_uniform_rows_give_minus_log_v(V, dtype, algo):
     assert np.all(np.abs(logp - target) <= 2 * ulp), (logp, target)
 
 
-@pytest.mark.parametrize("algo", [1, 2, 3])
+@pytest.mark.parametrize("algo", [1, 2, 3, 4])
 def test_clip_saturation_and_two_call_ratio(algo):
     """old == new (two-call protocol) gives rho = 1 exactly and c = -A s/N; clip saturation zeroes whole rows."""
     cfg = synth.CONFIGS["qwen3-4b"]
@@ -244,7 +245,7 @@ def test_clip_saturation_and_two_call_ratio(algo):
     assert torch.count_nonzero(work[nz]) == 0
 
 
-@pytest.mark.parametrize("algo", [1, 2, 3])
+@pytest.mark.parametrize("algo", [1, 2, 3, 4])
 def test_determinism_and_microbatch_invariance(algo):
     cfg = synth.CONFIGS["qwen3-4b"]
     b = synth.make_batch(cfg, 0, 2 * cfg.G)
@@ -262,7 +263,7 @@ def test_determinism_and_microbatch_invariance(algo):
 
 
 @pytest.mark.parametrize("name", ["qwen3-4b", "qwen2.5-7b", "qwen3-32b", "qwen3-30b-a3b"])
-@pytest.mark.parametrize("algo_name", ["quad_reg", "quad_reg_exact", "row_l2"])
+@pytest.mark.parametrize("algo_name", ["quad_reg", "quad_reg_exact", "oct_reg", "row_l2"])
 def test_full_config_sampled_rows(name, algo_name):
     """BASELINE.json full sizes, the bench's micro-batch (32768 rows) and launch configuration: sampled rows
     of the first and the last micro-batch against the oracle, plus the row-sum invariant on every row."""
@@ -311,7 +312,7 @@ def test_full_config_sampled_rows(name, algo_name):
 def test_nonfinite_rows_flagged():
     from paper_2508_05387_b200 import abi
     V = 4096
-    for dtype, algo in (("bf16", 1), ("bf16", 2), ("bf16", 3), ("f32", 1)):
+    for dtype, algo in (("bf16", 1), ("bf16", 2), ("bf16", 3), ("bf16", 4), ("f32", 1)):
         dt = torch.bfloat16 if dtype == "bf16" else torch.float32
         z = torch.zeros(6, V, dtype=dt, device="cuda")
         z[0, 3] = float("nan")
@@ -334,7 +335,7 @@ def test_nonfinite_rows_flagged():
 
 @pytest.mark.parametrize("V,ld,algo", [(1000, 1008, 1), (1001, 1008, 1), (151935, 151936, 1), (151935, 151936, 2),
                                        (40001, 40008, 2), (40001, 40008, 3), (155648, 155648, 2), (33, 40, 2),
-                                       (32768, 32768, 3)])
+                                       (32768, 32768, 3), (151935, 151936, 4), (40001, 40008, 4), (65, 72, 4)])
 def test_ragged_vocab_and_padding_untouched(V, ld, algo):
     """V not a multiple of the 8-element vector: tail handling; columns V..ld-1 are never written."""
     from paper_2508_05387_b200 import abi

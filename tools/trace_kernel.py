@@ -48,7 +48,7 @@ def main():
     M = min(args.rows, info.n_tokens)
     logits = torch.empty(M, cfg.V, dtype=torch.bfloat16, device="cuda")
     rows_cap = 1024
-    trace = torch.zeros(64 * rows_cap * 8, dtype=torch.int64, device="cuda")
+    trace = torch.zeros(64 * rows_cap * 16, dtype=torch.int64, device="cuda")
     out = {}
     for name in args.algos.split(","):
         algo = abi.ALGO_NAMES[name]
@@ -64,12 +64,21 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             abi._lib.echo_trace_set(None, 0)
-        t = trace.view(64, rows_cap, 8).cpu().numpy().astype(np.float64)
+        t = trace.view(64, rows_cap, 16).cpu().numpy().astype(np.float64)
         valid = (t[:, :, 0] > 0) & (t[:, :, 5] > 0)
         ph = {}
         for k, lab in ((1, "pass1a"), (2, "max+pass1b"), (3, "barrier1"), (4, "merge+epilogue"), (5, "pass2")):
             d = (t[:, :, k] - t[:, :, k - 1])[valid]
             ph[lab] = float(d.mean())
+        if (t[:, :, 6] > 0).any():
+            ph["merge:before_send"] = float((t[:, :, 6] - t[:, :, 3])[valid].mean())
+            ph["merge:wait_peers"] = float((t[:, :, 7] - t[:, :, 6])[valid].mean())
+            ph["merge:after_wait"] = float((t[:, :, 4] - t[:, :, 7])[valid].mean())
+        if (t[:, :, 12] > 0).any():
+            for lab, k0, k1 in (("1a:wait_full", 0, 8), ("1a:lds", 8, 9), ("1a:consumed+tma", 9, 10),
+                                ("1b:exp_loop", 10, 11), ("1b:warp_reduce", 11, 2), ("merge:cta_reduce", 3, 12),
+                                ("merge:send", 12, 6)):
+                ph[lab] = float((t[:, :, k1] - t[:, :, k0])[valid].mean())
         nxt = (t[:, 1:, 0] - t[:, :-1, 5])[valid[:, 1:] & valid[:, :-1]]
         ph["loop"] = float(nxt.mean()) if nxt.size else 0.0
         rowt = (t[:, 1:, 0] - t[:, :-1, 0])[valid[:, 1:] & valid[:, :-1]]
