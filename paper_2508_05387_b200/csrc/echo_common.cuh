@@ -166,6 +166,10 @@ ECHO_DEVINL void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_
       : "memory");
 }
 
+// Order this thread's earlier generic-proxy shared-memory accesses (and, after a CTA barrier, those of the
+// threads it synchronised with) before its subsequent async-proxy (TMA) accesses.
+ECHO_DEVINL void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // ---------------------------------------------------------------- clusters / DSMEM
 ECHO_DEVINL uint32_t cluster_ctarank() {
   uint32_t r;

@@ -49,7 +49,7 @@ template <class C>
 struct __align__(128) QuadSmem {
   uint8_t ring[C::kRing][C::kChunk];
   uint64_t full[4];      // per row (it % 4): all chunks of the row landed (one complete_tx per chunk)
-  uint64_t consumed[4];  // per row (it % 4): all 8 warps copied the row into registers
+
   uint64_t xbar[2];
   uint4 xbuf[2][C::kCtas];  // cluster partials {m, s, z_a, -} per row parity and source rank
   float red_m[C::kWarps];
@@ -107,13 +107,13 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
   const QuadGeom g = quad_geom<C>(V, rank);
   const int nchunks = g.nchunks;
   const int32_t c0 = g.c0, c1 = g.c1;
-  const uint32_t full0 = smem_u32(&sm.full[0]), cons0 = smem_u32(&sm.consumed[0]), ring0 = smem_u32(&sm.ring[0][0]);
+  const uint32_t full0 = smem_u32(&sm.full[0]), ring0 = smem_u32(&sm.ring[0][0]);
   const uint32_t my_rows = p.n_rows > (int64_t)cid ? (uint32_t)((p.n_rows - 1 - cid) / ncl + 1) : 0u;
 
   if (tid == 0) {
     for (int i = 0; i < 4; ++i) {
       mbar_init(full0 + 8 * i, 1);
-      mbar_init(cons0 + 8 * i, C::kWarps);
+
     }
     mbar_init(smem_u32(&sm.xbar[0]), 1);
     mbar_init(smem_u32(&sm.xbar[1]), 1);
@@ -153,7 +153,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     }
 
     ECHO_TRACE_MARK(p, it, 0);
-    // ---- pass 1a: one wait for the whole row, then ring -> registers; each warp marks the row consumed
+    // ---- pass 1a: one wait for the whole row, then ring -> registers
     uint4 v[C::kRegChunks];
     if (nchunks > 0) mbar_wait(full0 + 8 * (it & 3u), (it >> 2) & 1u);
     ECHO_TRACE_MARK(p, it, 8);
@@ -173,15 +173,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     }
     __syncwarp();
     ECHO_TRACE_MARK(p, it, 9);
-    if (lane == 0) mbar_arrive(cons0 + 8 * (it & 3u));
-    // warp 0 streams the next row into the slots just released (its chunks only overlap rows <= it)
-    if (warp == 0 && it + 1 < my_rows && nchunks > 0) {
-      if (lane == 0) mbar_wait(cons0 + 8 * (it & 3u), (it >> 2) & 1u);
-      __syncwarp();
-      quad_issue_row<C>(p, g, cid, ncl, it + 1, lane, full0, ring0, ld_pol);
-    }
     ECHO_TRACE_MARK(p, it, 10);
-    __syncwarp();
 
     ECHO_TRACE_MARK(p, it, 1);
     uint32_t mx2 = kBf16NegInf2;
@@ -228,6 +220,12 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     ECHO_TRACE_MARK(p, it, 2);
     named_bar_sync(kQBar, C::kThreads);
     ECHO_TRACE_MARK(p, it, 3);
+    // every warp has copied row `it` out of the ring: warp 1 streams row it+1 into the slots (its chunks only
+    // overlap rows <= it), off the critical path of warp 0's merge
+    if (warp == 1 % C::kWarps && it + 1 < my_rows && nchunks > 0) {
+      fence_proxy_async_smem();
+      quad_issue_row<C>(p, g, cid, ncl, it + 1, lane, full0, ring0, ld_pol);
+    }
 
     // ---- CTA merge (warp 0), cluster merge (st.async to every peer), epilogue (lane 0)
     if (warp == 0) {
