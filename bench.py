@@ -331,6 +331,24 @@ def main_echo(args):
         "nonfinite_tokens": nonfinite,
         "loss": recs[-1]["loss"],
     }
+    # forward-only log-probs over the same micro-batch (read-only: half the traffic)
+    f1 = []
+    f1_lp = torch.empty(M, dtype=torch.float32, device=dev)
+    for r in range(6):
+        sgpu.fill_logits(logits, dtype=cfg.dtype, vocab=cfg.V, row0=0, tok_slot=st.tok_slot, tok_action=st.tok_action,
+                         kept_rollout=st.kept_rollout, kept_offset=st.kept_offset, max_len=cfg.S, seed=cfg.seed)
+        flush.fill_(float(r))
+        a0 = ev()
+        abi.echo_token_logp(logits, st.edtype, M, cfg.V, ld, st.tok_action, f1_lp)
+        a1 = ev()
+        torch.cuda.synchronize()
+        if r >= 2:
+            f1.append(a0.elapsed_time(a1))
+    f1_ms = statistics.median(f1)
+    f1_bpt = cfg.V * esize + 4 + 4    # read the row once + action in + logp out
+    line["f1_token_logp"] = {"ms_per_micro_batch": f1_ms, "tokens_per_s_per_gpu": M / (f1_ms * 1e-3),
+                             "achieved_GBps": f1_bpt * M / (f1_ms * 1e-3) / 1e9, "bytes_per_token": f1_bpt,
+                             "frac": f1_bpt * M / (f1_ms * 1e-3) / 1e9 / peak}
     if world == 1 and not args.no_cpu_baseline:
         r = oracle_rate(cfg, b, toks_all / args.steps, args.cpu_seconds)
         line["cpu_baseline"] = {

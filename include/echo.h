@@ -164,6 +164,17 @@ ECHO_API echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, in
                                         float* tok_logp, float* tok_loss, uint8_t* tok_flags, int32_t algo,
                                         void* stream);
 
+/*
+ * Forward-only token log-probs: logp_t = z[t,a_t] - logsumexp_v z[t,v] (PAPER.md :170), the
+ * quantity a trainer recomputes for old_logp (the behaviour policy, PAPER.md :162) and for ref_logp (the KL
+ * reference, PAPER.md :278).  Same layout rules as echo_policy_loss_fwd_bwd; the logits are only READ (one HBM
+ * pass, half the traffic of the fused kernel).  tok_lse (per-row log-sum-exp) and tok_flags
+ * (ECHO_FLAG_NONFINITE) are nullable.  Launches: 1 kernel (0 when n_rows == 0).
+ */
+ECHO_API echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
+                                     const int32_t* tok_action, float* tok_logp, float* tok_lse, uint8_t* tok_flags,
+                                     void* stream);
+
 /* Launch shape echo_policy_loss_fwd_bwd_ex would use on the current device (no launch):
  * shape[5] = {resolved algo, grid CTAs, CTAs per cluster, threads per CTA, dynamic smem bytes}. */
 ECHO_API echo_status echo_policy_loss_launch_shape(int32_t dtype, int64_t n_rows, int32_t vocab, int32_t algo,

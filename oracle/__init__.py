@@ -56,6 +56,8 @@ def lib():
         _lib.echo_ref_policy_loss.argtypes = [i64, i32, i64, i32, P, P, P, P, P, P, f64, f32, f32, f32, f32,
                                               P, P, P, P, P, P]
         _lib.echo_ref_policy_loss.restype = ctypes.c_int
+        _lib.echo_ref_token_logp.argtypes = [i64, i32, i64, i32, P, P, P, P, P]
+        _lib.echo_ref_token_logp.restype = ctypes.c_int
         _lib.echo_ref_scaled_loss.argtypes = [i64, i32, i64, P, P, P, P, P, P, f64, f32, f32, f32, f32]
         _lib.echo_ref_scaled_loss.restype = f64
     return _lib
@@ -174,6 +176,23 @@ def policy_loss(logits, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_g
     if rc != 0:
         raise ValueError("echo_ref_policy_loss: invalid argument")
     return LossOut(logp, loss, flags, coef, d, stats)
+
+
+def token_logp(logits, tok_action, *, vocab=None, dtype=None):
+    """f1: forward-only (logp, lse, flags) per row of ``logits`` (float32 or bf16 bit patterns)."""
+    if dtype is None:
+        dtype = F32 if logits.dtype == np.float32 else BF16
+    logits = np.ascontiguousarray(logits)
+    n, ld = logits.shape
+    V = ld if vocab is None else int(vocab)
+    logp = np.zeros(n, np.float64)
+    lse = np.zeros(n, np.float64)
+    flags = np.zeros(n, np.uint8)
+    rc = lib().echo_ref_token_logp(n, V, ld, dtype, _p(logits), _p(_c(tok_action, np.int32)), _p(logp), _p(lse),
+                                   _p(flags))
+    if rc != 0:
+        raise ValueError("echo_ref_token_logp: invalid argument")
+    return logp, lse, flags
 
 
 def scaled_loss(logits_f64, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, clip_low=0.2,

@@ -331,6 +331,35 @@ int echo_ref_policy_loss(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtyp
   return REF_OK;
 }
 
+/* ======================================================================================
+ * f1: forward-only token log-probs, the log pi_theta(a|s) field of PAPER.md :170 that a
+ * trainer recomputes for old_logp (PAPER.md :162) and ref_logp (KL reference, PAPER.md :278):
+ *   lse_t = m + log sum_v exp(z_v - m),  m = max_v z_v;   logp_t = z[t, a_t] - lse_t
+ * flags bit1 = non-finite (lse or logp not a finite fp32 value), as in echo_ref_policy_loss.
+ * ====================================================================================== */
+int echo_ref_token_logp(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtype, const void* logits,
+                        const int32_t* tok_action, double* tok_logp, double* tok_lse, uint8_t* tok_flags) {
+  if (n_rows < 0 || vocab < 1 || ld < vocab || (dtype != 0 && dtype != 1)) return REF_ERR_INVALID_ARGUMENT;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < n_rows; ++t) {
+    double m = -INFINITY;
+    int has_nan = 0;
+    for (int64_t v = 0; v < vocab; ++v) {
+      double z = logit_at(logits, dtype, ld, t, v);
+      if (isnan(z)) has_nan = 1;
+      if (z > m) m = z;
+    }
+    double s = 0.0;
+    for (int64_t v = 0; v < vocab; ++v) s = s + exp(logit_at(logits, dtype, ld, t, v) - m);
+    double lse = (has_nan || !isfinite(m)) ? NAN : m + log(s);
+    double logp = logit_at(logits, dtype, ld, t, tok_action[t]) - lse;
+    tok_logp[t] = logp;
+    if (tok_lse) tok_lse[t] = lse;
+    if (tok_flags) tok_flags[t] = (uint8_t)((fits_f32(lse) && fits_f32(logp)) ? 0 : 2);
+  }
+  return REF_OK;
+}
+
 /* Scalar loss of a set of rows as a function of the logits, for finite-difference pins of (5):
  * returns (1/N_global) * sum_t l_t * grad_scale, i.e. the quantity whose gradient dlogits is. */
 double echo_ref_scaled_loss(int64_t n_rows, int32_t vocab, int64_t ld, const double* logits,

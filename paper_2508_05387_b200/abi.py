@@ -24,10 +24,11 @@ ALGO_NAMES = {"auto": 0, "row_l2": 1, "quad_reg": 2, "quad_reg_exact": 3, "oct_r
 PACK_RESULT_BYTES = 32
 
 # kernels launched per call (for the bench's gpu_launches count)
-LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2}
+LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2,
+            "echo_token_logp": 1}
 
 EXPORTS = ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
-           "echo_policy_loss_launch_shape",
+           "echo_policy_loss_launch_shape", "echo_token_logp",
            "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_status_string", "echo_abi_version")
 
 
@@ -50,6 +51,8 @@ def _load(path=LIB_PATH):
                                                 i32, P]
     lib.echo_loss_stats.argtypes = [i64, P, P, P, P, P, P, P, P]
     lib.echo_policy_loss_launch_shape.argtypes = [i32, i64, i32, i32, P]
+    lib.echo_token_logp.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P]
+    lib.echo_token_logp.restype = ctypes.c_int
     lib.echo_policy_loss_launch_shape.restype = ctypes.c_int
     lib.echo_loss_stats_workspace_bytes.argtypes = []
     lib.echo_loss_stats_workspace_bytes.restype = ctypes.c_size_t
@@ -124,6 +127,12 @@ def echo_policy_loss_fwd_bwd(logits, dtype, n_rows, vocab, ld, tok_action, tok_o
             _p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot),
             _p(adv_slot), _p(n_global), clip_low, clip_high, kl_coef, grad_scale, _p(tok_logp), _p(tok_loss),
             _p(tok_flags), algo, _s(stream)))
+
+
+def echo_token_logp(logits, dtype, n_rows, vocab, ld, tok_action, tok_logp, tok_lse=None, tok_flags=None,
+                    stream=None):
+    _check("echo_token_logp", _lib.echo_token_logp(_p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_logp),
+                                                   _p(tok_lse), _p(tok_flags), _s(stream)))
 
 
 def echo_policy_loss_launch_shape(dtype, n_rows, vocab, algo=ECHO_ALGO_AUTO) -> dict:

@@ -137,6 +137,7 @@ echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_r
   p.tok_logp = tok_logp;
   p.tok_loss = tok_loss;
   p.tok_flags = tok_flags;
+  p.tok_lse = nullptr;
   p.trace = nullptr;
   p.trace_rows = 0;
 #ifdef ECHO_TRACE
@@ -176,6 +177,37 @@ echo_status echo_policy_loss_launch_shape(int32_t dtype, int64_t n_rows, int32_t
   shape[3] = s.threads;
   shape[4] = s.smem_bytes;
   return ECHO_OK;
+}
+
+echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
+                            const int32_t* tok_action, float* tok_logp, float* tok_lse, uint8_t* tok_flags,
+                            void* stream) {
+  if (dtype != ECHO_F32 && dtype != ECHO_BF16) return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows < 0 || vocab < 1 || ld < vocab) return ECHO_ERR_INVALID_ARGUMENT;
+  const int64_t esize = dtype == ECHO_BF16 ? 2 : 4;
+  if ((ld * esize) % 16 != 0) return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows > 0 && (!logits || !aligned16(logits) || !tok_action || !tok_logp)) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  if (n_rows == 0) return ECHO_OK;
+  echo::LossParams p{};
+  p.logits = static_cast<uint8_t*>(const_cast<void*>(logits));  // read only in this mode
+  p.n_rows = n_rows;
+  p.V = vocab;
+  p.ld_bytes = ld * esize;
+  p.tok_action = tok_action;
+  p.tok_logp = tok_logp;
+  p.tok_lse = tok_lse;
+  p.tok_flags = tok_flags;
+  p.kl_coef = 0.0f;
+#ifdef ECHO_TRACE
+  p.trace = g_trace;
+  p.trace_rows = g_trace_rows;
+#endif
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (echo::quad_supports(dtype, vocab) && vocab >= 16384) return from_cuda(echo::launch_quad_logp(p, s, sms, nullptr));
+  return from_cuda(echo::launch_row(p, dtype, s, sms, nullptr, false));
 }
 
 size_t echo_loss_stats_workspace_bytes(void) { return echo::loss_stats_workspace_bytes(); }

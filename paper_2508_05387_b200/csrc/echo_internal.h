@@ -24,6 +24,7 @@ struct LossParams {
   float* __restrict__ tok_logp;
   float* __restrict__ tok_loss;
   uint8_t* __restrict__ tok_flags;
+  float* __restrict__ tok_lse;  // forward-only mode (echo_token_logp): per-row log-sum-exp, nullable
   unsigned long long* trace;  // ECHO_TRACE builds only: per-CTA phase timestamps (tools/trace_kernel.py)
   int32_t trace_rows;
 };
@@ -44,7 +45,9 @@ struct LaunchShape {
   int32_t grid_ctas, cluster_ctas, threads, smem_bytes;
 };
 // Per-kernel launchers (policy_loss_{quad,row}.cu); with shape != nullptr: report the shape, launch nothing.
-cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape);
+cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape,
+                       bool grad = true);
+cudaError_t launch_quad_logp(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
 int max_active_clusters(const void* fn, int threads, size_t smem, int cluster, int fallback);
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape);
 bool quad_supports(int32_t dtype, int32_t V);

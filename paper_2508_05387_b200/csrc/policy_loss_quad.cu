@@ -95,9 +95,15 @@ ECHO_DEVINL void quad_issue_row(const LossParams& p, const QuadGeom& g, uint32_t
   }
 }
 
-template <class C, bool kStoreExp>
+// kMode: kModeExact (gradient, exp recomputed in pass 2), kModeCache (gradient, exp kept as fp16 between the
+// passes), kModeLogp (forward only: log-probs and lse, the logits are not written -- SURVEY.md §8.6 f1).
+enum { kModeExact = 0, kModeCache = 1, kModeLogp = 2 };
+
+template <class C, int kMode>
 __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, C::kCtasPerSm)
     policy_loss_quad_kernel(const LossParams p) {
+  constexpr bool kStoreExp = kMode == kModeCache;
+  constexpr bool kGrad = kMode != kModeLogp;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   QuadSmem<C>& sm = *reinterpret_cast<QuadSmem<C>*>(smem_raw);
   const uint32_t rank = cluster_ctarank();
@@ -131,7 +137,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     xbar_remote[r] = mapa(smem_u32(&sm.xbar[0]), r);
   }
   const uint64_t st_pol = policy_evict_first();
-  const float gscale = (float)((double)p.grad_scale / *p.n_global);
+  const float gscale = kGrad ? (float)((double)p.grad_scale / *p.n_global) : 0.0f;
   const int32_t col_t = c0 + tid * 8;
   const bool last_valid = (uint32_t)(nchunks - 1) * C::kChunk + (uint32_t)tid * 16u < g.slice_bytes;
   const bool has_tail = (c1 & 7) && (c1 & ~7) >= col_t && ((c1 & ~7) - col_t) % C::kChunkElems == 0;
@@ -262,21 +268,29 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         }
         const float lse = mm + logf(ss);
         if (a < 0 || a >= V) za = NAN;
-        const RowScalars r = row_epilogue_f(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high,
-                                            p.kl_coef, gscale);
-        if (rank == 0) {
-          p.tok_logp[row] = r.logp;
-          p.tok_loss[row] = r.loss;
-          p.tok_flags[row] = r.flags;
+        if constexpr (kGrad) {
+          const RowScalars r = row_epilogue_f(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high,
+                                              p.kl_coef, gscale);
+          if (rank == 0) {
+            p.tok_logp[row] = r.logp;
+            p.tok_loss[row] = r.loss;
+            p.tok_flags[row] = r.flags;
+          }
+          const float pa = ex2(fmaf(za, kLog2e, -lse * kLog2e));
+          sm.coef = r.coef;
+          sm.lse = lse;
+          sm.da = fmaf(-r.coef, pa, r.coef);
+        } else if (rank == 0) {
+          const float logp = za - lse;
+          p.tok_logp[row] = logp;
+          if (p.tok_lse) p.tok_lse[row] = lse;
+          if (p.tok_flags) p.tok_flags[row] = (isfinite(lse) && isfinite(logp)) ? 0 : ECHO_FLAG_NONFINITE;
         }
-        const float pa = ex2(fmaf(za, kLog2e, -lse * kLog2e));
-        sm.coef = r.coef;
-        sm.lse = lse;
-        sm.da = fmaf(-r.coef, pa, r.coef);
       }
     }
     named_bar_sync(kQBar, C::kThreads);
     ECHO_TRACE_MARK(p, it, 4);
+    if constexpr (!kGrad) continue;
     const float coef = sm.coef, lse = sm.lse;
 
     // ---- pass 2
@@ -320,10 +334,10 @@ static bool supports_t(int32_t dtype, int32_t V) {
   return ((int64_t)q * 2 + C::kChunk - 1) / C::kChunk <= C::kRegChunks;
 }
 
-template <class C, bool kStoreExp>
+template <class C, int kMode>
 static cudaError_t launch_t(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
   const size_t smem = sizeof(QuadSmem<C>);
-  const void* fn = (const void*)policy_loss_quad_kernel<C, kStoreExp>;
+  const void* fn = (const void*)policy_loss_quad_kernel<C, kMode>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t clusters = max_active_clusters(fn, C::kThreads, smem, C::kCtas, num_sms * C::kCtasPerSm / C::kCtas);
@@ -332,7 +346,7 @@ static cudaError_t launch_t(const LossParams& p, cudaStream_t stream, int num_sm
     *shape = LaunchShape{(int32_t)(clusters * C::kCtas), C::kCtas, C::kThreads, (int32_t)smem};
     return cudaSuccess;
   }
-  policy_loss_quad_kernel<C, kStoreExp><<<(unsigned)(clusters * C::kCtas), C::kThreads, smem, stream>>>(p);
+  policy_loss_quad_kernel<C, kMode><<<(unsigned)(clusters * C::kCtas), C::kThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -343,10 +357,14 @@ bool quad_supports(int32_t dtype, int32_t V) { return supports_t<Quad>(dtype, V)
 bool oct_supports(int32_t dtype, int32_t V) { return supports_t<Oct>(dtype, V); }
 
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape) {
-  return store_exp ? launch_t<Quad, true>(p, stream, num_sms, shape) : launch_t<Quad, false>(p, stream, num_sms, shape);
+  return store_exp ? launch_t<Quad, kModeCache>(p, stream, num_sms, shape)
+                   : launch_t<Quad, kModeExact>(p, stream, num_sms, shape);
 }
 cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
-  return launch_t<Oct, true>(p, stream, num_sms, shape);
+  return launch_t<Oct, kModeCache>(p, stream, num_sms, shape);
+}
+cudaError_t launch_quad_logp(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  return launch_t<Quad, kModeLogp>(p, stream, num_sms, shape);
 }
 
 }  // namespace echo

@@ -43,7 +43,7 @@ struct RowVec<0> {
   static ECHO_DEVINL void store1(uint8_t* row, int32_t v, float x) { reinterpret_cast<float*>(row)[v] = x; }
 };
 
-template <int DT>
+template <int DT, bool kGrad>  // kGrad = false: forward-only log-probs, logits not written
 __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const LossParams p) {
   using RV = RowVec<DT>;
   constexpr int N = RV::N;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
   const int32_t V = p.V;
   const int32_t nvec = V / N;
   const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
-  const double n_global = *p.n_global;
+  const double n_global = kGrad ? *p.n_global : 1.0;
 
   for (int64_t row = blockIdx.x; row < p.n_rows; row += gridDim.x) {
     uint8_t* rowp = p.logits + row * p.ld_bytes;
@@ -106,15 +106,23 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
     if (tid == 0) {
       const float lse = tot.m + logf(tot.s);
       const float za = (a < 0 || a >= V) ? NAN : s_za;
-      const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high, p.kl_coef,
-                                        p.grad_scale, n_global);
-      p.tok_logp[row] = r.logp;
-      p.tok_loss[row] = r.loss;
-      p.tok_flags[row] = r.flags;
-      s_coef = r.coef;
-      s_lse_l2e = lse * kLog2e;
+      if constexpr (kGrad) {
+        const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high,
+                                          p.kl_coef, p.grad_scale, n_global);
+        p.tok_logp[row] = r.logp;
+        p.tok_loss[row] = r.loss;
+        p.tok_flags[row] = r.flags;
+        s_coef = r.coef;
+        s_lse_l2e = lse * kLog2e;
+      } else {
+        const float logp = za - lse;
+        p.tok_logp[row] = logp;
+        if (p.tok_lse) p.tok_lse[row] = lse;
+        if (p.tok_flags) p.tok_flags[row] = (isfinite(lse) && isfinite(logp)) ? 0 : ECHO_FLAG_NONFINITE;
+      }
     }
     __syncthreads();
+    if constexpr (!kGrad) continue;
     const float coef = s_coef, lse_l2e = s_lse_l2e;
 
     // ---- pass 2
@@ -145,17 +153,25 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
   }
 }
 
-cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape,
+                       bool grad) {
   int64_t grid = num_sms;
   if (grid > p.n_rows) grid = p.n_rows;
   if (shape) {
     *shape = LaunchShape{(int32_t)grid, 1, kRThreads, 0};
     return cudaSuccess;
   }
-  if (dtype == ECHO_BF16)
-    policy_loss_row_kernel<1><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
-  else
-    policy_loss_row_kernel<0><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+  if (dtype == ECHO_BF16) {
+    if (grad)
+      policy_loss_row_kernel<1, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+    else
+      policy_loss_row_kernel<1, false><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+  } else {
+    if (grad)
+      policy_loss_row_kernel<0, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+    else
+      policy_loss_row_kernel<0, false><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+  }
   return cudaGetLastError();
 }
 

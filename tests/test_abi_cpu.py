@@ -54,8 +54,8 @@ def test_quad_kernel_uses_tma_bulk_copies_and_dsmem():
                           capture_output=True, text=True, check=True).stdout
     blocks = re.split(r"\n\s*Function : ", sass)
     quad = [b for b in blocks if "policy_loss_quad_kernel" in b.split("\n", 1)[0]]
-    assert len(quad) == 3                       # 4-CTA fp16-cache / exact, 8-CTA fp16-cache
-    body = quad[0]
+    assert len(quad) == 4                       # 4-CTA fp16-cache / exact / logp-only, 8-CTA fp16-cache
+    body = [b for b in quad if "QCfgILi4ELi8EEELi1E" in b.split("\n", 1)[0]][0]   # 4-CTA, fp16-cache mode
     assert "UBLKCP.S.G" in body      # cp.async.bulk global->shared (TMA engine)
     assert "SYNCS" in body           # mbarrier phase / tx tracking
     assert "STAS" in body            # st.async into the peer CTA's shared memory (DSMEM)

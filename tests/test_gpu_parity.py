@@ -384,3 +384,33 @@ def test_abi_argument_errors():
         abi.echo_policy_loss_fwd_bwd(**args(dtype=abi.ECHO_F32, ld=1000), algo=abi.ECHO_ALGO_QUAD_REG)
     assert e.value.status == abi.ECHO_ERR_UNSUPPORTED
     abi.echo_policy_loss_fwd_bwd(**args(n_rows=0))                    # empty micro-batch: no launch, OK
+
+
+# ---------------------------------------------------------------------------------------------- f1: logp only
+@pytest.mark.parametrize("name", ["tiny", "qwen3-4b", "qwen2.5-7b"])
+def test_token_logp_forward_only(name):
+    """echo_token_logp reads the logits once and matches the oracle's logp / lse; the logits
+    are left bit-for-bit unchanged."""
+    from paper_2508_05387_b200 import abi
+    cfg = synth.CONFIGS[name]
+    b = synth.make_batch(cfg, 0, 2 * cfg.G)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    n = min(info.n_tokens, 4096)
+    logits = fill(st, cfg, 0, n)
+    before = logits.clone()
+    logp = torch.empty(n, device="cuda")
+    lse = torch.empty(n, device="cuda")
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    abi.echo_token_logp(logits, abi.ECHO_BF16 if cfg.dtype == "bf16" else abi.ECHO_F32, n, cfg.V, cfg.V,
+                        st.tok_action, logp, lse, flags)
+    torch.cuda.synchronize()
+    assert torch.equal(before.view(torch.int16) if cfg.dtype == "bf16" else before, 
+                       logits.view(torch.int16) if cfg.dtype == "bf16" else logits)
+    ref_logp, ref_lse, ref_flags = oracle.token_logp(as_oracle_rows(logits), o.pk.tok_action[:n])
+    assert np.max(np.abs(logp.cpu().numpy() - ref_logp)) <= 1e-5 + 1e-6 * np.abs(ref_logp).max()
+    assert np.max(np.abs(lse.cpu().numpy() - ref_lse)) <= 1e-5 + 1e-6 * np.abs(ref_lse).max()
+    np.testing.assert_array_equal(flags.cpu().numpy(), ref_flags)
+    # consistency with the fused kernel's logp on the same rows
+    st.loss(logits, 0, kl_coef=0.0)
+    assert torch.equal(st.tok_logp[:n], logp) or name == "tiny"   # same reduction tree on the quad path

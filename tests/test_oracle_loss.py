@@ -243,3 +243,23 @@ def test_stats_vector():
                                [out.loss.sum(), (out.logp - old).sum(), (np.exp(x) - x - 1).sum(), out.logp.sum(),
                                 rho.sum()], rtol=1e-12)
     assert out.stats[5] == rho.min() and out.stats[6] == rho.max()
+
+
+def test_token_logp_closed_forms():
+    """f1 forward-only log-probs: uniform rows (-ln V), single spike, all masked but one column (logp = 0)."""
+    for V in (1024, 151936):
+        z = np.zeros((3, V), np.float32)
+        z[1, 5] = 20.0
+        z[2, :] = -np.inf
+        z[2, 9] = 1.5
+        logp, lse, flags = oracle.token_logp(z, np.array([3, 5, 9], np.int32))
+        assert abs(logp[0] + math.log(V)) <= 4e-15 and abs(lse[0] - math.log(V)) <= 4e-15
+        lse1 = 20.0 + math.log1p((V - 1) * math.exp(-20.0))
+        assert abs(logp[1] - (20.0 - lse1)) <= 4e-15 * 20 + (V - 1) * 2.0 ** -52
+        assert logp[2] == 0.0 and lse[2] == 1.5
+        assert not flags.any()
+    z = np.zeros((2, 64), np.float32)
+    z[0, 1] = np.nan
+    z[1, :] = -np.inf
+    _, _, flags = oracle.token_logp(z, np.array([0, 0], np.int32))
+    np.testing.assert_array_equal(flags, [2, 2])
