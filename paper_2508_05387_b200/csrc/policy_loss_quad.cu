@@ -80,18 +80,20 @@ ECHO_DEVINL QuadGeom quad_geom(int32_t V, uint32_t rank) {
   return g;
 }
 
-// Issue all chunks of row iteration `it` (one lane per chunk, expect_tx by lane 0 on the row's barrier).
+// Issue chunks [from, to) of this cluster's row-major chunk stream (row iteration q / nchunks, chunk q % nchunks)
+// into ring slot q % kRing, one lane per chunk.  The lane that issues a row's chunk 0 arms that row's barrier
+// with the row's byte count (tx may transiently go negative; the phase cannot complete before the arrive).
 template <class C>
-ECHO_DEVINL void quad_issue_row(const LossParams& p, const QuadGeom& g, uint32_t cid, uint32_t ncl, uint32_t it,
-                                int lane, uint32_t full0, uint32_t ring0, uint64_t pol) {
-  const uint32_t bar = full0 + 8 * (it & 3u);
-  if (lane == 0) mbar_arrive_expect_tx(bar, g.slice_bytes);
-  const int64_t row = (int64_t)cid + (int64_t)it * ncl;
-  const uint8_t* src = p.logits + row * p.ld_bytes + (int64_t)g.c0 * 2;
-  for (int c = lane; c < g.nchunks; c += 32) {
-    const uint32_t slot = (it * (uint32_t)g.nchunks + c) % C::kRing;
-    const uint32_t nb = min((uint32_t)C::kChunk, g.slice_bytes - (uint32_t)c * C::kChunk);
-    bulk_g2s(ring0 + slot * C::kChunk, src + (int64_t)c * C::kChunk, nb, bar, pol);
+ECHO_DEVINL void quad_issue_chunks(const LossParams& p, const QuadGeom& g, uint32_t cid, uint32_t ncl, uint32_t from,
+                                   uint32_t to, int lane, uint32_t full0, uint32_t ring0, uint64_t pol) {
+  for (uint32_t q = from + (uint32_t)lane; q < to; q += 32) {
+    const uint32_t r = q / (uint32_t)g.nchunks, c = q % (uint32_t)g.nchunks;
+    const uint32_t bar = full0 + 8 * (r & 3u);
+    if (c == 0) mbar_arrive_expect_tx(bar, g.slice_bytes);
+    const int64_t row = (int64_t)cid + (int64_t)r * ncl;
+    const uint8_t* src = p.logits + row * p.ld_bytes + (int64_t)g.c0 * 2 + (int64_t)c * C::kChunk;
+    const uint32_t nb = min((uint32_t)C::kChunk, g.slice_bytes - c * C::kChunk);
+    bulk_g2s(ring0 + (q % C::kRing) * C::kChunk, src, nb, bar, pol);
   }
 }
 
@@ -128,7 +130,14 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
   cluster_sync_all();
 
   const uint64_t ld_pol = policy_evict_first();
-  if (warp == 0 && my_rows > 0 && nchunks > 0) quad_issue_row<C>(p, g, cid, ncl, 0, lane, full0, ring0, ld_pol);
+  // warp 1 streams the rows: the ring holds ~1.4 rows, so row it+1 and the head of row it+2 are in flight while
+  // row it is reduced; slots are refilled once the CTA barrier after pass 1b shows row it has been copied out
+  const uint32_t total_chunks = my_rows * (uint32_t)nchunks;
+  uint32_t issued = 0;
+  if (warp == 1 % C::kWarps && nchunks > 0) {
+    issued = min(total_chunks, (uint32_t)C::kRing);
+    quad_issue_chunks<C>(p, g, cid, ncl, 0, issued, lane, full0, ring0, ld_pol);
+  }
 
   uint32_t xbuf_remote[C::kCtas], xbar_remote[C::kCtas];
 #pragma unroll
@@ -228,9 +237,13 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     ECHO_TRACE_MARK(p, it, 3);
     // every warp has copied row `it` out of the ring: warp 1 streams row it+1 into the slots (its chunks only
     // overlap rows <= it), off the critical path of warp 0's merge
-    if (warp == 1 % C::kWarps && it + 1 < my_rows && nchunks > 0) {
-      fence_proxy_async_smem();
-      quad_issue_row<C>(p, g, cid, ncl, it + 1, lane, full0, ring0, ld_pol);
+    if (warp == 1 % C::kWarps && nchunks > 0) {
+      const uint32_t upto = min(total_chunks, (it + 1) * (uint32_t)nchunks + (uint32_t)C::kRing);
+      if (upto > issued) {
+        fence_proxy_async_smem();
+        quad_issue_chunks<C>(p, g, cid, ncl, issued, upto, lane, full0, ring0, ld_pol);
+        issued = upto;
+      }
     }
 
     // ---- CTA merge (warp 0), cluster merge (st.async to every peer), epilogue (lane 0)
