@@ -40,7 +40,7 @@ struct QCfg {
   static constexpr int kChunk = kThreads * 16;          // one 16-byte vector per thread
   static constexpr int kChunkElems = kChunk / 2;
   static constexpr int kCtasPerSm = 16 / kWarps;
-  static constexpr int kRing = 27;                      // staging ring slots (~1.4 slices)
+  static constexpr int kRing = kCtasPerSm == 2 ? 28 : 27;  // staging ring slots (~1.5 slices; fills the SM)
   static constexpr int kRegChunks = 19;                 // V <= kCtas * 19 * kChunkElems = 155648
 };
 constexpr int kQBar = 1;                                // named barrier id
