@@ -94,7 +94,9 @@ typedef struct {
  *   n_rollouts R (multiple of group_size), group_size G >= 2, max_len S >= 1, vocab V >= 1.
  *   version[R] int64, resp_len[R] int32; action / old_logp / ref_logp are padded row-major [R x S]
  *   (position j of rollout i at i*S + j; positions >= resp_len[i] are never read).  ref_logp may be
- *   NULL (then tok_ref must be NULL too).  rollout_base = global id of local rollout 0.
+ *   NULL (then tok_ref must be NULL too).  aux [R x S] is an optional per-token payload packed like old_logp
+ *   into tok_aux (e.g. the PPO-GAE advantages of echo_gae_advantage; both NULL or both set).
+ *   rollout_base = global id of local rollout 0.
  * Outputs (ascending, stable compaction; tokens rollout-major):
  *   kept_rollout[R]   global ids of kept rollouts (first n_rollouts_kept entries written)
  *   kept_offset[R+1]  CSR offsets into the token arrays (first n_rollouts_kept + 1 entries written)
@@ -106,13 +108,27 @@ typedef struct {
  * Launches: 3 kernels.  Integer / bit-copy work only: results are bit-exact.
  */
 ECHO_API echo_status echo_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len, int32_t vocab,
-                            int64_t t_train, int32_t max_lag, int64_t rollout_base,
-                            const int64_t* version, const int32_t* resp_len,
-                            const int32_t* action, const float* old_logp, const float* ref_logp,
-                            int64_t token_capacity,
-                            int32_t* kept_rollout, int64_t* kept_offset,
-                            int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
-                            echo_pack_result* result, void* stream);
+                                     int64_t t_train, int32_t max_lag, int64_t rollout_base,
+                                     const int64_t* version, const int32_t* resp_len,
+                                     const int32_t* action, const float* old_logp, const float* ref_logp,
+                                     const float* aux, int64_t token_capacity,
+                                     int32_t* kept_rollout, int64_t* kept_offset,
+                                     int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
+                                     float* tok_aux, echo_pack_result* result, void* stream);
+
+/*
+ * f4: PPO-GAE advantages over the per-step `rewards` and `values` of each trajectory (PAPER.md
+ * :163-164, the fields "required by PPO and its popular variants", :170-171).  For rollout i, t = L_i-1 .. 0:
+ *   delta_t = r_t + gamma V_{t+1} - V_t   (V_{L_i} = bootstrap_value[i]; 0 when bootstrap_value is NULL, i.e.
+ *                                          terminal trajectories)
+ *   A_t = delta_t + gamma lambda A_{t+1}  (A_{L_i} = 0);   returns_t = A_t + V_t   (returns nullable)
+ * rewards / values / adv / returns are padded row-major [R x S]; positions >= resp_len[i] are neither read nor
+ * written.  fp64 with round-to-nearest, no contraction, in this order: bit-identical to a sequential fp64 loop.
+ * Launches: 1 kernel.
+ */
+ECHO_API echo_status echo_gae_advantage(int32_t n_rollouts, int32_t max_len, const int32_t* resp_len,
+                                        const float* rewards, const float* values, const float* bootstrap_value,
+                                        float gamma, float lam, float* adv, float* returns, void* stream);
 
 /*
  * (2) GRPO group-relative advantage (PAPER.md :374 names GRPO; formula SPEC.md :209-213):
@@ -175,6 +191,35 @@ ECHO_API echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t 
                                      const int32_t* tok_action, float* tok_logp, float* tok_lse, uint8_t* tok_flags,
                                      void* stream);
 
+/* f4 loss variants ("PPO, KL-constrained PPO, GRPO ... or emerging variants", PAPER.md :278). */
+enum { ECHO_KL_K3 = 0, /* exp(ref - logp) - (ref - logp) - 1: unbiased, non-negative (the default, reading R5) */
+       ECHO_KL_K1 = 1, /* logp - ref (SPEC.md :244's estimator, here against pi_ref)                           */
+       ECHO_KL_K2 = 2  /* (logp - ref)^2 / 2                                                                   */ };
+
+typedef struct {
+  float clip_low, clip_high; /* PPO ratio clip [1 - clip_low, 1 + clip_high] (SPEC.md :219, :243: 0.2 / 0.2)  */
+  float clip_dual;           /* dual clip c > 1: for A < 0 the loss is capped at -A c (0 = off)              */
+  float kl_coef;             /* beta (PAPER.md :376-382: 0.001 or 0)                                         */
+  float grad_scale;          /* s: multiplies every gradient coefficient                                     */
+  int32_t kl_estimator;      /* ECHO_KL_*                                                                    */
+} echo_loss_config;
+
+/*
+ * General form of echo_policy_loss_fwd_bwd (which is this call with tok_adv = tok_weight = NULL, clip_dual = 0,
+ * kl_estimator = ECHO_KL_K3):
+ *   A_t = tok_adv ? tok_adv[t] : adv_slot[tok_slot[t]]   -- per-token advantages, e.g. PPO-GAE (echo_gae_advantage)
+ *   w_t = tok_weight ? tok_weight[t] : 1 / *n_global      -- per-token loss weights, e.g. sequence-mean aggregation
+ *                                                           (w_t = 1 / (n_sequences L_i)); n_global may then be NULL
+ *   c_t = grad_scale * w_t * dl_t/dlogp ; tok_loss[t] = l_t (unweighted); the step loss is sum_t w_t l_t.
+ * cfg is a HOST pointer.  Same layout, launches and errors as echo_policy_loss_fwd_bwd.
+ */
+ECHO_API echo_status echo_policy_loss_fwd_bwd_v2(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab,
+                                                 int64_t ld, const int32_t* tok_action, const float* tok_old,
+                                                 const float* tok_ref, const int32_t* tok_slot, const float* adv_slot,
+                                                 const float* tok_adv, const float* tok_weight, const double* n_global,
+                                                 const echo_loss_config* cfg, float* tok_logp, float* tok_loss,
+                                                 uint8_t* tok_flags, int32_t algo, void* stream);
+
 /* Launch shape echo_policy_loss_fwd_bwd_ex would use on the current device (no launch):
  * shape[5] = {resolved algo, grid CTAs, CTAs per cluster, threads per CTA, dynamic smem bytes}. */
 ECHO_API echo_status echo_policy_loss_launch_shape(int32_t dtype, int64_t n_rows, int32_t vocab, int32_t algo,
@@ -182,18 +227,20 @@ ECHO_API echo_status echo_policy_loss_launch_shape(int32_t dtype, int64_t n_rows
 
 /*
  * Statistics of the per-token outputs over n_tokens packed tokens (all micro-batches of the step):
- *   loss_stats[10] = {sum l_t, sum (logp - old), sum k3(ref, logp) (0 if tok_ref NULL), n_clipped,
- *                     n_nonfinite, rho_min, rho_max, sum logp, n_tokens, sum rho}
+ *   loss_stats[11] = {sum l_t, sum (logp - old), sum k3(ref, logp) (0 if tok_ref NULL), n_clipped,
+ *                     n_nonfinite, rho_min, rho_max, sum logp, n_tokens, sum rho, sum w_t l_t}
  *   evaluated in fp64 from the fp32 per-token values (rho = exp(logp - old), k3 = e^x - x - 1 with
  *   x = ref - logp); rho statistics over rows without ECHO_FLAG_NONFINITE (rho_min = +inf, rho_max = -inf
- *   when there are none).  Fixed-order fp64 reduction: bitwise reproducible for a given n_tokens.
+ *   when there are none); w_t = tok_weight[t] (nullable: 1).  The step loss is sum l_t / N_global, or
+ *   sum w_t l_t with per-token weights (echo_policy_loss_fwd_bwd_v2).  Fixed-order fp64 reduction:
+ *   bitwise reproducible for a given n_tokens.
  * workspace: device buffer of echo_loss_stats_workspace_bytes() bytes (no initialisation needed).
  * Launches: 2 kernels.
  */
 ECHO_API size_t echo_loss_stats_workspace_bytes(void);
-ECHO_API echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp, const float* tok_old,
-                            const float* tok_ref, const uint8_t* tok_flags, double* workspace, double* loss_stats,
-                            void* stream);
+ECHO_API echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp,
+                                     const float* tok_old, const float* tok_ref, const float* tok_weight,
+                                     const uint8_t* tok_flags, double* workspace, double* loss_stats, void* stream);
 
 /* Human-readable name of a status code (static storage). */
 ECHO_API const char* echo_status_string(echo_status status);

@@ -48,17 +48,20 @@ def lib():
         _lib = ctypes.CDLL(build())
         P = ctypes.c_void_p
         i32, i64, f32, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double
-        _lib.echo_ref_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, i64,
-                                             P, P, P, P, P, P, ctypes.POINTER(_PackResult)]
+        _lib.echo_ref_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, P, i64,
+                                             P, P, P, P, P, P, P, ctypes.POINTER(_PackResult)]
+        _lib.echo_ref_gae_advantage.argtypes = [i32, i32, P, P, P, P, f32, f32, P, P]
+        _lib.echo_ref_gae_advantage.restype = ctypes.c_int
         _lib.echo_ref_pack_batch.restype = ctypes.c_int
         _lib.echo_ref_group_advantage.argtypes = [i32, i32, f32, P, P, i64, P, P, P]
         _lib.echo_ref_group_advantage.restype = ctypes.c_int
-        _lib.echo_ref_policy_loss.argtypes = [i64, i32, i64, i32, P, P, P, P, P, P, f64, f32, f32, f32, f32,
-                                              P, P, P, P, P, P]
+        _lib.echo_ref_policy_loss.argtypes = [i64, i32, i64, i32, P, P, P, P, P, P, P, P, f64, f32, f32, f32, f32,
+                                              i32, f32, P, P, P, P, P, P]
         _lib.echo_ref_policy_loss.restype = ctypes.c_int
         _lib.echo_ref_token_logp.argtypes = [i64, i32, i64, i32, P, P, P, P, P]
         _lib.echo_ref_token_logp.restype = ctypes.c_int
-        _lib.echo_ref_scaled_loss.argtypes = [i64, i32, i64, P, P, P, P, P, P, f64, f32, f32, f32, f32]
+        _lib.echo_ref_scaled_loss.argtypes = [i64, i32, i64, P, P, P, P, P, P, P, P, f64, f32, f32, f32, f32, i32,
+                                              f32]
         _lib.echo_ref_scaled_loss.restype = f64
     return _lib
 
@@ -84,10 +87,11 @@ class PackOut:
     tok_action: np.ndarray
     tok_old: np.ndarray
     tok_ref: np.ndarray | None
+    tok_aux: np.ndarray | None = None
 
 
 def pack_batch(version, resp_len, action, old_logp, ref_logp, *, group_size, max_len, vocab, t_train, max_lag,
-               rollout_base=0, token_capacity=None) -> PackOut:
+               rollout_base=0, token_capacity=None, aux=None) -> PackOut:
     """(1) lag filter + pack.  ``action``/``old_logp``/``ref_logp`` are padded ``[R, S]``."""
     version = _c(version, np.int64)
     resp_len = _c(resp_len, np.int32)
@@ -103,18 +107,35 @@ def pack_batch(version, resp_len, action, old_logp, ref_logp, *, group_size, max
     tok_action = np.zeros(n_alloc, np.int32)
     tok_old = np.zeros(n_alloc, np.float32)
     tok_ref = np.zeros(n_alloc, np.float32) if ref_logp is not None else None
+    aux = None if aux is None else _c(aux, np.float32).reshape(-1)
+    tok_aux = np.zeros(n_alloc, np.float32) if aux is not None else None
     res = _PackResult()
     rc = lib().echo_ref_pack_batch(R, group_size, max_len, vocab, t_train, max_lag, rollout_base,
-                                   _p(version), _p(resp_len), _p(action), _p(old_logp), _p(ref_logp), cap,
+                                   _p(version), _p(resp_len), _p(action), _p(old_logp), _p(ref_logp), _p(aux), cap,
                                    _p(kept_rollout), _p(kept_offset), _p(tok_slot), _p(tok_action), _p(tok_old),
-                                   _p(tok_ref), ctypes.byref(res))
+                                   _p(tok_ref), _p(tok_aux), ctypes.byref(res))
     if rc != 0:
         raise ValueError(f"echo_ref_pack_batch: invalid argument (rc={rc})")
     n = int(res.n_tokens) if res.n_tokens <= cap else 0
     nk = int(res.n_rollouts_kept)
     return PackOut(int(res.status), int(res.first_bad_rollout), int(res.n_groups_kept), nk, int(res.n_tokens),
                    kept_rollout[:nk].copy(), kept_offset[:nk + 1].copy(), tok_slot[:n].copy(), tok_action[:n].copy(),
-                   tok_old[:n].copy(), None if tok_ref is None else tok_ref[:n].copy())
+                   tok_old[:n].copy(), None if tok_ref is None else tok_ref[:n].copy(),
+                   None if tok_aux is None else tok_aux[:n].copy())
+
+
+def gae_advantage(resp_len, rewards, values, *, gamma, lam, bootstrap=None):
+    """f4: PPO-GAE advantages and returns, padded [R, S] float32 (positions >= L left at 0)."""
+    rewards = _c(rewards, np.float32)
+    values = _c(values, np.float32)
+    R, S = rewards.shape
+    adv = np.zeros((R, S), np.float32)
+    ret = np.zeros((R, S), np.float32)
+    rc = lib().echo_ref_gae_advantage(R, S, _p(_c(resp_len, np.int32)), _p(rewards), _p(values),
+                                      _p(_c(bootstrap, np.float32)), gamma, lam, _p(adv), _p(ret))
+    if rc != 0:
+        raise ValueError("echo_ref_gae_advantage: invalid argument")
+    return adv, ret
 
 
 def group_advantage(reward, kept_rollout, *, group_size, eps=1e-8, rollout_base=0, want_f64=False):
@@ -146,8 +167,12 @@ class LossOut:
     stats: np.ndarray
 
 
+KL_K3, KL_K1, KL_K2 = 0, 1, 2
+
+
 def policy_loss(logits, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, vocab=None, dtype=None,
-                clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0, want_dlogits=True) -> LossOut:
+                clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0, want_dlogits=True, tok_adv=None,
+                tok_weight=None, clip_dual=0.0, kl_estimator=KL_K3) -> LossOut:
     """(3)-(5) for every row of ``logits``.
 
     ``logits`` is a 2-D numpy array: float32 (dtype F32) or uint16 bf16 bit patterns (dtype BF16).
@@ -169,10 +194,13 @@ def policy_loss(logits, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_g
     coef = np.zeros(n, np.float64)
     flags = np.zeros(n, np.uint8)
     d = np.zeros((n, V), np.float64) if want_dlogits else None
-    stats = np.zeros(10, np.float64)
+    tok_adv = _c(tok_adv, np.float32)
+    tok_weight = _c(tok_weight, np.float32)
+    stats = np.zeros(11, np.float64)
     rc = lib().echo_ref_policy_loss(n, V, ld, dtype, _p(logits), _p(tok_action), _p(tok_old), _p(tok_ref),
-                                    _p(tok_slot), _p(adv_slot), float(n_global), clip_low, clip_high, kl_coef,
-                                    grad_scale, _p(logp), _p(loss), _p(flags), _p(coef), _p(d), _p(stats))
+                                    _p(tok_slot), _p(adv_slot), _p(tok_adv), _p(tok_weight), float(n_global),
+                                    clip_low, clip_high, clip_dual, kl_coef, kl_estimator, grad_scale, _p(logp),
+                                    _p(loss), _p(flags), _p(coef), _p(d), _p(stats))
     if rc != 0:
         raise ValueError("echo_ref_policy_loss: invalid argument")
     return LossOut(logp, loss, flags, coef, d, stats)
@@ -196,11 +224,13 @@ def token_logp(logits, tok_action, *, vocab=None, dtype=None):
 
 
 def scaled_loss(logits_f64, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, clip_low=0.2,
-                clip_high=0.2, kl_coef=0.0, grad_scale=1.0) -> float:
-    """grad_scale * sum_t l_t / N_global as a function of fp64 logits (for finite differences)."""
+                clip_high=0.2, kl_coef=0.0, grad_scale=1.0, tok_adv=None, tok_weight=None, clip_dual=0.0,
+                kl_estimator=KL_K3) -> float:
+    """grad_scale * sum_t w_t l_t as a function of fp64 logits (for finite differences)."""
     z = np.ascontiguousarray(logits_f64, dtype=np.float64)
     n, V = z.shape
     return float(lib().echo_ref_scaled_loss(n, V, V, _p(z), _p(_c(tok_action, np.int32)), _p(_c(tok_old, np.float32)),
                                             _p(_c(tok_ref, np.float32)), _p(_c(tok_slot, np.int32)),
-                                            _p(_c(adv_slot, np.float32)), float(n_global), clip_low, clip_high,
-                                            kl_coef, grad_scale))
+                                            _p(_c(adv_slot, np.float32)), _p(_c(tok_adv, np.float32)),
+                                            _p(_c(tok_weight, np.float32)), float(n_global), clip_low, clip_high,
+                                            clip_dual, kl_coef, kl_estimator, grad_scale))

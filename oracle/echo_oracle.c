@@ -91,9 +91,9 @@ int echo_ref_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len,
                         int64_t t_train, int32_t max_lag, int64_t rollout_base,
                         const int64_t* version, const int32_t* resp_len,
                         const int32_t* action, const float* old_logp, const float* ref_logp,
-                        int64_t token_capacity,
+                        const float* aux, int64_t token_capacity,
                         int32_t* kept_rollout, int64_t* kept_offset,
-                        int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
+                        int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref, float* tok_aux,
                         echo_ref_pack_result* result) {
   if (n_rollouts < 0 || group_size < 2 || max_len < 1 || vocab < 1 || max_lag < 0) return REF_ERR_INVALID_ARGUMENT;
   if (n_rollouts % group_size != 0) return REF_ERR_INVALID_ARGUMENT;
@@ -155,6 +155,7 @@ int echo_ref_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len,
         tok_action[t] = action[i * S + j];
         tok_old[t] = old_logp[i * S + j];
         if (ref_logp && tok_ref) tok_ref[t] = ref_logp[i * S + j];
+        if (aux && tok_aux) tok_aux[t] = aux[i * S + j];
       }
     }
   }
@@ -240,22 +241,47 @@ int echo_ref_group_advantage(int32_t n_rollouts_kept, int32_t group_size, float 
  * flags: bit0 = clipped; bit1 = non-finite (lse, logp, rho, l_t or c_t not a finite value that an
  * fp32 output can hold -- R11).
  * stats (nullable, sequential fp64 over rows): {sum l, sum (logp-old), sum kl_k3 (if ref),
- *   n_clipped, n_nonfinite, rho_min, rho_max, sum logp, n_rows, sum rho}, rho stats over
+ *   n_clipped, n_nonfinite, rho_min, rho_max, sum logp, n_rows, sum rho, sum w l}, rho stats over
  *   finite rows only.
+ * f4 options: tok_adv / tok_weight (nullable, see adv_of), clip_dual (c > 1: for A < 0 the loss is capped at
+ *   -A c with zero gradient), kl_estimator (REF_KL_*).
  * dlogits (nullable) is [n_rows x vocab] doubles.
  * ====================================================================================== */
 static int fits_f32(double x) { return isfinite(x) && fabs(x) <= (double)FLT_MAX; }
 
+/* The KL estimators of f4 (x = ref - logp): k3 = e^x - x - 1 (default, R5), k1 = logp - ref, k2 = (logp - ref)^2/2;
+ * kl_value / kl_dlogp return the estimator and its derivative with respect to logp. */
+enum { REF_KL_K3 = 0, REF_KL_K1 = 1, REF_KL_K2 = 2 };
+static double kl_value(int est, double x) {
+  if (est == REF_KL_K1) return -x;
+  if (est == REF_KL_K2) return 0.5 * x * x;
+  return exp(x) - x - 1.0;
+}
+static double kl_dlogp(int est, double x) {
+  if (est == REF_KL_K1) return 1.0;
+  if (est == REF_KL_K2) return -x;
+  return 1.0 - exp(x);
+}
+
+/* Per-token advantage (f4: tok_adv, e.g. PPO-GAE, else the rollout's GRPO advantage) and loss weight
+ * (f4: tok_weight, e.g. sequence-mean aggregation, else 1 / N_global -- reading R6). */
+static double adv_of(const float* tok_adv, const int32_t* tok_slot, const float* adv_slot, int64_t t) {
+  return tok_adv ? (double)tok_adv[t] : (double)adv_slot[tok_slot[t]];
+}
+
 int echo_ref_policy_loss(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtype, const void* logits,
                          const int32_t* tok_action, const float* tok_old, const float* tok_ref,
-                         const int32_t* tok_slot, const float* adv_slot, double n_global,
-                         float clip_low, float clip_high, float kl_coef, float grad_scale,
+                         const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
+                         const float* tok_weight, double n_global,
+                         float clip_low, float clip_high, float clip_dual, float kl_coef, int32_t kl_estimator,
+                         float grad_scale,
                          double* tok_logp, double* tok_loss, uint8_t* tok_flags, double* tok_coef,
                          double* dlogits, double* stats) {
   if (n_rows < 0 || vocab < 1 || ld < vocab || (dtype != 0 && dtype != 1)) return REF_ERR_INVALID_ARGUMENT;
   if (kl_coef > 0.0f && tok_ref == NULL) return REF_ERR_INVALID_ARGUMENT;
+  if (kl_estimator < REF_KL_K3 || kl_estimator > REF_KL_K2) return REF_ERR_INVALID_ARGUMENT;
   const double lo = 1.0 - (double)clip_low, hi = 1.0 + (double)clip_high;
-  const double beta = (double)kl_coef;
+  const double beta = (double)kl_coef, dual = (double)clip_dual;
 
 #pragma omp parallel for schedule(dynamic, 16)
   for (int64_t t = 0; t < n_rows; ++t) {
@@ -274,21 +300,26 @@ int echo_ref_policy_loss(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtyp
     double logp = logit_at(logits, dtype, ld, t, a) - lse;
 
     /* (4) clipped importance-ratio surrogate + optional KL to the reference policy */
-    double A = (double)adv_slot[tok_slot[t]];
+    double A = adv_of(tok_adv, tok_slot, adv_slot, t);
     double rho = exp(logp - (double)tok_old[t]);
     int clipped = (A > 0.0 && rho > hi) || (A < 0.0 && rho < lo);
     double rho_c = rho < lo ? lo : (rho > hi ? hi : rho);
     double un = -A * rho, cl = -A * rho_c;
     double pg = un > cl ? un : cl;
+    if (dual > 1.0 && A < 0.0 && pg > -A * dual) { /* dual clip: loss capped at -A c, no gradient */
+      pg = -A * dual;
+      clipped = 1;
+    }
     double kl = 0.0, dkl = 0.0;
     if (beta > 0.0) {
       double x = (double)tok_ref[t] - logp;
-      kl = exp(x) - x - 1.0;
-      dkl = 1.0 - exp(x);
+      kl = kl_value(kl_estimator, x);
+      dkl = kl_dlogp(kl_estimator, x);
     }
     double loss = pg + beta * kl;
     double dl_dlogp = (clipped ? 0.0 : -A * rho) + beta * dkl;
-    double c = (double)grad_scale * dl_dlogp / n_global;
+    double w = tok_weight ? (double)tok_weight[t] : 1.0 / n_global;
+    double c = (double)grad_scale * w * dl_dlogp;
     int nonfinite = !(fits_f32(lse) && fits_f32(logp) && fits_f32(rho) && fits_f32(loss) && fits_f32(c));
 
     tok_logp[t] = logp;
@@ -306,7 +337,7 @@ int echo_ref_policy_loss(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtyp
   }
 
   if (stats) {
-    double acc[10] = {0, 0, 0, 0, 0, INFINITY, -INFINITY, 0, 0, 0};
+    double acc[11] = {0, 0, 0, 0, 0, INFINITY, -INFINITY, 0, 0, 0, 0};
     for (int64_t t = 0; t < n_rows; ++t) {
       double logp = tok_logp[t];
       acc[0] = acc[0] + tok_loss[t];
@@ -325,8 +356,36 @@ int echo_ref_policy_loss(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtyp
       }
       acc[7] = acc[7] + logp;
       acc[8] = acc[8] + 1.0;
+      acc[10] = acc[10] + (tok_weight ? (double)tok_weight[t] : 1.0) * tok_loss[t];
     }
-    for (int q = 0; q < 10; ++q) stats[q] = acc[q];
+    for (int q = 0; q < 11; ++q) stats[q] = acc[q];
+  }
+  return REF_OK;
+}
+
+/* ======================================================================================
+ * f4: PPO-GAE advantages (Schulman et al., generalised advantage estimation) over each
+ * trajectory's per-step rewards and values (PAPER.md :163-164, :170-171), written as its definition:
+ *   delta_t = r_t + gamma V_{t+1} - V_t  (V_L = bootstrap or 0),  A_t = delta_t + gamma lambda A_{t+1} (A_L = 0),
+ *   returns_t = A_t + V_t;  fp64, backwards over t, rounded to fp32.
+ * ====================================================================================== */
+int echo_ref_gae_advantage(int32_t n_rollouts, int32_t max_len, const int32_t* resp_len, const float* rewards,
+                           const float* values, const float* bootstrap, float gamma, float lam, float* adv,
+                           float* returns) {
+  if (n_rollouts < 0 || max_len < 1) return REF_ERR_INVALID_ARGUMENT;
+  const double g = (double)gamma, gl = (double)gamma * (double)lam;
+  for (int64_t i = 0; i < n_rollouts; ++i) {
+    int64_t L = resp_len[i] < 0 ? 0 : (resp_len[i] > max_len ? max_len : resp_len[i]);
+    double v_next = bootstrap ? (double)bootstrap[i] : 0.0;
+    double a = 0.0;
+    for (int64_t t = L - 1; t >= 0; --t) {
+      double v = (double)values[i * max_len + t];
+      double delta = ((double)rewards[i * max_len + t] + g * v_next) - v;
+      a = delta + gl * a;
+      adv[i * max_len + t] = (float)a;
+      if (returns) returns[i * max_len + t] = (float)(a + v);
+      v_next = v;
+    }
   }
   return REF_OK;
 }
@@ -361,13 +420,15 @@ int echo_ref_token_logp(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtype
 }
 
 /* Scalar loss of a set of rows as a function of the logits, for finite-difference pins of (5):
- * returns (1/N_global) * sum_t l_t * grad_scale, i.e. the quantity whose gradient dlogits is. */
+ * returns grad_scale * sum_t w_t l_t (w_t = tok_weight[t] or 1 / N_global), i.e. the quantity whose gradient
+ * dlogits is. */
 double echo_ref_scaled_loss(int64_t n_rows, int32_t vocab, int64_t ld, const double* logits,
                             const int32_t* tok_action, const float* tok_old, const float* tok_ref,
-                            const int32_t* tok_slot, const float* adv_slot, double n_global,
-                            float clip_low, float clip_high, float kl_coef, float grad_scale) {
+                            const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
+                            const float* tok_weight, double n_global, float clip_low, float clip_high,
+                            float clip_dual, float kl_coef, int32_t kl_estimator, float grad_scale) {
   const double lo = 1.0 - (double)clip_low, hi = 1.0 + (double)clip_high;
-  const double beta = (double)kl_coef;
+  const double beta = (double)kl_coef, dual = (double)clip_dual;
   double total = 0.0;
   for (int64_t t = 0; t < n_rows; ++t) {
     const double* z = logits + t * ld;
@@ -376,17 +437,16 @@ double echo_ref_scaled_loss(int64_t n_rows, int32_t vocab, int64_t ld, const dou
     double s = 0.0;
     for (int64_t v = 0; v < vocab; ++v) s = s + exp(z[v] - m);
     double logp = z[tok_action[t]] - (m + log(s));
-    double A = (double)adv_slot[tok_slot[t]];
+    double A = adv_of(tok_adv, tok_slot, adv_slot, t);
     double rho = exp(logp - (double)tok_old[t]);
     double rho_c = rho < lo ? lo : (rho > hi ? hi : rho);
     double un = -A * rho, cl = -A * rho_c;
     double pg = un > cl ? un : cl;
+    if (dual > 1.0 && A < 0.0 && pg > -A * dual) pg = -A * dual;
     double kl = 0.0;
-    if (beta > 0.0) {
-      double x = (double)tok_ref[t] - logp;
-      kl = exp(x) - x - 1.0;
-    }
-    total = total + (pg + beta * kl);
+    if (beta > 0.0) kl = kl_value(kl_estimator, (double)tok_ref[t] - logp);
+    double w = tok_weight ? (double)tok_weight[t] : 1.0 / n_global;
+    total = total + w * (pg + beta * kl);
   }
-  return (double)grad_scale * total / n_global;
+  return (double)grad_scale * total;
 }

@@ -25,11 +25,20 @@ PACK_RESULT_BYTES = 32
 
 # kernels launched per call (for the bench's gpu_launches count)
 LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2,
-            "echo_token_logp": 1}
+            "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1}
 
 EXPORTS = ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
-           "echo_policy_loss_launch_shape", "echo_token_logp",
+           "echo_policy_loss_launch_shape", "echo_token_logp", "echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage",
            "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_status_string", "echo_abi_version")
+
+
+ECHO_KL_K3, ECHO_KL_K1, ECHO_KL_K2 = range(3)
+
+
+class LossConfig(ctypes.Structure):
+    """echo_loss_config (include/echo.h)."""
+    _fields_ = [("clip_low", ctypes.c_float), ("clip_high", ctypes.c_float), ("clip_dual", ctypes.c_float),
+                ("kl_coef", ctypes.c_float), ("grad_scale", ctypes.c_float), ("kl_estimator", ctypes.c_int32)]
 
 
 class EchoError(RuntimeError):
@@ -44,14 +53,20 @@ def _load(path=LIB_PATH):
     lib = ctypes.CDLL(path)
     P = ctypes.c_void_p
     i32, i64, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float
-    lib.echo_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, i64, P, P, P, P, P, P, P, P]
+    lib.echo_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, P, i64, P, P, P, P, P, P, P, P,
+                                    P]
+    lib.echo_gae_advantage.argtypes = [i32, i32, P, P, P, P, f32, f32, P, P, P]
+    lib.echo_gae_advantage.restype = ctypes.c_int
     lib.echo_group_advantage.argtypes = [i32, i32, f32, P, P, i64, P, P, P, P]
     lib.echo_policy_loss_fwd_bwd.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P, P, f32, f32, f32, f32, P, P, P, P]
     lib.echo_policy_loss_fwd_bwd_ex.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P, P, f32, f32, f32, f32, P, P, P,
                                                 i32, P]
-    lib.echo_loss_stats.argtypes = [i64, P, P, P, P, P, P, P, P]
+    lib.echo_loss_stats.argtypes = [i64, P, P, P, P, P, P, P, P, P]
     lib.echo_policy_loss_launch_shape.argtypes = [i32, i64, i32, i32, P]
     lib.echo_token_logp.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P]
+    lib.echo_policy_loss_fwd_bwd_v2.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P, P, P, P,
+                                                ctypes.POINTER(LossConfig), P, P, P, i32, P]
+    lib.echo_policy_loss_fwd_bwd_v2.restype = ctypes.c_int
     lib.echo_token_logp.restype = ctypes.c_int
     lib.echo_policy_loss_launch_shape.restype = ctypes.c_int
     lib.echo_loss_stats_workspace_bytes.argtypes = []
@@ -60,7 +75,7 @@ def _load(path=LIB_PATH):
     lib.echo_status_string.restype = ctypes.c_char_p
     lib.echo_abi_version.restype = i32
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
-               "echo_loss_stats"):
+               "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2"):
         getattr(lib, fn).restype = ctypes.c_int
     return lib
 
@@ -100,11 +115,18 @@ def echo_status_string(status: int) -> str:
 
 def echo_pack_batch(n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, version, resp_len, action,
                     old_logp, ref_logp, token_capacity, kept_rollout, kept_offset, tok_slot, tok_action, tok_old,
-                    tok_ref, result, stream=None):
+                    tok_ref, result, stream=None, aux=None, tok_aux=None):
     _check("echo_pack_batch", _lib.echo_pack_batch(
         n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, _p(version), _p(resp_len), _p(action),
-        _p(old_logp), _p(ref_logp), token_capacity, _p(kept_rollout), _p(kept_offset), _p(tok_slot), _p(tok_action),
-        _p(tok_old), _p(tok_ref), _p(result), _s(stream)))
+        _p(old_logp), _p(ref_logp), _p(aux), token_capacity, _p(kept_rollout), _p(kept_offset), _p(tok_slot),
+        _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_aux), _p(result), _s(stream)))
+
+
+def echo_gae_advantage(n_rollouts, max_len, resp_len, rewards, values, bootstrap_value, gamma, lam, adv,
+                       returns=None, stream=None):
+    _check("echo_gae_advantage", _lib.echo_gae_advantage(
+        n_rollouts, max_len, _p(resp_len), _p(rewards), _p(values), _p(bootstrap_value), gamma, lam, _p(adv),
+        _p(returns), _s(stream)))
 
 
 def echo_group_advantage(n_rollouts, group_size, eps, reward, kept_rollout, rollout_base, pack, adv_slot, adv_stats,
@@ -129,6 +151,15 @@ def echo_policy_loss_fwd_bwd(logits, dtype, n_rows, vocab, ld, tok_action, tok_o
             _p(tok_flags), algo, _s(stream)))
 
 
+def echo_policy_loss_fwd_bwd_v2(logits, dtype, n_rows, vocab, ld, tok_action, tok_old, tok_ref, tok_slot, adv_slot,
+                                tok_adv, tok_weight, n_global, cfg: LossConfig, tok_logp, tok_loss, tok_flags,
+                                algo=ECHO_ALGO_AUTO, stream=None):
+    _check("echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage", _lib.echo_policy_loss_fwd_bwd_v2(
+        _p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot), _p(adv_slot),
+        _p(tok_adv), _p(tok_weight), _p(n_global), ctypes.byref(cfg), _p(tok_logp), _p(tok_loss), _p(tok_flags), algo,
+        _s(stream)))
+
+
 def echo_token_logp(logits, dtype, n_rows, vocab, ld, tok_action, tok_logp, tok_lse=None, tok_flags=None,
                     stream=None):
     _check("echo_token_logp", _lib.echo_token_logp(_p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_logp),
@@ -146,10 +177,11 @@ def echo_loss_stats_workspace_bytes() -> int:
     return int(_lib.echo_loss_stats_workspace_bytes())
 
 
-def echo_loss_stats(n_tokens, tok_loss, tok_logp, tok_old, tok_ref, tok_flags, workspace, loss_stats, stream=None):
+def echo_loss_stats(n_tokens, tok_loss, tok_logp, tok_old, tok_ref, tok_flags, workspace, loss_stats, stream=None,
+                    tok_weight=None):
     _check("echo_loss_stats", _lib.echo_loss_stats(
-        n_tokens, _p(tok_loss), _p(tok_logp), _p(tok_old), _p(tok_ref), _p(tok_flags), _p(workspace), _p(loss_stats),
-        _s(stream)))
+        n_tokens, _p(tok_loss), _p(tok_logp), _p(tok_old), _p(tok_ref), _p(tok_weight), _p(tok_flags), _p(workspace),
+        _p(loss_stats), _s(stream)))
 
 
 def parse_pack_result(raw: bytes) -> dict:

@@ -60,10 +60,10 @@ const char* echo_status_string(echo_status s) {
 
 echo_status echo_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len, int32_t vocab, int64_t t_train,
                             int32_t max_lag, int64_t rollout_base, const int64_t* version, const int32_t* resp_len,
-                            const int32_t* action, const float* old_logp, const float* ref_logp,
+                            const int32_t* action, const float* old_logp, const float* ref_logp, const float* aux,
                             int64_t token_capacity, int32_t* kept_rollout, int64_t* kept_offset, int32_t* tok_slot,
-                            int32_t* tok_action, float* tok_old, float* tok_ref, echo_pack_result* result,
-                            void* stream) {
+                            int32_t* tok_action, float* tok_old, float* tok_ref, float* tok_aux,
+                            echo_pack_result* result, void* stream) {
   if (n_rollouts < 0 || group_size < 2 || max_len < 1 || vocab < 1 || max_lag < 0 || token_capacity < 0)
     return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rollouts % group_size != 0) return ECHO_ERR_INVALID_ARGUMENT;
@@ -72,13 +72,27 @@ echo_status echo_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_
     return ECHO_ERR_INVALID_ARGUMENT;
   if (token_capacity > 0 && (!tok_slot || !tok_action || !tok_old)) return ECHO_ERR_INVALID_ARGUMENT;
   if ((ref_logp == nullptr) != (tok_ref == nullptr)) return ECHO_ERR_INVALID_ARGUMENT;
+  if ((aux == nullptr) != (tok_aux == nullptr)) return ECHO_ERR_INVALID_ARGUMENT;
   int sms = 0;
   echo_status st = device_sms(&sms);
   if (st != ECHO_OK) return st;
   return from_cuda(echo::launch_pack(n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, version,
-                                     resp_len, action, old_logp, ref_logp, token_capacity, kept_rollout, kept_offset,
-                                     tok_slot, tok_action, tok_old, tok_ref, result,
+                                     resp_len, action, old_logp, ref_logp, aux, token_capacity, kept_rollout,
+                                     kept_offset, tok_slot, tok_action, tok_old, tok_ref, tok_aux, result,
                                      static_cast<cudaStream_t>(stream), sms));
+}
+
+echo_status echo_gae_advantage(int32_t n_rollouts, int32_t max_len, const int32_t* resp_len, const float* rewards,
+                               const float* values, const float* bootstrap_value, float gamma, float lam, float* adv,
+                               float* returns, void* stream) {
+  if (n_rollouts < 0 || max_len < 1 || !(gamma >= 0.0f && gamma <= 1.0f) || !(lam >= 0.0f && lam <= 1.0f))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rollouts > 0 && (!resp_len || !rewards || !values || !adv)) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  return from_cuda(echo::launch_gae(n_rollouts, max_len, resp_len, rewards, values, bootstrap_value, gamma, lam, adv,
+                                    returns, static_cast<cudaStream_t>(stream)));
 }
 
 echo_status echo_group_advantage(int32_t n_rollouts, int32_t group_size, float eps, const float* reward,
@@ -95,23 +109,27 @@ echo_status echo_group_advantage(int32_t n_rollouts, int32_t group_size, float e
                                                 adv_stats, static_cast<cudaStream_t>(stream)));
 }
 
-echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
+echo_status echo_policy_loss_fwd_bwd_v2(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
                                         const int32_t* tok_action, const float* tok_old, const float* tok_ref,
-                                        const int32_t* tok_slot, const float* adv_slot, const double* n_global,
-                                        float clip_low, float clip_high, float kl_coef, float grad_scale,
+                                        const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
+                                        const float* tok_weight, const double* n_global, const echo_loss_config* cfg,
                                         float* tok_logp, float* tok_loss, uint8_t* tok_flags, int32_t algo,
                                         void* stream) {
+  if (!cfg) return ECHO_ERR_INVALID_ARGUMENT;
   if (dtype != ECHO_F32 && dtype != ECHO_BF16) return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rows < 0 || vocab < 1 || ld < vocab) return ECHO_ERR_INVALID_ARGUMENT;
   const int64_t esize = dtype == ECHO_BF16 ? 2 : 4;
   if ((ld * esize) % 16 != 0) return ECHO_ERR_INVALID_ARGUMENT;
-  if (!(clip_low >= 0.0f && clip_low < 1.0f && clip_high >= 0.0f) || !(kl_coef >= 0.0f)) return ECHO_ERR_INVALID_ARGUMENT;
-  if (!n_global) return ECHO_ERR_INVALID_ARGUMENT;
+  if (!(cfg->clip_low >= 0.0f && cfg->clip_low < 1.0f && cfg->clip_high >= 0.0f) || !(cfg->kl_coef >= 0.0f) ||
+      !(cfg->clip_dual == 0.0f || cfg->clip_dual > 1.0f) || cfg->kl_estimator < ECHO_KL_K3 ||
+      cfg->kl_estimator > ECHO_KL_K2)
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (!n_global && !tok_weight) return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rows > 0) {
-    if (!logits || !aligned16(logits) || !tok_action || !tok_old || !tok_slot || !adv_slot || !tok_logp ||
-        !tok_loss || !tok_flags)
+    if (!logits || !aligned16(logits) || !tok_action || !tok_old || !tok_logp || !tok_loss || !tok_flags)
       return ECHO_ERR_INVALID_ARGUMENT;
-    if (kl_coef > 0.0f && !tok_ref) return ECHO_ERR_INVALID_ARGUMENT;
+    if (!tok_adv && (!tok_slot || !adv_slot)) return ECHO_ERR_INVALID_ARGUMENT;
+    if (cfg->kl_coef > 0.0f && !tok_ref) return ECHO_ERR_INVALID_ARGUMENT;
   }
   int sms = 0;
   echo_status st = device_sms(&sms);
@@ -119,7 +137,7 @@ echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_r
   if (n_rows == 0) return ECHO_OK;
   st = resolve_algo(dtype, vocab, &algo);
   if (st != ECHO_OK) return st;
-  echo::LossParams p;
+  echo::LossParams p{};
   p.logits = static_cast<uint8_t*>(logits);
   p.n_rows = n_rows;
   p.V = vocab;
@@ -130,10 +148,14 @@ echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_r
   p.tok_slot = tok_slot;
   p.adv_slot = adv_slot;
   p.n_global = n_global;
-  p.clip_low = clip_low;
-  p.clip_high = clip_high;
-  p.kl_coef = kl_coef;
-  p.grad_scale = grad_scale;
+  p.clip_low = cfg->clip_low;
+  p.clip_high = cfg->clip_high;
+  p.kl_coef = cfg->kl_coef;
+  p.grad_scale = cfg->grad_scale;
+  p.clip_dual = cfg->clip_dual;
+  p.kl_estimator = cfg->kl_estimator;
+  p.tok_adv = tok_adv;
+  p.tok_weight = tok_weight;
   p.tok_logp = tok_logp;
   p.tok_loss = tok_loss;
   p.tok_flags = tok_flags;
@@ -145,6 +167,19 @@ echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_r
   p.trace_rows = g_trace_rows;
 #endif
   return from_cuda(echo::launch_policy_loss(p, dtype, algo, static_cast<cudaStream_t>(stream), sms));
+}
+
+echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
+                                        const int32_t* tok_action, const float* tok_old, const float* tok_ref,
+                                        const int32_t* tok_slot, const float* adv_slot, const double* n_global,
+                                        float clip_low, float clip_high, float kl_coef, float grad_scale,
+                                        float* tok_logp, float* tok_loss, uint8_t* tok_flags, int32_t algo,
+                                        void* stream) {
+  if (!n_global) return ECHO_ERR_INVALID_ARGUMENT;
+  const echo_loss_config cfg{clip_low, clip_high, 0.0f, kl_coef, grad_scale, ECHO_KL_K3};
+  return echo_policy_loss_fwd_bwd_v2(logits, dtype, n_rows, vocab, ld, tok_action, tok_old, tok_ref, tok_slot,
+                                     adv_slot, nullptr, nullptr, n_global, &cfg, tok_logp, tok_loss, tok_flags, algo,
+                                     stream);
 }
 
 echo_status echo_policy_loss_fwd_bwd(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
@@ -213,15 +248,15 @@ echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, i
 size_t echo_loss_stats_workspace_bytes(void) { return echo::loss_stats_workspace_bytes(); }
 
 echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp, const float* tok_old,
-                            const float* tok_ref, const uint8_t* tok_flags, double* workspace, double* loss_stats,
-                            void* stream) {
+                            const float* tok_ref, const float* tok_weight, const uint8_t* tok_flags, double* workspace,
+                            double* loss_stats, void* stream) {
   if (n_tokens < 0 || !workspace || !loss_stats) return ECHO_ERR_INVALID_ARGUMENT;
   if (n_tokens > 0 && (!tok_loss || !tok_logp || !tok_old || !tok_flags)) return ECHO_ERR_INVALID_ARGUMENT;
   int sms = 0;
   echo_status st = device_sms(&sms);
   if (st != ECHO_OK) return st;
-  return from_cuda(echo::launch_loss_stats(n_tokens, tok_loss, tok_logp, tok_old, tok_ref, tok_flags, workspace,
-                                           loss_stats, static_cast<cudaStream_t>(stream)));
+  return from_cuda(echo::launch_loss_stats(n_tokens, tok_loss, tok_logp, tok_old, tok_ref, tok_weight, tok_flags,
+                                           workspace, loss_stats, static_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"

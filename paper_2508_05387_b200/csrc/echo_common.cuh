@@ -236,57 +236,48 @@ ECHO_DEVINL MaxSum warp_maxsum(MaxSum v) {
 
 // ---------------------------------------------------------------- the per-row scalar epilogue (4)
 struct RowScalars {
-  float logp, loss, coef;  // coef = c_t: dl/dlogp * grad_scale / N_global
+  float logp, loss, coef;  // coef = c_t: dl/dlogp * scale  (scale = grad_scale * w_t, w_t = 1/N_global or tok_weight)
   uint8_t flags;
 };
-// lse: log-sum-exp of the row; za: logit at the action.
-ECHO_DEVINL RowScalars row_epilogue(float lse, float za, float old, float ref, float adv, float clip_low,
-                                    float clip_high, float kl_coef, float grad_scale, double n_global) {
-  RowScalars r;
-  float logp = za - lse;
-  float rho = expf(logp - old);
-  float lo = 1.0f - clip_low, hi = 1.0f + clip_high;
-  bool clipped = (adv > 0.0f && rho > hi) || (adv < 0.0f && rho < lo);
-  float rho_c = fminf(fmaxf(rho, lo), hi);
-  float pg = fmaxf(-adv * rho, -adv * rho_c);
-  float kl = 0.0f, dkl = 0.0f;
-  if (kl_coef > 0.0f) {
-    float x = ref - logp;
-    float ex = expf(x);
-    kl = ex - x - 1.0f;
-    dkl = 1.0f - ex;
-  }
-  float loss = pg + kl_coef * kl;
-  float dl = (clipped ? 0.0f : -adv * rho) + kl_coef * dkl;
-  float coef = (float)((double)grad_scale * (double)dl / n_global);
-  bool finite = isfinite(lse) && isfinite(logp) && isfinite(rho) && isfinite(loss) && isfinite(coef);
-  r.logp = logp;
-  r.loss = loss;
-  r.coef = coef;
-  r.flags = (uint8_t)((clipped ? ECHO_FLAG_CLIPPED : 0) | (finite ? 0 : ECHO_FLAG_NONFINITE));
-  return r;
-}
-
-// Same epilogue with the coefficient scale s / N_global folded into one fp32 factor (per-kernel constant).
-ECHO_DEVINL RowScalars row_epilogue_f(float lse, float za, float old, float ref, float adv, float clip_low,
-                                      float clip_high, float kl_coef, float gscale) {
+struct LossOpts {
+  float clip_low, clip_high, clip_dual, kl_coef;
+  int32_t kl_estimator;  // ECHO_KL_K3 | ECHO_KL_K1 | ECHO_KL_K2
+};
+// lse: log-sum-exp of the row; za: logit at the action; adv: the token's advantage; scale: grad_scale * w_t.
+//   rho = exp(logp - old); pg = max(-A rho, -A clip(rho, 1-lo, 1+hi)) (SPEC.md :219); dual clip (A < 0,
+//   rho > c): pg = -A c; KL to pi_ref by the selected estimator (x = ref - logp): k3 e^x - x - 1 (default),
+//   k1 -x, k2 x^2/2; l_t = pg + beta kl; c_t = scale * ([not clipped](-A rho) + beta dkl/dlogp).
+ECHO_DEVINL RowScalars row_epilogue(float lse, float za, float old, float ref, float adv, const LossOpts& o,
+                                    float scale) {
   RowScalars r;
   const float logp = za - lse;
   const float rho = expf(logp - old);
-  const float lo = 1.0f - clip_low, hi = 1.0f + clip_high;
-  const bool clipped = (adv > 0.0f && rho > hi) || (adv < 0.0f && rho < lo);
+  const float lo = 1.0f - o.clip_low, hi = 1.0f + o.clip_high;
+  bool clipped = (adv > 0.0f && rho > hi) || (adv < 0.0f && rho < lo);
   const float rho_c = fminf(fmaxf(rho, lo), hi);
-  const float pg = fmaxf(-adv * rho, -adv * rho_c);
-  float kl = 0.0f, dkl = 0.0f;
-  if (kl_coef > 0.0f) {
-    const float x = ref - logp;
-    const float ex = expf(x);
-    kl = ex - x - 1.0f;
-    dkl = 1.0f - ex;
+  float pg = fmaxf(-adv * rho, -adv * rho_c);
+  if (o.clip_dual > 1.0f && adv < 0.0f && pg > -adv * o.clip_dual) {
+    pg = -adv * o.clip_dual;
+    clipped = true;
   }
-  const float loss = pg + kl_coef * kl;
-  const float dl = (clipped ? 0.0f : -adv * rho) + kl_coef * dkl;
-  const float coef = dl * gscale;
+  float kl = 0.0f, dkl = 0.0f;
+  if (o.kl_coef > 0.0f) {
+    const float x = ref - logp;
+    if (o.kl_estimator == ECHO_KL_K1) {
+      kl = -x;
+      dkl = 1.0f;
+    } else if (o.kl_estimator == ECHO_KL_K2) {
+      kl = 0.5f * x * x;
+      dkl = -x;
+    } else {
+      const float ex = expf(x);
+      kl = ex - x - 1.0f;
+      dkl = 1.0f - ex;
+    }
+  }
+  const float loss = pg + o.kl_coef * kl;
+  const float dl = (clipped ? 0.0f : -adv * rho) + o.kl_coef * dkl;
+  const float coef = dl * scale;
   const bool finite = isfinite(lse) && isfinite(logp) && isfinite(rho) && isfinite(loss) && isfinite(coef);
   r.logp = logp;
   r.loss = loss;

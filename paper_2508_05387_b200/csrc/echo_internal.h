@@ -21,6 +21,10 @@ struct LossParams {
   const float* __restrict__ adv_slot;
   const double* __restrict__ n_global;
   float clip_low, clip_high, kl_coef, grad_scale;
+  float clip_dual;                          // dual-clip constant c (> 1 enables), f4
+  int32_t kl_estimator;                     // ECHO_KL_*, f4
+  const float* __restrict__ tok_adv;        // per-token advantages (nullable: adv_slot[tok_slot])
+  const float* __restrict__ tok_weight;     // per-token loss weights (nullable: 1 / N_global)
   float* __restrict__ tok_logp;
   float* __restrict__ tok_loss;
   uint8_t* __restrict__ tok_flags;
@@ -31,9 +35,10 @@ struct LossParams {
 
 cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_train, int32_t max_lag,
                         int64_t rollout_base, const int64_t* version, const int32_t* resp_len, const int32_t* action,
-                        const float* old_logp, const float* ref_logp, int64_t cap, int32_t* kept_rollout,
-                        int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
-                        echo_pack_result* res, cudaStream_t stream, int num_sms);
+                        const float* old_logp, const float* ref_logp, const float* aux, int64_t cap,
+                        int32_t* kept_rollout, int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action,
+                        float* tok_old, float* tok_ref, float* tok_aux, echo_pack_result* res, cudaStream_t stream,
+                        int num_sms);
 
 cudaError_t launch_group_advantage(int32_t G, float eps, int64_t rollout_base, const float* reward,
                                    const int32_t* kept_rollout, const echo_pack_result* pack, float* adv_slot,
@@ -57,9 +62,12 @@ cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, La
 cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms,
                                LaunchShape* shape = nullptr);
 
+cudaError_t launch_gae(int32_t R, int32_t S, const int32_t* resp_len, const float* rewards, const float* values,
+                       const float* bootstrap, float gamma, float lam, float* adv, float* ret, cudaStream_t stream);
+
 size_t loss_stats_workspace_bytes();
 cudaError_t launch_loss_stats(int64_t n, const float* tok_loss, const float* tok_logp, const float* tok_old,
-                              const float* tok_ref, const uint8_t* tok_flags, double* ws, double* out,
-                              cudaStream_t stream);
+                              const float* tok_ref, const float* tok_weight, const uint8_t* tok_flags, double* ws,
+                              double* out, cudaStream_t stream);
 
 }  // namespace echo

@@ -1,7 +1,7 @@
 // loss_stats.cu -- fixed-order fp64 reduction of the per-token outputs into the 10-entry stats vector.
 //
 //   loss_stats = {sum l, sum (logp-old), sum k3(ref,logp), n_clipped, n_nonfinite, rho_min, rho_max,
-//                 sum logp, n_tokens, sum rho}
+//                 sum logp, n_tokens, sum rho, sum w l}
 // Launch 1: kStatBlocks (fixed) blocks; block b owns tokens [b*n/B, (b+1)*n/B) and reduces them with a
 // fixed thread-strided loop + fixed shuffle tree into workspace[b].  Launch 2: one warp per statistic folds
 // the B partials in a fixed order (contiguous lane ranges, then an xor tree).  The partition depends only on n_tokens, so the result is bitwise
@@ -13,7 +13,7 @@ namespace echo {
 
 constexpr int kStatBlocks = 296;  // 2 x 148 SMs
 constexpr int kStatThreads = 256;
-constexpr int kNStat = 10;
+constexpr int kNStat = 11;
 
 struct Acc {
   double v[kNStat];
@@ -33,7 +33,8 @@ ECHO_DEVINL void acc_merge(Acc& a, const Acc& b) {
 
 __global__ void __launch_bounds__(kStatThreads) loss_stats_partial_kernel(
     int64_t n, const float* __restrict__ tok_loss, const float* __restrict__ tok_logp, const float* __restrict__ tok_old,
-    const float* __restrict__ tok_ref, const uint8_t* __restrict__ tok_flags, double* __restrict__ ws) {
+    const float* __restrict__ tok_ref, const float* __restrict__ tok_weight, const uint8_t* __restrict__ tok_flags,
+    double* __restrict__ ws) {
   __shared__ double s[kStatThreads / 32][kNStat];
   const int64_t lo = (int64_t)blockIdx.x * n / kStatBlocks, hi = (int64_t)(blockIdx.x + 1) * n / kStatBlocks;
   Acc a;
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(kStatThreads) loss_stats_partial_kernel(
     }
     a.v[7] += (double)logp;
     a.v[8] += 1.0;
+    a.v[10] += (tok_weight ? (double)tok_weight[t] : 1.0) * (double)tok_loss[t];
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -107,10 +109,10 @@ __global__ void __launch_bounds__(32 * kNStat) loss_stats_final_kernel(const dou
 size_t loss_stats_workspace_bytes() { return sizeof(double) * kStatBlocks * kNStat; }
 
 cudaError_t launch_loss_stats(int64_t n, const float* tok_loss, const float* tok_logp, const float* tok_old,
-                              const float* tok_ref, const uint8_t* tok_flags, double* ws, double* out,
-                              cudaStream_t stream) {
+                              const float* tok_ref, const float* tok_weight, const uint8_t* tok_flags, double* ws,
+                              double* out, cudaStream_t stream) {
   loss_stats_partial_kernel<<<kStatBlocks, kStatThreads, 0, stream>>>(n, tok_loss, tok_logp, tok_old, tok_ref,
-                                                                      tok_flags, ws);
+                                                                      tok_weight, tok_flags, ws);
   loss_stats_final_kernel<<<1, 32 * kNStat, 0, stream>>>(ws, out);
   return cudaGetLastError();
 }

@@ -112,9 +112,10 @@ __global__ void __launch_bounds__(kScanThreads) pack_scan_kernel(
 
 __global__ void __launch_bounds__(256) pack_gather_kernel(
     int32_t S, int32_t V, int64_t rollout_base, int64_t cap, const int32_t* __restrict__ action,
-    const float* __restrict__ old_logp, const float* __restrict__ ref_logp, const int32_t* __restrict__ kept_rollout,
-    const int64_t* __restrict__ kept_offset, int32_t* __restrict__ tok_slot, int32_t* __restrict__ tok_action,
-    float* __restrict__ tok_old, float* __restrict__ tok_ref, echo_pack_result* __restrict__ res) {
+    const float* __restrict__ old_logp, const float* __restrict__ ref_logp, const float* __restrict__ aux,
+    const int32_t* __restrict__ kept_rollout, const int64_t* __restrict__ kept_offset, int32_t* __restrict__ tok_slot,
+    int32_t* __restrict__ tok_action, float* __restrict__ tok_old, float* __restrict__ tok_ref,
+    float* __restrict__ tok_aux, echo_pack_result* __restrict__ res) {
   __shared__ unsigned long long s_bad;
   const int32_t n_kept = res->n_rollouts_kept;
   const bool write = res->n_tokens <= cap;
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(256) pack_gather_kernel(
         tok_action[off + j] = a;
         tok_old[off + j] = old_logp[src + j];
         if (tok_ref) tok_ref[off + j] = ref_logp[src + j];
+        if (tok_aux) tok_aux[off + j] = aux[src + j];
       }
     }
     __syncthreads();
@@ -157,14 +159,16 @@ __global__ void pack_finalize_kernel(int64_t rollout_base, int64_t cap, echo_pac
 
 cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_train, int32_t max_lag,
                         int64_t rollout_base, const int64_t* version, const int32_t* resp_len, const int32_t* action,
-                        const float* old_logp, const float* ref_logp, int64_t cap, int32_t* kept_rollout,
-                        int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
-                        echo_pack_result* res, cudaStream_t stream, int num_sms) {
+                        const float* old_logp, const float* ref_logp, const float* aux, int64_t cap,
+                        int32_t* kept_rollout, int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action,
+                        float* tok_old, float* tok_ref, float* tok_aux, echo_pack_result* res, cudaStream_t stream,
+                        int num_sms) {
   pack_scan_kernel<<<1, kScanThreads, 0, stream>>>(R, G, S, t_train, max_lag, rollout_base, version, resp_len,
                                                    kept_rollout, kept_offset, res);
   int grid = R < num_sms * 8 ? (R > 0 ? R : 1) : num_sms * 8;
-  pack_gather_kernel<<<grid, 256, 0, stream>>>(S, V, rollout_base, cap, action, old_logp, ref_logp, kept_rollout,
-                                               kept_offset, tok_slot, tok_action, tok_old, tok_ref, res);
+  pack_gather_kernel<<<grid, 256, 0, stream>>>(S, V, rollout_base, cap, action, old_logp, ref_logp, aux,
+                                               kept_rollout, kept_offset, tok_slot, tok_action, tok_old, tok_ref,
+                                               tok_aux, res);
   pack_finalize_kernel<<<1, 1, 0, stream>>>(rollout_base, cap, res);
   return cudaGetLastError();
 }

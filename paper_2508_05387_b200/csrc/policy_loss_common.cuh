@@ -23,14 +23,22 @@ namespace echo {
 
 // ====================================================================== shared per-row helpers
 struct RowMeta {
-  float old, ref, adv;
+  float old, ref, adv, w;  // w: per-token loss weight (1 when the 1 / N_global scale applies)
 };
 ECHO_DEVINL RowMeta load_meta(const LossParams& p, int64_t row) {
   RowMeta m;
   m.old = p.tok_old[row];
   m.ref = (p.kl_coef > 0.0f) ? p.tok_ref[row] : 0.0f;
-  m.adv = p.adv_slot[p.tok_slot[row]];
+  m.adv = p.tok_adv ? p.tok_adv[row] : p.adv_slot[p.tok_slot[row]];
+  m.w = p.tok_weight ? p.tok_weight[row] : 1.0f;
   return m;
+}
+ECHO_DEVINL LossOpts loss_opts(const LossParams& p) {
+  return LossOpts{p.clip_low, p.clip_high, p.clip_dual, p.kl_coef, p.kl_estimator};
+}
+// grad_scale / N_global, or grad_scale alone when per-token weights carry the normalisation
+ECHO_DEVINL float base_scale(const LossParams& p) {
+  return p.tok_weight ? p.grad_scale : (float)((double)p.grad_scale / *p.n_global);
 }
 
 // Online update of (m, s) with N values already in registers.  -inf entries contribute 0.

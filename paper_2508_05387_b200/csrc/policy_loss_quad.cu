@@ -146,7 +146,8 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     xbar_remote[r] = mapa(smem_u32(&sm.xbar[0]), r);
   }
   const uint64_t st_pol = policy_evict_first();
-  const float gscale = kGrad ? (float)((double)p.grad_scale / *p.n_global) : 0.0f;
+  const float gscale = kGrad ? base_scale(p) : 0.0f;
+  const LossOpts opts = loss_opts(p);
   const int32_t col_t = c0 + tid * 8;
   const bool last_valid = (uint32_t)(nchunks - 1) * C::kChunk + (uint32_t)tid * 16u < g.slice_bytes;
   const bool has_tail = (c1 & 7) && (c1 & ~7) >= col_t && ((c1 & ~7) - col_t) % C::kChunkElems == 0;
@@ -282,8 +283,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         const float lse = mm + logf(ss);
         if (a < 0 || a >= V) za = NAN;
         if constexpr (kGrad) {
-          const RowScalars r = row_epilogue_f(lse, za, meta.old, meta.ref, meta.adv, p.clip_low, p.clip_high,
-                                              p.kl_coef, gscale);
+          const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, opts, gscale * meta.w);
           if (rank == 0) {
             p.tok_logp[row] = r.logp;
             p.tok_loss[row] = r.loss;

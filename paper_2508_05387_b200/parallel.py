@@ -56,7 +56,7 @@ def allreduce_max_(t: torch.Tensor, group=None) -> torch.Tensor:
 STATS1 = ("n_tokens", "sum_adv", "sum_adv2", "sum_reward", "sum_reward2", "n_zero_std_groups", "n_rollouts_kept",
           "n_groups_kept", "n_groups_dropped")
 LOSS_STATS = ("sum_loss", "sum_logp_minus_old", "sum_kl_k3", "n_clipped", "n_nonfinite", "rho_min", "rho_max",
-              "sum_logp", "n_tokens", "sum_rho")
+              "sum_logp", "n_tokens", "sum_rho", "sum_weighted_loss")
 
 
 def reduce_loss_stats_(stats: torch.Tensor, group=None) -> torch.Tensor:

@@ -121,23 +121,36 @@ class LearnerStep:
 
     # ------------------------------------------------------------------ (3)-(5)
     def loss(self, logits: torch.Tensor, row0: int, *, clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0,
-             algo=None, stream=None):
-        """Fused loss fwd+bwd over packed rows [row0, row0 + logits.shape[0]); logits become dlogits."""
+             algo=None, stream=None, tok_adv=None, tok_weight=None, clip_dual=0.0, kl_estimator=abi.ECHO_KL_K3):
+        """Fused loss fwd+bwd over packed rows [row0, row0 + logits.shape[0]); logits become dlogits.
+
+        f4 options (echo_policy_loss_fwd_bwd_v2): ``tok_adv`` / ``tok_weight`` are full-length per-token device
+        arrays (per-token advantages, e.g. GAE; per-token loss weights, e.g. sequence-mean), ``clip_dual`` and
+        ``kl_estimator`` select the dual clip and the KL estimator."""
         n_rows, ld = logits.shape
         sl = slice(row0, row0 + n_rows)
-        abi.echo_policy_loss_fwd_bwd(logits, self.edtype, n_rows, self.V, ld, self.tok_action[sl], self.tok_old[sl],
-                                     self.tok_ref[sl] if (self.tok_ref is not None and kl_coef > 0) else None,
-                                     self.tok_slot[sl], self.adv_slot, self.stats1[0:1], clip_low, clip_high, kl_coef,
-                                     grad_scale, self.tok_logp[sl], self.tok_loss[sl], self.tok_flags[sl],
-                                     stream=stream, algo=algo)
+        ref = self.tok_ref[sl] if (self.tok_ref is not None and kl_coef > 0) else None
+        if tok_adv is None and tok_weight is None and clip_dual == 0.0 and kl_estimator == abi.ECHO_KL_K3:
+            abi.echo_policy_loss_fwd_bwd(logits, self.edtype, n_rows, self.V, ld, self.tok_action[sl], self.tok_old[sl],
+                                         ref, self.tok_slot[sl], self.adv_slot, self.stats1[0:1], clip_low, clip_high,
+                                         kl_coef, grad_scale, self.tok_logp[sl], self.tok_loss[sl], self.tok_flags[sl],
+                                         stream=stream, algo=algo)
+        else:
+            cfg = abi.LossConfig(clip_low, clip_high, clip_dual, kl_coef, grad_scale, kl_estimator)
+            abi.echo_policy_loss_fwd_bwd_v2(logits, self.edtype, n_rows, self.V, ld, self.tok_action[sl],
+                                            self.tok_old[sl], ref, self.tok_slot[sl], self.adv_slot,
+                                            None if tok_adv is None else tok_adv[sl],
+                                            None if tok_weight is None else tok_weight[sl], self.stats1[0:1], cfg,
+                                            self.tok_logp[sl], self.tok_loss[sl], self.tok_flags[sl],
+                                            algo=abi.ECHO_ALGO_AUTO if algo is None else algo, stream=stream)
         self.launches += abi.LAUNCHES["echo_policy_loss_fwd_bwd"] if n_rows > 0 else 0
 
     # ------------------------------------------------------------------ statistics
-    def finish(self, read_back: bool = True) -> dict | None:
+    def finish(self, read_back: bool = True, tok_weight=None) -> dict | None:
         n = self.pack_info.n_tokens
         abi.echo_loss_stats(n, self.tok_loss, self.tok_logp, self.tok_old,
                             self.tok_ref if self.tok_ref is not None else None, self.tok_flags, self.ws,
-                            self.loss_stats)
+                            self.loss_stats, tok_weight=tok_weight)
         self.launches += abi.LAUNCHES["echo_loss_stats"]
         reduce_loss_stats_(self.loss_stats, self.group)
         if not read_back:
@@ -148,7 +161,10 @@ class LearnerStep:
         v = self.stats_host.tolist()
         out = dict(zip(STATS1, v[: len(STATS1)]))
         out.update({"loss/" + k: x for k, x in zip(LOSS_STATS, v[len(STATS1):])})
-        out["loss"] = out["loss/sum_loss"] / out["n_tokens"] if out["n_tokens"] else 0.0
+        if tok_weight is not None:
+            out["loss"] = out["loss/sum_weighted_loss"]
+        else:
+            out["loss"] = out["loss/sum_loss"] / out["n_tokens"] if out["n_tokens"] else 0.0
         return out
 
     def d2h_bytes(self) -> int:

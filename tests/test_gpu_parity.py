@@ -414,3 +414,79 @@ def test_token_logp_forward_only(name):
     # consistency with the fused kernel's logp on the same rows
     st.loss(logits, 0, kl_coef=0.0)
     assert torch.equal(st.tok_logp[:n], logp) or name == "tiny"   # same reduction tree on the quad path
+
+
+# ---------------------------------------------------------------------------------------------- f4: variants
+def test_gae_bit_exact_and_packed_aux():
+    """PPO-GAE advantages (echo_gae_advantage) bit-identical to the fp64 oracle; echo_pack_batch carries them."""
+    from paper_2508_05387_b200 import abi
+    rng = np.random.default_rng(3)
+    for R, S in ((16, 64), (512, 2048)):
+        L = rng.integers(1, S + 1, R).astype(np.int32)
+        r = rng.normal(size=(R, S)).astype(np.float32)
+        v = rng.normal(size=(R, S)).astype(np.float32)
+        boot = rng.normal(size=R).astype(np.float32)
+        ref_adv, ref_ret = oracle.gae_advantage(L, r, v, gamma=0.99, lam=0.95, bootstrap=boot)
+        c = lambda x: torch.from_numpy(x).cuda()
+        adv = torch.zeros(R, S, device="cuda")
+        ret = torch.zeros(R, S, device="cuda")
+        abi.echo_gae_advantage(R, S, c(L), c(r), c(v), c(boot), 0.99, 0.95, adv, ret)
+        assert adv.cpu().numpy().tobytes() == ref_adv.tobytes()
+        assert ret.cpu().numpy().tobytes() == ref_ret.tobytes()
+    # packed through echo_pack_batch's aux payload
+    cfg = synth.CONFIGS["tiny"]
+    b = synth.make_batch(cfg, lengths="ragged")
+    aux = rng.normal(size=(cfg.R, cfg.S)).astype(np.float32)
+    st, info = device_step(cfg, b)
+    from paper_2508_05387_b200 import abi as a2
+    tok_aux = torch.zeros(st.cap, device="cuda")
+    a2.echo_pack_batch(cfg.R, cfg.G, cfg.S, cfg.V, synth.T_TRAIN, cfg.max_lag, 0, st.version, st.resp_len, st.action,
+                       st.old_logp, st.ref_logp, st.cap, st.kept_rollout, st.kept_offset, st.tok_slot, st.tok_action,
+                       st.tok_old, st.tok_ref, st.pack_result, aux=torch.from_numpy(aux).cuda(), tok_aux=tok_aux)
+    pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,
+                           vocab=cfg.V, t_train=synth.T_TRAIN, max_lag=cfg.max_lag, aux=aux)
+    assert tok_aux[:pk.n_tokens].cpu().numpy().tobytes() == pk.tok_aux.tobytes()
+
+
+@pytest.mark.parametrize("name,algo", [("tiny", None), ("qwen3-4b", 2), ("qwen3-4b", 3), ("qwen3-4b", 1)])
+@pytest.mark.parametrize("est,dual", [(1, 0.0), (2, 3.0), (0, 2.0)])
+def test_loss_variants_v2(name, algo, est, dual):
+    """echo_policy_loss_fwd_bwd_v2: per-token advantages, sequence-mean weights, KL estimator, dual clip."""
+    from paper_2508_05387_b200 import abi
+    cfg = synth.CONFIGS[name]
+    b = synth.make_batch(cfg, 0, 2 * cfg.G if name != "tiny" else cfg.R)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    n = min(info.n_tokens, 2048)
+    rng = np.random.default_rng(est * 10 + int(dual))
+    tok_adv = (rng.normal(size=info.n_tokens) * 1.5).astype(np.float32)
+    L = np.diff(o.pk.kept_offset)
+    w = (1.0 / (o.pk.n_rollouts_kept * L[o.pk.tok_slot])).astype(np.float32)
+    old = o.pk.tok_old.copy()
+    old[: n // 2] = (old[: n // 2] + rng.normal(size=n // 2) * 1.5).astype(np.float32)   # push some rho past c
+    st.tok_old[: info.n_tokens] = torch.from_numpy(old).cuda()
+    logits = fill(st, cfg, 0, n)
+    z = as_oracle_rows(logits)
+    kl = 0.05
+    kw = dict(n_global=info.n_tokens, kl_coef=kl, tok_adv=tok_adv[:n], tok_weight=w[:n], clip_dual=dual,
+              kl_estimator=est)
+    probe = oracle.policy_loss(z, o.pk.tok_action[:n], old[:n], o.pk.tok_ref[:n], o.pk.tok_slot[:n], o.adv, **kw)
+    s = pow2_scale_for(np.abs(probe.dlogits).max())
+    ref = oracle.policy_loss(z, o.pk.tok_action[:n], old[:n], o.pk.tok_ref[:n], o.pk.tok_slot[:n], o.adv,
+                             grad_scale=s, **kw)
+    st.loss(logits, 0, kl_coef=kl, grad_scale=s, algo=algo, tok_adv=torch.from_numpy(tok_adv).cuda(),
+            tok_weight=torch.from_numpy(w).cuda(), clip_dual=dual, kl_estimator=est)
+    rho = np.exp(ref.logp - old[:n].astype(np.float64))
+    keep = np.abs(rho - dual) > 1e-5 if dual else np.ones(n, bool)
+    sens = (np.abs(tok_adv[:n]) * rho + kl * np.maximum(1.0, np.exp(o.pk.tok_ref[:n] - ref.logp))) * s * w[:n]
+    cs = sens * 1e-6 * (1 + np.abs(ref.logp)) + 1e-6 * np.abs(ref.coef)
+    sub = lambda x: x[keep]
+    import copy
+    r2 = copy.copy(ref)
+    r2.logp, r2.loss, r2.flags, r2.coef, r2.dlogits = (sub(ref.logp), sub(ref.loss), sub(ref.flags), sub(ref.coef),
+                                                       ref.dlogits[keep])
+    check_rows(d_gpu=logits.float().cpu().numpy()[keep], logp_gpu=sub(st.tok_logp[:n].cpu().numpy()),
+               loss_gpu=sub(st.tok_loss[:n].cpu().numpy()), flags_gpu=sub(st.tok_flags[:n].cpu().numpy()), ref=r2,
+               dtype=cfg.dtype, old=sub(old[:n]), cslack=sub(cs))
+    if dual:
+        assert (ref.flags & 1).any()
