@@ -154,7 +154,7 @@ def echo_policy_loss_fwd_bwd(logits, dtype, n_rows, vocab, ld, tok_action, tok_o
 def echo_policy_loss_fwd_bwd_v2(logits, dtype, n_rows, vocab, ld, tok_action, tok_old, tok_ref, tok_slot, adv_slot,
                                 tok_adv, tok_weight, n_global, cfg: LossConfig, tok_logp, tok_loss, tok_flags,
                                 algo=ECHO_ALGO_AUTO, stream=None):
-    _check("echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage", _lib.echo_policy_loss_fwd_bwd_v2(
+    _check("echo_policy_loss_fwd_bwd_v2", _lib.echo_policy_loss_fwd_bwd_v2(
         _p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot), _p(adv_slot),
         _p(tok_adv), _p(tok_weight), _p(n_global), ctypes.byref(cfg), _p(tok_logp), _p(tok_loss), _p(tok_flags), algo,
         _s(stream)))

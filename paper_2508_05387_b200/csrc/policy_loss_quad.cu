@@ -147,7 +147,6 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
   }
   const uint64_t st_pol = policy_evict_first();
   const float gscale = kGrad ? base_scale(p) : 0.0f;
-  const LossOpts opts = loss_opts(p);
   const int32_t col_t = c0 + tid * 8;
   const bool last_valid = (uint32_t)(nchunks - 1) * C::kChunk + (uint32_t)tid * 16u < g.slice_bytes;
   const bool has_tail = (c1 & 7) && (c1 & ~7) >= col_t && ((c1 & ~7) - col_t) % C::kChunkElems == 0;
@@ -173,16 +172,22 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     uint4 v[C::kRegChunks];
     if (nchunks > 0) mbar_wait(full0 + 8 * (it & 3u), (it >> 2) & 1u);
     ECHO_TRACE_MARK(p, it, 8);
+    const uint32_t slot0 = (it * (uint32_t)nchunks) % C::kRing;
+    // the thread's vector of the last chunk is masked once, in its own ring slot, so the unrolled copy below stays
+    // branch-free (the slot is re-filled only after barrier 1 + fence.proxy.async)
+    if (nchunks > 0 && (!last_valid || has_tail)) {
+      const uint32_t slot = (slot0 + (uint32_t)nchunks - 1u) % C::kRing;
+      const uint32_t addr = ring0 + slot * C::kChunk + my_off;
+      const uint4 w = last_valid ? mask_tail(lds_v4(addr), c1 & 7)
+                                 : make_uint4(kBf16NegInf2, kBf16NegInf2, kBf16NegInf2, kBf16NegInf2);
+      sts_v4(addr, w);
+    }
 #pragma unroll
     for (int c = 0; c < C::kRegChunks; ++c) {
       if (c < nchunks) {
-        const uint32_t slot = (it * (uint32_t)nchunks + c) % C::kRing;
-        uint4 w = lds_v4(ring0 + slot * C::kChunk + my_off);
-        if (c == nchunks - 1) {
-          if (!last_valid) w = make_uint4(kBf16NegInf2, kBf16NegInf2, kBf16NegInf2, kBf16NegInf2);
-          if (has_tail) w = mask_tail(w, c1 & 7);
-        }
-        v[c] = w;
+        uint32_t slot = slot0 + (uint32_t)c;
+        if (slot >= (uint32_t)C::kRing) slot -= C::kRing;
+        v[c] = lds_v4(ring0 + slot * C::kChunk + my_off);
       } else {
         v[c] = make_uint4(kBf16NegInf2, kBf16NegInf2, kBf16NegInf2, kBf16NegInf2);
       }
@@ -283,7 +288,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         const float lse = mm + logf(ss);
         if (a < 0 || a >= V) za = NAN;
         if constexpr (kGrad) {
-          const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, opts, gscale * meta.w);
+          const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, loss_opts(p), gscale * meta.w);
           if (rank == 0) {
             p.tok_logp[row] = r.logp;
             p.tok_loss[row] = r.loss;
@@ -312,6 +317,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     const uint64_t nlse2 = f2(-lse * kLog2e, -lse * kLog2e);
     uint8_t* const row_base = p.logits + row * p.ld_bytes;
     uint8_t* const dst = row_base + (int64_t)col_t * 2;
+    uint4 vtail = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
     for (int c = 0; c < C::kRegChunks; ++c) {
       if (c < nchunks) {
@@ -328,12 +334,13 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
           }
           w[k] = pack_bf16x2(d0, d1);
         }
-        if (c < nstore)
-          stg_v4_hint(dst + (int64_t)c * C::kChunk, v[c], st_pol);
-        else if (has_tail && c == nchunks - 1)
-          store_partial8(reinterpret_cast<__nv_bfloat16*>(dst + (int64_t)c * C::kChunk), v[c], c1 & 7);
+        if (c < nstore) stg_v4_hint(dst + (int64_t)c * C::kChunk, v[c], st_pol);
+        if (c == nchunks - 1) vtail = v[c];
       }
     }
+    // one partial store after the unrolled loop (not one copy per chunk): keeps the loop body in the I-cache
+    if (has_tail)
+      store_partial8(reinterpret_cast<__nv_bfloat16*>(dst + (int64_t)(nchunks - 1) * C::kChunk), vtail, c1 & 7);
     ECHO_TRACE_MARK(p, it, 5);
     if (own_a) reinterpret_cast<__nv_bfloat16*>(row_base)[a] = __float2bfloat16_rn(sm.da);
   }

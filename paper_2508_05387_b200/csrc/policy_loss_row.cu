@@ -54,7 +54,6 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
   const int32_t nvec = V / N;
   const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
   const float gscale = kGrad ? base_scale(p) : 0.0f;
-  const LossOpts opts = loss_opts(p);
 
   for (int64_t row = blockIdx.x; row < p.n_rows; row += gridDim.x) {
     uint8_t* rowp = p.logits + row * p.ld_bytes;
@@ -108,7 +107,7 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
       const float lse = tot.m + logf(tot.s);
       const float za = (a < 0 || a >= V) ? NAN : s_za;
       if constexpr (kGrad) {
-        const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, opts, gscale * meta.w);
+        const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, loss_opts(p), gscale * meta.w);
         p.tok_logp[row] = r.logp;
         p.tok_loss[row] = r.loss;
         p.tok_flags[row] = r.flags;
