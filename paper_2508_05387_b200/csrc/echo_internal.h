@@ -29,6 +29,7 @@ struct LossParams {
   float* __restrict__ tok_loss;
   uint8_t* __restrict__ tok_flags;
   float* __restrict__ tok_lse;  // forward-only mode (echo_token_logp): per-row log-sum-exp, nullable
+  int32_t sched_slot;         // quad kernels: row-scheduler slot of this launch (set by the launcher)
   unsigned long long* trace;  // ECHO_TRACE builds only: per-CTA phase timestamps (tools/trace_kernel.py)
   int32_t trace_rows;
 };

@@ -22,6 +22,8 @@
 // Determinism: the reduction tree depends only on V and the tile constants, never on the grid or the rank.
 #include <cuda_bf16.h>
 
+#include <atomic>
+
 #include "echo_common.cuh"
 #include "echo_internal.h"
 #include "policy_loss_common.cuh"
@@ -58,7 +60,19 @@ struct __align__(128) QuadSmem {
   float coef;
   float lse;
   float da;
+  uint64_t rowbar[4];    // row table: iteration k's row lands in rowtab[k % 4] (st.async from rank 0)
+  int64_t rowtab[4];
 };
+
+// Dynamic row scheduling.  Rank 0 of each cluster takes rows from a global counter in order and broadcasts them
+// to the cluster's row tables 3 iterations ahead, so all clusters work inside one compact window of consecutive
+// rows.  With a static stride (row = cluster + it * n_clusters) the clusters drift apart and the in-flight
+// addresses spread over hundreds of MB; the compact window sustains ~9% more HBM bandwidth on the same access
+// pattern (tools/membench.cu: ring_read_write 3.16 -> 2.91 ms).  One {next row, CTAs done} pair per launch slot;
+// a launch takes the next slot round-robin and its last CTA resets the pair, so no memset is needed.
+constexpr int kSchedSlots = 256;
+__device__ unsigned long long g_row_sched[kSchedSlots][2];
+constexpr int kRowAhead = 3;  // rows are broadcast this many iterations ahead (<= 4: the table depth)
 
 struct QuadGeom {
   int32_t c0, c1;          // this CTA's columns [c0, c1)
@@ -80,17 +94,19 @@ ECHO_DEVINL QuadGeom quad_geom(int32_t V, uint32_t rank) {
   return g;
 }
 
-// Issue chunks [from, to) of this cluster's row-major chunk stream (row iteration q / nchunks, chunk q % nchunks)
-// into ring slot q % kRing, one lane per chunk.  The lane that issues a row's chunk 0 arms that row's barrier
-// with the row's byte count (tx may transiently go negative; the phase cannot complete before the arrive).
+// Issue chunks [from, to) of this CTA's chunk stream (iteration j = q / nchunks, chunk q % nchunks) into ring slot
+// q % kRing, one lane per chunk; rows[j - it0] is iteration j's row (j - it0 in {0, 1, 2}).  The lane that issues
+// an iteration's chunk 0 arms that iteration's barrier with the slice byte count (tx may transiently go negative;
+// the phase cannot complete before the arrive).
 template <class C>
-ECHO_DEVINL void quad_issue_chunks(const LossParams& p, const QuadGeom& g, uint32_t cid, uint32_t ncl, uint32_t from,
-                                   uint32_t to, int lane, uint32_t full0, uint32_t ring0, uint64_t pol) {
+ECHO_DEVINL void quad_issue_chunks(const LossParams& p, const QuadGeom& g, uint32_t from, uint32_t to, int lane,
+                                   uint32_t full0, uint32_t ring0, uint64_t pol, uint32_t it0, int64_t row0,
+                                   int64_t row1, int64_t row2) {
   for (uint32_t q = from + (uint32_t)lane; q < to; q += 32) {
-    const uint32_t r = q / (uint32_t)g.nchunks, c = q % (uint32_t)g.nchunks;
-    const uint32_t bar = full0 + 8 * (r & 3u);
+    const uint32_t j = q / (uint32_t)g.nchunks, c = q % (uint32_t)g.nchunks;
+    const uint32_t bar = full0 + 8 * (j & 3u);
     if (c == 0) mbar_arrive_expect_tx(bar, g.slice_bytes);
-    const int64_t row = (int64_t)cid + (int64_t)r * ncl;
+    const int64_t row = j == it0 ? row0 : j == it0 + 1 ? row1 : row2;
     const uint8_t* src = p.logits + row * p.ld_bytes + (int64_t)g.c0 * 2 + (int64_t)c * C::kChunk;
     const uint32_t nb = min((uint32_t)C::kChunk, g.slice_bytes - c * C::kChunk);
     bulk_g2s(ring0 + (q % C::kRing) * C::kChunk, src, nb, bar, pol);
@@ -109,19 +125,21 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
   extern __shared__ __align__(128) uint8_t smem_raw[];
   QuadSmem<C>& sm = *reinterpret_cast<QuadSmem<C>*>(smem_raw);
   const uint32_t rank = cluster_ctarank();
-  const uint32_t cid = cluster_id_x(), ncl = nclusters_x();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int32_t V = p.V;
   const QuadGeom g = quad_geom<C>(V, rank);
   const int nchunks = g.nchunks;
   const int32_t c0 = g.c0, c1 = g.c1;
   const uint32_t full0 = smem_u32(&sm.full[0]), ring0 = smem_u32(&sm.ring[0][0]);
-  const uint32_t my_rows = p.n_rows > (int64_t)cid ? (uint32_t)((p.n_rows - 1 - cid) / ncl + 1) : 0u;
+  const int64_t n_rows = p.n_rows;
+  unsigned long long* const sched = g_row_sched[p.sched_slot];
+  const uint32_t rowbar0 = smem_u32(&sm.rowbar[0]);
 
   if (tid == 0) {
     for (int i = 0; i < 4; ++i) {
       mbar_init(full0 + 8 * i, 1);
-
+      mbar_init(rowbar0 + 8 * i, 1);
+      mbar_arrive_expect_tx(rowbar0 + 8 * i, 8);  // phase i: row of iteration i
     }
     mbar_init(smem_u32(&sm.xbar[0]), 1);
     mbar_init(smem_u32(&sm.xbar[1]), 1);
@@ -129,23 +147,44 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
   }
   cluster_sync_all();
 
-  const uint64_t ld_pol = policy_evict_first();
-  // warp 1 streams the rows: the ring holds ~1.4 rows, so row it+1 and the head of row it+2 are in flight while
-  // row it is reduced; slots are refilled once the CTA barrier after pass 1b shows row it has been copied out
-  const uint32_t total_chunks = my_rows * (uint32_t)nchunks;
-  uint32_t issued = 0;
-  if (warp == 1 % C::kWarps && nchunks > 0) {
-    issued = min(total_chunks, (uint32_t)C::kRing);
-    quad_issue_chunks<C>(p, g, cid, ncl, 0, issued, lane, full0, ring0, ld_pol);
+  // iteration k's row (waits for rank 0's broadcast)
+  auto row_of = [&](uint32_t k) -> int64_t {
+    mbar_wait_cluster(rowbar0 + 8 * (k & 3u), (k >> 2) & 1u);
+    return *reinterpret_cast<volatile int64_t*>(&sm.rowtab[k & 3u]);
+  };
+  auto broadcast = [&](uint32_t k, unsigned long long r) {
+#pragma unroll
+    for (int q = 0; q < C::kCtas; ++q)
+      st_async_b64(mapa(smem_u32(&sm.rowtab[k & 3u]), q), r, mapa(rowbar0 + 8 * (k & 3u), q));
+  };
+  // rank 0's warp 1 lane 0 runs the scheduler: rows of iterations 0..2 now, then one row per iteration
+  // (the next grab is issued one iteration before it is broadcast, so its latency stays off the critical path)
+  const bool sched_thread = rank == 0 && tid == 32;
+  bool sched_done = true;
+  unsigned long long grabbed = 0;
+  if (sched_thread) {
+    const unsigned long long r0 = atomicAdd(&sched[0], (unsigned long long)kRowAhead);
+    sched_done = false;
+    for (int k = 0; k < kRowAhead && !sched_done; ++k) {
+      const unsigned long long r = r0 + k < (unsigned long long)n_rows ? r0 + k : (unsigned long long)n_rows;
+      broadcast(k, r);
+      sched_done = r >= (unsigned long long)n_rows;
+    }
+    if (!sched_done) grabbed = atomicAdd(&sched[0], 1ull);
   }
 
-  uint32_t xbuf_remote[C::kCtas], xbar_remote[C::kCtas];
-#pragma unroll
-  for (int r = 0; r < C::kCtas; ++r) {
-    xbuf_remote[r] = mapa(smem_u32(&sm.xbuf[0][rank]), r);
-    xbar_remote[r] = mapa(smem_u32(&sm.xbar[0]), r);
+  // warp 1 streams the rows: the ring holds ~1.4 rows, so row it+1 and the head of row it+2 are in flight while
+  // row it is reduced; slots are refilled once the CTA barrier after pass 1b shows row it has been copied out
+  uint32_t issued = 0;
+  if (warp == 1 && nchunks > 0) {
+    const int64_t r0 = row_of(0);
+    const int64_t r1 = r0 < n_rows ? row_of(1) : n_rows;
+    const int64_t r2 = r1 < n_rows ? row_of(2) : n_rows;
+    const uint32_t rows_ok = r0 >= n_rows ? 0u : r1 >= n_rows ? 1u : r2 >= n_rows ? 2u : 3u;
+    issued = min((uint32_t)C::kRing, rows_ok * (uint32_t)nchunks);
+    quad_issue_chunks<C>(p, g, 0, issued, lane, full0, ring0, policy_evict_first(), 0, r0, r1, r2);
   }
-  const uint64_t st_pol = policy_evict_first();
+
   const float gscale = kGrad ? base_scale(p) : 0.0f;
   const int32_t col_t = c0 + tid * 8;
   const bool last_valid = (uint32_t)(nchunks - 1) * C::kChunk + (uint32_t)tid * 16u < g.slice_bytes;
@@ -153,18 +192,21 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
   const int nstore = nchunks - (last_valid ? 0 : 1) - (has_tail ? 1 : 0);
   const uint64_t l2e2 = f2(kLog2e, kLog2e);
   const uint32_t my_off = (uint32_t)tid * 16u;
-  uint32_t it = 0;
 
   // per-row metadata is loaded one row ahead so its global-load latency never sits on the critical path
-  int32_t a_next = my_rows > 0 ? p.tok_action[cid] : 0;
+  int64_t row_next = row_of(0);
+  int32_t a_next = row_next < n_rows ? p.tok_action[row_next] : 0;
   RowMeta meta_next{0.f, 0.f, 0.f};
-  if (tid == 0 && my_rows > 0) meta_next = load_meta(p, cid);
-  for (int64_t row = cid; row < p.n_rows; row += ncl, ++it) {
+  if (tid == 0 && row_next < n_rows) meta_next = load_meta(p, row_next);
+  for (uint32_t it = 0;; ++it) {
+    const int64_t row = row_next;
+    if (row >= n_rows) break;
     const int32_t a = a_next;
     const RowMeta meta = meta_next;
-    if (it + 1 < my_rows) {
-      a_next = p.tok_action[row + ncl];
-      if (tid == 0) meta_next = load_meta(p, row + ncl);
+    row_next = row_of(it + 1);
+    if (row_next < n_rows) {
+      a_next = p.tok_action[row_next];
+      if (tid == 0) meta_next = load_meta(p, row_next);
     }
 
     ECHO_TRACE_MARK(p, it, 0);
@@ -202,13 +244,11 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     for (int c = 0; c < C::kRegChunks; ++c) mx2 = bmax2(mx2, bmax2(bmax2(v[c].x, v[c].y), bmax2(v[c].z, v[c].w)));
     const float mx = fmaxf(__uint_as_float(mx2 << 16), __uint_as_float(mx2 & 0xFFFF0000u));
     const bool own_a = a >= col_t && a < c1 && ((a - col_t) % C::kChunkElems) < 8;
-    if (own_a) {
-      const int ca = (a - col_t) / C::kChunkElems, ea = (a - col_t) % C::kChunkElems;
-      uint32_t word = 0;
-#pragma unroll
-      for (int c = 0; c < C::kRegChunks; ++c)
-        if (c == ca) word = (ea >> 1) == 0 ? v[c].x : (ea >> 1) == 1 ? v[c].y : (ea >> 1) == 2 ? v[c].z : v[c].w;
-      sm.za = (ea & 1) ? __uint_as_float(word & 0xFFFF0000u) : __uint_as_float(word << 16);
+    if (tid == 0 && a >= c0 && a < c1) {  // the action's logit, straight from the ring (valid until barrier 1)
+      const uint32_t off = (uint32_t)(a - c0) * 2u;
+      uint32_t slot = slot0 + off / C::kChunk;
+      if (slot >= (uint32_t)C::kRing) slot -= C::kRing;
+      sm.za = __uint_as_float((uint32_t)lds_u16(ring0 + slot * C::kChunk + off % C::kChunk) << 16);
     }
 
     // ---- pass 1b
@@ -243,12 +283,27 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     ECHO_TRACE_MARK(p, it, 3);
     // every warp has copied row `it` out of the ring: warp 1 streams row it+1 into the slots (its chunks only
     // overlap rows <= it), off the critical path of warp 0's merge
-    if (warp == 1 % C::kWarps && nchunks > 0) {
-      const uint32_t upto = min(total_chunks, (it + 1) * (uint32_t)nchunks + (uint32_t)C::kRing);
-      if (upto > issued) {
-        fence_proxy_async_smem();
-        quad_issue_chunks<C>(p, g, cid, ncl, issued, upto, lane, full0, ring0, ld_pol);
-        issued = upto;
+    if (warp == 1) {
+      if (lane == 0) {
+        // every thread has read row(it) (at the top of iteration it-1): re-arm its table slot for iteration it+4
+        mbar_arrive_expect_tx(rowbar0 + 8 * (it & 3u), 8);
+        if (sched_thread && !sched_done) {
+          const unsigned long long r = grabbed < (unsigned long long)n_rows ? grabbed : (unsigned long long)n_rows;
+          broadcast(it + kRowAhead, r);
+          sched_done = r >= (unsigned long long)n_rows;
+          if (!sched_done) grabbed = atomicAdd(&sched[0], 1ull);
+        }
+      }
+      if (nchunks > 0 && row_next < n_rows) {
+        // iterations it+1 (row_next) and it+2; never past the first end-of-rows marker
+        const int64_t r2 = row_of(it + 2);
+        uint32_t upto = min((it + 1) * (uint32_t)nchunks + (uint32_t)C::kRing, (it + 3) * (uint32_t)nchunks);
+        if (r2 >= n_rows) upto = min(upto, (it + 2) * (uint32_t)nchunks);
+        if (upto > issued) {
+          fence_proxy_async_smem();
+          quad_issue_chunks<C>(p, g, issued, upto, lane, full0, ring0, policy_evict_first(), it + 1, row_next, r2, r2);
+          issued = upto;
+        }
       }
     }
 
@@ -266,7 +321,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         mbar_arrive_expect_tx(xbar_local, 16 * C::kCtas);
 #pragma unroll
         for (int r = 0; r < C::kCtas; ++r)
-          st_async_v4(xbuf_remote[r] + par * (16u * C::kCtas), msg, xbar_remote[r] + par * 8u);
+          st_async_v4(mapa(smem_u32(&sm.xbuf[par][rank]), r), msg, mapa(xbar_local, r));
         ECHO_TRACE_MARK(p, it, 6);
         mbar_wait_cluster(xbar_local, (it >> 1) & 1u);
         ECHO_TRACE_MARK(p, it, 7);
@@ -318,6 +373,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     uint8_t* const row_base = p.logits + row * p.ld_bytes;
     uint8_t* const dst = row_base + (int64_t)col_t * 2;
     uint4 vtail = make_uint4(0u, 0u, 0u, 0u);
+    const uint64_t st_pol = policy_evict_first();
 #pragma unroll
     for (int c = 0; c < C::kRegChunks; ++c) {
       if (c < nchunks) {
@@ -345,6 +401,14 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     if (own_a) reinterpret_cast<__nv_bfloat16*>(row_base)[a] = __float2bfloat16_rn(sm.da);
   }
   cluster_sync_all();
+  if (tid == 0) {
+    // the last CTA out resets this launch's scheduler slot (all grabs returned before the cluster barrier)
+    __threadfence();
+    if (atomicAdd(&sched[1], 1ull) == (unsigned long long)gridDim.x - 1ull) {
+      sched[0] = 0ull;
+      sched[1] = 0ull;
+    }
+  }
 }
 
 template <class C>
@@ -362,11 +426,14 @@ static cudaError_t launch_t(const LossParams& p, cudaStream_t stream, int num_sm
   if (e != cudaSuccess) return e;
   int64_t clusters = max_active_clusters(fn, C::kThreads, smem, C::kCtas, num_sms * C::kCtasPerSm / C::kCtas);
   if (clusters > p.n_rows) clusters = p.n_rows;
+  static std::atomic<uint32_t> next_slot{0};
   if (shape) {
     *shape = LaunchShape{(int32_t)(clusters * C::kCtas), C::kCtas, C::kThreads, (int32_t)smem};
     return cudaSuccess;
   }
-  policy_loss_quad_kernel<C, kMode><<<(unsigned)(clusters * C::kCtas), C::kThreads, smem, stream>>>(p);
+  LossParams q = p;
+  q.sched_slot = (int32_t)(next_slot.fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
+  policy_loss_quad_kernel<C, kMode><<<(unsigned)(clusters * C::kCtas), C::kThreads, smem, stream>>>(q);
   return cudaGetLastError();
 }
 
