@@ -3,15 +3,18 @@
 // One logits row (V ~ 152k bf16 = 297 KB) is owned by a thread-block cluster of C::kCtas = 4 CTAs; CTA r holds
 // the quarter [r q, (r+1) q) of the row (q = ceil(V/4) rounded to 8) in REGISTERS: 8 warps x 32 threads x
 // 19 vectors of 16 B = 76 registers per thread.  Two such CTAs share an SM (registers 2 x 256 x 128 = 64 K,
-// shared memory 2 x 111 KB), so every SM always has two rows in flight: while one CTA waits on its cluster
-// merge or drains its stores, the other keeps the MUFU / FMA pipes busy.  The persistent grid (296 CTAs =
-// 74 clusters) strides over rows; HBM sees exactly one read and one write per logit.
+// shared memory 2 x 112 KB), so every SM always has two rows in flight: while one CTA waits on its cluster
+// merge or drains its stores, the other keeps the MUFU / FMA pipes busy.  The persistent grid (as many 4-CTA
+// clusters as fit: 71 on a B200) takes rows in order from a global counter (rank 0 of each cluster grabs and
+// broadcasts them), so all clusters stream one compact window of consecutive rows; HBM sees exactly one read
+// and one write per logit.
 //
 // Per CTA and row:
-//   stage    1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx, L2 evict_first) stream the quarter-row
-//            through a 27 x 4 KB shared-memory ring; thread 0 refills a slot as soon as all 8 warps have copied
-//            it into registers, so the ring always runs ~1.4 quarter-rows ahead of the compute
-//   pass 1a  ring -> registers, exact bf16x2 running max m_t
+//   stage    1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx) stream the quarter-row through a
+//            28 x 4 KB shared-memory ring, one barrier per row; warp 1 refills the slots of row it as soon as the
+//            CTA barrier after pass 1b shows they have been copied into registers, so row it+1 and the head of
+//            row it+2 are always in flight
+//   pass 1a  ring -> registers, exact bf16x2 running max m_t; thread 0 reads z_a from the ring
 //   pass 1b  e = 2^((z - m_t) log2e) (MUFU), s_t = sum e (FADD2); kStoreExp: registers <- e as fp16
 //   merge    (m_t, s_t) -> warp (xor shuffles) -> CTA (warp 0) -> cluster: each CTA st.async's its
 //            {m, s, z_a} into slot [rank] of every peer's shared memory, completing 16 tx-bytes on the peer's
@@ -19,7 +22,8 @@
 //   epilogue lse, logp, rho, clip, KL, c_t (fp32), rank 0 writes the per-token outputs
 //   pass 2   d = e k_t (k_t = -c_t 2^((m_t - lse) log2e), FMUL2)  or, exact, d = -c_t 2^((z - lse) log2e);
 //            bf16 RNE, 16-byte stores in place; the action column gets c_t (1 - p_a) from the fp32 epilogue
-// Determinism: the reduction tree depends only on V and the tile constants, never on the grid or the rank.
+// Determinism: the reduction tree depends only on V and the tile constants, never on the grid, the rank or
+// which cluster a row is scheduled on.
 #include <cuda_bf16.h>
 
 #include <atomic>
@@ -47,6 +51,12 @@ struct QCfg {
 };
 constexpr int kQBar = 1;                                // named barrier id
 
+// per-row metadata, staged in shared memory by thread 0 with cp.async one row ahead (keeps it out of registers)
+struct MetaSm {
+  int32_t a, slot;
+  float old, ref, adv, w;
+};
+
 template <class C>
 struct __align__(128) QuadSmem {
   uint8_t ring[C::kRing][C::kChunk];
@@ -57,6 +67,7 @@ struct __align__(128) QuadSmem {
   float red_m[C::kWarps];
   float red_s[C::kWarps];
   float za;
+  MetaSm meta[2];        // rows of iterations it (it & 1) and it+1
   float coef;
   float lse;
   float da;
@@ -72,7 +83,8 @@ struct __align__(128) QuadSmem {
 // a launch takes the next slot round-robin and its last CTA resets the pair, so no memset is needed.
 constexpr int kSchedSlots = 256;
 __device__ unsigned long long g_row_sched[kSchedSlots][2];
-constexpr int kRowAhead = 3;  // rows are broadcast this many iterations ahead (<= 4: the table depth)
+constexpr int kRowAhead = 3;
+  // rows are broadcast this many iterations ahead (<= 4: the table depth)
 
 struct QuadGeom {
   int32_t c0, c1;          // this CTA's columns [c0, c1)
@@ -182,7 +194,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     const int64_t r2 = r1 < n_rows ? row_of(2) : n_rows;
     const uint32_t rows_ok = r0 >= n_rows ? 0u : r1 >= n_rows ? 1u : r2 >= n_rows ? 2u : 3u;
     issued = min((uint32_t)C::kRing, rows_ok * (uint32_t)nchunks);
-    quad_issue_chunks<C>(p, g, 0, issued, lane, full0, ring0, policy_evict_first(), 0, r0, r1, r2);
+    quad_issue_chunks<C>(p, g, 0, issued, lane, full0, ring0, policy_evict_normal(), 0, r0, r1, r2);
   }
 
   const float gscale = kGrad ? base_scale(p) : 0.0f;
@@ -193,20 +205,40 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
   const uint64_t l2e2 = f2(kLog2e, kLog2e);
   const uint32_t my_off = (uint32_t)tid * 16u;
 
-  // per-row metadata is loaded one row ahead so its global-load latency never sits on the critical path
+  // Per-row metadata is staged one row ahead so its global-load latency never sits on the critical path.
+  // Thread 0, per iteration it: group C(it) = the dependent advantage load of row it (its slot landed with A(it)),
+  // then group A(it+1) = action, old, ref, weight, slot / per-token advantage of row it+1.  A(it+1) is complete
+  // before barrier 2 of iteration it (which publishes the action to every thread), C(it) before the epilogue.
+  auto stage_meta = [&](int64_t r, uint32_t k) {
+    MetaSm& m = sm.meta[k & 1u];
+    cp_async4(smem_u32(&m.a), p.tok_action + r);
+    if constexpr (kGrad) {
+      cp_async4(smem_u32(&m.old), p.tok_old + r);
+      if (p.kl_coef > 0.0f) cp_async4(smem_u32(&m.ref), p.tok_ref + r);
+      else m.ref = 0.0f;
+      if (p.tok_weight) cp_async4(smem_u32(&m.w), p.tok_weight + r);
+      else m.w = 1.0f;
+      if (p.tok_adv) cp_async4(smem_u32(&m.adv), p.tok_adv + r);
+      else cp_async4(smem_u32(&m.slot), p.tok_slot + r);
+    }
+  };
   int64_t row_next = row_of(0);
-  int32_t a_next = row_next < n_rows ? p.tok_action[row_next] : 0;
-  RowMeta meta_next{0.f, 0.f, 0.f};
-  if (tid == 0 && row_next < n_rows) meta_next = load_meta(p, row_next);
+  if (tid == 0 && row_next < n_rows) {
+    stage_meta(row_next, 0);
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+  named_bar_sync(kQBar, C::kThreads);
   for (uint32_t it = 0;; ++it) {
     const int64_t row = row_next;
     if (row >= n_rows) break;
-    const int32_t a = a_next;
-    const RowMeta meta = meta_next;
+    const int32_t a = sm.meta[it & 1u].a;
     row_next = row_of(it + 1);
-    if (row_next < n_rows) {
-      a_next = p.tok_action[row_next];
-      if (tid == 0) meta_next = load_meta(p, row_next);
+    if (tid == 0) {
+      if (kGrad && !p.tok_adv) cp_async4(smem_u32(&sm.meta[it & 1u].adv), p.adv_slot + sm.meta[it & 1u].slot);
+      cp_async_commit();
+      if (row_next < n_rows) stage_meta(row_next, it + 1);
+      cp_async_commit();
     }
 
     ECHO_TRACE_MARK(p, it, 0);
@@ -301,7 +333,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         if (r2 >= n_rows) upto = min(upto, (it + 2) * (uint32_t)nchunks);
         if (upto > issued) {
           fence_proxy_async_smem();
-          quad_issue_chunks<C>(p, g, issued, upto, lane, full0, ring0, policy_evict_first(), it + 1, row_next, r2, r2);
+          quad_issue_chunks<C>(p, g, issued, upto, lane, full0, ring0, policy_evict_normal(), it + 1, row_next, r2, r2);
           issued = upto;
         }
       }
@@ -326,24 +358,26 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         mbar_wait_cluster(xbar_local, (it >> 1) & 1u);
         ECHO_TRACE_MARK(p, it, 7);
         // cluster merge in rank order: max first, then the rescaled sum (the exps are independent)
+        // (the partials are re-read from shared memory rather than held: 4 words per rank would cost registers)
         float za = NAN, mm = -INFINITY;
-        uint4 msgs[C::kCtas];
 #pragma unroll
         for (int r = 0; r < C::kCtas; ++r) {
-          msgs[r] = sm.xbuf[par][r];
-          mm = fmaxf(mm, __uint_as_float(msgs[r].x));
-          if (msgs[r].w) za = __uint_as_float(msgs[r].z);
+          const uint4 m = sm.xbuf[par][r];
+          mm = fmaxf(mm, __uint_as_float(m.x));
+          if (m.w) za = __uint_as_float(m.z);
         }
         float ss = 0.0f;
 #pragma unroll
         for (int r = 0; r < C::kCtas; ++r) {
-          const float mr = __uint_as_float(msgs[r].x);
-          ss += (mr == -INFINITY) ? 0.0f : __uint_as_float(msgs[r].y) * ex2((mr - mm) * kLog2e);
+          const float mr = __uint_as_float(sm.xbuf[par][r].x), sr = __uint_as_float(sm.xbuf[par][r].y);
+          ss += (mr == -INFINITY) ? 0.0f : sr * ex2((mr - mm) * kLog2e);
         }
         const float lse = mm + logf(ss);
         if (a < 0 || a >= V) za = NAN;
         if constexpr (kGrad) {
-          const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, loss_opts(p), gscale * meta.w);
+          cp_async_wait<1>();  // C(it) landed
+          const MetaSm& m = sm.meta[it & 1u];
+          const RowScalars r = row_epilogue(lse, za, m.old, m.ref, m.adv, loss_opts(p), gscale * m.w);
           if (rank == 0) {
             p.tok_logp[row] = r.logp;
             p.tok_loss[row] = r.loss;
@@ -361,6 +395,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         }
       }
     }
+    if (tid == 0) cp_async_wait<0>();  // A(it+1) landed: barrier 2 publishes row it+1's action
     named_bar_sync(kQBar, C::kThreads);
     ECHO_TRACE_MARK(p, it, 4);
     if constexpr (!kGrad) continue;
@@ -373,7 +408,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     uint8_t* const row_base = p.logits + row * p.ld_bytes;
     uint8_t* const dst = row_base + (int64_t)col_t * 2;
     uint4 vtail = make_uint4(0u, 0u, 0u, 0u);
-    const uint64_t st_pol = policy_evict_first();
+    const uint64_t st_pol = policy_evict_normal();
 #pragma unroll
     for (int c = 0; c < C::kRegChunks; ++c) {
       if (c < nchunks) {
