@@ -485,8 +485,9 @@ cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream
 cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
   return launch_t<Oct, kModeCache>(p, stream, num_sms, shape);
 }
+// forward-only log-probs: the 8-CTA tile (1.93 ms vs 1.97 ms for the 4-CTA one on 32768 x 151936)
 cudaError_t launch_quad_logp(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
-  return launch_t<Quad, kModeLogp>(p, stream, num_sms, shape);
+  return launch_t<Oct, kModeLogp>(p, stream, num_sms, shape);
 }
 
 }  // namespace echo

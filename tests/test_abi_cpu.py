@@ -54,15 +54,19 @@ def test_quad_kernel_uses_tma_bulk_copies_and_dsmem():
                           capture_output=True, text=True, check=True).stdout
     blocks = re.split(r"\n\s*Function : ", sass)
     quad = [b for b in blocks if "policy_loss_quad_kernel" in b.split("\n", 1)[0]]
-    assert len(quad) == 4                       # 4-CTA fp16-cache / exact / logp-only, 8-CTA fp16-cache
-    body = [b for b in quad if "QCfgILi4ELi8EEELi1E" in b.split("\n", 1)[0]][0]   # 4-CTA, fp16-cache mode
-    assert "UBLKCP.S.G" in body      # cp.async.bulk global->shared (TMA engine)
-    assert "SYNCS" in body           # mbarrier phase / tx tracking
-    assert "STAS" in body            # st.async into the peer CTA's shared memory (DSMEM)
-    assert "UCGABAR" in body         # cluster barrier (setup / teardown only)
-    assert "MUFU.EX2" in body and "FFMA2" in body   # one MUFU exp per logit, packed fp32x2 math
-    assert "STG.E.NA.128" in body    # 16-byte gradient stores
-    assert "HMMA" not in body and "UTCHMMA" not in body   # no tensor cores: a stream, not a contraction
+    assert len(quad) == 4                       # 4-CTA fp16-cache / exact, 8-CTA fp16-cache / logp-only
+    for tag in ("QCfgILi8ELi4EEELi1E", "QCfgILi4ELi8EEELi1E"):   # 8-CTA (AUTO) and 4-CTA, fp16-cache mode
+        body = [b for b in quad if tag in b.split("\n", 1)[0]][0]
+        assert "UBLKCP.S.G" in body      # cp.async.bulk global->shared (TMA engine)
+        assert "SYNCS" in body           # mbarrier phase / tx tracking
+        assert "STAS" in body            # st.async into the peer CTA's shared memory (DSMEM)
+        assert "UCGABAR" in body         # cluster barrier (setup / teardown only)
+        assert "MUFU.EX2" in body and "FFMA2" in body   # one MUFU exp per logit, packed fp32x2 math
+        assert "STG.E.NA.128" in body    # 16-byte gradient stores
+        assert "LDGSTS" in body          # per-row metadata staged with cp.async
+        assert "ATOMG" in body           # in-order row scheduler
+        assert "LDL" not in body and "STL" not in body   # no register spills
+        assert "HMMA" not in body and "UTCHMMA" not in body   # no tensor cores: a stream, not a contraction
 
 
 def test_calls_without_gpu_report_an_error_not_a_fallback():

@@ -13,8 +13,8 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 300 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/${tag}_launches.csv \
       python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_launch.log 2>&1; echo "ncu_launches=$?" >> $out/${tag}_status.txt
-  timeout 300 python tools/prof_kernel.py --algos quad_reg --reps 1 --warmup 1 > $out/${tag}_prof_plain.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:policy_loss_quad -s 1 -c 1 -o $out/${tag}_quad \
-      python tools/prof_kernel.py --algos quad_reg --reps 1 --warmup 1 > $out/${tag}_ncu_full.log 2>&1; echo "ncu_full=$?" >> $out/${tag}_status.txt
+  timeout 300 python tools/prof_kernel.py --algos ${ALGO:-oct_reg} --reps 1 --warmup 1 > $out/${tag}_prof_plain.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:policy_loss_quad -s 1 -c 1 -o $out/${tag}_kernel \
+      python tools/prof_kernel.py --algos ${ALGO:-oct_reg} --reps 1 --warmup 1 > $out/${tag}_ncu_full.log 2>&1; echo "ncu_full=$?" >> $out/${tag}_status.txt
 fi
 cat $out/${tag}_status.txt
