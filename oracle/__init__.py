@@ -56,12 +56,12 @@ def lib():
         _lib.echo_ref_group_advantage.argtypes = [i32, i32, f32, P, P, i64, P, P, P]
         _lib.echo_ref_group_advantage.restype = ctypes.c_int
         _lib.echo_ref_policy_loss.argtypes = [i64, i32, i64, i32, P, P, P, P, P, P, P, P, f64, f32, f32, f32, f32,
-                                              i32, f32, P, P, P, P, P, P]
+                                              i32, f32, f32, P, P, P, P, P, P, P]
         _lib.echo_ref_policy_loss.restype = ctypes.c_int
         _lib.echo_ref_token_logp.argtypes = [i64, i32, i64, i32, P, P, P, P, P]
         _lib.echo_ref_token_logp.restype = ctypes.c_int
         _lib.echo_ref_scaled_loss.argtypes = [i64, i32, i64, P, P, P, P, P, P, P, P, f64, f32, f32, f32, f32, i32,
-                                              f32]
+                                              f32, f32]
         _lib.echo_ref_scaled_loss.restype = f64
     return _lib
 
@@ -165,6 +165,7 @@ class LossOut:
     coef: np.ndarray
     dlogits: np.ndarray | None
     stats: np.ndarray
+    entropy: np.ndarray
 
 
 KL_K3, KL_K1, KL_K2 = 0, 1, 2
@@ -172,7 +173,7 @@ KL_K3, KL_K1, KL_K2 = 0, 1, 2
 
 def policy_loss(logits, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, vocab=None, dtype=None,
                 clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0, want_dlogits=True, tok_adv=None,
-                tok_weight=None, clip_dual=0.0, kl_estimator=KL_K3) -> LossOut:
+                tok_weight=None, clip_dual=0.0, kl_estimator=KL_K3, entropy_coef=0.0) -> LossOut:
     """(3)-(5) for every row of ``logits``.
 
     ``logits`` is a 2-D numpy array: float32 (dtype F32) or uint16 bf16 bit patterns (dtype BF16).
@@ -197,13 +198,14 @@ def policy_loss(logits, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_g
     tok_adv = _c(tok_adv, np.float32)
     tok_weight = _c(tok_weight, np.float32)
     stats = np.zeros(11, np.float64)
+    ent = np.zeros(n, np.float64)
     rc = lib().echo_ref_policy_loss(n, V, ld, dtype, _p(logits), _p(tok_action), _p(tok_old), _p(tok_ref),
                                     _p(tok_slot), _p(adv_slot), _p(tok_adv), _p(tok_weight), float(n_global),
-                                    clip_low, clip_high, clip_dual, kl_coef, kl_estimator, grad_scale, _p(logp),
-                                    _p(loss), _p(flags), _p(coef), _p(d), _p(stats))
+                                    clip_low, clip_high, clip_dual, kl_coef, kl_estimator, grad_scale, entropy_coef,
+                                    _p(logp), _p(loss), _p(flags), _p(coef), _p(ent), _p(d), _p(stats))
     if rc != 0:
         raise ValueError("echo_ref_policy_loss: invalid argument")
-    return LossOut(logp, loss, flags, coef, d, stats)
+    return LossOut(logp, loss, flags, coef, d, stats, ent)
 
 
 def token_logp(logits, tok_action, *, vocab=None, dtype=None):
@@ -225,7 +227,7 @@ def token_logp(logits, tok_action, *, vocab=None, dtype=None):
 
 def scaled_loss(logits_f64, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, clip_low=0.2,
                 clip_high=0.2, kl_coef=0.0, grad_scale=1.0, tok_adv=None, tok_weight=None, clip_dual=0.0,
-                kl_estimator=KL_K3) -> float:
+                kl_estimator=KL_K3, entropy_coef=0.0) -> float:
     """grad_scale * sum_t w_t l_t as a function of fp64 logits (for finite differences)."""
     z = np.ascontiguousarray(logits_f64, dtype=np.float64)
     n, V = z.shape
@@ -233,4 +235,4 @@ def scaled_loss(logits_f64, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *,
                                             _p(_c(tok_ref, np.float32)), _p(_c(tok_slot, np.int32)),
                                             _p(_c(adv_slot, np.float32)), _p(_c(tok_adv, np.float32)),
                                             _p(_c(tok_weight, np.float32)), float(n_global), clip_low, clip_high,
-                                            clip_dual, kl_coef, kl_estimator, grad_scale))
+                                            clip_dual, kl_coef, kl_estimator, grad_scale, entropy_coef))

@@ -244,7 +244,11 @@ int echo_ref_group_advantage(int32_t n_rollouts_kept, int32_t group_size, float 
  *   n_clipped, n_nonfinite, rho_min, rho_max, sum logp, n_rows, sum rho, sum w l}, rho stats over
  *   finite rows only.
  * f4 options: tok_adv / tok_weight (nullable, see adv_of), clip_dual (c > 1: for A < 0 the loss is capped at
- *   -A c with zero gradient), kl_estimator (REF_KL_*).
+ *   -A c with zero gradient), kl_estimator (REF_KL_*), and the entropy bonus (entropy_coef eta >= 0):
+ *       H_t  = -sum_v p_v log p_v   (p_v = exp(z_v - lse); masked -inf logits contribute 0, the limit p log p -> 0)
+ *       l_t  = pg + beta kl - eta H_t
+ *       dH/dz_v = -p_v (log p_v + H_t), so  d[t,v] = c_t (delta_{v,a} - p_v) + s w_t eta p_v (log p_v + H_t)
+ *   tok_entropy (nullable) receives H_t; with eta > 0, H_t joins the non-finite check.
  * dlogits (nullable) is [n_rows x vocab] doubles.
  * ====================================================================================== */
 static int fits_f32(double x) { return isfinite(x) && fabs(x) <= (double)FLT_MAX; }
@@ -274,14 +278,15 @@ int echo_ref_policy_loss(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtyp
                          const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
                          const float* tok_weight, double n_global,
                          float clip_low, float clip_high, float clip_dual, float kl_coef, int32_t kl_estimator,
-                         float grad_scale,
+                         float grad_scale, float entropy_coef,
                          double* tok_logp, double* tok_loss, uint8_t* tok_flags, double* tok_coef,
-                         double* dlogits, double* stats) {
+                         double* tok_entropy, double* dlogits, double* stats) {
   if (n_rows < 0 || vocab < 1 || ld < vocab || (dtype != 0 && dtype != 1)) return REF_ERR_INVALID_ARGUMENT;
   if (kl_coef > 0.0f && tok_ref == NULL) return REF_ERR_INVALID_ARGUMENT;
   if (kl_estimator < REF_KL_K3 || kl_estimator > REF_KL_K2) return REF_ERR_INVALID_ARGUMENT;
   const double lo = 1.0 - (double)clip_low, hi = 1.0 + (double)clip_high;
-  const double beta = (double)kl_coef, dual = (double)clip_dual;
+  const double beta = (double)kl_coef, dual = (double)clip_dual, eta = (double)entropy_coef;
+  if (entropy_coef < 0.0f) return REF_ERR_INVALID_ARGUMENT;
 
 #pragma omp parallel for schedule(dynamic, 16)
   for (int64_t t = 0; t < n_rows; ++t) {
@@ -316,22 +321,38 @@ int echo_ref_policy_loss(int64_t n_rows, int32_t vocab, int64_t ld, int32_t dtyp
       kl = kl_value(kl_estimator, x);
       dkl = kl_dlogp(kl_estimator, x);
     }
-    double loss = pg + beta * kl;
+    /* f4 entropy bonus: H = -sum_v p_v log p_v over the unmasked logits */
+    double H = 0.0;
+    if (eta > 0.0 || tok_entropy) {
+      for (int64_t v = 0; v < vocab; ++v) {
+        double z = logit_at(logits, dtype, ld, t, v);
+        if (z == -INFINITY) continue;
+        double lp = z - lse;
+        H = H - exp(lp) * lp;
+      }
+    }
+    double loss = pg + beta * kl - eta * H;
     double dl_dlogp = (clipped ? 0.0 : -A * rho) + beta * dkl;
     double w = tok_weight ? (double)tok_weight[t] : 1.0 / n_global;
     double c = (double)grad_scale * w * dl_dlogp;
-    int nonfinite = !(fits_f32(lse) && fits_f32(logp) && fits_f32(rho) && fits_f32(loss) && fits_f32(c));
+    double e = (double)grad_scale * w * eta;
+    int nonfinite = !(fits_f32(lse) && fits_f32(logp) && fits_f32(rho) && fits_f32(loss) && fits_f32(c) &&
+                      (eta == 0.0 || fits_f32(H)));
 
     tok_logp[t] = logp;
     tok_loss[t] = loss;
     tok_flags[t] = (uint8_t)((clipped ? 1 : 0) | (nonfinite ? 2 : 0));
     if (tok_coef) tok_coef[t] = c;
+    if (tok_entropy) tok_entropy[t] = H;
 
     /* (5) gradient of the loss with respect to every logit of the row */
     if (dlogits) {
       for (int64_t v = 0; v < vocab; ++v) {
-        double p = exp(logit_at(logits, dtype, ld, t, v) - lse);
-        dlogits[t * (int64_t)vocab + v] = c * ((v == a ? 1.0 : 0.0) - p);
+        double z = logit_at(logits, dtype, ld, t, v);
+        double p = exp(z - lse);
+        double g = c * ((v == a ? 1.0 : 0.0) - p);
+        if (eta > 0.0 && z != -INFINITY) g = g + e * p * ((z - lse) + H);
+        dlogits[t * (int64_t)vocab + v] = g;
       }
     }
   }
@@ -426,9 +447,10 @@ double echo_ref_scaled_loss(int64_t n_rows, int32_t vocab, int64_t ld, const dou
                             const int32_t* tok_action, const float* tok_old, const float* tok_ref,
                             const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
                             const float* tok_weight, double n_global, float clip_low, float clip_high,
-                            float clip_dual, float kl_coef, int32_t kl_estimator, float grad_scale) {
+                            float clip_dual, float kl_coef, int32_t kl_estimator, float grad_scale,
+                            float entropy_coef) {
   const double lo = 1.0 - (double)clip_low, hi = 1.0 + (double)clip_high;
-  const double beta = (double)kl_coef, dual = (double)clip_dual;
+  const double beta = (double)kl_coef, dual = (double)clip_dual, eta = (double)entropy_coef;
   double total = 0.0;
   for (int64_t t = 0; t < n_rows; ++t) {
     const double* z = logits + t * ld;
@@ -436,7 +458,11 @@ double echo_ref_scaled_loss(int64_t n_rows, int32_t vocab, int64_t ld, const dou
     for (int64_t v = 0; v < vocab; ++v) if (z[v] > m) m = z[v];
     double s = 0.0;
     for (int64_t v = 0; v < vocab; ++v) s = s + exp(z[v] - m);
-    double logp = z[tok_action[t]] - (m + log(s));
+    double lse = m + log(s);
+    double logp = z[tok_action[t]] - lse;
+    double H = 0.0;
+    for (int64_t v = 0; v < vocab; ++v)
+      if (z[v] != -INFINITY) H = H - exp(z[v] - lse) * (z[v] - lse);
     double A = adv_of(tok_adv, tok_slot, adv_slot, t);
     double rho = exp(logp - (double)tok_old[t]);
     double rho_c = rho < lo ? lo : (rho > hi ? hi : rho);
@@ -446,7 +472,7 @@ double echo_ref_scaled_loss(int64_t n_rows, int32_t vocab, int64_t ld, const dou
     double kl = 0.0;
     if (beta > 0.0) kl = kl_value(kl_estimator, (double)tok_ref[t] - logp);
     double w = tok_weight ? (double)tok_weight[t] : 1.0 / n_global;
-    total = total + w * (pg + beta * kl);
+    total = total + w * (pg + beta * kl - eta * H);
   }
   return (double)grad_scale * total;
 }

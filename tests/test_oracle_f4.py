@@ -119,3 +119,72 @@ def test_finite_differences_variants(est, dual, seed):
         assert abs(fd - d) <= 1e-5 * abs(d), (t, v, fd, d)
         checked += 1
     assert checked >= 60
+
+
+def test_entropy_closed_forms():
+    """H_t = -sum p log p: uniform rows give ln V, a row with one unmasked logit gives 0, a two-point row with
+    logits (0, d) gives the binary entropy ln(1 + e^d) - d e^d / (1 + e^d)."""
+    V = 97
+    n = 3
+    z = np.zeros((n, V), np.float32)
+    z[1, :] = -np.inf
+    z[1, 5] = 3.0
+    d = 1.75
+    z[2, :] = -np.inf
+    z[2, 0], z[2, 1] = 0.0, d
+    act = np.array([0, 5, 1], np.int32)
+    out = oracle.policy_loss(z, act, np.zeros(n, np.float32), None, np.zeros(n, np.int32), np.zeros(1, np.float32),
+                             n_global=n, entropy_coef=0.5)
+    assert abs(out.entropy[0] - math.log(V)) <= 1e-13
+    assert out.entropy[1] == 0.0
+    q = math.exp(d) / (1 + math.exp(d))
+    assert abs(out.entropy[2] - (-(1 - q) * math.log(1 - q) - q * math.log(q))) <= 1e-14
+    # A = 0, no KL: the loss is -eta H
+    np.testing.assert_allclose(out.loss, -0.5 * out.entropy, rtol=0, atol=1e-15)   # 0.5 is exact in fp32
+    # the masked columns of the one-hot row get an exactly zero gradient
+    assert np.all(out.dlogits[1][np.isinf(z[1])] == 0)
+
+
+def test_entropy_term_is_additive_and_bounded():
+    z, act, old, ref, slot, adv, base = _problem(4)
+    n = len(act)
+    a = oracle.policy_loss(z, act, old, ref, slot, adv, n_global=n, kl_coef=0.01)
+    b = oracle.policy_loss(z, act, old, ref, slot, adv, n_global=n, kl_coef=0.01, entropy_coef=0.05)
+    assert np.all(b.entropy >= 0) and np.all(b.entropy <= math.log(z.shape[1]) + 1e-12)
+    eta = float(np.float32(0.05))                                # the coefficient crosses the ABI as fp32
+    np.testing.assert_allclose(b.loss - a.loss, -eta * b.entropy, rtol=1e-12, atol=1e-14)
+    np.testing.assert_array_equal(a.coef, b.coef)               # the (delta - p) coefficient is unchanged
+    # each gradient row of the entropy part sums to zero: sum_v p_v (log p_v + H) = -H + H
+    np.testing.assert_allclose(b.dlogits.sum(axis=1), 0.0, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_finite_differences_entropy(seed):
+    """Central differences of grad_scale * sum_t w_t (pg + beta kl - eta H) against dlogits with eta > 0."""
+    rng = np.random.default_rng(70 + seed)
+    z, act, old, ref, slot, adv, base = _problem(seed, n=16, V=120)
+    n = len(act)
+    kw = dict(n_global=n, kl_coef=0.2, entropy_coef=0.3, grad_scale=float(n))
+    out = oracle.policy_loss(z, act, old, ref, slot, adv, **kw)
+    rho = np.exp(out.logp - old.astype(np.float64))
+    dmax = np.abs(out.dlogits).max()
+    checked = 0
+    for _ in range(3000):
+        if checked >= 80:
+            break
+        t = int(rng.integers(0, n))
+        if np.min(np.abs(rho[t] - np.array([0.8, 1.2]))) < 1e-2:
+            continue
+        v = int(act[t]) if rng.random() < 0.2 else int(rng.integers(0, z.shape[1]))
+        d = out.dlogits[t, v]
+        if abs(d) <= 1e-3 * dmax:
+            continue
+        row = z[t:t + 1].astype(np.float64)
+        args = (act[t:t + 1], old[t:t + 1], ref[t:t + 1], slot[t:t + 1], adv)
+        zp, zm = row.copy(), row.copy()
+        zp[0, v] += 1e-4
+        zm[0, v] -= 1e-4
+        fd = (oracle.scaled_loss(zp, *args, **kw) - oracle.scaled_loss(zm, *args, **kw)) / 2e-4
+        assert abs(fd - d) <= 1e-5 * abs(d), (t, v, fd, d)
+        checked += 1
+    assert checked >= 40
