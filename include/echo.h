@@ -203,23 +203,30 @@ typedef struct {
   float kl_coef;             /* beta (PAPER.md :376-382: 0.001 or 0)                                         */
   float grad_scale;          /* s: multiplies every gradient coefficient                                     */
   int32_t kl_estimator;      /* ECHO_KL_*                                                                    */
+  float entropy_coef;        /* eta >= 0: entropy bonus, l_t -= eta H_t (0 = off)                            */
 } echo_loss_config;
 
 /*
- * General form of echo_policy_loss_fwd_bwd (which is this call with tok_adv = tok_weight = NULL, clip_dual = 0,
- * kl_estimator = ECHO_KL_K3):
+ * General form of echo_policy_loss_fwd_bwd (which is this call with tok_adv = tok_weight = tok_entropy = NULL,
+ * clip_dual = 0, kl_estimator = ECHO_KL_K3, entropy_coef = 0):
  *   A_t = tok_adv ? tok_adv[t] : adv_slot[tok_slot[t]]   -- per-token advantages, e.g. PPO-GAE (echo_gae_advantage)
  *   w_t = tok_weight ? tok_weight[t] : 1 / *n_global      -- per-token loss weights, e.g. sequence-mean aggregation
  *                                                           (w_t = 1 / (n_sequences L_i)); n_global may then be NULL
  *   c_t = grad_scale * w_t * dl_t/dlogp ; tok_loss[t] = l_t (unweighted); the step loss is sum_t w_t l_t.
- * cfg is a HOST pointer.  Same layout, launches and errors as echo_policy_loss_fwd_bwd.
+ * Entropy bonus (entropy_coef = eta > 0): H_t = -sum_v p_v log p_v (masked -inf logits contribute 0),
+ *   l_t = pg + beta kl - eta H_t, and d[t,v] = c_t (delta_{v,a} - p_v) + grad_scale w_t eta p_v (log p_v + H_t).
+ *   tok_entropy (nullable, f32[n_rows]) receives H_t.  With eta > 0 or tok_entropy set, the kernel also keeps
+ *   sum_v z_v e^{z_v - m} in pass 1 and recomputes p_v from the logits in pass 2 (fp32 end to end, one more
+ *   exponential per logit); explicit QUAD_REG and QUAD_REG_EXACT both run the 4-CTA entropy variant.
+ * cfg is a HOST pointer.  Same layout, launches and errors as echo_policy_loss_fwd_bwd, plus
+ * ECHO_ERR_INVALID_ARGUMENT for entropy_coef < 0 or not finite.
  */
 ECHO_API echo_status echo_policy_loss_fwd_bwd_v2(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab,
                                                  int64_t ld, const int32_t* tok_action, const float* tok_old,
                                                  const float* tok_ref, const int32_t* tok_slot, const float* adv_slot,
                                                  const float* tok_adv, const float* tok_weight, const double* n_global,
                                                  const echo_loss_config* cfg, float* tok_logp, float* tok_loss,
-                                                 uint8_t* tok_flags, int32_t algo, void* stream);
+                                                 uint8_t* tok_flags, float* tok_entropy, int32_t algo, void* stream);
 
 /* Launch shape echo_policy_loss_fwd_bwd_ex would use on the current device (no launch):
  * shape[5] = {resolved algo, grid CTAs, CTAs per cluster, threads per CTA, dynamic smem bytes}. */

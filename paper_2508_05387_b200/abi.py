@@ -38,7 +38,8 @@ ECHO_KL_K3, ECHO_KL_K1, ECHO_KL_K2 = range(3)
 class LossConfig(ctypes.Structure):
     """echo_loss_config (include/echo.h)."""
     _fields_ = [("clip_low", ctypes.c_float), ("clip_high", ctypes.c_float), ("clip_dual", ctypes.c_float),
-                ("kl_coef", ctypes.c_float), ("grad_scale", ctypes.c_float), ("kl_estimator", ctypes.c_int32)]
+                ("kl_coef", ctypes.c_float), ("grad_scale", ctypes.c_float), ("kl_estimator", ctypes.c_int32),
+                ("entropy_coef", ctypes.c_float)]
 
 
 class EchoError(RuntimeError):
@@ -65,7 +66,7 @@ def _load(path=LIB_PATH):
     lib.echo_policy_loss_launch_shape.argtypes = [i32, i64, i32, i32, P]
     lib.echo_token_logp.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P]
     lib.echo_policy_loss_fwd_bwd_v2.argtypes = [P, i32, i64, i32, i64, P, P, P, P, P, P, P, P,
-                                                ctypes.POINTER(LossConfig), P, P, P, i32, P]
+                                                ctypes.POINTER(LossConfig), P, P, P, P, i32, P]
     lib.echo_policy_loss_fwd_bwd_v2.restype = ctypes.c_int
     lib.echo_token_logp.restype = ctypes.c_int
     lib.echo_policy_loss_launch_shape.restype = ctypes.c_int
@@ -153,11 +154,11 @@ def echo_policy_loss_fwd_bwd(logits, dtype, n_rows, vocab, ld, tok_action, tok_o
 
 def echo_policy_loss_fwd_bwd_v2(logits, dtype, n_rows, vocab, ld, tok_action, tok_old, tok_ref, tok_slot, adv_slot,
                                 tok_adv, tok_weight, n_global, cfg: LossConfig, tok_logp, tok_loss, tok_flags,
-                                algo=ECHO_ALGO_AUTO, stream=None):
+                                tok_entropy=None, algo=ECHO_ALGO_AUTO, stream=None):
     _check("echo_policy_loss_fwd_bwd_v2", _lib.echo_policy_loss_fwd_bwd_v2(
         _p(logits), dtype, n_rows, vocab, ld, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot), _p(adv_slot),
-        _p(tok_adv), _p(tok_weight), _p(n_global), ctypes.byref(cfg), _p(tok_logp), _p(tok_loss), _p(tok_flags), algo,
-        _s(stream)))
+        _p(tok_adv), _p(tok_weight), _p(n_global), ctypes.byref(cfg), _p(tok_logp), _p(tok_loss), _p(tok_flags),
+        _p(tok_entropy), algo, _s(stream)))
 
 
 def echo_token_logp(logits, dtype, n_rows, vocab, ld, tok_action, tok_logp, tok_lse=None, tok_flags=None,

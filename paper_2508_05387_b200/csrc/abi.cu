@@ -1,4 +1,6 @@
 // abi.cu -- the extern "C" entry points of libecho (include/echo.h): argument validation + launches.
+#include <cfloat>
+
 #include <cuda_bf16.h>
 
 #include "echo_internal.h"
@@ -47,7 +49,7 @@ extern "C" ECHO_API void echo_trace_set(unsigned long long* buf, int32_t rows) {
 
 extern "C" {
 
-int32_t echo_abi_version(void) { return 1; }
+int32_t echo_abi_version(void) { return 2; }
 
 const char* echo_status_string(echo_status s) {
   switch (s) {
@@ -114,8 +116,8 @@ echo_status echo_policy_loss_fwd_bwd_v2(void* logits, int32_t dtype, int64_t n_r
                                         const int32_t* tok_action, const float* tok_old, const float* tok_ref,
                                         const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
                                         const float* tok_weight, const double* n_global, const echo_loss_config* cfg,
-                                        float* tok_logp, float* tok_loss, uint8_t* tok_flags, int32_t algo,
-                                        void* stream) {
+                                        float* tok_logp, float* tok_loss, uint8_t* tok_flags, float* tok_entropy,
+                                        int32_t algo, void* stream) {
   if (!cfg) return ECHO_ERR_INVALID_ARGUMENT;
   if (dtype != ECHO_F32 && dtype != ECHO_BF16) return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rows < 0 || vocab < 1 || ld < vocab) return ECHO_ERR_INVALID_ARGUMENT;
@@ -123,7 +125,7 @@ echo_status echo_policy_loss_fwd_bwd_v2(void* logits, int32_t dtype, int64_t n_r
   if ((ld * esize) % 16 != 0) return ECHO_ERR_INVALID_ARGUMENT;
   if (!(cfg->clip_low >= 0.0f && cfg->clip_low < 1.0f && cfg->clip_high >= 0.0f) || !(cfg->kl_coef >= 0.0f) ||
       !(cfg->clip_dual == 0.0f || cfg->clip_dual > 1.0f) || cfg->kl_estimator < ECHO_KL_K3 ||
-      cfg->kl_estimator > ECHO_KL_K2)
+      cfg->kl_estimator > ECHO_KL_K2 || !(cfg->entropy_coef >= 0.0f && cfg->entropy_coef <= FLT_MAX))
     return ECHO_ERR_INVALID_ARGUMENT;
   if (!n_global && !tok_weight) return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rows > 0) {
@@ -157,6 +159,8 @@ echo_status echo_policy_loss_fwd_bwd_v2(void* logits, int32_t dtype, int64_t n_r
   p.kl_estimator = cfg->kl_estimator;
   p.tok_adv = tok_adv;
   p.tok_weight = tok_weight;
+  p.entropy_coef = cfg->entropy_coef;
+  p.tok_entropy = tok_entropy;
   p.tok_logp = tok_logp;
   p.tok_loss = tok_loss;
   p.tok_flags = tok_flags;
@@ -177,10 +181,10 @@ echo_status echo_policy_loss_fwd_bwd_ex(void* logits, int32_t dtype, int64_t n_r
                                         float* tok_logp, float* tok_loss, uint8_t* tok_flags, int32_t algo,
                                         void* stream) {
   if (!n_global) return ECHO_ERR_INVALID_ARGUMENT;
-  const echo_loss_config cfg{clip_low, clip_high, 0.0f, kl_coef, grad_scale, ECHO_KL_K3};
+  const echo_loss_config cfg{clip_low, clip_high, 0.0f, kl_coef, grad_scale, ECHO_KL_K3, 0.0f};
   return echo_policy_loss_fwd_bwd_v2(logits, dtype, n_rows, vocab, ld, tok_action, tok_old, tok_ref, tok_slot,
-                                     adv_slot, nullptr, nullptr, n_global, &cfg, tok_logp, tok_loss, tok_flags, algo,
-                                     stream);
+                                     adv_slot, nullptr, nullptr, n_global, &cfg, tok_logp, tok_loss, tok_flags,
+                                     nullptr, algo, stream);
 }
 
 echo_status echo_policy_loss_fwd_bwd(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,

@@ -71,6 +71,7 @@ ECHO_DEVINL uint32_t bmax2(uint32_t a, uint32_t b) {
   return d;
 }
 constexpr uint32_t kBf16NegInf2 = 0xFF80FF80u;
+constexpr uint32_t kBf16NegBig2 = 0xF14AF14Au;  // bf16 -1.0e30 twice: the entropy path's stand-in for -inf
 
 ECHO_DEVINL float ex2(float x) {
   float y;
@@ -263,21 +264,43 @@ ECHO_DEVINL MaxSum warp_maxsum(MaxSum v) {
   return MaxSum{mx, t};
 }
 
+// (m, s, t) with t = sum x e^{x - m}: the entropy path's third accumulator, rescaled like s.
+struct MaxSum3 {
+  MaxSum ms;
+  float t;
+};
+ECHO_DEVINL MaxSum3 warp_maxsum3(float m, float s, float t) {
+  float mx = m;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float f = (m == -INFINITY) ? 0.0f : ex2((m - mx) * kLog2e);
+  float ss = s * f, tt = t * f;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    tt += __shfl_xor_sync(0xffffffffu, tt, o);
+  }
+  return MaxSum3{MaxSum{mx, ss}, tt};
+}
+
 // ---------------------------------------------------------------- the per-row scalar epilogue (4)
 struct RowScalars {
   float logp, loss, coef;  // coef = c_t: dl/dlogp * scale  (scale = grad_scale * w_t, w_t = 1/N_global or tok_weight)
+  float ecoef;             // scale * eta: the entropy term's gradient factor (0 when off)
   uint8_t flags;
 };
 struct LossOpts {
   float clip_low, clip_high, clip_dual, kl_coef;
   int32_t kl_estimator;  // ECHO_KL_K3 | ECHO_KL_K1 | ECHO_KL_K2
+  float entropy_coef;    // eta (0 = off)
 };
 // lse: log-sum-exp of the row; za: logit at the action; adv: the token's advantage; scale: grad_scale * w_t.
 //   rho = exp(logp - old); pg = max(-A rho, -A clip(rho, 1-lo, 1+hi)) (SPEC.md :219); dual clip (A < 0,
 //   rho > c): pg = -A c; KL to pi_ref by the selected estimator (x = ref - logp): k3 e^x - x - 1 (default),
-//   k1 -x, k2 x^2/2; l_t = pg + beta kl; c_t = scale * ([not clipped](-A rho) + beta dkl/dlogp).
+//   k1 -x, k2 x^2/2; l_t = pg + beta kl - eta H (H: the row's entropy, only read when eta > 0);
+//   c_t = scale * ([not clipped](-A rho) + beta dkl/dlogp).
 ECHO_DEVINL RowScalars row_epilogue(float lse, float za, float old, float ref, float adv, const LossOpts& o,
-                                    float scale) {
+                                    float scale, float H = 0.0f) {
   RowScalars r;
   const float logp = za - lse;
   const float rho = expf(logp - old);
@@ -304,13 +327,16 @@ ECHO_DEVINL RowScalars row_epilogue(float lse, float za, float old, float ref, f
       dkl = 1.0f - ex;
     }
   }
-  const float loss = pg + o.kl_coef * kl;
+  const bool ent = o.entropy_coef > 0.0f;
+  const float loss = pg + o.kl_coef * kl - (ent ? o.entropy_coef * H : 0.0f);
   const float dl = (clipped ? 0.0f : -adv * rho) + o.kl_coef * dkl;
   const float coef = dl * scale;
-  const bool finite = isfinite(lse) && isfinite(logp) && isfinite(rho) && isfinite(loss) && isfinite(coef);
+  const bool finite = isfinite(lse) && isfinite(logp) && isfinite(rho) && isfinite(loss) && isfinite(coef) &&
+                      (!ent || isfinite(H));
   r.logp = logp;
   r.loss = loss;
   r.coef = coef;
+  r.ecoef = scale * o.entropy_coef;
   r.flags = (uint8_t)((clipped ? ECHO_FLAG_CLIPPED : 0) | (finite ? 0 : ECHO_FLAG_NONFINITE));
   return r;
 }

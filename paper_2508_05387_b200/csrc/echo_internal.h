@@ -23,6 +23,8 @@ struct LossParams {
   float clip_low, clip_high, kl_coef, grad_scale;
   float clip_dual;                          // dual-clip constant c (> 1 enables), f4
   int32_t kl_estimator;                     // ECHO_KL_*, f4
+  float entropy_coef;                       // eta: entropy bonus, f4
+  float* __restrict__ tok_entropy;          // per-token entropy output (nullable), f4
   const float* __restrict__ tok_adv;        // per-token advantages (nullable: adv_slot[tok_slot])
   const float* __restrict__ tok_weight;     // per-token loss weights (nullable: 1 / N_global)
   float* __restrict__ tok_logp;

@@ -34,7 +34,7 @@ ECHO_DEVINL RowMeta load_meta(const LossParams& p, int64_t row) {
   return m;
 }
 ECHO_DEVINL LossOpts loss_opts(const LossParams& p) {
-  return LossOpts{p.clip_low, p.clip_high, p.clip_dual, p.kl_coef, p.kl_estimator};
+  return LossOpts{p.clip_low, p.clip_high, p.clip_dual, p.kl_coef, p.kl_estimator, p.entropy_coef};
 }
 // grad_scale / N_global, or grad_scale alone when per-token weights carry the normalisation
 ECHO_DEVINL float base_scale(const LossParams& p) {
@@ -58,6 +58,31 @@ ECHO_DEVINL void online_update(MaxSum& acc, const float (&x)[N]) {
   acc.s += t;
 }
 
+// Same with the entropy accumulator t = sum x e^{x - m} (masked -inf entries contribute 0).
+template <int N>
+ECHO_DEVINL void online_update3(MaxSum& acc, float& t, const float (&x)[N]) {
+  float cm = x[0];
+#pragma unroll
+  for (int e = 1; e < N; ++e) cm = fmaxf(cm, x[e]);
+  if (cm > acc.m) {
+    const float f = ex2((acc.m - cm) * kLog2e);
+    acc.s = acc.s * f;
+    t = t * f;
+    acc.m = cm;
+  }
+  const float mb = (acc.m == -INFINITY) ? 0.0f : acc.m * kLog2e;
+  float ss = 0.0f, tt = 0.0f;
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    const float xe = fmaxf(x[e], -1.0e30f);
+    const float ev = ex2(fmaf(xe, kLog2e, -mb));
+    ss += ev;
+    tt = fmaf(ev, xe, tt);
+  }
+  acc.s += ss;
+  t += tt;
+}
+
 ECHO_DEVINL void unpack8(const uint4& w, float (&x)[8]) {
   x[0] = bf16lo(w.x); x[1] = bf16hi(w.x);
   x[2] = bf16lo(w.y); x[3] = bf16hi(w.y);
@@ -72,6 +97,20 @@ ECHO_DEVINL void grad_values(float (&x)[N], int32_t col0, int32_t a, float coef,
   for (int e = 0; e < N; ++e) {
     const float p = ex2(fmaf(x[e], kLog2e, -lse_l2e));
     x[e] = (col0 + e == a) ? fmaf(-coef, p, coef) : -coef * p;
+  }
+}
+
+// With the entropy term: d_v = c (delta_{v,a} - p_v) + e p_v (z_v - lse + H); masked -inf entries get the plain
+// c (delta - p) = 0.
+template <int N>
+ECHO_DEVINL void grad_values_ent(float (&x)[N], int32_t col0, int32_t a, float coef, float lse_l2e, float lse, float H,
+                                 float ecoef) {
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    const float p = ex2(fmaf(x[e], kLog2e, -lse_l2e));
+    float d = (col0 + e == a) ? fmaf(-coef, p, coef) : -coef * p;
+    if (x[e] != -INFINITY) d = fmaf(ecoef * p, x[e] - lse + H, d);
+    x[e] = d;
   }
 }
 

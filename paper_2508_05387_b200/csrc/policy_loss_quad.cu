@@ -66,11 +66,14 @@ struct __align__(128) QuadSmem {
   uint4 xbuf[2][C::kCtas];  // cluster partials {m, s, z_a, -} per row parity and source rank
   float red_m[C::kWarps];
   float red_s[C::kWarps];
+  float red_t[C::kWarps];  // kModeEntropy: sum z e^{z - m} per warp
   float za;
   MetaSm meta[2];        // rows of iterations it (it & 1) and it+1
   float coef;
   float lse;
   float da;
+  float ent_k;           // kModeEntropy: eta s w (H - lse) - c_t
+  float ent_e;           // kModeEntropy: eta s w
   uint64_t rowbar[4];    // row table: iteration k's row lands in rowtab[k % 4] (st.async from rank 0)
   int64_t rowtab[4];
 };
@@ -87,6 +90,7 @@ constexpr int kRowAhead = 3;
   // rows are broadcast this many iterations ahead (<= 4: the table depth)
 
 struct QuadGeom {
+  int32_t q;               // slice width: rank r owns [r q, min((r+1) q, V))
   int32_t c0, c1;          // this CTA's columns [c0, c1)
   uint32_t slice_bytes;    // bytes loaded per row (c1 rounded up to 8 columns)
   int nchunks;             // ring chunks per row
@@ -96,6 +100,7 @@ template <class C>
 ECHO_DEVINL QuadGeom quad_geom(int32_t V, uint32_t rank) {
   QuadGeom g;
   const int32_t q = ((V + C::kCtas - 1) / C::kCtas + 7) & ~7;
+  g.q = q;
   // slices start on 8-column boundaries; a rank past the end gets an empty slice [V8, V8)
   const int32_t v8 = (V + 7) & ~7;
   g.c0 = min((int32_t)rank * q, v8);
@@ -127,13 +132,16 @@ ECHO_DEVINL void quad_issue_chunks(const LossParams& p, const QuadGeom& g, uint3
 
 // kMode: kModeExact (gradient, exp recomputed in pass 2), kModeCache (gradient, exp kept as fp16 between the
 // passes), kModeLogp (forward only: log-probs and lse, the logits are not written -- SURVEY.md §8.6 f1).
-enum { kModeExact = 0, kModeCache = 1, kModeLogp = 2 };
+// kModeEntropy: kModeExact plus the entropy bonus (f4): pass 1 also accumulates t = sum z e^{z - m}, the cluster
+// merge carries (m, s, t), H = lse - t / s, and pass 2 adds the entropy gradient p (log p + H) eta s w.
+enum { kModeExact = 0, kModeCache = 1, kModeLogp = 2, kModeEntropy = 3 };
 
 template <class C, int kMode>
 __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, C::kCtasPerSm)
     policy_loss_quad_kernel(const LossParams p) {
   constexpr bool kStoreExp = kMode == kModeCache;
   constexpr bool kGrad = kMode != kModeLogp;
+  constexpr bool kEnt = kMode == kModeEntropy;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   QuadSmem<C>& sm = *reinterpret_cast<QuadSmem<C>*>(smem_raw);
   const uint32_t rank = cluster_ctarank();
@@ -286,18 +294,22 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     // ---- pass 1b
     const float mb = (mx == -INFINITY) ? 0.0f : mx * kLog2e;
     const uint64_t nmb2 = f2(-mb, -mb);
-    uint64_t s2 = f2(0.0f, 0.0f);
+    uint64_t s2 = f2(0.0f, 0.0f), t2 = f2(0.0f, 0.0f);
 #pragma unroll
     for (int c = 0; c < C::kRegChunks; ++c) {
       if (c < nchunks) {
         uint32_t* w = &v[c].x;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+          // entropy: masked -inf logits are clamped to -1e30 so that e z = 0 (not NaN) here and in pass 2
+          if (kEnt) w[k] = bmax2(w[k], kBf16NegBig2);
+          const uint64_t z2 = bf2_to_f2(w[k]);
           float e0, e1;
-          f2split(fma2(bf2_to_f2(w[k]), l2e2, nmb2), e0, e1);
+          f2split(fma2(z2, l2e2, nmb2), e0, e1);
           e0 = ex2(e0);
           e1 = ex2(e1);
           s2 = add2(s2, f2(e0, e1));
+          if (kEnt) t2 = fma2(f2(e0, e1), z2, t2);
           if (kStoreExp) w[k] = pack_f16x2(e0, e1);
         }
       }
@@ -305,10 +317,17 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     float slo, shi;
     f2split(s2, slo, shi);
     ECHO_TRACE_MARK(p, it, 11);
-    const MaxSum acc = warp_maxsum(MaxSum{mx, slo + shi});
+    float tsum = 0.0f;
+    if (kEnt) {
+      float tlo, thi;
+      f2split(t2, tlo, thi);
+      tsum = tlo + thi;
+    }
+    const MaxSum3 acc = kEnt ? warp_maxsum3(mx, slo + shi, tsum) : MaxSum3{warp_maxsum(MaxSum{mx, slo + shi}), 0.0f};
     if (lane == 0) {
-      sm.red_m[warp] = acc.m;
-      sm.red_s[warp] = acc.s;
+      sm.red_m[warp] = acc.ms.m;
+      sm.red_s[warp] = acc.ms.s;
+      if (kEnt) sm.red_t[warp] = acc.t;
     }
     ECHO_TRACE_MARK(p, it, 2);
     named_bar_sync(kQBar, C::kThreads);
@@ -341,14 +360,21 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
 
     // ---- CTA merge (warp 0), cluster merge (st.async to every peer), epilogue (lane 0)
     if (warp == 0) {
-      MaxSum mine = lane < C::kWarps ? MaxSum{sm.red_m[lane], sm.red_s[lane]} : MaxSum{-INFINITY, 0.0f};
-      mine = warp_maxsum(mine);
+      MaxSum3 mine;
+      if (kEnt) {
+        mine = warp_maxsum3(lane < C::kWarps ? sm.red_m[lane] : -INFINITY, lane < C::kWarps ? sm.red_s[lane] : 0.0f,
+                            lane < C::kWarps ? sm.red_t[lane] : 0.0f);
+      } else {
+        mine.ms = warp_maxsum(lane < C::kWarps ? MaxSum{sm.red_m[lane], sm.red_s[lane]} : MaxSum{-INFINITY, 0.0f});
+        mine.t = 0.0f;
+      }
       ECHO_TRACE_MARK(p, it, 12);
       if (lane == 0) {
         const uint32_t par = it & 1u;
         const bool owner = (a >= c0 && a < c1);
-        const uint4 msg = make_uint4(__float_as_uint(mine.m), __float_as_uint(mine.s),
-                                     __float_as_uint(owner ? sm.za : 0.0f), owner ? 1u : 0u);
+        // {m, s, t, z_a}: the receivers take z_a from the rank that owns column a (a / q)
+        const uint4 msg = make_uint4(__float_as_uint(mine.ms.m), __float_as_uint(mine.ms.s), __float_as_uint(mine.t),
+                                     __float_as_uint(owner ? sm.za : 0.0f));
         const uint32_t xbar_local = smem_u32(&sm.xbar[par]);
         mbar_arrive_expect_tx(xbar_local, 16 * C::kCtas);
 #pragma unroll
@@ -359,34 +385,39 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         ECHO_TRACE_MARK(p, it, 7);
         // cluster merge in rank order: max first, then the rescaled sum (the exps are independent)
         // (the partials are re-read from shared memory rather than held: 4 words per rank would cost registers)
-        float za = NAN, mm = -INFINITY;
+        float mm = -INFINITY;
 #pragma unroll
-        for (int r = 0; r < C::kCtas; ++r) {
-          const uint4 m = sm.xbuf[par][r];
-          mm = fmaxf(mm, __uint_as_float(m.x));
-          if (m.w) za = __uint_as_float(m.z);
-        }
-        float ss = 0.0f;
+        for (int r = 0; r < C::kCtas; ++r) mm = fmaxf(mm, __uint_as_float(sm.xbuf[par][r].x));
+        float ss = 0.0f, tt = 0.0f;
 #pragma unroll
         for (int r = 0; r < C::kCtas; ++r) {
           const float mr = __uint_as_float(sm.xbuf[par][r].x), sr = __uint_as_float(sm.xbuf[par][r].y);
-          ss += (mr == -INFINITY) ? 0.0f : sr * ex2((mr - mm) * kLog2e);
+          const float f = (mr == -INFINITY) ? 0.0f : ex2((mr - mm) * kLog2e);
+          ss += sr * f;
+          if (kEnt) tt += __uint_as_float(sm.xbuf[par][r].z) * f;
         }
         const float lse = mm + logf(ss);
-        if (a < 0 || a >= V) za = NAN;
+        const float za = (a < 0 || a >= V) ? NAN : __uint_as_float(sm.xbuf[par][a / g.q].w);
         if constexpr (kGrad) {
           cp_async_wait<1>();  // C(it) landed
           const MetaSm& m = sm.meta[it & 1u];
-          const RowScalars r = row_epilogue(lse, za, m.old, m.ref, m.adv, loss_opts(p), gscale * m.w);
+          const float H = kEnt ? lse - tt / ss : 0.0f;  // -sum p log p = lse - sum p z
+          const RowScalars r = row_epilogue(lse, za, m.old, m.ref, m.adv, loss_opts(p), gscale * m.w, H);
           if (rank == 0) {
             p.tok_logp[row] = r.logp;
             p.tok_loss[row] = r.loss;
             p.tok_flags[row] = r.flags;
+            if (kEnt && p.tok_entropy) p.tok_entropy[row] = H;
           }
           const float pa = ex2(fmaf(za, kLog2e, -lse * kLog2e));
           sm.coef = r.coef;
           sm.lse = lse;
           sm.da = fmaf(-r.coef, pa, r.coef);
+          if (kEnt) {
+            sm.ent_e = r.ecoef;
+            sm.ent_k = fmaf(r.ecoef, H - lse, -r.coef);
+            sm.da = fmaf(r.ecoef * pa, za - lse + H, sm.da);  // c (1 - p_a) + e p_a (log p_a + H)
+          }
         } else if (rank == 0) {
           const float logp = za - lse;
           p.tok_logp[row] = logp;
@@ -400,6 +431,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     ECHO_TRACE_MARK(p, it, 4);
     if constexpr (!kGrad) continue;
     const float coef = sm.coef, lse = sm.lse;
+    const uint64_t ee2 = kEnt ? f2(sm.ent_e, sm.ent_e) : 0ull, ek2 = kEnt ? f2(sm.ent_k, sm.ent_k) : 0ull;
 
     // ---- pass 2
     const float kt = mx == -INFINITY ? 0.0f : -coef * ex2((mx - lse) * kLog2e);
@@ -418,6 +450,12 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
           float d0, d1;
           if (kStoreExp) {
             f2split(mul2(f2(f16lo(w[k]), f16hi(w[k])), k2), d0, d1);
+          } else if (kEnt) {
+            // d = p (e (z - lse + H) - c) = p (e z + k),  k = e (H - lse) - c
+            const uint64_t z2 = bf2_to_f2(w[k]);
+            float t0, t1;
+            f2split(fma2(z2, l2e2, nlse2), t0, t1);
+            f2split(mul2(f2(ex2(t0), ex2(t1)), fma2(z2, ee2, ek2)), d0, d1);
           } else {
             float t0, t1;
             f2split(fma2(bf2_to_f2(w[k]), l2e2, nlse2), t0, t1);
@@ -478,11 +516,14 @@ using Oct = QCfg<8, 4>;
 bool quad_supports(int32_t dtype, int32_t V) { return supports_t<Quad>(dtype, V); }
 bool oct_supports(int32_t dtype, int32_t V) { return supports_t<Oct>(dtype, V); }
 
+static bool wants_entropy(const LossParams& p) { return p.entropy_coef > 0.0f || p.tok_entropy != nullptr; }
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  if (wants_entropy(p)) return launch_t<Quad, kModeEntropy>(p, stream, num_sms, shape);
   return store_exp ? launch_t<Quad, kModeCache>(p, stream, num_sms, shape)
                    : launch_t<Quad, kModeExact>(p, stream, num_sms, shape);
 }
 cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  if (wants_entropy(p)) return launch_t<Oct, kModeEntropy>(p, stream, num_sms, shape);
   return launch_t<Oct, kModeCache>(p, stream, num_sms, shape);
 }
 // forward-only log-probs: the 8-CTA tile (1.93 ms vs 1.97 ms for the 4-CTA one on 32768 x 151936)

@@ -43,12 +43,13 @@ struct RowVec<0> {
   static ECHO_DEVINL void store1(uint8_t* row, int32_t v, float x) { reinterpret_cast<float*>(row)[v] = x; }
 };
 
-template <int DT, bool kGrad>  // kGrad = false: forward-only log-probs, logits not written
+// kGrad = false: forward-only log-probs, logits not written; kEnt: the f4 entropy bonus
+template <int DT, bool kGrad, bool kEnt = false>
 __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const LossParams p) {
   using RV = RowVec<DT>;
   constexpr int N = RV::N;
-  __shared__ float s_m[kRWarps], s_s[kRWarps];
-  __shared__ float s_za, s_coef, s_lse_l2e;
+  __shared__ float s_m[kRWarps], s_s[kRWarps], s_t[kRWarps];
+  __shared__ float s_za, s_coef, s_lse_l2e, s_lse, s_H, s_ecoef;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int32_t V = p.V;
   const int32_t nvec = V / N;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
 
     // ---- pass 1
     MaxSum acc{-INFINITY, 0.0f};
+    float tacc = 0.0f;
     for (int32_t v0 = tid; v0 < nvec; v0 += kRThreads * kRUnroll) {
       uint4 w[kRUnroll];
 #pragma unroll
@@ -86,33 +88,50 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
             for (int e = 0; e < N; ++e)
               if (col + e == a) s_za = x[e];
           }
-          online_update<N>(acc, x);
+          if (kEnt) online_update3<N>(acc, tacc, x);
+          else online_update<N>(acc, x);
         }
       }
     }
     for (int32_t col = nvec * N + tid; col < V; col += kRThreads) {  // ragged tail (V % N)
       float x[1] = {RV::load1(rowp, col)};
       if (col == a) s_za = x[0];
-      online_update<1>(acc, x);
+      if (kEnt) online_update3<1>(acc, tacc, x);
+      else online_update<1>(acc, x);
     }
-    acc = warp_maxsum(acc);
+    if (kEnt) {
+      const MaxSum3 a3 = warp_maxsum3(acc.m, acc.s, tacc);
+      acc = a3.ms;
+      tacc = a3.t;
+    } else {
+      acc = warp_maxsum(acc);
+    }
     if (lane == 0) {
       s_m[warp] = acc.m;
       s_s[warp] = acc.s;
+      if (kEnt) s_t[warp] = tacc;
     }
     __syncthreads();
-    MaxSum tot{-INFINITY, 0.0f};
-    if (warp == 0) tot = warp_maxsum(MaxSum{s_m[lane], s_s[lane]});  // kRWarps == 32: one lane per warp
+    MaxSum3 tot{MaxSum{-INFINITY, 0.0f}, 0.0f};
+    if (warp == 0) {  // kRWarps == 32: one lane per warp
+      if (kEnt) tot = warp_maxsum3(s_m[lane], s_s[lane], s_t[lane]);
+      else tot.ms = warp_maxsum(MaxSum{s_m[lane], s_s[lane]});
+    }
     if (tid == 0) {
-      const float lse = tot.m + logf(tot.s);
+      const float lse = tot.ms.m + logf(tot.ms.s);
       const float za = (a < 0 || a >= V) ? NAN : s_za;
       if constexpr (kGrad) {
-        const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, loss_opts(p), gscale * meta.w);
+        const float H = kEnt ? lse - tot.t / tot.ms.s : 0.0f;
+        const RowScalars r = row_epilogue(lse, za, meta.old, meta.ref, meta.adv, loss_opts(p), gscale * meta.w, H);
         p.tok_logp[row] = r.logp;
         p.tok_loss[row] = r.loss;
         p.tok_flags[row] = r.flags;
+        if (kEnt && p.tok_entropy) p.tok_entropy[row] = H;
         s_coef = r.coef;
         s_lse_l2e = lse * kLog2e;
+        s_lse = lse;
+        s_H = H;
+        s_ecoef = r.ecoef;
       } else {
         const float logp = za - lse;
         p.tok_logp[row] = logp;
@@ -122,7 +141,7 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
     }
     __syncthreads();
     if constexpr (!kGrad) continue;
-    const float coef = s_coef, lse_l2e = s_lse_l2e;
+    const float coef = s_coef, lse_l2e = s_lse_l2e, lse = s_lse, H = s_H, ecoef = s_ecoef;
 
     // ---- pass 2
     for (int32_t v0 = tid; v0 < nvec; v0 += kRThreads * kRUnroll) {
@@ -138,14 +157,16 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
         if (v < nvec) {
           float x[N];
           RV::unpack(w[u], x);
-          grad_values<N>(x, v * N, a, coef, lse_l2e);
+          if (kEnt) grad_values_ent<N>(x, v * N, a, coef, lse_l2e, lse, H, ecoef);
+          else grad_values<N>(x, v * N, a, coef, lse_l2e);
           stg_v4_hint(rowp + (int64_t)v * 16, RV::pack(x), pol_drop);
         }
       }
     }
     for (int32_t col = nvec * N + tid; col < V; col += kRThreads) {
       float x[1] = {RV::load1(rowp, col)};
-      grad_values<1>(x, col, a, coef, lse_l2e);
+      if (kEnt) grad_values_ent<1>(x, col, a, coef, lse_l2e, lse, H, ecoef);
+      else grad_values<1>(x, col, a, coef, lse_l2e);
       RV::store1(rowp, col, x[0]);
     }
     __syncthreads();  // s_* reuse by the next row
@@ -160,13 +181,18 @@ cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, 
     *shape = LaunchShape{(int32_t)grid, 1, kRThreads, 0};
     return cudaSuccess;
   }
+  const bool ent = grad && (p.entropy_coef > 0.0f || p.tok_entropy != nullptr);
   if (dtype == ECHO_BF16) {
-    if (grad)
+    if (ent)
+      policy_loss_row_kernel<1, true, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+    else if (grad)
       policy_loss_row_kernel<1, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
     else
       policy_loss_row_kernel<1, false><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
   } else {
-    if (grad)
+    if (ent)
+      policy_loss_row_kernel<0, true, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+    else if (grad)
       policy_loss_row_kernel<0, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
     else
       policy_loss_row_kernel<0, false><<<(unsigned)grid, kRThreads, 0, stream>>>(p);

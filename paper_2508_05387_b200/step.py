@@ -121,27 +121,31 @@ class LearnerStep:
 
     # ------------------------------------------------------------------ (3)-(5)
     def loss(self, logits: torch.Tensor, row0: int, *, clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0,
-             algo=None, stream=None, tok_adv=None, tok_weight=None, clip_dual=0.0, kl_estimator=abi.ECHO_KL_K3):
+             algo=None, stream=None, tok_adv=None, tok_weight=None, clip_dual=0.0, kl_estimator=abi.ECHO_KL_K3,
+             entropy_coef=0.0, tok_entropy=None):
         """Fused loss fwd+bwd over packed rows [row0, row0 + logits.shape[0]); logits become dlogits.
 
         f4 options (echo_policy_loss_fwd_bwd_v2): ``tok_adv`` / ``tok_weight`` are full-length per-token device
         arrays (per-token advantages, e.g. GAE; per-token loss weights, e.g. sequence-mean), ``clip_dual`` and
-        ``kl_estimator`` select the dual clip and the KL estimator."""
+        ``kl_estimator`` select the dual clip and the KL estimator, ``entropy_coef`` the entropy bonus; ``tok_entropy``
+        (full-length f32 device array, nullable) receives the per-token entropies."""
         n_rows, ld = logits.shape
         sl = slice(row0, row0 + n_rows)
         ref = self.tok_ref[sl] if (self.tok_ref is not None and kl_coef > 0) else None
-        if tok_adv is None and tok_weight is None and clip_dual == 0.0 and kl_estimator == abi.ECHO_KL_K3:
+        if (tok_adv is None and tok_weight is None and clip_dual == 0.0 and kl_estimator == abi.ECHO_KL_K3
+                and entropy_coef == 0.0 and tok_entropy is None):
             abi.echo_policy_loss_fwd_bwd(logits, self.edtype, n_rows, self.V, ld, self.tok_action[sl], self.tok_old[sl],
                                          ref, self.tok_slot[sl], self.adv_slot, self.stats1[0:1], clip_low, clip_high,
                                          kl_coef, grad_scale, self.tok_logp[sl], self.tok_loss[sl], self.tok_flags[sl],
                                          stream=stream, algo=algo)
         else:
-            cfg = abi.LossConfig(clip_low, clip_high, clip_dual, kl_coef, grad_scale, kl_estimator)
+            cfg = abi.LossConfig(clip_low, clip_high, clip_dual, kl_coef, grad_scale, kl_estimator, entropy_coef)
             abi.echo_policy_loss_fwd_bwd_v2(logits, self.edtype, n_rows, self.V, ld, self.tok_action[sl],
                                             self.tok_old[sl], ref, self.tok_slot[sl], self.adv_slot,
                                             None if tok_adv is None else tok_adv[sl],
                                             None if tok_weight is None else tok_weight[sl], self.stats1[0:1], cfg,
                                             self.tok_logp[sl], self.tok_loss[sl], self.tok_flags[sl],
+                                            tok_entropy=None if tok_entropy is None else tok_entropy[sl],
                                             algo=abi.ECHO_ALGO_AUTO if algo is None else algo, stream=stream)
         self.launches += abi.LAUNCHES["echo_policy_loss_fwd_bwd"] if n_rows > 0 else 0
 

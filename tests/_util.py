@@ -57,7 +57,7 @@ def coef_slack(ref: oracle.LossOut, old, tok_ref, adv_tok, kl_coef, grad_scale, 
 
 
 def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dtype: str, clip=(0.2, 0.2),
-               old=None, cslack=None):
+               old=None, cslack=None, eslack=None, loss_atol=1e-6):
     """Element-wise parity of a set of rows; returns number of gradient rows compared.
 
     logp: |d| <= 1e-5 + 1e-6 |logp|; l_t: rtol 1e-5 (+1e-6 abs); dlogits (bf16): |d| <= ulp_bf16(d_ref) + 4e-6 |c_t|
@@ -65,7 +65,8 @@ def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dty
     north_star bar max|d| <= 2e-3 (checked by the callers at max|d_ref| in [0.25, 0.5));
     (fp32): |d| <= 1e-5 |d_ref| + 4e-6 |c_t| + slack_t, where slack_t (coef_slack) bounds the error the fp32
     log-prob propagates into c_t.  Rows whose reference ratio sits within 1e-5 of a clip boundary decide
-    "clipped" in different precisions (fp64 vs fp32): only logp is compared there.
+    "clipped" in different precisions (fp64 vs fp32): only logp is compared there.  eslack (per element, the
+    entropy term's fp32 error bound) and loss_atol widen the bars for the entropy variant.
     """
     logp_gpu = np.asarray(logp_gpu, np.float64)
     assert np.all(np.abs(logp_gpu - ref.logp) <= 1e-5 + 1e-6 * np.abs(ref.logp)), \
@@ -75,12 +76,16 @@ def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dty
     ok = ~near & ((ref.flags & 2) == 0)
     np.testing.assert_array_equal(np.asarray(flags_gpu)[ok], ref.flags[ok])
     loss_gpu = np.asarray(loss_gpu, np.float64)
-    assert np.all(np.abs(loss_gpu - ref.loss)[ok] <= 1e-5 * np.abs(ref.loss[ok]) + 1e-6)
+    lt = loss_atol if np.isscalar(loss_atol) else np.asarray(loss_atol)[ok]
+    assert np.all(np.abs(loss_gpu - ref.loss)[ok] <= 1e-5 * np.abs(ref.loss[ok]) + lt), \
+        f"loss max err {np.max(np.abs(loss_gpu - ref.loss)[ok])}"
     d = np.asarray(d_gpu, np.float64)[ok]
     dr = ref.dlogits[ok]
     c = np.abs(ref.coef[ok])[:, None]
     slack = 0.0 if cslack is None else np.asarray(cslack)[ok][:, None]
     base = bf16_ulp(dr) if dtype == "bf16" else 1e-5 * np.abs(dr)      # faithful bf16 rounding: within 1 ulp
+    if eslack is not None:
+        slack = slack + np.asarray(eslack)[ok]
     tol = np.broadcast_to(base + 4e-6 * c + slack, d.shape)
     err = np.abs(d - dr)
     bad = err > tol + 1e-30

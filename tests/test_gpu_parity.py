@@ -490,3 +490,43 @@ def test_loss_variants_v2(name, algo, est, dual):
                dtype=cfg.dtype, old=sub(old[:n]), cslack=sub(cs))
     if dual:
         assert (ref.flags & 1).any()
+
+
+@pytest.mark.parametrize("name,algo", [("tiny", None), ("qwen3-4b", None), ("qwen3-4b", 2), ("qwen3-4b", 3),
+                                       ("qwen3-4b", 1)])
+def test_entropy_bonus_v2(name, algo):
+    """f4 entropy bonus through echo_policy_loss_fwd_bwd_v2: per-token entropies, l_t = pg + beta kl - eta H_t and
+    the entropy gradient, including rows with masked (-inf) vocabulary columns."""
+    from paper_2508_05387_b200 import abi
+    cfg = synth.CONFIGS[name]
+    b = synth.make_batch(cfg, 0, 2 * cfg.G if name != "tiny" else cfg.R)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    n = min(info.n_tokens, 1024)
+    logits = fill(st, cfg, 0, n)
+    V = cfg.V
+    logits[:8, V // 3: V // 3 + 257] = float("-inf")         # masked columns (e.g. a vocabulary mask)
+    z = as_oracle_rows(logits)
+    kl, eta = 0.05, 0.01
+    args = (o.pk.tok_action[:n], o.pk.tok_old[:n], o.pk.tok_ref[:n], o.pk.tok_slot[:n], o.adv)
+    kw = dict(n_global=info.n_tokens, kl_coef=kl, entropy_coef=eta)
+    probe = oracle.policy_loss(z, *args, **kw)
+    s = pow2_scale_for(np.abs(probe.dlogits).max())
+    ref = oracle.policy_loss(z, *args, grad_scale=s, **kw)
+    ent = torch.full((st.cap,), float("nan"), device="cuda")
+    st.loss(logits, 0, kl_coef=kl, grad_scale=s, algo=algo, entropy_coef=eta, tok_entropy=ent)
+    H = ent[:n].cpu().numpy().astype(np.float64)
+    _, lse, _ = oracle.token_logp(z, o.pk.tok_action[:n], vocab=V)
+    hbar = 3e-5 * (1 + np.abs(lse) + np.abs(ref.entropy))
+    assert np.all(np.abs(H - ref.entropy) <= hbar), np.max(np.abs(H - ref.entropy) / hbar)
+    zf = (z.astype(np.float64) if cfg.dtype != "bf16" else
+          (z.astype(np.uint32) << 16).view(np.float32).astype(np.float64))
+    zf = np.where(np.isinf(zf), 0.0, zf)
+    p = np.exp(np.where(np.isinf(ref.dlogits), 0.0, zf - lse[:, None]))
+    e = s * eta / info.n_tokens
+    es = e * p * (np.abs(zf) + np.abs(lse)[:, None] + np.abs(ref.entropy)[:, None] + 1) * 3e-5
+    check_rows(d_gpu=logits.float().cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
+               loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
+               dtype=cfg.dtype, old=o.pk.tok_old[:n], eslack=es, loss_atol=1e-6 + eta * hbar)
+    # masked columns: exactly zero gradient
+    assert torch.all(logits[:8, V // 3: V // 3 + 257] == 0)
