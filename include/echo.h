@@ -250,6 +250,19 @@ ECHO_API echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, co
                                      const float* tok_old, const float* tok_ref, const float* tok_weight,
                                      const uint8_t* tok_flags, double* workspace, double* loss_stats, void* stream);
 
+/*
+ * f3: token-balanced resharding after the stale filter (PAPER.md :224 drops whole groups, so the
+ * ranks' kept-token counts diverge; the data-parallel learners of PAPER.md :258-261 then wait for the busiest).
+ * paper_2508_05387_b200/parallel.py moves whole kept rollouts between ranks (NCCL all-to-all of the packed arrays,
+ * contiguous in global rollout order); the receiver rebuilds the CSR of echo_pack_batch from the received lengths:
+ *   kept_offset[i] = sum_{j<i} max(lengths[j], 0),  kept_offset[n] = total;  tok_slot[t] = i for t in
+ *   [kept_offset[i], kept_offset[i+1]).
+ * lengths: device int32[n]; kept_offset: device int64[n+1]; tok_slot: device int32[total] (nullable: offsets
+ * only).  Launches: 1 kernel (scan), +1 (fill) when n > 0 and tok_slot is set.  Bit-exact.
+ */
+ECHO_API echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* kept_offset,
+                                           int32_t* tok_slot, void* stream);
+
 /* Human-readable name of a status code (static storage). */
 ECHO_API const char* echo_status_string(echo_status status);
 

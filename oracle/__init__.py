@@ -63,6 +63,8 @@ def lib():
         _lib.echo_ref_scaled_loss.argtypes = [i64, i32, i64, P, P, P, P, P, P, P, P, f64, f32, f32, f32, f32, i32,
                                               f32, f32]
         _lib.echo_ref_scaled_loss.restype = f64
+        _lib.echo_ref_csr_from_lengths.argtypes = [i32, P, P, P]
+        _lib.echo_ref_csr_from_lengths.restype = ctypes.c_int
     return _lib
 
 
@@ -236,3 +238,16 @@ def scaled_loss(logits_f64, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *,
                                             _p(_c(adv_slot, np.float32)), _p(_c(tok_adv, np.float32)),
                                             _p(_c(tok_weight, np.float32)), float(n_global), clip_low, clip_high,
                                             clip_dual, kl_coef, kl_estimator, grad_scale, entropy_coef))
+
+
+def csr_from_lengths(lengths):
+    """f3: (kept_offset int64[n+1], tok_slot int32[total]) of kept rollouts with these lengths."""
+    lengths = _c(lengths, np.int32)
+    n = len(lengths)
+    off = np.zeros(n + 1, np.int64)
+    total = int(np.maximum(lengths, 0).sum())
+    slot = np.zeros(max(total, 1), np.int32)
+    rc = lib().echo_ref_csr_from_lengths(n, _p(lengths), _p(off), _p(slot))
+    if rc != 0:
+        raise ValueError("echo_ref_csr_from_lengths: invalid argument")
+    return off, slot[:total]

@@ -476,3 +476,21 @@ double echo_ref_scaled_loss(int64_t n_rows, int32_t vocab, int64_t ld, const dou
   }
   return (double)grad_scale * total;
 }
+
+/* ======================================================================================
+ * f3: the CSR of (1) rebuilt from kept-rollout lengths after token-balanced resharding
+ * (PAPER.md :224 drops whole groups; rollouts are then moved between ranks whole):
+ *   kept_offset[0] = 0, kept_offset[i+1] = kept_offset[i] + max(lengths[i], 0);  tok_slot[t] = i for
+ *   kept_offset[i] <= t < kept_offset[i+1].
+ * ====================================================================================== */
+int echo_ref_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* kept_offset, int32_t* tok_slot) {
+  if (n < 0) return REF_ERR_INVALID_ARGUMENT;
+  kept_offset[0] = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t len = lengths[i] > 0 ? lengths[i] : 0;
+    kept_offset[i + 1] = kept_offset[i] + len;
+    if (tok_slot)
+      for (int64_t t = kept_offset[i]; t < kept_offset[i + 1]; ++t) tok_slot[t] = i;
+  }
+  return REF_OK;
+}

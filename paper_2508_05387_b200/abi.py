@@ -25,11 +25,12 @@ PACK_RESULT_BYTES = 32
 
 # kernels launched per call (for the bench's gpu_launches count)
 LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2,
-            "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1}
+            "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1, "echo_csr_from_lengths": 2}
 
 EXPORTS = ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
            "echo_policy_loss_launch_shape", "echo_token_logp", "echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage",
-           "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_status_string", "echo_abi_version")
+           "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_csr_from_lengths", "echo_status_string",
+           "echo_abi_version")
 
 
 ECHO_KL_K3, ECHO_KL_K1, ECHO_KL_K2 = range(3)
@@ -75,8 +76,9 @@ def _load(path=LIB_PATH):
     lib.echo_status_string.argtypes = [ctypes.c_int]
     lib.echo_status_string.restype = ctypes.c_char_p
     lib.echo_abi_version.restype = i32
+    lib.echo_csr_from_lengths.argtypes = [i32, P, P, P, P]
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
-               "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2"):
+               "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths"):
         getattr(lib, fn).restype = ctypes.c_int
     return lib
 
@@ -172,6 +174,11 @@ def echo_policy_loss_launch_shape(dtype, n_rows, vocab, algo=ECHO_ALGO_AUTO) -> 
     _check("echo_policy_loss_launch_shape",
            _lib.echo_policy_loss_launch_shape(dtype, n_rows, vocab, algo, ctypes.cast(buf, ctypes.c_void_p)))
     return dict(zip(("algo", "grid_ctas", "cluster_ctas", "threads", "smem_bytes"), list(buf)))
+
+
+def echo_csr_from_lengths(n, lengths, kept_offset, tok_slot=None, stream=None):
+    _check("echo_csr_from_lengths", _lib.echo_csr_from_lengths(n, _p(lengths), _p(kept_offset), _p(tok_slot),
+                                                                _s(stream)))
 
 
 def echo_loss_stats_workspace_bytes() -> int:

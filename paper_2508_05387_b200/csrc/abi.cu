@@ -250,6 +250,16 @@ echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, i
   return from_cuda(echo::launch_row(p, dtype, s, sms, nullptr, false));
 }
 
+echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* kept_offset, int32_t* tok_slot,
+                                  void* stream) {
+  if (n < 0 || !kept_offset || (n > 0 && !lengths)) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  return from_cuda(echo::launch_csr_from_lengths(n, lengths, kept_offset, tok_slot,
+                                                 static_cast<cudaStream_t>(stream), sms));
+}
+
 size_t echo_loss_stats_workspace_bytes(void) { return echo::loss_stats_workspace_bytes(); }
 
 echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp, const float* tok_old,

@@ -68,6 +68,9 @@ cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cud
 cudaError_t launch_gae(int32_t R, int32_t S, const int32_t* resp_len, const float* rewards, const float* values,
                        const float* bootstrap, float gamma, float lam, float* adv, float* ret, cudaStream_t stream);
 
+cudaError_t launch_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* offsets, int32_t* tok_slot,
+                                    cudaStream_t stream, int num_sms);
+
 size_t loss_stats_workspace_bytes();
 cudaError_t launch_loss_stats(int64_t n, const float* tok_loss, const float* tok_logp, const float* tok_old,
                               const float* tok_ref, const float* tok_weight, const uint8_t* tok_flags, double* ws,

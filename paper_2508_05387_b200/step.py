@@ -4,6 +4,8 @@
     pack       echo_pack_batch                 (1) lag filter + pack; one 32-byte D2H read sizes the logits
     advantage  echo_group_advantage            (2) GRPO advantage
     stats1     all-reduce {N, advantage/reward sums, group counts} -> N_global stays on the device
+    rebalance  (f3, optional) move whole kept rollouts between ranks so every rank holds ~N_global / W tokens:
+               NCCL all-to-all of the packed arrays, echo_csr_from_lengths rebuilds the CSR
     loss       echo_policy_loss_fwd_bwd        (3)-(5) once per micro-batch of logits rows (in place)
     finish     echo_loss_stats + all-reduce    statistics of the step, read back for logging
 
@@ -16,7 +18,7 @@ from dataclasses import dataclass
 import torch
 
 from . import abi
-from .parallel import allreduce_sum_, reduce_loss_stats_, LOSS_STATS, STATS1
+from .parallel import allreduce_sum_, exchange, reduce_loss_stats_, reshard_plan, LOSS_STATS, STATS1
 
 
 @dataclass
@@ -69,6 +71,9 @@ class LearnerStep:
         self.ws = torch.empty(abi.echo_loss_stats_workspace_bytes() // 8, dtype=torch.float64, **e)
         self.loss_stats = torch.empty(len(LOSS_STATS), dtype=torch.float64, **e)
         # pinned host staging for the two reads of a step
+        self._packed = {k: getattr(self, k) for k in ("kept_rollout", "kept_offset", "tok_slot", "tok_action", "tok_old",
+                                                       "tok_ref", "adv_slot")}   # rebalance() swaps these
+        self._cap0 = cap
         self.pack_host = torch.empty(abi.PACK_RESULT_BYTES, dtype=torch.uint8, pin_memory=True)
         self.stats_host = torch.empty(len(STATS1) + len(LOSS_STATS), dtype=torch.float64, pin_memory=True)
         self.pack_info: PackInfo | None = None
@@ -90,6 +95,9 @@ class LearnerStep:
     def pack(self, *, t_train: int, max_lag: int, rollout_base: int = 0, n_rollouts: int | None = None,
              read_back: bool = True) -> PackInfo | None:
         R = self.R if n_rollouts is None else n_rollouts
+        for k, v in self._packed.items():          # undo a previous step's rebalance()
+            setattr(self, k, v)
+        self.cap = self._cap0
         abi.echo_pack_batch(R, self.G, self.S, self.V, t_train, max_lag, rollout_base, self.version, self.resp_len,
                             self.action, self.old_logp, self.ref_logp, self.cap, self.kept_rollout, self.kept_offset,
                             self.tok_slot, self.tok_action, self.tok_old, self.tok_ref, self.pack_result)
@@ -118,6 +126,50 @@ class LearnerStep:
         self.stats1[8] = float(n_groups - info.n_groups_kept)
         allreduce_sum_(self.stats1, self.group)
         return self.stats1[0:1]
+
+    # ------------------------------------------------------------------ f3
+    def rebalance(self) -> dict:
+        """Token-balanced resharding after the stale filter (call after reduce_counts).
+
+        Every rank's kept rollouts form a contiguous block of the global kept sequence (rank-major = group order);
+        ``parallel.reshard_plan`` splits that sequence into W contiguous ranges of ~N_global / W tokens and the
+        packed per-rollout (global id, advantage, length) and per-token (action, old, ref) arrays move there with
+        one all-to-all each.  The receiver rebuilds kept_offset / tok_slot with echo_csr_from_lengths.  Returns the
+        plan (tokens per rank before and after).  One host sync (the lengths of the kept rollouts)."""
+        import numpy as np
+        import torch.distributed as dist
+        info = self.pack_info
+        n_r, n_t = info.n_rollouts_kept, info.n_tokens
+        if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(self.group) == 1:
+            return {"tokens_before": [n_t], "tokens_after": [n_t]}
+        world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        off = self.kept_offset[: n_r + 1].cpu().numpy()
+        lens = np.diff(off).astype(np.int32)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, lens, group=self.group)
+        counts = [len(x) for x in gathered]
+        plan = reshard_plan(counts, np.concatenate(gathered), world, rank)
+        lens_d = torch.from_numpy(lens).to(self.device)
+        kept_rollout, adv_slot, lens_r = exchange([self.kept_rollout[:n_r], self.adv_slot[:n_r], lens_d],
+                                                  plan["send_rollouts"], plan["recv_rollouts"], self.group)
+        tok = [self.tok_action[:n_t], self.tok_old[:n_t]] + ([self.tok_ref[:n_t]] if self.tok_ref is not None else [])
+        tok = exchange(tok, plan["send_tokens"], plan["recv_tokens"], self.group)
+        new_r, new_t = sum(plan["recv_rollouts"]), sum(plan["recv_tokens"])
+        kept_offset = torch.empty(new_r + 1, dtype=torch.int64, device=self.device)
+        tok_slot = torch.empty(max(new_t, 1), dtype=torch.int32, device=self.device)
+        abi.echo_csr_from_lengths(new_r, lens_r, kept_offset, tok_slot)
+        self.launches += abi.LAUNCHES["echo_csr_from_lengths"]
+        self.kept_rollout, self.adv_slot, self.kept_offset, self.tok_slot = kept_rollout, adv_slot, kept_offset, tok_slot
+        self.tok_action, self.tok_old = tok[0], tok[1]
+        self.tok_ref = tok[2] if self.tok_ref is not None else None
+        if new_t > self.cap:                         # per-token outputs sized for the new share
+            e = dict(device=self.device)
+            self.cap = new_t
+            self.tok_logp = torch.empty(new_t, dtype=torch.float32, **e)
+            self.tok_loss = torch.empty(new_t, dtype=torch.float32, **e)
+            self.tok_flags = torch.empty(new_t, dtype=torch.uint8, **e)
+        self.pack_info = PackInfo(info.status, info.first_bad_rollout, info.n_groups_kept, new_r, new_t)
+        return plan
 
     # ------------------------------------------------------------------ (3)-(5)
     def loss(self, logits: torch.Tensor, row0: int, *, clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0,

@@ -505,7 +505,13 @@ def test_entropy_bonus_v2(name, algo):
     n = min(info.n_tokens, 1024)
     logits = fill(st, cfg, 0, n)
     V = cfg.V
-    logits[:8, V // 3: V // 3 + 257] = float("-inf")         # masked columns (e.g. a vocabulary mask)
+    act8 = st.tok_action[:8].long()
+    za8 = logits[torch.arange(8, device="cuda"), act8].clone()
+    logits[:8, V // 3: V // 3 + 257] = float("-inf")         # masked columns (e.g. a vocabulary mask) ...
+    logits[torch.arange(8, device="cuda"), act8] = za8         # ... never the sampled action
+    masked = torch.zeros(8, V, dtype=torch.bool, device="cuda")
+    masked[:, V // 3: V // 3 + 257] = True
+    masked[torch.arange(8, device="cuda"), act8] = False
     z = as_oracle_rows(logits)
     kl, eta = 0.05, 0.01
     args = (o.pk.tok_action[:n], o.pk.tok_old[:n], o.pk.tok_ref[:n], o.pk.tok_slot[:n], o.adv)
@@ -529,4 +535,20 @@ def test_entropy_bonus_v2(name, algo):
                loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
                dtype=cfg.dtype, old=o.pk.tok_old[:n], eslack=es, loss_atol=1e-6 + eta * hbar)
     # masked columns: exactly zero gradient
-    assert torch.all(logits[:8, V // 3: V // 3 + 257] == 0)
+    assert torch.all(logits[:8, :V][masked] == 0)
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 1023, 1024, 1025, 5000])
+def test_csr_from_lengths_bit_exact(n):
+    """f3: echo_csr_from_lengths against the oracle (bit-exact), including zero / negative lengths and n spanning
+    several scan blocks."""
+    from paper_2508_05387_b200 import abi
+    rng = np.random.default_rng(n)
+    L = rng.integers(-2, 300, n).astype(np.int32)
+    off_ref, slot_ref = oracle.csr_from_lengths(L)
+    off = torch.full((n + 1,), -7, dtype=torch.int64, device="cuda")
+    slot = torch.full((max(len(slot_ref), 1),), -7, dtype=torch.int32, device="cuda")
+    abi.echo_csr_from_lengths(n, torch.from_numpy(L).cuda() if n else None, off, slot)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(off.cpu().numpy(), off_ref)
+    np.testing.assert_array_equal(slot[: len(slot_ref)].cpu().numpy(), slot_ref)

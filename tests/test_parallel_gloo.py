@@ -95,3 +95,119 @@ def test_two_rank_step_equals_single_rank(world):
     # the union of rank outputs is the single-rank output (global ids, W-invariant per-token coefficients)
     np.testing.assert_array_equal(np.concatenate([out[r][2] for r in range(world)]), pk.kept_rollout)
     np.testing.assert_array_equal(np.concatenate([out[r][3] for r in range(world)]), lo.coef)
+
+
+# ------------------------------------------------------------------------------------------------ f3
+from paper_2508_05387_b200.parallel import balanced_bounds, exchange, reshard_plan  # noqa: E402
+
+
+def test_balanced_bounds_nearest_prefix_and_load_bound():
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        n = int(rng.integers(0, 40))
+        L = rng.integers(0, 50, n)
+        W = int(rng.integers(1, 9))
+        b = balanced_bounds(L, W)
+        pre = np.concatenate([[0], np.cumsum(L)])
+        N = pre[-1]
+        assert len(b) == W + 1 and b[0] == 0 and b[-1] == n and all(x <= y for x, y in zip(b, b[1:]))
+        for k in range(1, W):
+            t = k * N / W
+            best = np.min(np.abs(pre - t))
+            # the boundary's prefix is the nearest one to k N / W unless monotonicity pinned it to b_{k-1}
+            assert abs(pre[b[k]] - t) == best or b[k] == b[k - 1]
+        loads = [pre[b[k + 1]] - pre[b[k]] for k in range(W)]
+        if n:
+            assert max(loads) <= N / W + L.max() + 1e-9
+
+
+def test_reshard_plan_is_a_consistent_all_to_all():
+    rng = np.random.default_rng(4)
+    for _ in range(100):
+        W = int(rng.integers(1, 7))
+        counts = rng.integers(0, 9, W)
+        L = rng.integers(1, 30, counts.sum())
+        plans = [reshard_plan(counts, L, W, r) for r in range(W)]
+        for r in range(W):
+            for k in range(W):
+                assert plans[r]["send_rollouts"][k] == plans[k]["recv_rollouts"][r]
+                assert plans[r]["send_tokens"][k] == plans[k]["recv_tokens"][r]
+            assert sum(plans[r]["send_rollouts"]) == counts[r]
+            assert sum(plans[r]["recv_tokens"]) == plans[0]["tokens_after"][r]
+        assert sum(plans[0]["tokens_after"]) == L.sum()
+
+
+def _rebalance_worker(rank, world, port, cfg_name, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.CONFIGS[cfg_name]
+        g0, g1 = shard_groups(cfg.P, world, rank)
+        pk, adv, stats1 = _step_stats(cfg, g0 * cfg.G, g1 * cfg.G)
+        s1 = torch.tensor(stats1, dtype=torch.float64)
+        allreduce_sum_(s1)
+        lens = np.diff(pk.kept_offset[: pk.n_rollouts_kept + 1]).astype(np.int32)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, lens)
+        plan = reshard_plan([len(x) for x in gathered], np.concatenate(gathered), world, rank)
+        ro = [torch.from_numpy(pk.kept_rollout[: pk.n_rollouts_kept].copy()), torch.from_numpy(adv.copy()),
+              torch.from_numpy(lens)]
+        to = [torch.from_numpy(x[: pk.n_tokens].copy()) for x in (pk.tok_action, pk.tok_old, pk.tok_ref)]
+        kr, ad, ln = exchange(ro, plan["send_rollouts"], plan["recv_rollouts"])
+        ta, told, tref = exchange(to, plan["send_tokens"], plan["recv_tokens"])
+        off, slot = oracle.csr_from_lengths(ln.numpy())
+        keys = kr.numpy()[slot].astype(np.int64) * cfg.S + (np.arange(len(slot)) - off[slot])
+        z = synth.logits_rows(keys, ta.numpy(), cfg.V, cfg.seed, "f32")
+        lo = oracle.policy_loss(z, ta.numpy(), told.numpy(), tref.numpy(), slot, ad.numpy(), n_global=float(s1[0]),
+                                kl_coef=cfg.kl_coef, want_dlogits=False)
+        st = torch.tensor(lo.stats, dtype=torch.float64)
+        reduce_loss_stats_(st)
+        out[rank] = (plan, kr.numpy().copy(), keys, lo.coef.copy(), st.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rebalanced_step_equals_single_rank(world):
+    """f3: after the exchange every rank holds a contiguous, token-balanced range of the global kept sequence,
+    and the per-token results and step statistics equal the single-rank step's."""
+    cfg = synth.CONFIGS["tiny"]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_rebalance_worker, args=(world, _free_port(), "tiny", out), nprocs=world, join=True)
+    pk, adv, stats1 = _step_stats(cfg, 0, cfg.R)
+    keys = (pk.kept_rollout[pk.tok_slot].astype(np.int64) * cfg.S
+            + (np.arange(pk.n_tokens, dtype=np.int64) - pk.kept_offset[pk.tok_slot]))
+    z = synth.logits_rows(keys, pk.tok_action, cfg.V, cfg.seed, "f32")
+    lo = oracle.policy_loss(z, pk.tok_action, pk.tok_old, pk.tok_ref, pk.tok_slot, adv, n_global=pk.n_tokens,
+                            kl_coef=cfg.kl_coef, want_dlogits=False)
+    plan = out[0][0]
+    before, after = plan["tokens_before"], plan["tokens_after"]
+    assert max(after) - min(after) <= max(before) - min(before)
+    assert max(after) <= pk.n_tokens / world + cfg.S
+    np.testing.assert_array_equal(np.concatenate([out[r][1] for r in range(world)]), pk.kept_rollout)
+    np.testing.assert_array_equal(np.concatenate([out[r][2] for r in range(world)]), keys)
+    np.testing.assert_array_equal(np.concatenate([out[r][3] for r in range(world)]), lo.coef)
+    st = out[0][4]
+    np.testing.assert_allclose(st[[0, 1, 2, 7, 9]], lo.stats[[0, 1, 2, 7, 9]], rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(st[[3, 4, 8]], lo.stats[[3, 4, 8]])
+
+
+def test_csr_from_lengths_oracle_matches_pack():
+    """The oracle's CSR rebuild reproduces pack's kept_offset / tok_slot from the kept lengths."""
+    cfg = synth.CONFIGS["tiny"]
+    b = synth.make_batch(cfg, lengths="ragged")
+    pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,
+                           vocab=cfg.V, t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
+    off, slot = oracle.csr_from_lengths(np.diff(pk.kept_offset[: pk.n_rollouts_kept + 1]))
+    np.testing.assert_array_equal(off, pk.kept_offset[: pk.n_rollouts_kept + 1])
+    np.testing.assert_array_equal(slot, pk.tok_slot[: pk.n_tokens])
+    # brute force on small inputs
+    rng = np.random.default_rng(9)
+    for _ in range(50):
+        L = rng.integers(-2, 6, int(rng.integers(0, 12))).astype(np.int32)
+        off, slot = oracle.csr_from_lengths(L)
+        exp = np.concatenate([[i] * max(int(x), 0) for i, x in enumerate(L)] + [[]]).astype(np.int32)
+        np.testing.assert_array_equal(slot, exp)
+        assert off[-1] == len(exp) and off[0] == 0
