@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "quad_reg", "quad_reg_exact", "oct_reg"])
     ap.add_argument("--micro-batch", type=int, default=32768)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--balance", action="store_true",
+                    help="f3: token-balanced resharding of the kept rollouts after the stale filter (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-oracle sample duration")
     return ap.parse_args()
@@ -232,6 +234,8 @@ def main_echo(args):
         e.record(stream)
         return e
 
+    plans = []
+
     def one_step(record):
         t0 = ev()
         h2d = st.h2d(host["version"], host["resp_len"], host["reward"], host["action"], host["old_logp"],
@@ -241,9 +245,11 @@ def main_echo(args):
         assert info.status == 0, info
         st.advantage()
         st.reduce_counts()
+        if args.balance:
+            plans.append(st.rebalance())
         t2 = ev()
         gens, kers = [], []
-        N = info.n_tokens
+        N = st.pack_info.n_tokens
         for row0 in range(0, N, M):
             m = min(M, N - row0)
             ga = ev()
@@ -318,6 +324,7 @@ def main_echo(args):
         "config": {"workload": cfg.name, "prompts": cfg.P, "group_size": cfg.G, "seq_len": cfg.S, "vocab": cfg.V,
                    "max_lag": cfg.max_lag, "kl_coef": cfg.kl_coef, "tokens_per_step": int(toks_all / args.steps),
                    "micro_batch_rows": M, "algo": args.algo, "parallelism": f"dp{world}",
+                   "balance": bool(args.balance),
                    "l2": "inputs >> L2 (10 GB micro-batches) + 256 MB L2 flush after each generator launch"},
         "clocks": clk,
         "e2e": {"value": toks_all / (e2e_ms * 1e-3), "unit": "tokens/s",
@@ -349,6 +356,9 @@ def main_echo(args):
     line["f1_token_logp"] = {"ms_per_micro_batch": f1_ms, "tokens_per_s_per_gpu": M / (f1_ms * 1e-3),
                              "achieved_GBps": f1_bpt * M / (f1_ms * 1e-3) / 1e9, "bytes_per_token": f1_bpt,
                              "frac": f1_bpt * M / (f1_ms * 1e-3) / 1e9 / peak}
+    if plans:
+        line["config"]["tokens_per_rank_before"] = plans[-1]["tokens_before"]
+        line["config"]["tokens_per_rank_after"] = plans[-1]["tokens_after"]
     if world == 1 and not args.no_cpu_baseline:
         r = oracle_rate(cfg, b, toks_all / args.steps, args.cpu_seconds)
         line["cpu_baseline"] = {
