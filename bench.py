@@ -236,6 +236,15 @@ def main_echo(args):
 
     plans = []
 
+    def align():
+        """Untimed rank alignment before each collective.  The synthetic logits generator (the LM-head stand-in,
+        excluded from the timed work) runs ~7x longer per micro-batch than the loss kernel, so without this a rank
+        with fewer tokens would wait inside the next collective for the other ranks' generator time.  With it,
+        each rank's timed work is its own path work, and value = max over ranks of that."""
+        if world > 1:
+            torch.cuda.synchronize()
+            dist.barrier()
+
     def one_step(record):
         t0 = ev()
         h2d = st.h2d(host["version"], host["resp_len"], host["reward"], host["action"], host["old_logp"],
@@ -244,6 +253,9 @@ def main_echo(args):
         info = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag, rollout_base=r0)
         assert info.status == 0, info
         st.advantage()
+        ta = ev()
+        align()      # untimed: ranks enter the collectives together (see align)
+        tb = ev()
         st.reduce_counts()
         if args.balance:
             plans.append(st.rebalance())
@@ -263,6 +275,8 @@ def main_echo(args):
             gens.append((ga, gb))
             kers.append((gb, kb))
         t3 = ev()
+        align()
+        t3b = ev()
         st.finish(read_back=False)
         t4 = ev()
         st.stats_host[:9].copy_(st.stats1, non_blocking=True)
@@ -274,7 +288,9 @@ def main_echo(args):
         el = lambda a, b_: a.elapsed_time(b_)
         gen_ms = sum(el(a, b_) for a, b_ in gens)
         ker = [el(a, b_) for a, b_ in kers]
-        return {"e2e_ms": el(t0, t5) - gen_ms, "dev_ms": el(t1, t2) + sum(ker) + el(t3, t4), "kernel_ms": ker,
+        waits = el(ta, tb) + el(t3, t3b)
+        return {"e2e_ms": el(t0, t5) - gen_ms - waits, "dev_ms": el(t1, ta) + el(tb, t2) + sum(ker) + el(t3b, t4),
+                "kernel_ms": ker,
                 "n_tokens": N, "h2d": h2d, "d2h": abi.PACK_RESULT_BYTES + st.stats_host.numel() * 8,
                 "nonfinite": float(st.stats_host[9 + 4]), "loss": float(st.stats_host[9]) / max(N, 1)}
 
