@@ -65,6 +65,8 @@ def lib():
         _lib.echo_ref_scaled_loss.restype = f64
         _lib.echo_ref_csr_from_lengths.argtypes = [i32, P, P, P]
         _lib.echo_ref_csr_from_lengths.restype = ctypes.c_int
+        _lib.echo_ref_lmhead_logp.argtypes = [i64, i32, i32, P, P, P, P, P]
+        _lib.echo_ref_lmhead_logp.restype = ctypes.c_int
     return _lib
 
 
@@ -251,3 +253,18 @@ def csr_from_lengths(lengths):
     if rc != 0:
         raise ValueError("echo_ref_csr_from_lengths: invalid argument")
     return off, slot[:total]
+
+
+def lmhead_logp(hidden_bf16, weight_bf16, tok_action):
+    """f2: (logp, lse) of z = hidden @ weight^T (bf16 bit patterns, uint16) at the actions, fp64."""
+    h = np.ascontiguousarray(hidden_bf16, np.uint16)
+    w = np.ascontiguousarray(weight_bf16, np.uint16)
+    n, d = h.shape
+    V = w.shape[0]
+    assert w.shape[1] == d
+    logp = np.zeros(n, np.float64)
+    lse = np.zeros(n, np.float64)
+    rc = lib().echo_ref_lmhead_logp(n, d, V, _p(h), _p(w), _p(_c(tok_action, np.int32)), _p(logp), _p(lse))
+    if rc != 0:
+        raise ValueError("echo_ref_lmhead_logp: invalid argument")
+    return logp, lse

@@ -42,6 +42,7 @@
 #include <stdint.h>
 #include <stddef.h>
 #include <float.h>
+#include <stdlib.h>
 #include <string.h>
 
 /* ---- status codes (the oracle's own copies; kept independent of include/echo.h) ---- */
@@ -491,6 +492,38 @@ int echo_ref_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* kept_o
     kept_offset[i + 1] = kept_offset[i] + len;
     if (tok_slot)
       for (int64_t t = kept_offset[i]; t < kept_offset[i + 1]; ++t) tok_slot[t] = i;
+  }
+  return REF_OK;
+}
+
+/* ======================================================================================
+ * f2: the LM head fused with the log-softmax-and-gather of (3), forward only.  The logits are
+ * the LM head's output z[t, v] = sum_k h[t, k] W[v, k] (the model's final projection, PAPER.md :254-261
+ * "the learner ... computes gradients"), so the fused form never materialises the [tokens x vocab] matrix:
+ *   z[t, v] = sum_k h[t, k] W[v, k]   (bf16 inputs widened exactly to fp64, fp64 sums in k order)
+ *   lse_t = m + log sum_v exp(z[t, v] - m),  m = max_v z[t, v];   logp_t = z[t, a_t] - lse_t
+ * hidden: bf16 bit patterns [n_rows x d] row-major; weight: bf16 [vocab x d] row-major.
+ * ====================================================================================== */
+int echo_ref_lmhead_logp(int64_t n_rows, int32_t d, int32_t vocab, const uint16_t* hidden, const uint16_t* weight,
+                         const int32_t* tok_action, double* tok_logp, double* tok_lse) {
+  if (n_rows < 0 || d < 1 || vocab < 1) return REF_ERR_INVALID_ARGUMENT;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t t = 0; t < n_rows; ++t) {
+    double* z = (double*)malloc(sizeof(double) * (size_t)vocab);
+    double m = -INFINITY;
+    for (int64_t v = 0; v < vocab; ++v) {
+      double acc = 0.0;
+      for (int64_t k = 0; k < d; ++k)
+        acc = acc + widen_bf16(hidden[t * d + k]) * widen_bf16(weight[v * d + k]);
+      z[v] = acc;
+      if (acc > m) m = acc;
+    }
+    double s = 0.0;
+    for (int64_t v = 0; v < vocab; ++v) s = s + exp(z[v] - m);
+    double lse = m + log(s);
+    tok_logp[t] = z[tok_action[t]] - lse;
+    if (tok_lse) tok_lse[t] = lse;
+    free(z);
   }
   return REF_OK;
 }
