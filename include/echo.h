@@ -263,6 +263,23 @@ ECHO_API echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, co
 ECHO_API echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* kept_offset,
                                            int32_t* tok_slot, void* stream);
 
+/*
+ * f2: the LM head fused with (3), forward only.  The logits are the LM head's output
+ * z[t, v] = sum_k hidden[t, k] weight[v, k] (the model's last projection; PAPER.md :254-261, the learner computes
+ * log pi_theta(a|s) of PAPER.md :170 from them), and
+ *   lse_t = logsumexp_v z[t, v],   logp_t = z[t, a_t] - lse_t      (NaN when a_t is outside [0, vocab))
+ * are computed without materialising z: a tcgen05 tensor-core GEMM (bf16 inputs, fp32 accumulation in TMEM) whose
+ * epilogue reduces each 128 x 256 logits tile to per-row partials, then an ordered merge (deterministic).
+ * hidden: device bf16 [n_rows x d] row-major; weight: device bf16 [vocab x d] row-major; both 16-byte aligned,
+ * d % 8 == 0.  tok_lse nullable.  workspace: device buffer of echo_lmhead_workspace_bytes(n_rows, vocab) bytes
+ * (8 B per row per 256 vocabulary columns + 4 B per row; no initialisation needed).
+ * Launches: 2 kernels (0 when n_rows == 0).  ECHO_ERR_INVALID_ARGUMENT on bad sizes / pointers / alignment.
+ */
+ECHO_API size_t echo_lmhead_workspace_bytes(int64_t n_rows, int32_t vocab);
+ECHO_API echo_status echo_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d,
+                                      int32_t vocab, const int32_t* tok_action, float* tok_logp, float* tok_lse,
+                                      void* workspace, void* stream);
+
 /* Human-readable name of a status code (static storage). */
 ECHO_API const char* echo_status_string(echo_status status);
 

@@ -260,6 +260,28 @@ echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* ke
                                                  static_cast<cudaStream_t>(stream), sms));
 }
 
+size_t echo_lmhead_workspace_bytes(int64_t n_rows, int32_t vocab) {
+  if (n_rows < 0 || vocab < 1) return 0;
+  return echo::lmhead_workspace_bytes(n_rows, vocab);
+}
+
+echo_status echo_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab,
+                             const int32_t* tok_action, float* tok_logp, float* tok_lse, void* workspace,
+                             void* stream) {
+  if (n_rows < 0 || d < 8 || d % 8 != 0 || vocab < 1) return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows > 0 && (!hidden || !weight || !aligned16(hidden) || !aligned16(weight) || !tok_action || !tok_logp ||
+                     !workspace))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  if (n_rows == 0) return ECHO_OK;
+  const cudaError_t e = echo::launch_lmhead_logp(hidden, weight, n_rows, d, vocab, tok_action, tok_logp, tok_lse,
+                                                 workspace, static_cast<cudaStream_t>(stream), sms);
+  if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
+  return from_cuda(e);
+}
+
 size_t echo_loss_stats_workspace_bytes(void) { return echo::loss_stats_workspace_bytes(); }
 
 echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp, const float* tok_old,

@@ -1,0 +1,339 @@
+// lmhead.cu -- f2: the LM head fused with the log-softmax-and-gather of (3), forward only.
+//
+// logp_t = z[t, a_t] - logsumexp_v z[t, v],  z = h W^T  (h: [N x d] bf16 hidden states, W: [V x d] bf16 LM-head
+// weight).  The [N x V] logits are never written to HBM: the GEMM runs on the 5th-generation tensor cores with
+// the accumulator tile in TMEM, and its epilogue reduces every 128 x 256 logits tile to per-row partials
+// (max, sum of exp) and picks out z[t, a_t]; a small finalize kernel merges the partials of a row in vocab-tile
+// order (deterministic).  Traffic per token: 8 B x V/256 of partials instead of 2 x 2V B of logits.
+//
+// lmhead_tile_kernel: persistent, one CTA per SM, 6 warps, warp-specialised:
+//   warp 0 (one lane)  TMA producer: 2-D tensor-map tile loads (SWIZZLE_128B) of A = h[128 rows x 64 k] (16 KB)
+//                      and B = W[256 rows x 64 k] (32 KB) into a 4-stage shared-memory ring (full/empty mbarriers)
+//   warp 1             allocates 512 TMEM columns (two 128 x 256 fp32 accumulators); one lane issues
+//                      tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16, bf16 -> fp32) four per stage and
+//                      tcgen05.commit's the stage back to the producer and the finished accumulator to the epilogue
+//   warps 2-5          epilogue: tcgen05.ld 32 columns at a time (thread = row = TMEM lane), online max / sum of
+//                      exp2 over the tile's valid columns, z[t, a_t] when the action falls in the tile; partials
+//                      to the workspace; the accumulator is released as soon as it has been read, so the MMA of
+//                      the next tile overlaps this epilogue
+// Tiles are rasterised in groups of 16 token tiles x all vocab tiles (column-major inside a group), so the CTAs in
+// flight share a few MB of A and B in L2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "echo_common.cuh"
+#include "echo_internal.h"
+
+namespace echo {
+
+namespace lm {
+constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4, kUmmaK = 16;
+constexpr int kABytes = kBM * kBK * 2, kBBytes = kBN * kBK * 2, kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 192;
+constexpr int kGroupM = 16;  // token tiles per rasterisation group
+constexpr uint32_t kTmemCols = 512;
+
+struct Smem {
+  uint8_t a[kStages][kABytes];
+  uint8_t b[kStages][kBBytes];
+  uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+constexpr size_t kSmemBytes = sizeof(Smem) + 1024;  // + alignment slack (SWIZZLE_128B atoms need 1024-B alignment)
+
+// UMMA shared-memory descriptor of a K-major, SWIZZLE_128B operand tile whose rows are 128 B (64 bf16) apart and
+// whose 8-row swizzle atoms are 1024 B apart: start >> 4 | LBO 1 | SBO 64 (x16 B) | version 1 | layout 2 (SW128).
+ECHO_DEVINL uint64_t sw128_desc(uint32_t smem_addr) {
+  return (uint64_t)((smem_addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+// Instruction descriptor, kind::f16: fp32 accumulate (bits 4-5 = 1), A and B bf16 (bits 7-9, 10-12 = 1), both
+// K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(kBM >> 4) << 24);
+
+ECHO_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t x, int32_t y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+ECHO_DEVINL void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+ECHO_DEVINL void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+ECHO_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+ECHO_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+ECHO_DEVINL void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// tile u -> (token tile, vocab tile): groups of kGroupM token tiles, vocab-major inside a group
+ECHO_DEVINL void tile_coords(int64_t u, int32_t n_tt, int32_t n_vt, int32_t& tt, int32_t& vt) {
+  const int64_t per_group = (int64_t)kGroupM * n_vt;
+  const int32_t g = (int32_t)(u / per_group);
+  const int32_t rows_in_g = min(kGroupM, n_tt - g * kGroupM);
+  const int64_t r = u - (int64_t)g * per_group;
+  vt = (int32_t)(r / rows_in_g);
+  tt = g * kGroupM + (int32_t)(r % rows_in_g);
+}
+}  // namespace lm
+
+struct LmParams {
+  int64_t n_rows;
+  int32_t d, V, n_tt, n_vt, n_kb;
+  const int32_t* __restrict__ tok_action;
+  float* __restrict__ part_m;  // [n_vt][n_rows]
+  float* __restrict__ part_s;  // [n_vt][n_rows]
+  float* __restrict__ za;      // [n_rows]
+};
+
+__global__ void __launch_bounds__(lm::kThreads, 1)
+    lmhead_tile_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w,
+                       const LmParams p) {
+  using namespace lm;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(smem_u32(&sm.full[s]), 1);
+      mbar_init(smem_u32(&sm.empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&sm.tfull[b]), 1);
+      mbar_init(smem_u32(&sm.tempty[b]), 4);  // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_h)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int64_t u = blockIdx.x; u < n_tiles; u += gridDim.x) {
+        int32_t tt, vt;
+        tile_coords(u, p.n_tt, p.n_vt, tt, vt);
+        for (int32_t kb = 0; kb < p.n_kb; ++kb) {
+          mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
+          const uint32_t bar = smem_u32(&sm.full[stage]);
+          mbar_arrive_expect_tx(bar, kStageBytes);
+          tma_load_2d(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * kBM, bar);
+          tma_load_2d(smem_u32(sm.b[stage]), &map_w, kb * kBK, vt * kBN, bar);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, tc = 0;
+      for (int64_t u = blockIdx.x; u < n_tiles; u += gridDim.x, ++tc) {
+        const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
+        mbar_wait(smem_u32(&sm.tempty[buf]), aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + buf * kBN;
+        for (int32_t kb = 0; kb < p.n_kb; ++kb) {
+          mbar_wait(smem_u32(&sm.full[stage]), phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
+#pragma unroll
+          for (int k = 0; k < kBK / kUmmaK; ++k)
+            umma_bf16(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2),
+                      (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit(smem_u32(&sm.empty[stage]));  // the stage's smem is free once these MMAs have read it
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit(smem_u32(&sm.tfull[buf]));  // accumulator complete
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 2..5 = TMEM lane quadrants)
+    const int quad = warp & 3;
+    uint32_t tc = 0;
+    for (int64_t u = blockIdx.x; u < n_tiles; u += gridDim.x, ++tc) {
+      int32_t tt, vt;
+      tile_coords(u, p.n_tt, p.n_vt, tt, vt);
+      const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
+      const int64_t row = (int64_t)tt * kBM + quad * 32 + lane;
+      const bool row_ok = row < p.n_rows;
+      const int32_t a = row_ok ? p.tok_action[row] : -1;
+      const int32_t col0 = vt * kBN;
+      mbar_wait(smem_u32(&sm.tfull[buf]), aph);
+      tc_fence_after();
+      float m = -INFINITY, s = 0.0f, za = 0.0f;
+      bool found = false;
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + c * 32, r);
+        const int32_t cb = col0 + c * 32;
+        float cm = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float x = (cb + i < p.V) ? __uint_as_float(r[i]) : -INFINITY;
+          cm = fmaxf(cm, x);
+          if (cb + i == a) {
+            za = __uint_as_float(r[i]);
+            found = true;
+          }
+        }
+        if (cm > m) {
+          s = (m == -INFINITY) ? 0.0f : s * ex2((m - cm) * kLog2e);
+          m = cm;
+        }
+        if (m != -INFINITY) {
+          const float mb = m * kLog2e;
+          float acc = 0.0f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            acc += (cb + i < p.V) ? ex2(fmaf(__uint_as_float(r[i]), kLog2e, -mb)) : 0.0f;
+          s += acc;
+        }
+      }
+      // accumulator read out: hand it back to the MMA warp before the global writes
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&sm.tempty[buf]));
+      if (row_ok) {
+        p.part_m[(int64_t)vt * p.n_rows + row] = m;
+        p.part_s[(int64_t)vt * p.n_rows + row] = s;
+        if (found) p.za[row] = za;
+      }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+  }
+}
+
+// One thread per row: merge the row's vocab-tile partials in tile order (deterministic), then logp = z_a - lse.
+__global__ void __launch_bounds__(256) lmhead_finalize_kernel(int64_t n_rows, int32_t V, int32_t n_vt,
+                                                              const int32_t* __restrict__ tok_action,
+                                                              const float* __restrict__ part_m,
+                                                              const float* __restrict__ part_s,
+                                                              const float* __restrict__ za, float* __restrict__ tok_logp,
+                                                              float* __restrict__ tok_lse) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= n_rows) return;
+  float m = -INFINITY, s = 0.0f;
+  for (int32_t vt = 0; vt < n_vt; ++vt) {
+    const float mi = part_m[(int64_t)vt * n_rows + row], si = part_s[(int64_t)vt * n_rows + row];
+    const float mm = fmaxf(m, mi);
+    if (mm == -INFINITY) continue;
+    s = (m == -INFINITY ? 0.0f : s * ex2((m - mm) * kLog2e)) + (mi == -INFINITY ? 0.0f : si * ex2((mi - mm) * kLog2e));
+    m = mm;
+  }
+  const float lse = m + logf(s);
+  const int32_t a = tok_action[row];
+  tok_logp[row] = (a >= 0 && a < V) ? za[row] - lse : NAN;
+  if (tok_lse) tok_lse[row] = lse;
+}
+
+// ------------------------------------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+static bool make_map(CUtensorMap* map, const void* base, int64_t rows, int32_t d, uint32_t box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)lm::kBK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t lmhead_workspace_bytes(int64_t n_rows, int32_t V) {
+  const int64_t n_vt = (V + lm::kBN - 1) / lm::kBN;
+  return (size_t)(2 * n_vt + 1) * (size_t)n_rows * sizeof(float);
+}
+
+cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
+                               const int32_t* tok_action, float* tok_logp, float* tok_lse, void* workspace,
+                               cudaStream_t stream, int num_sms) {
+  if (n_rows == 0) return cudaSuccess;
+  CUtensorMap mh, mw;
+  if (!make_map(&mh, hidden, n_rows, d, lm::kBM) || !make_map(&mw, weight, V, d, lm::kBN)) return cudaErrorInvalidValue;
+  LmParams p;
+  p.n_rows = n_rows;
+  p.d = d;
+  p.V = V;
+  p.n_tt = (int32_t)((n_rows + lm::kBM - 1) / lm::kBM);
+  p.n_vt = (V + lm::kBN - 1) / lm::kBN;
+  p.n_kb = (d + lm::kBK - 1) / lm::kBK;
+  p.tok_action = tok_action;
+  float* ws = static_cast<float*>(workspace);
+  p.part_m = ws;
+  p.part_s = ws + (size_t)p.n_vt * n_rows;
+  p.za = ws + (size_t)2 * p.n_vt * n_rows;
+  cudaError_t e = cudaFuncSetAttribute(lmhead_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)lm::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
+  const int grid = (int)(n_tiles < num_sms ? n_tiles : num_sms);
+  lmhead_tile_kernel<<<grid, lm::kThreads, lm::kSmemBytes, stream>>>(mh, mw, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  lmhead_finalize_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, stream>>>(n_rows, V, p.n_vt, tok_action, p.part_m,
+                                                                              p.part_s, p.za, tok_logp, tok_lse);
+  return cudaGetLastError();
+}
+
+}  // namespace echo

@@ -74,6 +74,7 @@ class LearnerStep:
         self._packed = {k: getattr(self, k) for k in ("kept_rollout", "kept_offset", "tok_slot", "tok_action", "tok_old",
                                                        "tok_ref", "adv_slot")}   # rebalance() swaps these
         self._cap0 = cap
+        self._rebalanced = False
         self.pack_host = torch.empty(abi.PACK_RESULT_BYTES, dtype=torch.uint8, pin_memory=True)
         self.stats_host = torch.empty(len(STATS1) + len(LOSS_STATS), dtype=torch.float64, pin_memory=True)
         self.pack_info: PackInfo | None = None
@@ -95,9 +96,11 @@ class LearnerStep:
     def pack(self, *, t_train: int, max_lag: int, rollout_base: int = 0, n_rollouts: int | None = None,
              read_back: bool = True) -> PackInfo | None:
         R = self.R if n_rollouts is None else n_rollouts
-        for k, v in self._packed.items():          # undo a previous step's rebalance()
-            setattr(self, k, v)
-        self.cap = self._cap0
+        if self._rebalanced:                       # undo a previous step's rebalance()
+            for k, v in self._packed.items():
+                setattr(self, k, v)
+            self.cap = self._cap0
+            self._rebalanced = False
         abi.echo_pack_batch(R, self.G, self.S, self.V, t_train, max_lag, rollout_base, self.version, self.resp_len,
                             self.action, self.old_logp, self.ref_logp, self.cap, self.kept_rollout, self.kept_offset,
                             self.tok_slot, self.tok_action, self.tok_old, self.tok_ref, self.pack_result)
@@ -159,12 +162,12 @@ class LearnerStep:
         tok_slot = torch.empty(max(new_t, 1), dtype=torch.int32, device=self.device)
         abi.echo_csr_from_lengths(new_r, lens_r, kept_offset, tok_slot)
         self.launches += abi.LAUNCHES["echo_csr_from_lengths"]
+        self._rebalanced = True
         self.kept_rollout, self.adv_slot, self.kept_offset, self.tok_slot = kept_rollout, adv_slot, kept_offset, tok_slot
         self.tok_action, self.tok_old = tok[0], tok[1]
         self.tok_ref = tok[2] if self.tok_ref is not None else None
-        if new_t > self.cap:                         # per-token outputs sized for the new share
+        if new_t > self.tok_logp.numel():            # per-token outputs sized for the new share
             e = dict(device=self.device)
-            self.cap = new_t
             self.tok_logp = torch.empty(new_t, dtype=torch.float32, **e)
             self.tok_loss = torch.empty(new_t, dtype=torch.float32, **e)
             self.tok_flags = torch.empty(new_t, dtype=torch.uint8, **e)

@@ -552,3 +552,65 @@ def test_csr_from_lengths_bit_exact(n):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(off.cpu().numpy(), off_ref)
     np.testing.assert_array_equal(slot[: len(slot_ref)].cpu().numpy(), slot_ref)
+
+
+def _lmhead_case(n, d, V, seed, device="cuda"):
+    g = torch.Generator(device=device).manual_seed(seed)
+    h = torch.randn(n, d, generator=g, device=device).to(torch.bfloat16)
+    w = (torch.randn(V, d, generator=g, device=device) * (2.0 / math.sqrt(d))).to(torch.bfloat16)
+    act = torch.randint(0, V, (n,), generator=g, device=device, dtype=torch.int32)
+    return h, w, act
+
+
+def _lmhead_run(h, w, act):
+    from paper_2508_05387_b200 import abi
+    n, d = h.shape
+    V = w.shape[0]
+    ws = torch.empty(abi.echo_lmhead_workspace_bytes(n, V) // 4 + 1, dtype=torch.float32, device="cuda")
+    lp = torch.full((n,), float("nan"), device="cuda")
+    lse = torch.full((n,), float("nan"), device="cuda")
+    abi.echo_lmhead_logp(h, w, n, d, V, act, lp, lse, ws)
+    torch.cuda.synchronize()
+    return lp.cpu().numpy().astype(np.float64), lse.cpu().numpy().astype(np.float64)
+
+
+def _lmhead_tol(hb, wb, rows):
+    """Bound on the fp32-accumulated logit error: blocked summation (K/16 tensor-core steps of 16 products),
+    4 (K/16 + 16) 2^-24 max_v sum_k |h_k W_vk|, doubled for logp = z_a - lse."""
+    hf = (hb[rows].astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    wf = (wb.astype(np.uint32) << 16).view(np.float32)
+    B = (np.abs(hf).astype(np.float32) @ np.abs(wf).T).max(axis=1).astype(np.float64)
+    K = hb.shape[1]
+    return 2 * 4 * (K / 16 + 16) * 2.0 ** -24 * B
+
+
+@pytest.mark.parametrize("n,d,V", [(128, 64, 256), (300, 512, 1000), (129, 72, 257), (1, 2560, 4096),
+                                   (700, 256, 5000)])
+def test_lmhead_logp_small(n, d, V):
+    """f2: the fused LM-head log-prob against the fp64 oracle (every row), ragged token / vocab / K tiles."""
+    h, w, act = _lmhead_case(n, d, V, seed=n + d + V)
+    lp, lse = _lmhead_run(h, w, act)
+    hb = h.cpu().view(torch.int16).numpy().view(np.uint16)
+    wb = w.cpu().view(torch.int16).numpy().view(np.uint16)
+    lp_ref, lse_ref = oracle.lmhead_logp(hb, wb, act.cpu().numpy())
+    tol = _lmhead_tol(hb, wb, np.arange(n))
+    assert np.all(np.abs(lse - lse_ref) <= tol), np.max(np.abs(lse - lse_ref) / tol)
+    assert np.all(np.abs(lp - lp_ref) <= tol), np.max(np.abs(lp - lp_ref) / tol)
+
+
+def test_lmhead_logp_qwen_size_sampled_rows():
+    """f2 at the Qwen3-4B LM-head shape (d = 2560, V = 151936) over 4096 tokens; sampled rows against the oracle,
+    all rows finite and deterministic across two calls."""
+    n, d, V = 4096, 2560, 151936
+    h, w, act = _lmhead_case(n, d, V, seed=7)
+    lp, lse = _lmhead_run(h, w, act)
+    lp2, _ = _lmhead_run(h, w, act)
+    assert np.array_equal(lp.view(np.uint64), lp2.view(np.uint64))
+    assert np.all(np.isfinite(lp)) and np.all(lp <= 0)
+    rows = np.array([0, 1, 127, 128, 1000, 2047, 4095])
+    hb = h[rows].cpu().view(torch.int16).numpy().view(np.uint16)
+    wb = w.cpu().view(torch.int16).numpy().view(np.uint16)
+    lp_ref, lse_ref = oracle.lmhead_logp(hb, wb, act.cpu().numpy()[rows])
+    tol = _lmhead_tol(hb, wb, np.arange(len(rows)))
+    assert np.all(np.abs(lse[rows] - lse_ref) <= tol), np.max(np.abs(lse[rows] - lse_ref) / tol)
+    assert np.all(np.abs(lp[rows] - lp_ref) <= tol), np.max(np.abs(lp[rows] - lp_ref) / tol)
