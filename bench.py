@@ -34,6 +34,8 @@ import numpy as np  # noqa: E402
 METRIC = "policy-loss fwd+bwd tokens/sec and % HBM roofline at 1/2/4/8 B200"
 DEFAULT_CONFIG = "qwen3-4b"      # BASELINE.json configs[1]: the single-GPU configuration the metric is quoted on
 L2_FLUSH_BYTES = 256 << 20
+# LM-head hidden sizes of the BASELINE.json models (f2: the fused LM-head log-prob is measured at this shape)
+HIDDEN = {"tiny": 64, "qwen3-4b": 2560, "qwen2.5-7b": 3584, "qwen3-30b-a3b": 2048, "qwen3-32b": 5120}
 
 
 def parse():
@@ -49,6 +51,7 @@ def parse():
     ap.add_argument("--balance", action="store_true",
                     help="f3: token-balanced resharding of the kept rollouts after the stale filter (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-f2", action="store_true", help="skip the f2 fused LM-head measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-oracle sample duration")
     return ap.parse_args()
 
@@ -59,6 +62,15 @@ def measured_peak():
         with open(p) as f:
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, D2D copy)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def measured_bf16_peak():
+    """Dense bf16 tensor peak for a kernel timed alone: MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3, burst)."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, cuBLAS burst)"
+    return 2250.0, "fallback (nominal dense bf16)"
 
 
 def bytes_per_token(V, esize, kl):
@@ -372,6 +384,41 @@ def main_echo(args):
     line["f1_token_logp"] = {"ms_per_micro_batch": f1_ms, "tokens_per_s_per_gpu": M / (f1_ms * 1e-3),
                              "achieved_GBps": f1_bpt * M / (f1_ms * 1e-3) / 1e9, "bytes_per_token": f1_bpt,
                              "frac": f1_bpt * M / (f1_ms * 1e-3) / 1e9 / peak}
+    # the LM head fused with the log-prob (tensor-core bound), same micro-batch of tokens, against
+    # the unfused path (cuBLAS GEMM into the logits buffer, then echo_token_logp)
+    if cfg.dtype == "bf16" and not args.no_f2:
+        hd = HIDDEN.get(base.name, 2560)
+        gen = torch.Generator(device=dev).manual_seed(cfg.seed)
+        hid = torch.randn(M, hd, generator=gen, device=dev).to(torch.bfloat16)
+        wgt = (torch.randn(cfg.V, hd, generator=gen, device=dev) * (2.0 / hd ** 0.5)).to(torch.bfloat16)
+        ws2 = torch.empty(abi.echo_lmhead_workspace_bytes(M, cfg.V) // 4 + 1, dtype=torch.float32, device=dev)
+        lp2 = torch.empty(M, dtype=torch.float32, device=dev)
+        f2, f2u = [], []
+        for r in range(5):
+            flush.fill_(float(r))
+            a0 = ev()
+            abi.echo_lmhead_logp(hid, wgt, M, hd, cfg.V, st.tok_action, lp2, None, ws2)
+            a1 = ev()
+            flush.fill_(float(r))
+            b0 = ev()
+            torch.matmul(hid, wgt.t(), out=logits[:, :cfg.V])
+            abi.echo_token_logp(logits, st.edtype, M, cfg.V, ld, st.tok_action, f1_lp)
+            b1 = ev()
+            torch.cuda.synchronize()
+            if r >= 2:
+                f2.append(a0.elapsed_time(a1))
+                f2u.append(b0.elapsed_time(b1))
+        f2_ms, f2u_ms = statistics.median(f2), statistics.median(f2u)
+        fl = 2.0 * M * hd * cfg.V
+        pk = measured_bf16_peak()
+        line["f2_lmhead_logp"] = {
+            "ms_per_micro_batch": f2_ms, "tokens_per_s_per_gpu": M / (f2_ms * 1e-3), "hidden": hd,
+            "roofline": {"bound": "tensor", "achieved": fl / (f2_ms * 1e-3) / 1e12, "peak": pk[0], "unit": "TFLOP/s",
+                         "frac": fl / (f2_ms * 1e-3) / 1e12 / pk[0], "peak_source": pk[1],
+                         "flops_per_token": 2.0 * hd * cfg.V},
+            "unfused_ms": f2u_ms, "unfused": "torch.matmul (cuBLAS bf16) into the logits buffer + echo_token_logp",
+            "speedup_vs_unfused": f2u_ms / f2_ms}
+        del hid, wgt, ws2
     if plans:
         line["config"]["tokens_per_rank_before"] = plans[-1]["tokens_before"]
         line["config"]["tokens_per_rank_after"] = plans[-1]["tokens_after"]
