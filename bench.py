@@ -64,12 +64,14 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def measured_bf16_peak():
-    """Dense bf16 tensor peak for a kernel timed alone: MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3, burst)."""
+def measured_bf16_peak(sustained=False):
+    """Dense bf16 tensor peak: MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3, burst: a kernel timed alone) or
+    bf16_tflops_sustained (back to back for 4 s, power-capped clocks)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    key = "bf16_tflops_sustained" if sustained else "bf16_tflops"
     if os.path.exists(p):
         with open(p) as f:
-            return float(json.load(f)["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, cuBLAS burst)"
+            return float(json.load(f)[key]), f"measured (MEASURED_PEAKS.json {key}, cuBLAS)"
     return 2250.0, "fallback (nominal dense bf16)"
 
 
@@ -415,6 +417,7 @@ def main_echo(args):
             "ms_per_micro_batch": f2_ms, "tokens_per_s_per_gpu": M / (f2_ms * 1e-3), "hidden": hd,
             "roofline": {"bound": "tensor", "achieved": fl / (f2_ms * 1e-3) / 1e12, "peak": pk[0], "unit": "TFLOP/s",
                          "frac": fl / (f2_ms * 1e-3) / 1e12 / pk[0], "peak_source": pk[1],
+                         "frac_of_sustained": fl / (f2_ms * 1e-3) / 1e12 / measured_bf16_peak(sustained=True)[0],
                          "flops_per_token": 2.0 * hd * cfg.V},
             "unfused_ms": f2u_ms, "unfused": "torch.matmul (cuBLAS bf16) into the logits buffer + echo_token_logp",
             "speedup_vs_unfused": f2u_ms / f2_ms}

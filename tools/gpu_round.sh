@@ -18,3 +18,9 @@ if [ "${NCU:-1}" = "1" ]; then
       python tools/prof_kernel.py --algos ${ALGO:-oct_reg} --reps 1 --warmup 1 > $out/${tag}_ncu_full.log 2>&1; echo "ncu_full=$?" >> $out/${tag}_status.txt
 fi
 cat $out/${tag}_status.txt
+if [ "${NCU_F2:-1}" = "1" ]; then
+  timeout 300 python tools/prof_lmhead.py --reps 1 --no-unfused > $out/${tag}_f2_plain.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lmhead_tile -s 1 -c 1 -o $out/${tag}_f2 \
+      python tools/prof_lmhead.py --reps 1 --no-unfused > $out/${tag}_ncu_f2.log 2>&1; echo "ncu_f2=$?" >> $out/${tag}_status.txt
+fi
+cat $out/${tag}_status.txt
