@@ -64,9 +64,9 @@ struct __align__(128) QuadSmem {
 
   uint64_t xbar[2];
   uint4 xbuf[2][C::kCtas];  // cluster partials {m, s, z_a, -} per row parity and source rank
-  float red_m[C::kWarps];
-  float red_s[C::kWarps];
-  float red_t[C::kWarps];  // kModeEntropy: sum z e^{z - m} per warp
+  float red_m[2][C::kWarps];  // per row parity: in logp mode the next row's warps run ahead of warp 0's merge
+  float red_s[2][C::kWarps];
+  float red_t[2][C::kWarps];  // kModeEntropy: sum z e^{z - m} per warp
   float za;
   MetaSm meta[2];        // rows of iterations it (it & 1) and it+1
   float coef;
@@ -237,6 +237,53 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     cp_async_wait<0>();
   }
   named_bar_sync(kQBar, C::kThreads);
+  // Cluster merge of row k (lane 0 of warp 0): wait for the kCtas partials, merge them in rank order -- max first,
+  // then the rescaled sums (the exps are independent) -- and run the row's epilogue.  The partials are re-read from
+  // shared memory rather than held (4 words per rank would cost registers).
+  auto finish = [&](uint32_t k, int64_t row_k, int32_t a_k) {
+    const uint32_t par = k & 1u;
+    mbar_wait_cluster(smem_u32(&sm.xbar[par]), (k >> 1) & 1u);
+    ECHO_TRACE_MARK(p, k, 7);
+    float mm = -INFINITY;
+#pragma unroll
+    for (int r = 0; r < C::kCtas; ++r) mm = fmaxf(mm, __uint_as_float(sm.xbuf[par][r].x));
+    float ss = 0.0f, tt = 0.0f;
+#pragma unroll
+    for (int r = 0; r < C::kCtas; ++r) {
+      const float mr = __uint_as_float(sm.xbuf[par][r].x), sr = __uint_as_float(sm.xbuf[par][r].y);
+      const float f = (mr == -INFINITY) ? 0.0f : ex2((mr - mm) * kLog2e);
+      ss += sr * f;
+      if (kEnt) tt += __uint_as_float(sm.xbuf[par][r].z) * f;
+    }
+    const float lse = mm + logf(ss);
+    const float za = (a_k < 0 || a_k >= V) ? NAN : __uint_as_float(sm.xbuf[par][a_k / g.q].w);
+    if constexpr (kGrad) {
+      cp_async_wait<1>();  // C(k) landed
+      const MetaSm& m = sm.meta[k & 1u];
+      const float H = kEnt ? lse - tt / ss : 0.0f;  // -sum p log p = lse - sum p z
+      const RowScalars r = row_epilogue(lse, za, m.old, m.ref, m.adv, loss_opts(p), gscale * m.w, H);
+      if (rank == 0) {
+        p.tok_logp[row_k] = r.logp;
+        p.tok_loss[row_k] = r.loss;
+        p.tok_flags[row_k] = r.flags;
+        if (kEnt && p.tok_entropy) p.tok_entropy[row_k] = H;
+      }
+      const float pa = ex2(fmaf(za, kLog2e, -lse * kLog2e));
+      sm.coef = r.coef;
+      sm.lse = lse;
+      sm.da = fmaf(-r.coef, pa, r.coef);
+      if (kEnt) {
+        sm.ent_e = r.ecoef;
+        sm.ent_k = fmaf(r.ecoef, H - lse, -r.coef);
+        sm.da = fmaf(r.ecoef * pa, za - lse + H, sm.da);  // c (1 - p_a) + e p_a (log p_a + H)
+      }
+    } else if (rank == 0) {
+      const float logp = za - lse;
+      p.tok_logp[row_k] = logp;
+      if (p.tok_lse) p.tok_lse[row_k] = lse;
+      if (p.tok_flags) p.tok_flags[row_k] = (isfinite(lse) && isfinite(logp)) ? 0 : ECHO_FLAG_NONFINITE;
+    }
+  };
   for (uint32_t it = 0;; ++it) {
     const int64_t row = row_next;
     if (row >= n_rows) break;
@@ -325,9 +372,9 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     }
     const MaxSum3 acc = kEnt ? warp_maxsum3(mx, slo + shi, tsum) : MaxSum3{warp_maxsum(MaxSum{mx, slo + shi}), 0.0f};
     if (lane == 0) {
-      sm.red_m[warp] = acc.ms.m;
-      sm.red_s[warp] = acc.ms.s;
-      if (kEnt) sm.red_t[warp] = acc.t;
+      sm.red_m[it & 1u][warp] = acc.ms.m;
+      sm.red_s[it & 1u][warp] = acc.ms.s;
+      if (kEnt) sm.red_t[it & 1u][warp] = acc.t;
     }
     ECHO_TRACE_MARK(p, it, 2);
     named_bar_sync(kQBar, C::kThreads);
@@ -360,12 +407,14 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
 
     // ---- CTA merge (warp 0), cluster merge (st.async to every peer), epilogue (lane 0)
     if (warp == 0) {
+      const uint32_t rp = it & 1u;
       MaxSum3 mine;
       if (kEnt) {
-        mine = warp_maxsum3(lane < C::kWarps ? sm.red_m[lane] : -INFINITY, lane < C::kWarps ? sm.red_s[lane] : 0.0f,
-                            lane < C::kWarps ? sm.red_t[lane] : 0.0f);
+        mine = warp_maxsum3(lane < C::kWarps ? sm.red_m[rp][lane] : -INFINITY,
+                            lane < C::kWarps ? sm.red_s[rp][lane] : 0.0f, lane < C::kWarps ? sm.red_t[rp][lane] : 0.0f);
       } else {
-        mine.ms = warp_maxsum(lane < C::kWarps ? MaxSum{sm.red_m[lane], sm.red_s[lane]} : MaxSum{-INFINITY, 0.0f});
+        mine.ms = warp_maxsum(lane < C::kWarps ? MaxSum{sm.red_m[rp][lane], sm.red_s[rp][lane]}
+                                               : MaxSum{-INFINITY, 0.0f});
         mine.t = 0.0f;
       }
       ECHO_TRACE_MARK(p, it, 12);
@@ -381,49 +430,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         for (int r = 0; r < C::kCtas; ++r)
           st_async_v4(mapa(smem_u32(&sm.xbuf[par][rank]), r), msg, mapa(xbar_local, r));
         ECHO_TRACE_MARK(p, it, 6);
-        mbar_wait_cluster(xbar_local, (it >> 1) & 1u);
-        ECHO_TRACE_MARK(p, it, 7);
-        // cluster merge in rank order: max first, then the rescaled sum (the exps are independent)
-        // (the partials are re-read from shared memory rather than held: 4 words per rank would cost registers)
-        float mm = -INFINITY;
-#pragma unroll
-        for (int r = 0; r < C::kCtas; ++r) mm = fmaxf(mm, __uint_as_float(sm.xbuf[par][r].x));
-        float ss = 0.0f, tt = 0.0f;
-#pragma unroll
-        for (int r = 0; r < C::kCtas; ++r) {
-          const float mr = __uint_as_float(sm.xbuf[par][r].x), sr = __uint_as_float(sm.xbuf[par][r].y);
-          const float f = (mr == -INFINITY) ? 0.0f : ex2((mr - mm) * kLog2e);
-          ss += sr * f;
-          if (kEnt) tt += __uint_as_float(sm.xbuf[par][r].z) * f;
-        }
-        const float lse = mm + logf(ss);
-        const float za = (a < 0 || a >= V) ? NAN : __uint_as_float(sm.xbuf[par][a / g.q].w);
-        if constexpr (kGrad) {
-          cp_async_wait<1>();  // C(it) landed
-          const MetaSm& m = sm.meta[it & 1u];
-          const float H = kEnt ? lse - tt / ss : 0.0f;  // -sum p log p = lse - sum p z
-          const RowScalars r = row_epilogue(lse, za, m.old, m.ref, m.adv, loss_opts(p), gscale * m.w, H);
-          if (rank == 0) {
-            p.tok_logp[row] = r.logp;
-            p.tok_loss[row] = r.loss;
-            p.tok_flags[row] = r.flags;
-            if (kEnt && p.tok_entropy) p.tok_entropy[row] = H;
-          }
-          const float pa = ex2(fmaf(za, kLog2e, -lse * kLog2e));
-          sm.coef = r.coef;
-          sm.lse = lse;
-          sm.da = fmaf(-r.coef, pa, r.coef);
-          if (kEnt) {
-            sm.ent_e = r.ecoef;
-            sm.ent_k = fmaf(r.ecoef, H - lse, -r.coef);
-            sm.da = fmaf(r.ecoef * pa, za - lse + H, sm.da);  // c (1 - p_a) + e p_a (log p_a + H)
-          }
-        } else if (rank == 0) {
-          const float logp = za - lse;
-          p.tok_logp[row] = logp;
-          if (p.tok_lse) p.tok_lse[row] = lse;
-          if (p.tok_flags) p.tok_flags[row] = (isfinite(lse) && isfinite(logp)) ? 0 : ECHO_FLAG_NONFINITE;
-        }
+        finish(it, row, a);
       }
     }
     if (tid == 0) cp_async_wait<0>();  // A(it+1) landed: barrier 2 publishes row it+1's action

@@ -619,3 +619,29 @@ def test_lmhead_logp_qwen_size_sampled_rows():
     assert np.all(np.abs(lse[rows] - lse_ref) <= tol), np.max(np.abs(lse[rows] - lse_ref) / tol)
     assert np.all(np.abs(lp[rows] - lp_ref) <= tol), np.max(np.abs(lp[rows] - lp_ref) / tol)
     assert np.max(np.abs(lp[rows] - lp_ref)) <= 2e-4
+
+
+def test_lmhead_logp_edge_cases_and_errors():
+    """f2: out-of-range actions give NaN log-probs (finite lse); n_rows = 0 is a no-op; bad arguments are
+    reported, not launched."""
+    from paper_2508_05387_b200 import abi
+    n, d, V = 130, 128, 600
+    h, w, act = _lmhead_case(n, d, V, seed=5)
+    act[3] = -1
+    act[77] = V
+    lp, lse = _lmhead_run(h, w, act)
+    assert np.isnan(lp[3]) and np.isnan(lp[77]) and np.all(np.isfinite(lse))
+    ok = np.ones(n, bool)
+    ok[[3, 77]] = False
+    assert np.all(np.isfinite(lp[ok]))
+    ws = torch.empty(abi.echo_lmhead_workspace_bytes(n, V) // 4 + 1, dtype=torch.float32, device="cuda")
+    out = torch.empty(n, device="cuda")
+    abi.echo_lmhead_logp(h, w, 0, d, V, act, out, None, ws)                 # n_rows = 0: nothing to do
+    for bad in (dict(d=100), dict(d=0), dict(vocab=0)):
+        kw = dict(d=d, vocab=V)
+        kw.update(bad)
+        with pytest.raises(abi.EchoError):
+            abi.echo_lmhead_logp(h, w, n, kw["d"], kw["vocab"], act, out, None, ws)
+    with pytest.raises(abi.EchoError):                                      # misaligned hidden pointer
+        abi.echo_lmhead_logp(h.view(-1)[1:].data_ptr(), w, n - 1, d, V, act, out, None, ws)
+    assert abi.echo_lmhead_workspace_bytes(n, V) == (2 * 3 + 1) * n * 4
