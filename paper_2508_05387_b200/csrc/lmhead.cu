@@ -18,6 +18,13 @@
 //                      the next tile overlaps this epilogue
 // Tiles are rasterised in groups of 16 token tiles x all vocab tiles (column-major inside a group), so the CTAs in
 // flight share a few MB of A and B in L2.
+//
+// kPair (ECHO_LMHEAD_PAIR, the default): a 2-CTA cluster shares one 256 x 256 tile with tcgen05.mma.cta_group::2
+// (M = 256): each CTA stages its own 128 token rows of A and HALF of the 256 vocab rows of B, the leader CTA's one
+// thread issues the MMA over both CTAs' shared memory, and each CTA's TMEM receives its 128 rows.  B traffic from
+// L2 per token halves.  The TMA loads of both CTAs complete on the leader's full barrier (.cta_group::2), the
+// commits multicast to both CTAs' empty / accumulator-full barriers, and both epilogues release the accumulator
+// on the leader's barrier.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -30,19 +37,29 @@
 namespace echo {
 
 namespace lm {
-constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4, kUmmaK = 16;
-constexpr int kABytes = kBM * kBK * 2, kBBytes = kBN * kBK * 2, kStageBytes = kABytes + kBBytes;
+constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16;  // per-CTA token rows, tile vocab columns, K step
 constexpr int kThreads = 192;
 constexpr int kGroupM = 16;  // token tiles per rasterisation group
 constexpr uint32_t kTmemCols = 512;
 
+template <bool kPair>
+struct Cfg {
+  static constexpr int kCtas = kPair ? 2 : 1;
+  static constexpr int kBRows = kBN / kCtas;             // vocab rows of B staged by each CTA
+  static constexpr int kABytes = kBM * kBK * 2, kBBytes = kBRows * kBK * 2, kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = kPair ? 6 : 4;
+  static constexpr int kTileRows = kBM * kCtas;          // token rows of a (pair) tile
+};
+template <bool kPair>
 struct Smem {
-  uint8_t a[kStages][kABytes];
-  uint8_t b[kStages][kBBytes];
-  uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  using C = Cfg<kPair>;
+  uint8_t a[C::kStages][C::kABytes];
+  uint8_t b[C::kStages][C::kBBytes];
+  uint64_t full[C::kStages], empty[C::kStages], tfull[2], tempty[2];
   uint32_t tmem_base;
 };
-constexpr size_t kSmemBytes = sizeof(Smem) + 1024;  // + alignment slack (SWIZZLE_128B atoms need 1024-B alignment)
+template <bool kPair>
+constexpr size_t smem_bytes() { return sizeof(Smem<kPair>) + 1024; }  // + SWIZZLE_128B 1024-B alignment slack
 
 // UMMA shared-memory descriptor of a K-major, SWIZZLE_128B operand tile whose rows are 128 B (64 bf16) apart and
 // whose 8-row swizzle atoms are 1024 B apart: start >> 4 | LBO 1 | SBO 64 (x16 B) | version 1 | layout 2 (SW128).
@@ -51,26 +68,57 @@ ECHO_DEVINL uint64_t sw128_desc(uint32_t smem_addr) {
          ((uint64_t)2 << 61);
 }
 // Instruction descriptor, kind::f16: fp32 accumulate (bits 4-5 = 1), A and B bf16 (bits 7-9, 10-12 = 1), both
-// K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
-                            ((uint32_t)(kBM >> 4) << 24);
+// K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28 (M = 128 per CTA, 256 for the pair).
+template <bool kPair>
+constexpr uint32_t idesc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)((kBM * (kPair ? 2 : 1)) >> 4) << 24);
+}
 
+template <bool kPair>
 ECHO_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t x, int32_t y, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
-      : "memory");
+  if constexpr (kPair)  // completes on the leader CTA's barrier (bar is a shared::cluster address)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
 }
+template <bool kPair>
 ECHO_DEVINL void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
-      : "memory");
+  if constexpr (kPair)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc<true>()), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc<false>()), "r"(accumulate)
+        : "memory");
 }
+// Arrive on `bar` when the MMAs issued so far have completed: this CTA's barrier, or (pair) the barrier at the
+// same offset in both CTAs of the pair.
+template <bool kPair>
 ECHO_DEVINL void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+  if constexpr (kPair)
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            bar)
+        : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+ECHO_DEVINL void mbar_arrive_cluster(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 ECHO_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 ECHO_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -106,37 +154,51 @@ struct LmParams {
   float* __restrict__ za;      // [n_rows]
 };
 
+template <bool kPair>
 __global__ void __launch_bounds__(lm::kThreads, 1)
     lmhead_tile_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w,
                        const LmParams p) {
   using namespace lm;
+  using C = Cfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
+  Smem<kPair>& sm = *reinterpret_cast<Smem<kPair>*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const int64_t unit0 = kPair ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
+  const int64_t n_units = kPair ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
+  const bool leader = rank == 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < C::kStages; ++s) {
       mbar_init(smem_u32(&sm.full[s]), 1);
       mbar_init(smem_u32(&sm.empty[s]), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.tfull[b]), 1);
-      mbar_init(smem_u32(&sm.tempty[b]), 4);  // one arrival per epilogue warp
+      mbar_init(smem_u32(&sm.tempty[b]), 4 * C::kCtas);  // one arrival per epilogue warp (of both CTAs)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_h)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
-                 "n"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                   "n"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                   "n"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
@@ -144,16 +206,17 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (int64_t u = blockIdx.x; u < n_tiles; u += gridDim.x) {
+      for (int64_t u = unit0; u < n_tiles; u += n_units) {
         int32_t tt, vt;
         tile_coords(u, p.n_tt, p.n_vt, tt, vt);
         for (int32_t kb = 0; kb < p.n_kb; ++kb) {
           mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
-          const uint32_t bar = smem_u32(&sm.full[stage]);
-          mbar_arrive_expect_tx(bar, kStageBytes);
-          tma_load_2d(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * kBM, bar);
-          tma_load_2d(smem_u32(sm.b[stage]), &map_w, kb * kBK, vt * kBN, bar);
-          if (++stage == kStages) {
+          // both CTAs' bytes complete on the leader's full barrier; only the leader arms it (with both halves)
+          const uint32_t bar = kPair ? mapa(smem_u32(&sm.full[stage]), 0) : smem_u32(&sm.full[stage]);
+          if (leader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), C::kStageBytes * C::kCtas);
+          tma_load_2d<kPair>(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * C::kTileRows + (int32_t)rank * kBM, bar);
+          tma_load_2d<kPair>(smem_u32(sm.b[stage]), &map_w, kb * kBK, vt * kBN + (int32_t)rank * C::kBRows, bar);
+          if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1u;
           }
@@ -162,43 +225,44 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && leader) {  // pair: the leader's thread issues for both CTAs
       uint32_t stage = 0, phase = 0, tc = 0;
-      for (int64_t u = blockIdx.x; u < n_tiles; u += gridDim.x, ++tc) {
+      for (int64_t u = unit0; u < n_tiles; u += n_units, ++tc) {
         const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
-        mbar_wait(smem_u32(&sm.tempty[buf]), aph ^ 1u);
+        mbar_wait_cluster(smem_u32(&sm.tempty[buf]), aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem + buf * kBN;
         for (int32_t kb = 0; kb < p.n_kb; ++kb) {
-          mbar_wait(smem_u32(&sm.full[stage]), phase);
+          mbar_wait_cluster(smem_u32(&sm.full[stage]), phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
 #pragma unroll
           for (int k = 0; k < kBK / kUmmaK; ++k)
-            umma_bf16(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2),
-                      (kb > 0 || k > 0) ? 1u : 0u);
-          umma_commit(smem_u32(&sm.empty[stage]));  // the stage's smem is free once these MMAs have read it
-          if (++stage == kStages) {
+            umma_bf16<kPair>(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2),
+                             (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit<kPair>(smem_u32(&sm.empty[stage]));  // the stage's smem is free once these MMAs have read it
+          if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit(smem_u32(&sm.tfull[buf]));  // accumulator complete
+        umma_commit<kPair>(smem_u32(&sm.tfull[buf]));  // accumulator complete
       }
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5 = TMEM lane quadrants)
     const int quad = warp & 3;
     uint32_t tc = 0;
-    for (int64_t u = blockIdx.x; u < n_tiles; u += gridDim.x, ++tc) {
+    const uint32_t tempty_leader = kPair ? mapa(smem_u32(&sm.tempty[0]), 0) : smem_u32(&sm.tempty[0]);
+    for (int64_t u = unit0; u < n_tiles; u += n_units, ++tc) {
       int32_t tt, vt;
       tile_coords(u, p.n_tt, p.n_vt, tt, vt);
       const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
-      const int64_t row = (int64_t)tt * kBM + quad * 32 + lane;
+      const int64_t row = (int64_t)tt * C::kTileRows + (int64_t)rank * kBM + quad * 32 + lane;
       const bool row_ok = row < p.n_rows;
       const int32_t a = row_ok ? p.tok_action[row] : -1;
       const int32_t col0 = vt * kBN;
-      mbar_wait(smem_u32(&sm.tfull[buf]), aph);
+      mbar_wait_cluster(smem_u32(&sm.tfull[buf]), aph);
       tc_fence_after();
       float m = -INFINITY, s = 0.0f, za = 0.0f;
       bool found = false;
@@ -233,7 +297,10 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
       // accumulator read out: hand it back to the MMA warp before the global writes
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&sm.tempty[buf]));
+      if (lane == 0) {
+        if (kPair) mbar_arrive_cluster(tempty_leader + buf * 8u);
+        else mbar_arrive(smem_u32(&sm.tempty[buf]));
+      }
       if (row_ok) {
         p.part_m[(int64_t)vt * p.n_rows + row] = m;
         p.part_s[(int64_t)vt * p.n_rows + row] = s;
@@ -244,10 +311,14 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
 
   __syncwarp();
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
   }
 }
 
@@ -310,12 +381,25 @@ cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n
                                cudaStream_t stream, int num_sms) {
   if (n_rows == 0) return cudaSuccess;
   CUtensorMap mh, mw;
-  if (!make_map(&mh, hidden, n_rows, d, lm::kBM) || !make_map(&mw, weight, V, d, lm::kBN)) return cudaErrorInvalidValue;
+  if (!make_map(&mh, hidden, n_rows, d, lm::kBM) || !make_map(&mw, weight, V, d, lm::Cfg<
+#ifdef ECHO_LMHEAD_SINGLE
+      false
+#else
+      true
+#endif
+      >::kBRows))
+    return cudaErrorInvalidValue;
+#ifdef ECHO_LMHEAD_SINGLE
+  constexpr bool kPair = false;
+#else
+  constexpr bool kPair = true;
+#endif
+  using C = lm::Cfg<kPair>;
   LmParams p;
   p.n_rows = n_rows;
   p.d = d;
   p.V = V;
-  p.n_tt = (int32_t)((n_rows + lm::kBM - 1) / lm::kBM);
+  p.n_tt = (int32_t)((n_rows + C::kTileRows - 1) / C::kTileRows);
   p.n_vt = (V + lm::kBN - 1) / lm::kBN;
   p.n_kb = (d + lm::kBK - 1) / lm::kBK;
   p.tok_action = tok_action;
@@ -323,13 +407,26 @@ cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n
   p.part_m = ws;
   p.part_s = ws + (size_t)p.n_vt * n_rows;
   p.za = ws + (size_t)2 * p.n_vt * n_rows;
-  cudaError_t e = cudaFuncSetAttribute(lmhead_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)lm::kSmemBytes);
+  const void* fn = (const void*)lmhead_tile_kernel<kPair>;
+  const size_t smem = lm::smem_bytes<kPair>();
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
-  const int grid = (int)(n_tiles < num_sms ? n_tiles : num_sms);
-  lmhead_tile_kernel<<<grid, lm::kThreads, lm::kSmemBytes, stream>>>(mh, mw, p);
-  e = cudaGetLastError();
+  int64_t units = kPair ? max_active_clusters(fn, lm::kThreads, smem, 2, num_sms / 2) : num_sms;
+  if (units > n_tiles) units = n_tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(units * C::kCtas));
+  cfg.blockDim = dim3(lm::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = C::kCtas;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kPair>, mh, mw, p);
   if (e != cudaSuccess) return e;
   lmhead_finalize_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, stream>>>(n_rows, V, p.n_vt, tok_action, p.part_m,
                                                                               p.part_s, p.za, tok_logp, tok_lse);
