@@ -271,27 +271,37 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + c * 32, r);
         const int32_t cb = col0 + c * 32;
-        float cm = -INFINITY;
+        if (cb + 32 > p.V) {  // the vocabulary's last, partial chunk: columns >= V do not exist
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float x = (cb + i < p.V) ? __uint_as_float(r[i]) : -INFINITY;
-          cm = fmaxf(cm, x);
-          if (cb + i == a) {
-            za = __uint_as_float(r[i]);
-            found = true;
-          }
+          for (int i = 0; i < 32; ++i)
+            if (cb + i >= p.V) r[i] = 0xFF800000u;  // -inf
         }
+        if ((uint32_t)(a - cb) < 32u) {  // the action's column is in this chunk (one chunk in ~4700)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (cb + i == a) za = __uint_as_float(r[i]);
+          found = true;
+        }
+        float cm = __uint_as_float(r[0]);
+#pragma unroll
+        for (int i = 1; i < 32; ++i) cm = fmaxf(cm, __uint_as_float(r[i]));
         if (cm > m) {
           s = (m == -INFINITY) ? 0.0f : s * ex2((m - cm) * kLog2e);
           m = cm;
         }
         if (m != -INFINITY) {
-          const float mb = m * kLog2e;
-          float acc = 0.0f;
+          // 2^(z log2e - m log2e), packed fp32x2 FMA / add, one MUFU per logit
+          const uint64_t nmb2 = f2(-m * kLog2e, -m * kLog2e), l2e2 = f2(kLog2e, kLog2e);
+          uint64_t acc2 = f2(0.0f, 0.0f);
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            acc += (cb + i < p.V) ? ex2(fmaf(__uint_as_float(r[i]), kLog2e, -mb)) : 0.0f;
-          s += acc;
+          for (int i = 0; i < 32; i += 2) {
+            float e0, e1;
+            f2split(fma2(f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), l2e2, nmb2), e0, e1);
+            acc2 = add2(acc2, f2(ex2(e0), ex2(e1)));
+          }
+          float lo, hi;
+          f2split(acc2, lo, hi);
+          s += lo + hi;
         }
       }
       // accumulator read out: hand it back to the MMA warp before the global writes
