@@ -131,20 +131,21 @@ class LearnerStep:
         return self.stats1[0:1]
 
     # ------------------------------------------------------------------ f3
-    def rebalance(self) -> dict:
+    def rebalance(self, extra_tokens=()) -> dict:
         """Token-balanced resharding after the stale filter (call after reduce_counts).
 
         Every rank's kept rollouts form a contiguous block of the global kept sequence (rank-major = group order);
         ``parallel.reshard_plan`` splits that sequence into W contiguous ranges of ~N_global / W tokens and the
         packed per-rollout (global id, advantage, length) and per-token (action, old, ref) arrays move there with
         one all-to-all each.  The receiver rebuilds kept_offset / tok_slot with echo_csr_from_lengths.  Returns the
-        plan (tokens per rank before and after).  One host sync (the lengths of the kept rollouts)."""
+        plan (tokens per rank before and after; ``plan["extra"]`` holds the rebalanced ``extra_tokens``, e.g. the
+        packed per-token advantages of PPO-GAE or per-token weights).  One host sync (the kept rollouts' lengths)."""
         import numpy as np
         import torch.distributed as dist
         info = self.pack_info
         n_r, n_t = info.n_rollouts_kept, info.n_tokens
         if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(self.group) == 1:
-            return {"tokens_before": [n_t], "tokens_after": [n_t]}
+            return {"tokens_before": [n_t], "tokens_after": [n_t], "extra": [t[:n_t] for t in extra_tokens]}
         world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
         off = self.kept_offset[: n_r + 1].cpu().numpy()
         lens = np.diff(off).astype(np.int32)
@@ -156,7 +157,10 @@ class LearnerStep:
         kept_rollout, adv_slot, lens_r = exchange([self.kept_rollout[:n_r], self.adv_slot[:n_r], lens_d],
                                                   plan["send_rollouts"], plan["recv_rollouts"], self.group)
         tok = [self.tok_action[:n_t], self.tok_old[:n_t]] + ([self.tok_ref[:n_t]] if self.tok_ref is not None else [])
-        tok = exchange(tok, plan["send_tokens"], plan["recv_tokens"], self.group)
+        extra = [t[:n_t] for t in extra_tokens]
+        tok = exchange(tok + extra, plan["send_tokens"], plan["recv_tokens"], self.group)
+        plan["extra"] = tok[len(tok) - len(extra):]
+        tok = tok[: len(tok) - len(extra)]
         new_r, new_t = sum(plan["recv_rollouts"]), sum(plan["recv_tokens"])
         kept_offset = torch.empty(new_r + 1, dtype=torch.int64, device=self.device)
         tok_slot = torch.empty(max(new_t, 1), dtype=torch.int32, device=self.device)
@@ -173,6 +177,20 @@ class LearnerStep:
             self.tok_flags = torch.empty(new_t, dtype=torch.uint8, **e)
         self.pack_info = PackInfo(info.status, info.first_bad_rollout, info.n_groups_kept, new_r, new_t)
         return plan
+
+    # ------------------------------------------------------------------ f2
+    def token_logp_from_hidden(self, hidden, weight, out=None, lse=None, workspace=None):
+        """f2: log-probs of the packed actions straight from the final hidden states and the LM-head weight
+        (echo_lmhead_logp: the [tokens x vocab] logits are never materialised), e.g. to recompute old_logp or the
+        reference model's ref_logp.  hidden: bf16 [n x d] rows aligned with the packed tokens [0, n)."""
+        n, d = hidden.shape
+        out = torch.empty(n, dtype=torch.float32, device=self.device) if out is None else out
+        if workspace is None:
+            workspace = torch.empty(abi.echo_lmhead_workspace_bytes(n, self.V) // 4 + 1, dtype=torch.float32,
+                                    device=self.device)
+        abi.echo_lmhead_logp(hidden, weight, n, d, self.V, self.tok_action[:n], out, lse, workspace)
+        self.launches += abi.LAUNCHES["echo_lmhead_logp"]
+        return out
 
     # ------------------------------------------------------------------ (3)-(5)
     def loss(self, logits: torch.Tensor, row0: int, *, clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0,

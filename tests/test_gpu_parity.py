@@ -645,3 +645,23 @@ def test_lmhead_logp_edge_cases_and_errors():
     with pytest.raises(abi.EchoError):                                      # misaligned hidden pointer
         abi.echo_lmhead_logp(h.view(-1)[1:].data_ptr(), w, n - 1, d, V, act, out, None, ws)
     assert abi.echo_lmhead_workspace_bytes(n, V) == (2 * 3 + 1) * n * 4
+
+
+@pytest.mark.parametrize("d", [2048, 3584, 5120])
+def test_lmhead_logp_baseline_hidden_sizes(d):
+    """f2 at the other BASELINE.json models' hidden sizes (30B-A3B, 7B, 32B) on a Qwen vocabulary, through the
+    LearnerStep API (packed actions); sampled rows against the oracle."""
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, cfg.G)
+    st, info = device_step(cfg, b)
+    n = 384
+    g = torch.Generator(device="cuda").manual_seed(d)
+    h = torch.randn(n, d, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(cfg.V, d, generator=g, device="cuda") * (2.0 / math.sqrt(d))).to(torch.bfloat16)
+    lp = st.token_logp_from_hidden(h, w).cpu().numpy().astype(np.float64)
+    rows = np.array([0, 127, 128, 255, 256, 383])
+    hb = h[rows].cpu().view(torch.int16).numpy().view(np.uint16)
+    wb = w.cpu().view(torch.int16).numpy().view(np.uint16)
+    ref, _ = oracle.lmhead_logp(hb, wb, st.tok_action[:n].cpu().numpy()[rows])
+    tol = _lmhead_tol(hb, wb, np.arange(len(rows)))
+    assert np.all(np.abs(lp[rows] - ref) <= tol) and np.max(np.abs(lp[rows] - ref)) <= 2e-4

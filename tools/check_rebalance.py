@@ -52,7 +52,11 @@ def main():
         assert info.status == 0, info
         st.advantage()
         st.reduce_counts()
-        plan = st.rebalance() if balance else None
+        plan = None
+        if balance:
+            extra = st.tok_old[: st.pack_info.n_tokens].clone()      # an extra per-token array rides along
+            plan = st.rebalance(extra_tokens=[extra])
+            assert torch.equal(plan["extra"][0], st.tok_old[: st.pack_info.n_tokens]), "extra_tokens mismatch"
         N = st.pack_info.n_tokens if not args.max_rows else min(args.max_rows, st.pack_info.n_tokens)
         for row0 in range(0, N, M):
             m = min(M, N - row0)
