@@ -8,12 +8,13 @@
 // The path is a memory-bound stream (no contraction): the design goal is exactly one HBM read and one HBM
 // write per logit, 128-bit accesses, and nothing else on the memory bus.
 //
-// Kernels (one dispatch, echo_policy_loss_fwd_bwd_ex):
-//   ECHO_ALGO_QUAD_REG / _EXACT (policy_loss_quad.cu; bf16, V <= 155648) -- the B200 design: a 4-CTA cluster
-//     owns a row, each CTA keeps its quarter-row in registers, two CTAs (two rows) share an SM so that one row's
-//     MUFU-bound reduction overlaps the other's cluster merge and store burst; rows arrive through a TMA-fed
-//     shared-memory ring; the CTA partials are merged through DSMEM (st.async + mbarrier); exactly one HBM read
-//     and one HBM write per logit.
+// Kernels (one dispatch, echo_policy_loss_fwd_bwd_ex / _v2):
+//   ECHO_ALGO_OCT_REG (AUTO) / QUAD_REG / QUAD_REG_EXACT (policy_loss_quad.cu; bf16, V <= 155648) -- the B200
+//     design: an 8- (or 4-) CTA cluster owns a row, each CTA keeps its slice of the row in registers, 4 (or 2)
+//     CTAs -- rows -- share an SM so that one row's MUFU-bound reduction overlaps the others' cluster merges and
+//     store bursts; rows are handed out in order by a global counter and arrive through a TMA-fed shared-memory
+//     ring; the CTA partials are merged through DSMEM (st.async + mbarrier); exactly one HBM read and one HBM
+//     write per logit.
 //   ECHO_ALGO_ROW_L2 (policy_loss_row.cu; bf16 or fp32, any V) -- one 1024-thread CTA per row, persistent over
 //     rows; pass 1 loads with L2 evict_last, pass 2 re-loads (an L2 hit when the ~45 MB of rows in flight stay
 //     resident) with evict_first and stores in place.  Generic path for fp32 and out-of-range vocabularies.
@@ -30,8 +31,8 @@
 namespace echo {
 
 // ====================================================================== dispatch
-// How many 2-CTA clusters of `fn` can be resident at once (GPC shapes may strand SMs).  The persistent grids
-// are sized to exactly that, so the static row striding never leaves a cluster for a second wave.
+// How many clusters of `fn` can be resident at once (GPC shapes may strand SMs).  The persistent grids are sized
+// to exactly that, so no cluster waits for a second wave.
 int max_active_clusters(const void* fn, int threads, size_t smem, int cluster, int fallback) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cluster * 4096);
