@@ -665,3 +665,28 @@ def test_lmhead_logp_baseline_hidden_sizes(d):
     ref, _ = oracle.lmhead_logp(hb, wb, st.tok_action[:n].cpu().numpy()[rows])
     tol = _lmhead_tol(hb, wb, np.arange(len(rows)))
     assert np.all(np.abs(lp[rows] - ref) <= tol) and np.max(np.abs(lp[rows] - ref)) <= 2e-4
+
+
+def test_fp32_logits_qwen_vocab():
+    """fp32 logits at a Qwen vocabulary (the generic row kernel: AUTO's path for fp32) against the oracle."""
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, cfg.G)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    n = 96
+    logits = torch.zeros(n, cfg.V, dtype=torch.float32, device="cuda")
+    import synth.gpu as sgpu
+    sgpu.fill_logits(logits, dtype="f32", vocab=cfg.V, row0=0, tok_slot=st.tok_slot, tok_action=st.tok_action,
+                     kept_rollout=st.kept_rollout, kept_offset=st.kept_offset, max_len=cfg.S, seed=cfg.seed)
+    z = logits.cpu().numpy()
+    args = (o.pk.tok_action[:n], o.pk.tok_old[:n], o.pk.tok_ref[:n], o.pk.tok_slot[:n], o.adv)
+    N = info.n_tokens
+    ref = oracle.policy_loss(z, *args, n_global=N, kl_coef=cfg.kl_coef, grad_scale=float(N))
+    from paper_2508_05387_b200 import abi
+    st.edtype = abi.ECHO_F32                                        # (the LearnerStep was built for bf16 logits)
+    st.loss(logits, 0, kl_coef=cfg.kl_coef, grad_scale=float(N))
+    check_rows(d_gpu=logits.cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
+               loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
+               dtype="f32", old=o.pk.tok_old[:n],
+               cslack=coef_slack(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef,
+                                 float(N), N))

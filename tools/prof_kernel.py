@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--streams", action="store_true", help="also time torch in-place / copy streams")
+    ap.add_argument("--dtype", default=None, choices=[None, "bf16", "f32"], help="override the config's logits dtype")
     args = ap.parse_args()
 
     import __graft_entry__
@@ -36,10 +37,11 @@ def main():
     from paper_2508_05387_b200.step import LearnerStep
 
     cfg = synth.CONFIGS[args.config]
+    dt = args.dtype or cfg.dtype
     n_roll = -(-args.rows // cfg.S)
     n_roll = -(-n_roll // cfg.G) * cfg.G
     b = synth.make_batch(cfg, 0, n_roll)
-    st = LearnerStep(n_rollouts=n_roll, group_size=cfg.G, max_len=cfg.S, vocab=cfg.V, dtype=cfg.dtype)
+    st = LearnerStep(n_rollouts=n_roll, group_size=cfg.G, max_len=cfg.S, vocab=cfg.V, dtype=dt)
     st.h2d(*[torch.from_numpy(np.ascontiguousarray(x)) for x in (b.version, b.resp_len, b.reward, b.action,
                                                                  b.old_logp, b.ref_logp)])
     info = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
@@ -47,20 +49,21 @@ def main():
     st.reduce_counts()
     M = min(args.rows, info.n_tokens)
     ld = (cfg.V + 7) // 8 * 8
-    logits = torch.empty(M, ld, dtype=torch.bfloat16, device="cuda")
+    esize = 2 if dt == "bf16" else 4
+    logits = torch.empty(M, ld, dtype=torch.bfloat16 if dt == "bf16" else torch.float32, device="cuda")
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-    bpt = 2 * cfg.V * 2 + 21 + (4 if cfg.kl_coef > 0 else 0)
+    bpt = 2 * cfg.V * esize + 21 + (4 if cfg.kl_coef > 0 else 0)
     names = abi.ALGO_NAMES
     out = {"config": cfg.name, "rows": M, "bytes_per_token": bpt, "algos": {}}
 
     def regen():
-        sgpu.fill_logits(logits, dtype=cfg.dtype, vocab=cfg.V, row0=0, tok_slot=st.tok_slot, tok_action=st.tok_action,
+        sgpu.fill_logits(logits, dtype=dt, vocab=cfg.V, row0=0, tok_slot=st.tok_slot, tok_action=st.tok_action,
                          kept_rollout=st.kept_rollout, kept_offset=st.kept_offset, max_len=cfg.S, seed=cfg.seed)
         flush.fill_(1.0)
 
     for name in args.algos.split(","):
         algo = names[name]
-        shape = abi.echo_policy_loss_launch_shape(abi.ECHO_BF16, M, cfg.V, algo)
+        shape = abi.echo_policy_loss_launch_shape(abi.ECHO_BF16 if dt == "bf16" else abi.ECHO_F32, M, cfg.V, algo)
         times = []
         for r in range(args.warmup + args.reps):
             regen()
