@@ -1,6 +1,8 @@
 // policy_loss_row.cu -- ECHO_ALGO_ROW_L2 (see policy_loss.cu for the overview).
 #include <cuda_bf16.h>
 
+#include <atomic>
+
 #include "echo_common.cuh"
 #include "echo_internal.h"
 #include "policy_loss_common.cuh"
@@ -8,6 +10,11 @@
 namespace echo {
 
 // ====================================================================== ECHO_ALGO_ROW_L2
+// Rows are handed out in order by a global counter (one {next row, CTAs done} pair per launch slot, reset by the
+// launch's last CTA), so the CTAs work on one compact window of consecutive rows (see policy_loss_quad.cu).
+constexpr int kRowSchedSlots = 256;
+__device__ unsigned long long g_rowk_sched[kRowSchedSlots][2];
+
 constexpr int kRThreads = 1024;
 constexpr int kRWarps = kRThreads / 32;
 constexpr int kRUnroll = 4;
@@ -50,13 +57,20 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
   constexpr int N = RV::N;
   __shared__ float s_m[kRWarps], s_s[kRWarps], s_t[kRWarps];
   __shared__ float s_za, s_coef, s_lse_l2e, s_lse, s_H, s_ecoef;
+  __shared__ long long s_row;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int32_t V = p.V;
   const int32_t nvec = V / N;
   const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
   const float gscale = kGrad ? base_scale(p) : 0.0f;
 
-  for (int64_t row = blockIdx.x; row < p.n_rows; row += gridDim.x) {
+  unsigned long long* const sched = g_rowk_sched[p.sched_slot];
+  if (tid == 0) s_row = (long long)atomicAdd(&sched[0], 1ull);
+  __syncthreads();
+  for (int64_t row = s_row; row < p.n_rows; row = s_row) {
+    // the next row is grabbed now and published at the end-of-row barrier (its latency stays off the path)
+    unsigned long long next = 0;
+    if (tid == 0) next = atomicAdd(&sched[0], 1ull);
     uint8_t* rowp = p.logits + row * p.ld_bytes;
     const int32_t a = p.tok_action[row];
     RowMeta meta{0.f, 0.f, 0.f};
@@ -139,6 +153,7 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
         if (p.tok_flags) p.tok_flags[row] = (isfinite(lse) && isfinite(logp)) ? 0 : ECHO_FLAG_NONFINITE;
       }
     }
+    if (tid == 0) s_row = (long long)next;  // read by the loop condition after the barriers below
     __syncthreads();
     if constexpr (!kGrad) continue;
     const float coef = s_coef, lse_l2e = s_lse_l2e, lse = s_lse, H = s_H, ecoef = s_ecoef;
@@ -171,6 +186,13 @@ __global__ void __launch_bounds__(kRThreads, 1) policy_loss_row_kernel(const Los
     }
     __syncthreads();  // s_* reuse by the next row
   }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&sched[1], 1ull) == (unsigned long long)gridDim.x - 1ull) {
+      sched[0] = 0ull;
+      sched[1] = 0ull;
+    }
+  }
 }
 
 cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape,
@@ -181,21 +203,24 @@ cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, 
     *shape = LaunchShape{(int32_t)grid, 1, kRThreads, 0};
     return cudaSuccess;
   }
+  static std::atomic<uint32_t> next_slot{0};
+  LossParams q = p;
+  q.sched_slot = (int32_t)(next_slot.fetch_add(1, std::memory_order_relaxed) % kRowSchedSlots);
   const bool ent = grad && (p.entropy_coef > 0.0f || p.tok_entropy != nullptr);
   if (dtype == ECHO_BF16) {
     if (ent)
-      policy_loss_row_kernel<1, true, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+      policy_loss_row_kernel<1, true, true><<<(unsigned)grid, kRThreads, 0, stream>>>(q);
     else if (grad)
-      policy_loss_row_kernel<1, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+      policy_loss_row_kernel<1, true><<<(unsigned)grid, kRThreads, 0, stream>>>(q);
     else
-      policy_loss_row_kernel<1, false><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+      policy_loss_row_kernel<1, false><<<(unsigned)grid, kRThreads, 0, stream>>>(q);
   } else {
     if (ent)
-      policy_loss_row_kernel<0, true, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+      policy_loss_row_kernel<0, true, true><<<(unsigned)grid, kRThreads, 0, stream>>>(q);
     else if (grad)
-      policy_loss_row_kernel<0, true><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+      policy_loss_row_kernel<0, true><<<(unsigned)grid, kRThreads, 0, stream>>>(q);
     else
-      policy_loss_row_kernel<0, false><<<(unsigned)grid, kRThreads, 0, stream>>>(p);
+      policy_loss_row_kernel<0, false><<<(unsigned)grid, kRThreads, 0, stream>>>(q);
   }
   return cudaGetLastError();
 }
