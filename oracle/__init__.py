@@ -67,6 +67,8 @@ def lib():
         _lib.echo_ref_csr_from_lengths.restype = ctypes.c_int
         _lib.echo_ref_lmhead_logp.argtypes = [i64, i32, i32, P, P, P, P, P]
         _lib.echo_ref_lmhead_logp.restype = ctypes.c_int
+        _lib.echo_ref_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P]
+        _lib.echo_ref_staleness_histogram.restype = ctypes.c_int
     return _lib
 
 
@@ -268,3 +270,15 @@ def lmhead_logp(hidden_bf16, weight_bf16, tok_action):
     if rc != 0:
         raise ValueError("echo_ref_lmhead_logp: invalid argument")
     return logp, lse
+
+
+def staleness_histogram(version, resp_len, *, group_size, max_len, t_train, max_lag, n_bins):
+    """f3: int64 [4, n_bins + 2] = {kept rollouts, dropped rollouts, kept tokens, dropped tokens} per lag bin
+    (bin 0: future versions, 1 + lag for lag < n_bins, n_bins + 1: older)."""
+    v = _c(version, np.int64)
+    L = _c(resp_len, np.int32)
+    h = np.zeros((4, n_bins + 2), np.int64)
+    rc = lib().echo_ref_staleness_histogram(len(v), group_size, max_len, t_train, max_lag, _p(v), _p(L), n_bins, _p(h))
+    if rc != 0:
+        raise ValueError("echo_ref_staleness_histogram: invalid argument")
+    return h

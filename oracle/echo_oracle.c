@@ -527,3 +527,32 @@ int echo_ref_lmhead_logp(int64_t n_rows, int32_t d, int32_t vocab, const uint16_
   }
   return REF_OK;
 }
+
+/* ======================================================================================
+ * f3: the staleness histogram of a step -- the per-step log record of SPEC.md :604
+ * ({step, version, mean_return, staleness_histogram}) and the buffer's version_histogram (SPEC.md :373), with
+ * staleness = t_train - param_version (SPEC.md :701; PAPER.md :192, :224).  Per rollout i of group g = i / G:
+ *   lag_i = t_train - version[i];  kept_i = (t_train - version[g G] <= max_lag)   (the filter of (1), reading R1/R3)
+ *   bin(lag) = 0 if lag < 0 (a future version), 1 + lag if 0 <= lag < n_bins, n_bins + 1 otherwise
+ *   hist[0][bin] += kept_i, hist[1][bin] += !kept_i,
+ *   hist[2][bin] += kept_i * L_i, hist[3][bin] += !kept_i * L_i,   L_i = min(max(resp_len[i], 0), max_len)
+ * hist: int64 [4][n_bins + 2].
+ * ====================================================================================== */
+int echo_ref_staleness_histogram(int32_t n_rollouts, int32_t group_size, int32_t max_len, int64_t t_train,
+                                 int32_t max_lag, const int64_t* version, const int32_t* resp_len, int32_t n_bins,
+                                 int64_t* hist) {
+  if (n_rollouts < 0 || group_size < 1 || n_rollouts % group_size != 0 || max_len < 1 || n_bins < 1)
+    return REF_ERR_INVALID_ARGUMENT;
+  const int32_t nb = n_bins + 2;
+  for (int32_t k = 0; k < 4 * nb; ++k) hist[k] = 0;
+  for (int32_t i = 0; i < n_rollouts; ++i) {
+    int64_t lag = t_train - version[i];
+    int64_t lag0 = t_train - version[(i / group_size) * group_size];
+    int kept = lag0 <= (int64_t)max_lag;
+    int32_t bin = lag < 0 ? 0 : (lag < n_bins ? (int32_t)lag + 1 : n_bins + 1);
+    int64_t L = resp_len[i] < 0 ? 0 : (resp_len[i] > max_len ? max_len : resp_len[i]);
+    hist[(kept ? 0 : 1) * nb + bin] += 1;
+    hist[(kept ? 2 : 3) * nb + bin] += L;
+  }
+  return REF_OK;
+}

@@ -161,3 +161,38 @@ def test_empty_batch_and_all_dropped():
     out = oracle.pack_batch(e, e.astype(np.int32), np.zeros((0, 8), np.int32), np.zeros((0, 8), np.float32),
                             None, **kw)
     assert out.status == 0 and out.n_tokens == 0
+
+
+def test_staleness_histogram_pins():
+    """f3 staleness histogram: brute force per rollout; totals equal the pack's kept / dropped counts; the SPEC
+    audit example (sequential mode: every lag 0)."""
+    import synth
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        G = int(rng.integers(1, 5))
+        P = int(rng.integers(1, 9))
+        S = 16
+        t = 100
+        lag_g = rng.integers(-1, 7, P)
+        version = np.repeat(t - lag_g, G).astype(np.int64)
+        resp = rng.integers(-1, S + 3, P * G).astype(np.int32)
+        max_lag, nb = int(rng.integers(0, 4)), int(rng.integers(1, 6))
+        h = oracle.staleness_histogram(version, resp, group_size=G, max_len=S, t_train=t, max_lag=max_lag, n_bins=nb)
+        exp = np.zeros_like(h)
+        for i in range(P * G):
+            lag = t - version[i]
+            kept = (t - version[(i // G) * G]) <= max_lag
+            b = 0 if lag < 0 else (lag + 1 if lag < nb else nb + 1)
+            exp[0 if kept else 1, b] += 1
+            exp[2 if kept else 3, b] += min(max(int(resp[i]), 0), S)
+        np.testing.assert_array_equal(h, exp)
+        assert h[0].sum() + h[1].sum() == P * G
+    # sequential mode (the Qwen3-4B config, max_lag 0): all kept, all in the lag-0 bin, tokens = pack's n_tokens
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, 4 * cfg.G)
+    h = oracle.staleness_histogram(b.version, b.resp_len, group_size=cfg.G, max_len=cfg.S, t_train=synth.T_TRAIN,
+                                   max_lag=cfg.max_lag, n_bins=4)
+    assert h[0, 1] == 4 * cfg.G and h[0].sum() == h[0, 1] and h[1].sum() == 0
+    pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,
+                           vocab=cfg.V, t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
+    assert h[2].sum() == pk.n_tokens
