@@ -264,6 +264,19 @@ ECHO_API echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, in
                                            int32_t* tok_slot, void* stream);
 
 /*
+ * f3: the staleness histogram of a step (the per-step log's staleness_histogram, SPEC.md :604, and the buffer's
+ * version_histogram, SPEC.md :373; staleness = t_train - param_version, PAPER.md :192, :224).  Same rollout inputs
+ * and keep rule as echo_pack_batch (a rollout is kept iff its group's first version has t_train - v <= max_lag):
+ *   hist: device int64 [4][n_bins + 2] = {kept rollouts, dropped rollouts, kept tokens, dropped tokens} per bin;
+ *   bin 0 counts future versions (lag < 0), bin 1 + lag for 0 <= lag < n_bins, bin n_bins + 1 older rollouts;
+ *   tokens = min(max(resp_len, 0), max_len).  Every bin is written (no initialisation needed); integer counts,
+ *   bit-exact.  1 <= n_bins <= 4096.  Launches: 1 kernel.
+ */
+ECHO_API echo_status echo_staleness_histogram(int32_t n_rollouts, int32_t group_size, int32_t max_len,
+                                              int64_t t_train, int32_t max_lag, const int64_t* version,
+                                              const int32_t* resp_len, int32_t n_bins, int64_t* hist, void* stream);
+
+/*
  * f2: the LM head fused with (3), forward only.  The logits are the LM head's output
  * z[t, v] = sum_k hidden[t, k] weight[v, k] (the model's last projection; PAPER.md :254-261, the learner computes
  * log pi_theta(a|s) of PAPER.md :170 from them), and

@@ -26,12 +26,13 @@ PACK_RESULT_BYTES = 32
 # kernels launched per call (for the bench's gpu_launches count)
 LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2,
             "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1, "echo_csr_from_lengths": 2,
-            "echo_lmhead_logp": 2}
+            "echo_lmhead_logp": 2, "echo_staleness_histogram": 1}
 
 EXPORTS = ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
            "echo_policy_loss_launch_shape", "echo_token_logp", "echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage",
            "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_csr_from_lengths",
-           "echo_lmhead_workspace_bytes", "echo_lmhead_logp", "echo_status_string", "echo_abi_version")
+           "echo_lmhead_workspace_bytes", "echo_lmhead_logp", "echo_staleness_histogram", "echo_status_string",
+           "echo_abi_version")
 
 
 ECHO_KL_K3, ECHO_KL_K1, ECHO_KL_K2 = range(3)
@@ -78,11 +79,13 @@ def _load(path=LIB_PATH):
     lib.echo_status_string.restype = ctypes.c_char_p
     lib.echo_abi_version.restype = i32
     lib.echo_csr_from_lengths.argtypes = [i32, P, P, P, P]
+    lib.echo_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P, P]
     lib.echo_lmhead_workspace_bytes.argtypes = [i64, i32]
     lib.echo_lmhead_workspace_bytes.restype = ctypes.c_size_t
     lib.echo_lmhead_logp.argtypes = [P, P, i64, i32, i32, P, P, P, P, P]
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
-               "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths", "echo_lmhead_logp"):
+               "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths", "echo_lmhead_logp",
+               "echo_staleness_histogram"):
         getattr(lib, fn).restype = ctypes.c_int
     return lib
 
@@ -183,6 +186,13 @@ def echo_policy_loss_launch_shape(dtype, n_rows, vocab, algo=ECHO_ALGO_AUTO) -> 
 def echo_csr_from_lengths(n, lengths, kept_offset, tok_slot=None, stream=None):
     _check("echo_csr_from_lengths", _lib.echo_csr_from_lengths(n, _p(lengths), _p(kept_offset), _p(tok_slot),
                                                                 _s(stream)))
+
+
+def echo_staleness_histogram(n_rollouts, group_size, max_len, t_train, max_lag, version, resp_len, n_bins, hist,
+                             stream=None):
+    _check("echo_staleness_histogram", _lib.echo_staleness_histogram(n_rollouts, group_size, max_len, t_train, max_lag,
+                                                                      _p(version), _p(resp_len), n_bins, _p(hist),
+                                                                      _s(stream)))
 
 
 def echo_lmhead_workspace_bytes(n_rows, vocab) -> int:

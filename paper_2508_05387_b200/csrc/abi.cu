@@ -250,6 +250,19 @@ echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, i
   return from_cuda(echo::launch_row(p, dtype, s, sms, nullptr, false));
 }
 
+echo_status echo_staleness_histogram(int32_t n_rollouts, int32_t group_size, int32_t max_len, int64_t t_train,
+                                     int32_t max_lag, const int64_t* version, const int32_t* resp_len, int32_t n_bins,
+                                     int64_t* hist, void* stream) {
+  if (n_rollouts < 0 || group_size < 1 || n_rollouts % group_size != 0 || max_len < 1 || max_lag < 0 ||
+      n_bins < 1 || n_bins > 4096 || !hist || (n_rollouts > 0 && (!version || !resp_len)))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  return from_cuda(echo::launch_staleness_hist(n_rollouts, group_size, max_len, t_train, max_lag, version, resp_len,
+                                               n_bins, hist, static_cast<cudaStream_t>(stream)));
+}
+
 echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* kept_offset, int32_t* tok_slot,
                                   void* stream) {
   if (n < 0 || !kept_offset || (n > 0 && !lengths)) return ECHO_ERR_INVALID_ARGUMENT;

@@ -68,6 +68,9 @@ cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cud
 cudaError_t launch_gae(int32_t R, int32_t S, const int32_t* resp_len, const float* rewards, const float* values,
                        const float* bootstrap, float gamma, float lam, float* adv, float* ret, cudaStream_t stream);
 
+cudaError_t launch_staleness_hist(int32_t R, int32_t G, int32_t S, int64_t t_train, int32_t max_lag,
+                                  const int64_t* version, const int32_t* resp_len, int32_t n_bins, int64_t* hist,
+                                  cudaStream_t stream);
 cudaError_t launch_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* offsets, int32_t* tok_slot,
                                     cudaStream_t stream, int num_sms);
 

@@ -173,4 +173,38 @@ cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_tr
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------------- f3
+// Staleness histogram of a step (SPEC.md :373 version_histogram, :604 staleness_histogram): per rollout, lag =
+// t_train - version, kept by its group's version as in pack_scan_kernel; counts of rollouts and tokens per lag bin
+// for kept and dropped rollouts.  One CTA: shared-memory integer atomics (order-independent, bit-exact), then
+// plain stores of every bin (hist needs no initialisation).
+__global__ void __launch_bounds__(1024) staleness_hist_kernel(int32_t R, int32_t G, int32_t S, int64_t t_train,
+                                                              int32_t max_lag, const int64_t* __restrict__ version,
+                                                              const int32_t* __restrict__ resp_len, int32_t n_bins,
+                                                              long long* __restrict__ hist) {
+  extern __shared__ unsigned long long s_hist[];
+  const int32_t nb = n_bins + 2;
+  for (int32_t k = threadIdx.x; k < 4 * nb; k += blockDim.x) s_hist[k] = 0ull;
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < R; i += blockDim.x) {
+    const int64_t lag = t_train - version[i];
+    const bool kept = (t_train - version[(i / G) * G]) <= (int64_t)max_lag;
+    const int32_t bin = lag < 0 ? 0 : (lag < n_bins ? (int32_t)lag + 1 : n_bins + 1);
+    const int32_t L = min(max(resp_len[i], 0), S);
+    atomicAdd(&s_hist[(kept ? 0 : 1) * nb + bin], 1ull);
+    atomicAdd(&s_hist[(kept ? 2 : 3) * nb + bin], (unsigned long long)L);
+  }
+  __syncthreads();
+  for (int32_t k = threadIdx.x; k < 4 * nb; k += blockDim.x) hist[k] = (long long)s_hist[k];
+}
+
+cudaError_t launch_staleness_hist(int32_t R, int32_t G, int32_t S, int64_t t_train, int32_t max_lag,
+                                  const int64_t* version, const int32_t* resp_len, int32_t n_bins, int64_t* hist,
+                                  cudaStream_t stream) {
+  const size_t smem = (size_t)4 * (n_bins + 2) * sizeof(unsigned long long);
+  staleness_hist_kernel<<<1, 1024, smem, stream>>>(R, G, S, t_train, max_lag, version, resp_len, n_bins,
+                                                   reinterpret_cast<long long*>(hist));
+  return cudaGetLastError();
+}
+
 }  // namespace echo

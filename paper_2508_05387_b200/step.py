@@ -178,6 +178,18 @@ class LearnerStep:
         self.pack_info = PackInfo(info.status, info.first_bad_rollout, info.n_groups_kept, new_r, new_t)
         return plan
 
+    def staleness_histogram(self, *, t_train: int, max_lag: int, n_bins: int = 8, n_rollouts: int | None = None,
+                            reduce: bool = True) -> torch.Tensor:
+        """f3: this step's staleness histogram (echo_staleness_histogram; int64 [4, n_bins + 2]: kept / dropped
+        rollouts and tokens per lag bin), summed over the ranks of the process group (NCCL all-reduce)."""
+        R = self.R if n_rollouts is None else n_rollouts
+        h = torch.empty(4, n_bins + 2, dtype=torch.int64, device=self.device)
+        abi.echo_staleness_histogram(R, self.G, self.S, t_train, max_lag, self.version, self.resp_len, n_bins, h)
+        self.launches += abi.LAUNCHES["echo_staleness_histogram"]
+        if reduce:
+            allreduce_sum_(h, self.group)
+        return h
+
     # ------------------------------------------------------------------ f2
     def token_logp_from_hidden(self, hidden, weight, out=None, lse=None, workspace=None):
         """f2: log-probs of the packed actions straight from the final hidden states and the LM-head weight

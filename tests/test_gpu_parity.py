@@ -690,3 +690,18 @@ def test_fp32_logits_qwen_vocab():
                dtype="f32", old=o.pk.tok_old[:n],
                cslack=coef_slack(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef,
                                  float(N), N))
+
+
+@pytest.mark.parametrize("name", ["tiny", "qwen2.5-7b"])
+def test_staleness_histogram_bit_exact(name):
+    """f3: the step's staleness histogram through LearnerStep against the oracle (bit-exact), with ragged
+    lengths and stale groups (the 7B config drops 38 of 128 groups)."""
+    cfg = synth.CONFIGS[name]
+    b = synth.make_batch(cfg, lengths="ragged") if name == "tiny" else synth.make_batch(cfg)
+    st, info = device_step(cfg, b)
+    for nb in (1, 3, 8):
+        h = st.staleness_histogram(t_train=synth.T_TRAIN, max_lag=cfg.max_lag, n_bins=nb).cpu().numpy()
+        ref = oracle.staleness_histogram(b.version, b.resp_len, group_size=cfg.G, max_len=cfg.S, t_train=synth.T_TRAIN,
+                                         max_lag=cfg.max_lag, n_bins=nb)
+        np.testing.assert_array_equal(h, ref)
+        assert h[2].sum() == info.n_tokens
