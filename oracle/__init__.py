@@ -49,7 +49,7 @@ def lib():
         P = ctypes.c_void_p
         i32, i64, f32, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double
         _lib.echo_ref_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, P, i64,
-                                             P, P, P, P, P, P, P, ctypes.POINTER(_PackResult)]
+                                             P, P, P, P, P, P, P, ctypes.POINTER(_PackResult), i32]
         _lib.echo_ref_gae_advantage.argtypes = [i32, i32, P, P, P, P, f32, f32, P, P]
         _lib.echo_ref_gae_advantage.restype = ctypes.c_int
         _lib.echo_ref_pack_batch.restype = ctypes.c_int
@@ -67,7 +67,7 @@ def lib():
         _lib.echo_ref_csr_from_lengths.restype = ctypes.c_int
         _lib.echo_ref_lmhead_logp.argtypes = [i64, i32, i32, P, P, P, P, P]
         _lib.echo_ref_lmhead_logp.restype = ctypes.c_int
-        _lib.echo_ref_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P]
+        _lib.echo_ref_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P, i32]
         _lib.echo_ref_staleness_histogram.restype = ctypes.c_int
     return _lib
 
@@ -97,8 +97,9 @@ class PackOut:
 
 
 def pack_batch(version, resp_len, action, old_logp, ref_logp, *, group_size, max_len, vocab, t_train, max_lag,
-               rollout_base=0, token_capacity=None, aux=None) -> PackOut:
-    """(1) lag filter + pack.  ``action``/``old_logp``/``ref_logp`` are padded ``[R, S]``."""
+               rollout_base=0, token_capacity=None, aux=None, filter_mode=0) -> PackOut:
+    """(1) lag filter + pack.  ``action``/``old_logp``/``ref_logp`` are padded ``[R, S]``.  ``filter_mode`` 1 keeps
+    rollouts individually (f3 partial groups) instead of whole groups."""
     version = _c(version, np.int64)
     resp_len = _c(resp_len, np.int32)
     R = int(version.shape[0])
@@ -119,7 +120,7 @@ def pack_batch(version, resp_len, action, old_logp, ref_logp, *, group_size, max
     rc = lib().echo_ref_pack_batch(R, group_size, max_len, vocab, t_train, max_lag, rollout_base,
                                    _p(version), _p(resp_len), _p(action), _p(old_logp), _p(ref_logp), _p(aux), cap,
                                    _p(kept_rollout), _p(kept_offset), _p(tok_slot), _p(tok_action), _p(tok_old),
-                                   _p(tok_ref), _p(tok_aux), ctypes.byref(res))
+                                   _p(tok_ref), _p(tok_aux), ctypes.byref(res), filter_mode)
     if rc != 0:
         raise ValueError(f"echo_ref_pack_batch: invalid argument (rc={rc})")
     n = int(res.n_tokens) if res.n_tokens <= cap else 0
@@ -272,13 +273,14 @@ def lmhead_logp(hidden_bf16, weight_bf16, tok_action):
     return logp, lse
 
 
-def staleness_histogram(version, resp_len, *, group_size, max_len, t_train, max_lag, n_bins):
+def staleness_histogram(version, resp_len, *, group_size, max_len, t_train, max_lag, n_bins, filter_mode=0):
     """f3: int64 [4, n_bins + 2] = {kept rollouts, dropped rollouts, kept tokens, dropped tokens} per lag bin
     (bin 0: future versions, 1 + lag for lag < n_bins, n_bins + 1: older)."""
     v = _c(version, np.int64)
     L = _c(resp_len, np.int32)
     h = np.zeros((4, n_bins + 2), np.int64)
-    rc = lib().echo_ref_staleness_histogram(len(v), group_size, max_len, t_train, max_lag, _p(v), _p(L), n_bins, _p(h))
+    rc = lib().echo_ref_staleness_histogram(len(v), group_size, max_len, t_train, max_lag, _p(v), _p(L), n_bins, _p(h),
+                                            filter_mode)
     if rc != 0:
         raise ValueError("echo_ref_staleness_histogram: invalid argument")
     return h

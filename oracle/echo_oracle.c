@@ -87,6 +87,10 @@ static double logit_at(const void* logits, int dtype, int64_t ld, int64_t row, i
  * Errors are reported as (rollout, check) lexicographic minimum: checks for rollout i in the
  * order FUTURE(1) < MIXED(2) < BAD_LENGTH(3) < BAD_ACTION(4); CAPACITY(5) only when nothing
  * else failed.  On any data error only status / first_bad_rollout are specified.
+ * filter_mode (f3, SURVEY.md §8.6 "partial-group handling if per-rollout versions ever differ"):
+ *   0 (group)   the group's versions must agree (MIXED otherwise); keep / drop whole groups (reading R3)
+ *   1 (rollout) keep rollout i iff t_train - version[i] <= max_lag; groups may be partial, no MIXED check;
+ *               n_groups_kept counts the groups with at least one kept rollout
  * ====================================================================================== */
 int echo_ref_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len, int32_t vocab,
                         int64_t t_train, int32_t max_lag, int64_t rollout_base,
@@ -95,8 +99,9 @@ int echo_ref_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len,
                         const float* aux, int64_t token_capacity,
                         int32_t* kept_rollout, int64_t* kept_offset,
                         int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref, float* tok_aux,
-                        echo_ref_pack_result* result) {
+                        echo_ref_pack_result* result, int32_t filter_mode) {
   if (n_rollouts < 0 || group_size < 2 || max_len < 1 || vocab < 1 || max_lag < 0) return REF_ERR_INVALID_ARGUMENT;
+  if (filter_mode != 0 && filter_mode != 1) return REF_ERR_INVALID_ARGUMENT;
   if (n_rollouts % group_size != 0) return REF_ERR_INVALID_ARGUMENT;
   const int64_t R = n_rollouts, G = group_size, S = max_len;
 
@@ -109,17 +114,17 @@ int echo_ref_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len,
     int64_t first = (i / G) * G;
     int64_t key = INT64_MAX;
     if (version[i] > t_train) key = i * 8 + REF_DATA_FUTURE_VERSION;
-    else if (version[i] != version[first]) key = i * 8 + REF_DATA_MIXED_GROUP_VERSION;
+    else if (filter_mode == 0 && version[i] != version[first]) key = i * 8 + REF_DATA_MIXED_GROUP_VERSION;
     else if (resp_len[i] < 1 || resp_len[i] > max_len) key = i * 8 + REF_DATA_BAD_LENGTH;
     if (key < best_key) best_key = key;
   }
 
-  /* filter: one decision per group, from its (uniform) version */
+  /* filter: one decision per group from its (uniform) version, or one per rollout (filter_mode 1) */
   for (int64_t g = 0; g < R / G; ++g) {
-    int64_t lag = t_train - version[g * G];
-    int keep = (lag <= (int64_t)max_lag);
-    if (!keep) continue;
+    int any = 0;
     for (int64_t i = g * G; i < (g + 1) * G; ++i) {
+      int64_t lag = t_train - (filter_mode == 0 ? version[g * G] : version[i]);
+      if (lag > (int64_t)max_lag) continue;
       kept_rollout[n_rollouts_kept] = (int32_t)(rollout_base + i);
       kept_offset[n_rollouts_kept] = n_tokens;
       int64_t L = resp_len[i];
@@ -127,8 +132,9 @@ int echo_ref_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len,
       if (L > S) L = S;
       n_tokens += L;
       n_rollouts_kept += 1;
+      any = 1;
     }
-    n_groups_kept += 1;
+    n_groups_kept += any;
   }
   kept_offset[n_rollouts_kept] = n_tokens;
 
@@ -186,27 +192,35 @@ int echo_ref_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_len,
  * adv_f64 (nullable) receives A before the fp32 rounding.
  * Stats: per group {sum A, sum A^2, sum r, sum r^2} (A as the fp32 value), then summed over groups
  * in ascending order; adv_stats = {sum A, sum A^2, sum r, sum r^2, n_zero_std_groups, n_rollouts}.
+ * A group is the run of consecutive kept rollouts with the same kept_rollout[k] / G; with whole groups (pack
+ * filter_mode 0) every run has G members, with per-rollout filtering (filter_mode 1) a run has its n_g <= G
+ * surviving members and G is replaced by n_g in the mean and the std (f3 partial groups).
  * ====================================================================================== */
 int echo_ref_group_advantage(int32_t n_rollouts_kept, int32_t group_size, float eps,
                              const float* reward, const int32_t* kept_rollout, int64_t rollout_base,
                              float* adv_slot, double* adv_f64, double* adv_stats) {
-  if (group_size < 2 || n_rollouts_kept < 0 || n_rollouts_kept % group_size != 0) return REF_ERR_INVALID_ARGUMENT;
+  if (group_size < 2 || n_rollouts_kept < 0) return REF_ERR_INVALID_ARGUMENT;
   const int64_t G = group_size;
   double tot[4] = {0, 0, 0, 0};
   double n_zero_std = 0;
-  for (int64_t g0 = 0; g0 < n_rollouts_kept; g0 += G) {
+  int64_t g1;
+  for (int64_t g0 = 0; g0 < n_rollouts_kept; g0 = g1) {
+    const int64_t grp = ((int64_t)kept_rollout[g0]) / G;
+    g1 = g0 + 1;
+    while (g1 < n_rollouts_kept && ((int64_t)kept_rollout[g1]) / G == grp) ++g1;
+    const double n_g = (double)(g1 - g0);
     double sum = 0.0;
-    for (int64_t k = g0; k < g0 + G; ++k) sum = sum + (double)reward[kept_rollout[k] - rollout_base];
-    double mean = sum / (double)G;
+    for (int64_t k = g0; k < g1; ++k) sum = sum + (double)reward[kept_rollout[k] - rollout_base];
+    double mean = sum / n_g;
     double ss = 0.0;
-    for (int64_t k = g0; k < g0 + G; ++k) {
+    for (int64_t k = g0; k < g1; ++k) {
       double d = (double)reward[kept_rollout[k] - rollout_base] - mean;
       ss = ss + d * d;
     }
-    double std = sqrt(ss / (double)G);
+    double std = sqrt(ss / n_g);
     if (std == 0.0) n_zero_std += 1.0;
     double part[4] = {0, 0, 0, 0};
-    for (int64_t k = g0; k < g0 + G; ++k) {
+    for (int64_t k = g0; k < g1; ++k) {
       double r = (double)reward[kept_rollout[k] - rollout_base];
       double a64 = (r - mean) / (std + (double)eps);
       float a = (float)a64;
@@ -532,7 +546,8 @@ int echo_ref_lmhead_logp(int64_t n_rows, int32_t d, int32_t vocab, const uint16_
  * f3: the staleness histogram of a step -- the per-step log record of SPEC.md :604
  * ({step, version, mean_return, staleness_histogram}) and the buffer's version_histogram (SPEC.md :373), with
  * staleness = t_train - param_version (SPEC.md :701; PAPER.md :192, :224).  Per rollout i of group g = i / G:
- *   lag_i = t_train - version[i];  kept_i = (t_train - version[g G] <= max_lag)   (the filter of (1), reading R1/R3)
+ *   lag_i = t_train - version[i];  kept_i = (t_train - version[g G] <= max_lag)   (the filter of (1), reading R1/R3;
+ *   filter_mode 1: t_train - version[i] <= max_lag, the per-rollout filter)
  *   bin(lag) = 0 if lag < 0 (a future version), 1 + lag if 0 <= lag < n_bins, n_bins + 1 otherwise
  *   hist[0][bin] += kept_i, hist[1][bin] += !kept_i,
  *   hist[2][bin] += kept_i * L_i, hist[3][bin] += !kept_i * L_i,   L_i = min(max(resp_len[i], 0), max_len)
@@ -540,14 +555,14 @@ int echo_ref_lmhead_logp(int64_t n_rows, int32_t d, int32_t vocab, const uint16_
  * ====================================================================================== */
 int echo_ref_staleness_histogram(int32_t n_rollouts, int32_t group_size, int32_t max_len, int64_t t_train,
                                  int32_t max_lag, const int64_t* version, const int32_t* resp_len, int32_t n_bins,
-                                 int64_t* hist) {
+                                 int64_t* hist, int32_t filter_mode) {
   if (n_rollouts < 0 || group_size < 1 || n_rollouts % group_size != 0 || max_len < 1 || n_bins < 1)
     return REF_ERR_INVALID_ARGUMENT;
   const int32_t nb = n_bins + 2;
   for (int32_t k = 0; k < 4 * nb; ++k) hist[k] = 0;
   for (int32_t i = 0; i < n_rollouts; ++i) {
     int64_t lag = t_train - version[i];
-    int64_t lag0 = t_train - version[(i / group_size) * group_size];
+    int64_t lag0 = t_train - version[filter_mode == 0 ? (i / group_size) * group_size : i];
     int kept = lag0 <= (int64_t)max_lag;
     int32_t bin = lag < 0 ? 0 : (lag < n_bins ? (int32_t)lag + 1 : n_bins + 1);
     int64_t L = resp_len[i] < 0 ? 0 : (resp_len[i] > max_len ? max_len : resp_len[i]);

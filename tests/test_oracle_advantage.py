@@ -96,12 +96,27 @@ def test_stats_and_multi_group_layout():
     assert stats[4] == sum(1 for g in range(n_groups) if np.all(reward[g * G:(g + 1) * G] == reward[g * G]))
     np.testing.assert_allclose(stats[1], (a.astype(np.float64) ** 2).sum(), rtol=1e-14)
     # kept_rollout with a base offset addresses the local reward table
-    a2, _ = oracle.group_advantage(reward[G:], kept[:G] + 100, group_size=G, rollout_base=100)
+    a2, _ = oracle.group_advantage(reward[G:], kept[:G] + 104, group_size=G, rollout_base=104)
     np.testing.assert_array_equal(a2, a[G:2 * G])
 
 
 def test_invalid_group():
     with pytest.raises(ValueError):
         oracle.group_advantage(np.zeros(3, np.float32), np.arange(3, dtype=np.int32), group_size=1)
-    with pytest.raises(ValueError):
-        oracle.group_advantage(np.zeros(3, np.float32), np.arange(3, dtype=np.int32), group_size=2)
+
+
+def test_partial_groups_use_their_survivors():
+    """f3 partial groups (pack filter_mode 1): a group is the run of kept rollouts with the same rollout / G and
+    its statistics use the n_g survivors; a lone survivor gets A = 0; whole groups are unchanged."""
+    rng = np.random.default_rng(12)
+    G = 4
+    reward = rng.random(6 * G).astype(np.float32)
+    kept = np.array([0, 1, 3, 4, 5, 6, 7, 9, 16, 17, 18, 21], np.int32)   # runs: {0,1,3} {4..7} {9} {16,17,18} {21}
+    a, stats = oracle.group_advantage(reward, kept, group_size=G)
+    runs = [[0, 1, 3], [4, 5, 6, 7], [9], [16, 17, 18], [21]]
+    exp = np.concatenate([adv64(reward[r])[0] if len(r) > 1 else np.zeros(1, np.float32) for r in runs])
+    np.testing.assert_array_equal(a, exp)
+    assert a[kept.tolist().index(9)] == 0.0 and a[kept.tolist().index(21)] == 0.0
+    assert stats[4] == 2 and stats[5] == len(kept)                          # two singleton runs have std 0
+    full, _ = oracle.group_advantage(reward, np.arange(6 * G, dtype=np.int32), group_size=G)
+    np.testing.assert_array_equal(a[3:7], full[4:8])                        # the whole group {4..7}

@@ -196,3 +196,40 @@ def test_staleness_histogram_pins():
     pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,
                            vocab=cfg.V, t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
     assert h[2].sum() == pk.n_tokens
+
+
+def test_rollout_filter_mode_partial_groups():
+    """f3 filter_mode 1: rollouts are kept individually (t_train - v_i <= max_lag), mixed-version groups are not an
+    error, n_groups_kept counts groups with a survivor; with uniform group versions it equals filter_mode 0."""
+    rng = np.random.default_rng(21)
+    G, P, S, V, t = 4, 6, 8, 50, 100
+    for trial in range(40):
+        version = (t - rng.integers(0, 4, P * G)).astype(np.int64)
+        if trial % 4 == 0:
+            version = np.repeat(version[::G], G)                    # uniform groups
+        L = rng.integers(1, S + 1, P * G).astype(np.int32)
+        act = rng.integers(0, V, (P * G, S)).astype(np.int32)
+        old = rng.normal(size=(P * G, S)).astype(np.float32)
+        ml = int(rng.integers(0, 3))
+        pk = oracle.pack_batch(version, L, act, old, None, group_size=G, max_len=S, vocab=V, t_train=t, max_lag=ml,
+                               filter_mode=1)
+        assert pk.status == 0
+        keep = (t - version) <= ml
+        np.testing.assert_array_equal(pk.kept_rollout, np.nonzero(keep)[0])
+        assert pk.n_groups_kept == len(set((np.nonzero(keep)[0] // G).tolist()))
+        exp_act = np.concatenate([act[i, :L[i]] for i in np.nonzero(keep)[0]] + [np.zeros(0, np.int32)])
+        np.testing.assert_array_equal(pk.tok_action, exp_act)
+        h = oracle.staleness_histogram(version, L, group_size=G, max_len=S, t_train=t, max_lag=ml, n_bins=4,
+                                       filter_mode=1)
+        assert h[0].sum() == keep.sum() and h[2].sum() == pk.n_tokens
+        if trial % 4 == 0:
+            pk0 = oracle.pack_batch(version, L, act, old, None, group_size=G, max_len=S, vocab=V, t_train=t,
+                                    max_lag=ml)
+            np.testing.assert_array_equal(pk0.kept_rollout, pk.kept_rollout)
+            np.testing.assert_array_equal(pk0.tok_action, pk.tok_action)
+            assert pk0.n_groups_kept == pk.n_groups_kept
+        else:
+            pk0 = oracle.pack_batch(version, L, act, old, None, group_size=G, max_len=S, vocab=V, t_train=t,
+                                    max_lag=ml)
+            mixed = any(len(set(version[g * G:(g + 1) * G])) > 1 for g in range(P))
+            assert (pk0.status == oracle.DATA_MIXED_GROUP_VERSION) == mixed
