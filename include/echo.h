@@ -118,6 +118,23 @@ ECHO_API echo_status echo_pack_batch(int32_t n_rollouts, int32_t group_size, int
                                      float* tok_aux, echo_pack_result* result, void* stream);
 
 /*
+ * f3 ("partial-group handling if per-rollout versions ever differ"): echo_pack_batch with a
+ * filter mode.  ECHO_FILTER_GROUP is echo_pack_batch (one decision per group from its uniform version;
+ * MIXED_GROUP_VERSION otherwise).  ECHO_FILTER_ROLLOUT keeps rollout i iff t_train - version[i] <= max_lag, so a
+ * group may keep only some of its rollouts: no MIXED check, n_groups_kept counts the groups with at least one
+ * kept rollout, and echo_group_advantage normalises each group over its survivors.  Same outputs and launches.
+ */
+enum { ECHO_FILTER_GROUP = 0, ECHO_FILTER_ROLLOUT = 1 };
+ECHO_API echo_status echo_pack_batch_v2(int32_t n_rollouts, int32_t group_size, int32_t max_len, int32_t vocab,
+                                        int64_t t_train, int32_t max_lag, int64_t rollout_base,
+                                        const int64_t* version, const int32_t* resp_len,
+                                        const int32_t* action, const float* old_logp, const float* ref_logp,
+                                        const float* aux, int64_t token_capacity,
+                                        int32_t* kept_rollout, int64_t* kept_offset,
+                                        int32_t* tok_slot, int32_t* tok_action, float* tok_old, float* tok_ref,
+                                        float* tok_aux, echo_pack_result* result, int32_t filter_mode, void* stream);
+
+/*
  * f4: PPO-GAE advantages over the per-step `rewards` and `values` of each trajectory (PAPER.md
  * :163-164, the fields "required by PPO and its popular variants", :170-171).  For rollout i, t = L_i-1 .. 0:
  *   delta_t = r_t + gamma V_{t+1} - V_t   (V_{L_i} = bootstrap_value[i]; 0 when bootstrap_value is NULL, i.e.
@@ -133,8 +150,10 @@ ECHO_API echo_status echo_gae_advantage(int32_t n_rollouts, int32_t max_len, con
 
 /*
  * (2) GRPO group-relative advantage (PAPER.md :374 names GRPO; formula SPEC.md :209-213):
- *   for each kept group of G rollouts, in fp64 with round-to-nearest and no FMA contraction:
- *   mean = (sum r)/G, std = sqrt(sum (r - mean)^2 / G) (population), A = (r - mean)/(std + eps),
+ *   for each kept group -- the run of consecutive kept rollouts with the same global id / G: G rollouts, or its
+ *   n_g surviving rollouts after the per-rollout filter of echo_pack_batch_v2 -- in fp64 with round-to-nearest
+ *   and no FMA contraction:
+ *   mean = (sum r)/n_g, std = sqrt(sum (r - mean)^2 / n_g) (population), A = (r - mean)/(std + eps),
  *   rounded to fp32.  Every token of rollout i receives A_i through tok_slot (SPEC.md :209).
  * reward[R]: per-rollout return (sum of its per-step rewards, PAPER.md :164), indexed by local id.
  * kept_rollout / pack: outputs of echo_pack_batch on the same shard.
@@ -266,7 +285,8 @@ ECHO_API echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, in
 /*
  * f3: the staleness histogram of a step (the per-step log's staleness_histogram, SPEC.md :604, and the buffer's
  * version_histogram, SPEC.md :373; staleness = t_train - param_version, PAPER.md :192, :224).  Same rollout inputs
- * and keep rule as echo_pack_batch (a rollout is kept iff its group's first version has t_train - v <= max_lag):
+ * and keep rule as echo_pack_batch_v2 with filter_mode (ECHO_FILTER_GROUP: a rollout is kept iff its group's first
+ * version has t_train - v <= max_lag; ECHO_FILTER_ROLLOUT: iff its own version does):
  *   hist: device int64 [4][n_bins + 2] = {kept rollouts, dropped rollouts, kept tokens, dropped tokens} per bin;
  *   bin 0 counts future versions (lag < 0), bin 1 + lag for 0 <= lag < n_bins, bin n_bins + 1 older rollouts;
  *   tokens = min(max(resp_len, 0), max_len).  Every bin is written (no initialisation needed); integer counts,
@@ -274,7 +294,8 @@ ECHO_API echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, in
  */
 ECHO_API echo_status echo_staleness_histogram(int32_t n_rollouts, int32_t group_size, int32_t max_len,
                                               int64_t t_train, int32_t max_lag, const int64_t* version,
-                                              const int32_t* resp_len, int32_t n_bins, int64_t* hist, void* stream);
+                                              const int32_t* resp_len, int32_t n_bins, int64_t* hist,
+                                              int32_t filter_mode, void* stream);
 
 /*
  * f2: the LM head fused with (3), forward only.  The logits are the LM head's output

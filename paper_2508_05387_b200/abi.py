@@ -26,9 +26,9 @@ PACK_RESULT_BYTES = 32
 # kernels launched per call (for the bench's gpu_launches count)
 LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2,
             "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1, "echo_csr_from_lengths": 2,
-            "echo_lmhead_logp": 2, "echo_staleness_histogram": 1}
+            "echo_lmhead_logp": 2, "echo_staleness_histogram": 1, "echo_pack_batch_v2": 3}
 
-EXPORTS = ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
+EXPORTS = ("echo_pack_batch", "echo_pack_batch_v2", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
            "echo_policy_loss_launch_shape", "echo_token_logp", "echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage",
            "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_csr_from_lengths",
            "echo_lmhead_workspace_bytes", "echo_lmhead_logp", "echo_staleness_histogram", "echo_status_string",
@@ -59,6 +59,8 @@ def _load(path=LIB_PATH):
     i32, i64, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float
     lib.echo_pack_batch.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, P, i64, P, P, P, P, P, P, P, P,
                                     P]
+    lib.echo_pack_batch_v2.argtypes = [i32, i32, i32, i32, i64, i32, i64, P, P, P, P, P, P, i64, P, P, P, P, P, P, P,
+                                       P, i32, P]
     lib.echo_gae_advantage.argtypes = [i32, i32, P, P, P, P, f32, f32, P, P, P]
     lib.echo_gae_advantage.restype = ctypes.c_int
     lib.echo_group_advantage.argtypes = [i32, i32, f32, P, P, i64, P, P, P, P]
@@ -79,13 +81,13 @@ def _load(path=LIB_PATH):
     lib.echo_status_string.restype = ctypes.c_char_p
     lib.echo_abi_version.restype = i32
     lib.echo_csr_from_lengths.argtypes = [i32, P, P, P, P]
-    lib.echo_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P, P]
+    lib.echo_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P, i32, P]
     lib.echo_lmhead_workspace_bytes.argtypes = [i64, i32]
     lib.echo_lmhead_workspace_bytes.restype = ctypes.c_size_t
     lib.echo_lmhead_logp.argtypes = [P, P, i64, i32, i32, P, P, P, P, P]
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
                "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths", "echo_lmhead_logp",
-               "echo_staleness_histogram"):
+               "echo_staleness_histogram", "echo_pack_batch_v2"):
         getattr(lib, fn).restype = ctypes.c_int
     return lib
 
@@ -130,6 +132,18 @@ def echo_pack_batch(n_rollouts, group_size, max_len, vocab, t_train, max_lag, ro
         n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, _p(version), _p(resp_len), _p(action),
         _p(old_logp), _p(ref_logp), _p(aux), token_capacity, _p(kept_rollout), _p(kept_offset), _p(tok_slot),
         _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_aux), _p(result), _s(stream)))
+
+
+ECHO_FILTER_GROUP, ECHO_FILTER_ROLLOUT = 0, 1
+
+
+def echo_pack_batch_v2(n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, version, resp_len,
+                       action, old_logp, ref_logp, token_capacity, kept_rollout, kept_offset, tok_slot, tok_action,
+                       tok_old, tok_ref, result, filter_mode=ECHO_FILTER_GROUP, stream=None, aux=None, tok_aux=None):
+    _check("echo_pack_batch_v2", _lib.echo_pack_batch_v2(
+        n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, _p(version), _p(resp_len), _p(action),
+        _p(old_logp), _p(ref_logp), _p(aux), token_capacity, _p(kept_rollout), _p(kept_offset), _p(tok_slot),
+        _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_aux), _p(result), filter_mode, _s(stream)))
 
 
 def echo_gae_advantage(n_rollouts, max_len, resp_len, rewards, values, bootstrap_value, gamma, lam, adv,
@@ -189,10 +203,10 @@ def echo_csr_from_lengths(n, lengths, kept_offset, tok_slot=None, stream=None):
 
 
 def echo_staleness_histogram(n_rollouts, group_size, max_len, t_train, max_lag, version, resp_len, n_bins, hist,
-                             stream=None):
+                             filter_mode=0, stream=None):
     _check("echo_staleness_histogram", _lib.echo_staleness_histogram(n_rollouts, group_size, max_len, t_train, max_lag,
                                                                       _p(version), _p(resp_len), n_bins, _p(hist),
-                                                                      _s(stream)))
+                                                                      filter_mode, _s(stream)))
 
 
 def echo_lmhead_workspace_bytes(n_rows, vocab) -> int:

@@ -67,8 +67,21 @@ echo_status echo_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_
                             int64_t token_capacity, int32_t* kept_rollout, int64_t* kept_offset, int32_t* tok_slot,
                             int32_t* tok_action, float* tok_old, float* tok_ref, float* tok_aux,
                             echo_pack_result* result, void* stream) {
+  return echo_pack_batch_v2(n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, version, resp_len,
+                            action, old_logp, ref_logp, aux, token_capacity, kept_rollout, kept_offset, tok_slot,
+                            tok_action, tok_old, tok_ref, tok_aux, result, ECHO_FILTER_GROUP, stream);
+}
+
+echo_status echo_pack_batch_v2(int32_t n_rollouts, int32_t group_size, int32_t max_len, int32_t vocab,
+                               int64_t t_train, int32_t max_lag, int64_t rollout_base, const int64_t* version,
+                               const int32_t* resp_len, const int32_t* action, const float* old_logp,
+                               const float* ref_logp, const float* aux, int64_t token_capacity, int32_t* kept_rollout,
+                               int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action, float* tok_old,
+                               float* tok_ref, float* tok_aux, echo_pack_result* result, int32_t filter_mode,
+                               void* stream) {
   if (n_rollouts < 0 || group_size < 2 || max_len < 1 || vocab < 1 || max_lag < 0 || token_capacity < 0)
     return ECHO_ERR_INVALID_ARGUMENT;
+  if (filter_mode != ECHO_FILTER_GROUP && filter_mode != ECHO_FILTER_ROLLOUT) return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rollouts % group_size != 0) return ECHO_ERR_INVALID_ARGUMENT;
   if (rollout_base < 0 || rollout_base + (int64_t)n_rollouts > INT32_MAX) return ECHO_ERR_INVALID_ARGUMENT;
   if (!result || !kept_offset || (n_rollouts > 0 && (!version || !resp_len || !action || !old_logp || !kept_rollout)))
@@ -82,7 +95,7 @@ echo_status echo_pack_batch(int32_t n_rollouts, int32_t group_size, int32_t max_
   return from_cuda(echo::launch_pack(n_rollouts, group_size, max_len, vocab, t_train, max_lag, rollout_base, version,
                                      resp_len, action, old_logp, ref_logp, aux, token_capacity, kept_rollout,
                                      kept_offset, tok_slot, tok_action, tok_old, tok_ref, tok_aux, result,
-                                     static_cast<cudaStream_t>(stream), sms));
+                                     static_cast<cudaStream_t>(stream), sms, filter_mode));
 }
 
 echo_status echo_gae_advantage(int32_t n_rollouts, int32_t max_len, const int32_t* resp_len, const float* rewards,
@@ -252,15 +265,16 @@ echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, i
 
 echo_status echo_staleness_histogram(int32_t n_rollouts, int32_t group_size, int32_t max_len, int64_t t_train,
                                      int32_t max_lag, const int64_t* version, const int32_t* resp_len, int32_t n_bins,
-                                     int64_t* hist, void* stream) {
+                                     int64_t* hist, int32_t filter_mode, void* stream) {
   if (n_rollouts < 0 || group_size < 1 || n_rollouts % group_size != 0 || max_len < 1 || max_lag < 0 ||
-      n_bins < 1 || n_bins > 4096 || !hist || (n_rollouts > 0 && (!version || !resp_len)))
+      n_bins < 1 || n_bins > 4096 || !hist || (n_rollouts > 0 && (!version || !resp_len)) ||
+      (filter_mode != ECHO_FILTER_GROUP && filter_mode != ECHO_FILTER_ROLLOUT))
     return ECHO_ERR_INVALID_ARGUMENT;
   int sms = 0;
   echo_status st = device_sms(&sms);
   if (st != ECHO_OK) return st;
   return from_cuda(echo::launch_staleness_hist(n_rollouts, group_size, max_len, t_train, max_lag, version, resp_len,
-                                               n_bins, hist, static_cast<cudaStream_t>(stream)));
+                                               n_bins, hist, filter_mode, static_cast<cudaStream_t>(stream)));
 }
 
 echo_status echo_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* kept_offset, int32_t* tok_slot,

@@ -41,7 +41,7 @@ cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_tr
                         const float* old_logp, const float* ref_logp, const float* aux, int64_t cap,
                         int32_t* kept_rollout, int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action,
                         float* tok_old, float* tok_ref, float* tok_aux, echo_pack_result* res, cudaStream_t stream,
-                        int num_sms);
+                        int num_sms, int32_t filter_mode = 0);
 
 cudaError_t launch_group_advantage(int32_t G, float eps, int64_t rollout_base, const float* reward,
                                    const int32_t* kept_rollout, const echo_pack_result* pack, float* adv_slot,
@@ -70,7 +70,7 @@ cudaError_t launch_gae(int32_t R, int32_t S, const int32_t* resp_len, const floa
 
 cudaError_t launch_staleness_hist(int32_t R, int32_t G, int32_t S, int64_t t_train, int32_t max_lag,
                                   const int64_t* version, const int32_t* resp_len, int32_t n_bins, int64_t* hist,
-                                  cudaStream_t stream);
+                                  int32_t filter_mode, cudaStream_t stream);
 cudaError_t launch_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* offsets, int32_t* tok_slot,
                                     cudaStream_t stream, int num_sms);
 

@@ -20,8 +20,9 @@ constexpr unsigned long long kNoError = 0xFFFFFFFFFFFFFFFFull;
 __global__ void __launch_bounds__(kScanThreads) pack_scan_kernel(
     int32_t R, int32_t G, int32_t S, int64_t t_train, int32_t max_lag, int64_t rollout_base,
     const int64_t* __restrict__ version, const int32_t* __restrict__ resp_len, int32_t* __restrict__ kept_rollout,
-    int64_t* __restrict__ kept_offset, echo_pack_result* __restrict__ res) {
+    int64_t* __restrict__ kept_offset, echo_pack_result* __restrict__ res, int32_t filter_mode) {
   __shared__ unsigned long long s_err;
+  __shared__ int32_t s_groups;  // filter_mode 1: groups with at least one kept rollout
   __shared__ int32_t s_wkeep[32];
   __shared__ int64_t s_wtok[32];
   __shared__ int32_t s_carry_keep;
@@ -31,6 +32,7 @@ __global__ void __launch_bounds__(kScanThreads) pack_scan_kernel(
     s_err = kNoError;
     s_carry_keep = 0;
     s_carry_tok = 0;
+    s_groups = 0;
   }
   __syncthreads();
 
@@ -45,12 +47,18 @@ __global__ void __launch_bounds__(kScanThreads) pack_scan_kernel(
       unsigned long long key = kNoError;
       if (v > t_train)
         key = (unsigned long long)i * 8 + ECHO_DATA_FUTURE_VERSION;
-      else if (v != v0)
+      else if (filter_mode == 0 && v != v0)
         key = (unsigned long long)i * 8 + ECHO_DATA_MIXED_GROUP_VERSION;
       else if (L < 1 || L > S)
         key = (unsigned long long)i * 8 + ECHO_DATA_BAD_LENGTH;
       if (key != kNoError) atomicMin(&s_err, key);
-      keep = (t_train - v0) <= (int64_t)max_lag ? 1 : 0;
+      keep = (t_train - (filter_mode == 0 ? v0 : v)) <= (int64_t)max_lag ? 1 : 0;
+      if (filter_mode == 1 && keep) {  // the group's first survivor counts the group
+        bool first = true;
+        for (int32_t j = (i / G) * G; j < i; ++j)
+          if ((t_train - version[j]) <= (int64_t)max_lag) first = false;
+        if (first) atomicAdd(&s_groups, 1);
+      }
       len = keep ? (int64_t)min(max(L, 0), S) : 0;
     }
     // block-wide exclusive scan of (keep, len): warp inclusive scan, then warp totals
@@ -102,7 +110,7 @@ __global__ void __launch_bounds__(kScanThreads) pack_scan_kernel(
   if (tid == 0) {
     kept_offset[s_carry_keep] = s_carry_tok;
     res->n_rollouts_kept = s_carry_keep;
-    res->n_groups_kept = s_carry_keep / G;
+    res->n_groups_kept = filter_mode == 0 ? s_carry_keep / G : s_groups;
     res->n_tokens = s_carry_tok;
     res->internal = (int64_t)s_err;
     res->status = ECHO_DATA_OK;
@@ -162,9 +170,9 @@ cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_tr
                         const float* old_logp, const float* ref_logp, const float* aux, int64_t cap,
                         int32_t* kept_rollout, int64_t* kept_offset, int32_t* tok_slot, int32_t* tok_action,
                         float* tok_old, float* tok_ref, float* tok_aux, echo_pack_result* res, cudaStream_t stream,
-                        int num_sms) {
+                        int num_sms, int32_t filter_mode) {
   pack_scan_kernel<<<1, kScanThreads, 0, stream>>>(R, G, S, t_train, max_lag, rollout_base, version, resp_len,
-                                                   kept_rollout, kept_offset, res);
+                                                   kept_rollout, kept_offset, res, filter_mode);
   int grid = R < num_sms * 8 ? (R > 0 ? R : 1) : num_sms * 8;
   pack_gather_kernel<<<grid, 256, 0, stream>>>(S, V, rollout_base, cap, action, old_logp, ref_logp, aux,
                                                kept_rollout, kept_offset, tok_slot, tok_action, tok_old, tok_ref,
@@ -181,14 +189,14 @@ cudaError_t launch_pack(int32_t R, int32_t G, int32_t S, int32_t V, int64_t t_tr
 __global__ void __launch_bounds__(1024) staleness_hist_kernel(int32_t R, int32_t G, int32_t S, int64_t t_train,
                                                               int32_t max_lag, const int64_t* __restrict__ version,
                                                               const int32_t* __restrict__ resp_len, int32_t n_bins,
-                                                              long long* __restrict__ hist) {
+                                                              long long* __restrict__ hist, int32_t filter_mode) {
   extern __shared__ unsigned long long s_hist[];
   const int32_t nb = n_bins + 2;
   for (int32_t k = threadIdx.x; k < 4 * nb; k += blockDim.x) s_hist[k] = 0ull;
   __syncthreads();
   for (int32_t i = threadIdx.x; i < R; i += blockDim.x) {
     const int64_t lag = t_train - version[i];
-    const bool kept = (t_train - version[(i / G) * G]) <= (int64_t)max_lag;
+    const bool kept = (t_train - version[filter_mode == 0 ? (i / G) * G : i]) <= (int64_t)max_lag;
     const int32_t bin = lag < 0 ? 0 : (lag < n_bins ? (int32_t)lag + 1 : n_bins + 1);
     const int32_t L = min(max(resp_len[i], 0), S);
     atomicAdd(&s_hist[(kept ? 0 : 1) * nb + bin], 1ull);
@@ -200,10 +208,10 @@ __global__ void __launch_bounds__(1024) staleness_hist_kernel(int32_t R, int32_t
 
 cudaError_t launch_staleness_hist(int32_t R, int32_t G, int32_t S, int64_t t_train, int32_t max_lag,
                                   const int64_t* version, const int32_t* resp_len, int32_t n_bins, int64_t* hist,
-                                  cudaStream_t stream) {
+                                  int32_t filter_mode, cudaStream_t stream) {
   const size_t smem = (size_t)4 * (n_bins + 2) * sizeof(unsigned long long);
   staleness_hist_kernel<<<1, 1024, smem, stream>>>(R, G, S, t_train, max_lag, version, resp_len, n_bins,
-                                                   reinterpret_cast<long long*>(hist));
+                                                   reinterpret_cast<long long*>(hist), filter_mode);
   return cudaGetLastError();
 }
 

@@ -94,16 +94,19 @@ class LearnerStep:
 
     # ------------------------------------------------------------------ (1) + (2)
     def pack(self, *, t_train: int, max_lag: int, rollout_base: int = 0, n_rollouts: int | None = None,
-             read_back: bool = True) -> PackInfo | None:
+             read_back: bool = True, filter_mode: int = 0) -> PackInfo | None:
+        """(1): filter_mode abi.ECHO_FILTER_GROUP (whole groups, uniform versions) or ECHO_FILTER_ROLLOUT (f3:
+        per-rollout staleness filter; partial groups are normalised over their survivors in advantage())."""
         R = self.R if n_rollouts is None else n_rollouts
         if self._rebalanced:                       # undo a previous step's rebalance()
             for k, v in self._packed.items():
                 setattr(self, k, v)
             self.cap = self._cap0
             self._rebalanced = False
-        abi.echo_pack_batch(R, self.G, self.S, self.V, t_train, max_lag, rollout_base, self.version, self.resp_len,
-                            self.action, self.old_logp, self.ref_logp, self.cap, self.kept_rollout, self.kept_offset,
-                            self.tok_slot, self.tok_action, self.tok_old, self.tok_ref, self.pack_result)
+        abi.echo_pack_batch_v2(R, self.G, self.S, self.V, t_train, max_lag, rollout_base, self.version, self.resp_len,
+                               self.action, self.old_logp, self.ref_logp, self.cap, self.kept_rollout,
+                               self.kept_offset, self.tok_slot, self.tok_action, self.tok_old, self.tok_ref,
+                               self.pack_result, filter_mode)
         self.launches += abi.LAUNCHES["echo_pack_batch"]
         self._R_step, self._base = R, rollout_base
         if not read_back:
@@ -179,12 +182,13 @@ class LearnerStep:
         return plan
 
     def staleness_histogram(self, *, t_train: int, max_lag: int, n_bins: int = 8, n_rollouts: int | None = None,
-                            reduce: bool = True) -> torch.Tensor:
+                            reduce: bool = True, filter_mode: int = 0) -> torch.Tensor:
         """f3: this step's staleness histogram (echo_staleness_histogram; int64 [4, n_bins + 2]: kept / dropped
         rollouts and tokens per lag bin), summed over the ranks of the process group (NCCL all-reduce)."""
         R = self.R if n_rollouts is None else n_rollouts
         h = torch.empty(4, n_bins + 2, dtype=torch.int64, device=self.device)
-        abi.echo_staleness_histogram(R, self.G, self.S, t_train, max_lag, self.version, self.resp_len, n_bins, h)
+        abi.echo_staleness_histogram(R, self.G, self.S, t_train, max_lag, self.version, self.resp_len, n_bins, h,
+                                     filter_mode)
         self.launches += abi.LAUNCHES["echo_staleness_histogram"]
         if reduce:
             allreduce_sum_(h, self.group)

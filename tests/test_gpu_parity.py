@@ -705,3 +705,40 @@ def test_staleness_histogram_bit_exact(name):
                                          max_lag=cfg.max_lag, n_bins=nb)
         np.testing.assert_array_equal(h, ref)
         assert h[2].sum() == info.n_tokens
+
+
+def test_rollout_filter_partial_groups_bit_exact():
+    """f3 partial groups: per-rollout staleness filter (echo_pack_batch_v2, ECHO_FILTER_ROLLOUT) on groups whose
+    rollouts carry different versions; pack, the survivors-only group advantage and the histogram bit-exact."""
+    from paper_2508_05387_b200 import abi
+    cfg = synth.CONFIGS["qwen2.5-7b"]
+    b = synth.make_batch(cfg, 0, 32 * cfg.G, lengths="ragged")
+    rng = np.random.default_rng(3)
+    b.version = (synth.T_TRAIN - rng.integers(0, 5, len(b.version))).astype(np.int64)   # per-rollout versions
+    st = __import__("paper_2508_05387_b200.step", fromlist=["LearnerStep"]).LearnerStep(
+        n_rollouts=len(b.version), group_size=cfg.G, max_len=cfg.S, vocab=cfg.V, dtype=cfg.dtype)
+    st.h2d(*[torch.from_numpy(np.ascontiguousarray(x)) for x in (b.version, b.resp_len, b.reward, b.action,
+                                                                 b.old_logp, b.ref_logp)])
+    info = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag, filter_mode=abi.ECHO_FILTER_ROLLOUT)
+    pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,
+                           vocab=cfg.V, t_train=synth.T_TRAIN, max_lag=cfg.max_lag, filter_mode=1)
+    assert (info.status, info.n_rollouts_kept, info.n_groups_kept, info.n_tokens) == \
+        (pk.status, pk.n_rollouts_kept, pk.n_groups_kept, pk.n_tokens) and info.status == 0
+    assert 0 < pk.n_rollouts_kept < len(b.version) and pk.n_groups_kept <= 32
+    n, nt = pk.n_rollouts_kept, pk.n_tokens
+    np.testing.assert_array_equal(st.kept_rollout[:n].cpu().numpy(), pk.kept_rollout)
+    np.testing.assert_array_equal(st.kept_offset[:n + 1].cpu().numpy(), pk.kept_offset)
+    for a_, b_ in ((st.tok_slot, pk.tok_slot), (st.tok_action, pk.tok_action)):
+        np.testing.assert_array_equal(a_[:nt].cpu().numpy(), b_)
+    assert st.tok_old[:nt].cpu().numpy().tobytes() == pk.tok_old.tobytes()
+    st.advantage()
+    adv, stats = oracle.group_advantage(b.reward, pk.kept_rollout, group_size=cfg.G)
+    assert st.adv_slot[:n].cpu().numpy().tobytes() == adv.tobytes()
+    assert st.adv_stats.cpu().numpy().tobytes() == stats.tobytes()
+    h = st.staleness_histogram(t_train=synth.T_TRAIN, max_lag=cfg.max_lag, n_bins=4, filter_mode=1).cpu().numpy()
+    ref = oracle.staleness_histogram(b.version, b.resp_len, group_size=cfg.G, max_len=cfg.S, t_train=synth.T_TRAIN,
+                                     max_lag=cfg.max_lag, n_bins=4, filter_mode=1)
+    np.testing.assert_array_equal(h, ref)
+    # the same batch under the whole-group filter is a MIXED_GROUP_VERSION error
+    info0 = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
+    assert info0.status == abi.ECHO_DATA_MIXED_GROUP_VERSION
