@@ -742,3 +742,33 @@ def test_rollout_filter_partial_groups_bit_exact():
     # the same batch under the whole-group filter is a MIXED_GROUP_VERSION error
     info0 = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
     assert info0.status == abi.ECHO_DATA_MIXED_GROUP_VERSION
+
+
+def test_loss_kernel_replays_in_a_cuda_graph():
+    """The fused kernel captured in a CUDA graph and replayed (twice, on fresh logits) gives the eager results bit
+    for bit: the in-order row scheduler's counter slot resets itself at the end of every launch."""
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, 2 * cfg.G)
+    st, info = device_step(cfg, b)
+    n = 4096
+    src = fill(st, cfg, 0, n)
+    eager = src.clone()
+    st.loss(eager, 0, kl_coef=cfg.kl_coef)
+    lp_eager = st.tok_logp[:n].clone()
+    work = src.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        st.loss(work, 0, kl_coef=cfg.kl_coef, stream=s)          # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    work.copy_(src)
+    with torch.cuda.graph(g):
+        st.loss(work, 0, kl_coef=cfg.kl_coef)
+    for _ in range(2):
+        work.copy_(src)
+        st.tok_logp.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(work, eager)
+        assert torch.equal(st.tok_logp[:n], lp_eager)
