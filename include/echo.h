@@ -184,6 +184,12 @@ ECHO_API echo_status echo_group_advantage(int32_t n_rollouts, int32_t group_size
  * Outputs per row: tok_logp, tok_loss (l_t, fp32), tok_flags (ECHO_FLAG_*).  A row whose lse, logp, rho,
  *   l_t or c_t is not finite gets ECHO_FLAG_NONFINITE; its gradient row is unspecified.
  * Arithmetic: fp32 accumulation over the bf16/fp32 logits, gradient stored with round-to-nearest-even.
+ *   Deterministic: a row's reduction order depends only on vocab and the kernel, never on the grid, the stream,
+ *   the micro-batch split or which cluster the row is scheduled on.
+ * Concurrency: the kernels hand rows out from a per-launch counter slot (256 slots, round robin, each reset by its
+ *   launch's last CTA), so calls may run concurrently on different streams (up to 256 launches in flight) and are
+ *   capturable in CUDA graphs; a captured graph keeps its slot, so one graph must not be replayed concurrently
+ *   with itself.
  * Launches: 1 kernel (0 when n_rows == 0).
  */
 ECHO_API echo_status echo_policy_loss_fwd_bwd(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
