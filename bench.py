@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="echo", choices=["echo", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "quad_reg", "quad_reg_exact", "oct_reg"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "quad_reg", "quad_reg_exact", "oct_reg", "hex_reg"])
     ap.add_argument("--micro-batch", type=int, default=32768)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--balance", action="store_true",

@@ -19,8 +19,8 @@ ECHO_F32, ECHO_BF16 = 0, 1
 (ECHO_DATA_OK, ECHO_DATA_FUTURE_VERSION, ECHO_DATA_MIXED_GROUP_VERSION, ECHO_DATA_BAD_LENGTH, ECHO_DATA_BAD_ACTION,
  ECHO_DATA_CAPACITY) = range(6)
 ECHO_FLAG_CLIPPED, ECHO_FLAG_NONFINITE = 1, 2
-ECHO_ALGO_AUTO, ECHO_ALGO_ROW_L2, ECHO_ALGO_QUAD_REG, ECHO_ALGO_QUAD_REG_EXACT, ECHO_ALGO_OCT_REG = range(5)
-ALGO_NAMES = {"auto": 0, "row_l2": 1, "quad_reg": 2, "quad_reg_exact": 3, "oct_reg": 4}
+ECHO_ALGO_AUTO, ECHO_ALGO_ROW_L2, ECHO_ALGO_QUAD_REG, ECHO_ALGO_QUAD_REG_EXACT, ECHO_ALGO_OCT_REG, ECHO_ALGO_HEX_REG = range(6)
+ALGO_NAMES = {"auto": 0, "row_l2": 1, "quad_reg": 2, "quad_reg_exact": 3, "oct_reg": 4, "hex_reg": 5}
 PACK_RESULT_BYTES = 32
 
 # kernels launched per call (for the bench's gpu_launches count)

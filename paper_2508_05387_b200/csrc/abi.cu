@@ -26,12 +26,15 @@ echo_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ECHO_OK : ECHO_
 // ECHO_ALGO_AUTO -> the 8-CTA register-resident kernel for bf16 Qwen-size vocabularies (2.91 ms vs 2.94 ms for the
 // 4-CTA one on 32768 x 151936, profiles/), the row kernel otherwise; explicit choices are checked for support.
 echo_status resolve_algo(int32_t dtype, int32_t vocab, int32_t* algo) {
-  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_OCT_REG) return ECHO_ERR_INVALID_ARGUMENT;
+  if (*algo < ECHO_ALGO_AUTO || *algo > ECHO_ALGO_HEX_REG) return ECHO_ERR_INVALID_ARGUMENT;
   const bool quad_ok = echo::quad_supports(dtype, vocab);
   if (*algo == ECHO_ALGO_AUTO)
-    *algo = (echo::oct_supports(dtype, vocab) && vocab >= 16384) ? ECHO_ALGO_OCT_REG : ECHO_ALGO_ROW_L2;
+    *algo = (echo::oct_supports(dtype, vocab) && vocab >= 16384) ? ECHO_ALGO_OCT_REG
+            : echo::hex_supports(dtype, vocab) && vocab >= 16384 ? ECHO_ALGO_HEX_REG
+                                                                  : ECHO_ALGO_ROW_L2;
   if ((*algo == ECHO_ALGO_QUAD_REG || *algo == ECHO_ALGO_QUAD_REG_EXACT) && !quad_ok) return ECHO_ERR_UNSUPPORTED;
   if (*algo == ECHO_ALGO_OCT_REG && !echo::oct_supports(dtype, vocab)) return ECHO_ERR_UNSUPPORTED;
+  if (*algo == ECHO_ALGO_HEX_REG && !echo::hex_supports(dtype, vocab)) return ECHO_ERR_UNSUPPORTED;
   return ECHO_OK;
 }
 
@@ -259,7 +262,7 @@ echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, i
   p.trace_rows = g_trace_rows;
 #endif
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (echo::oct_supports(dtype, vocab) && vocab >= 16384) return from_cuda(echo::launch_quad_logp(p, s, sms, nullptr));
+  if (echo::hex_supports(dtype, vocab) && vocab >= 16384) return from_cuda(echo::launch_quad_logp(p, s, sms, nullptr));
   return from_cuda(echo::launch_row(p, dtype, s, sms, nullptr, false));
 }
 

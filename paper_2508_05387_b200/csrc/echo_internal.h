@@ -60,6 +60,8 @@ int max_active_clusters(const void* fn, int threads, size_t smem, int cluster, i
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape);
 bool quad_supports(int32_t dtype, int32_t V);
 bool oct_supports(int32_t dtype, int32_t V);
+bool hex_supports(int32_t dtype, int32_t V);
+cudaError_t launch_hex(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
 cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
 // Dispatch by algorithm; with shape != nullptr: fill in the launch shape and launch nothing.
 cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms,

@@ -38,6 +38,7 @@ namespace echo {
 // sub-partition) leaves 128 registers per thread, of which 76 hold the thread's 19 vectors of the row.
 //   QCfg<4, 8>: 4-CTA cluster, 2 CTAs (2 rows) per SM  -- ECHO_ALGO_QUAD_REG
 //   QCfg<8, 4>: 8-CTA cluster, 4 CTAs (4 rows) per SM  -- ECHO_ALGO_OCT_REG
+//   QCfg<16, 4>: 16-CTA cluster, 4 CTAs per SM          -- ECHO_ALGO_HEX_REG (vocabularies up to 311296)
 template <int kCtas_, int kWarps_>
 struct QCfg {
   static constexpr int kCtas = kCtas_;                  // CTAs per row (cluster size)
@@ -47,7 +48,7 @@ struct QCfg {
   static constexpr int kChunkElems = kChunk / 2;
   static constexpr int kCtasPerSm = 16 / kWarps;
   static constexpr int kRing = kCtasPerSm == 2 ? 28 : 27;  // staging ring slots (~1.5 slices; fills the SM)
-  static constexpr int kRegChunks = 19;                 // V <= kCtas * 19 * kChunkElems = 155648
+  static constexpr int kRegChunks = 19;                 // V <= kCtas * 19 * kChunkElems (155648 for 8 CTAs)
 };
 constexpr int kQBar = 1;                                // named barrier id
 
@@ -86,6 +87,7 @@ struct __align__(128) QuadSmem {
 // a launch takes the next slot round-robin and its last CTA resets the pair, so no memset is needed.
 constexpr int kSchedSlots = 256;
 __device__ unsigned long long g_row_sched[kSchedSlots][2];
+static std::atomic<uint32_t> g_next_sched_slot{0};  // shared by every tile / mode: one slot per launch
 constexpr int kRowAhead = 3;
   // rows are broadcast this many iterations ahead (<= 4: the table depth)
 
@@ -504,24 +506,29 @@ static cudaError_t launch_t(const LossParams& p, cudaStream_t stream, int num_sm
   const void* fn = (const void*)policy_loss_quad_kernel<C, kMode>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (C::kCtas > 8) {  // 16-CTA clusters are beyond the portable size: opt in
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   int64_t clusters = max_active_clusters(fn, C::kThreads, smem, C::kCtas, num_sms * C::kCtasPerSm / C::kCtas);
   if (clusters > p.n_rows) clusters = p.n_rows;
-  static std::atomic<uint32_t> next_slot{0};
   if (shape) {
     *shape = LaunchShape{(int32_t)(clusters * C::kCtas), C::kCtas, C::kThreads, (int32_t)smem};
     return cudaSuccess;
   }
   LossParams q = p;
-  q.sched_slot = (int32_t)(next_slot.fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
+  q.sched_slot = (int32_t)(g_next_sched_slot.fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
   policy_loss_quad_kernel<C, kMode><<<(unsigned)(clusters * C::kCtas), C::kThreads, smem, stream>>>(q);
   return cudaGetLastError();
 }
 
 using Quad = QCfg<4, 8>;
 using Oct = QCfg<8, 4>;
+using Hex = QCfg<16, 4>;  // 16-CTA cluster (non-portable size): vocabularies up to 311296 (Gemma / Llama-4 class)
 
 bool quad_supports(int32_t dtype, int32_t V) { return supports_t<Quad>(dtype, V); }
 bool oct_supports(int32_t dtype, int32_t V) { return supports_t<Oct>(dtype, V); }
+bool hex_supports(int32_t dtype, int32_t V) { return supports_t<Hex>(dtype, V); }
 
 static bool wants_entropy(const LossParams& p) { return p.entropy_coef > 0.0f || p.tok_entropy != nullptr; }
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape) {
@@ -533,8 +540,14 @@ cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, La
   if (wants_entropy(p)) return launch_t<Oct, kModeEntropy>(p, stream, num_sms, shape);
   return launch_t<Oct, kModeCache>(p, stream, num_sms, shape);
 }
-// forward-only log-probs: the 8-CTA tile (1.93 ms vs 1.97 ms for the 4-CTA one on 32768 x 151936)
+cudaError_t launch_hex(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  if (wants_entropy(p)) return launch_t<Hex, kModeEntropy>(p, stream, num_sms, shape);
+  return launch_t<Hex, kModeCache>(p, stream, num_sms, shape);
+}
+// forward-only log-probs: the 8-CTA tile (1.93 ms vs 1.97 ms for the 4-CTA one on 32768 x 151936), the 16-CTA
+// tile past its vocabulary range
 cudaError_t launch_quad_logp(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  if (!supports_t<Oct>(ECHO_BF16, p.V)) return launch_t<Hex, kModeLogp>(p, stream, num_sms, shape);
   return launch_t<Oct, kModeLogp>(p, stream, num_sms, shape);
 }
 

@@ -772,3 +772,47 @@ def test_loss_kernel_replays_in_a_cuda_graph():
         torch.cuda.synchronize()
         assert torch.equal(work, eager)
         assert torch.equal(st.tok_logp[:n], lp_eager)
+
+
+@pytest.mark.parametrize("V", [155656, 200003, 262144, 311296])
+def test_hex_tile_large_vocabularies(V):
+    """ECHO_ALGO_HEX_REG (16-CTA clusters, AUTO past 155648 columns): fwd+bwd, forward-only log-probs and the
+    entropy variant on Gemma / Llama-4-class vocabularies against the oracle (sampled rows, ragged V)."""
+    import dataclasses
+    from paper_2508_05387_b200 import abi
+    cfg = dataclasses.replace(synth.CONFIGS["qwen3-4b"], V=V)
+    b = synth.make_batch(cfg, 0, cfg.G)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    assert abi.echo_policy_loss_launch_shape(abi.ECHO_BF16, 64, V)["algo"] == abi.ECHO_ALGO_HEX_REG
+    n = 48
+    ld = (V + 7) // 8 * 8
+    logits = fill(st, cfg, 0, n, ld=ld)
+    z = as_oracle_rows(logits)[:, :V]
+    args = (o.pk.tok_action[:n], o.pk.tok_old[:n], o.pk.tok_ref[:n], o.pk.tok_slot[:n], o.adv)
+    N = info.n_tokens
+    # forward-only log-probs first (read-only)
+    lp = torch.empty(n, device="cuda")
+    abi.echo_token_logp(logits, abi.ECHO_BF16, n, V, ld, st.tok_action, lp)
+    lp_ref, _, _ = oracle.token_logp(z, o.pk.tok_action[:n], vocab=V, dtype=oracle.BF16)
+    assert np.all(np.abs(lp.cpu().numpy() - lp_ref) <= 1e-5 + 1e-6 * np.abs(lp_ref))
+    probe = oracle.policy_loss(z, *args, n_global=N, kl_coef=cfg.kl_coef)
+    s = pow2_scale_for(np.abs(probe.dlogits).max())
+    ref = oracle.policy_loss(z, *args, n_global=N, kl_coef=cfg.kl_coef, grad_scale=s)
+    work = logits.clone()
+    st.loss(work, 0, kl_coef=cfg.kl_coef, grad_scale=s)
+    check_rows(d_gpu=work[:, :V].float().cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
+               loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
+               dtype="bf16", old=o.pk.tok_old[:n],
+               cslack=coef_slack(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef, s, N))
+    assert torch.equal(work[:, V:], logits[:, V:])                      # padding untouched
+    # entropy variant on the same rows
+    eta = 0.01
+    ref_e = oracle.policy_loss(z, *args, n_global=N, kl_coef=cfg.kl_coef, grad_scale=s, entropy_coef=eta)
+    ent = torch.empty(st.cap, device="cuda")
+    work = logits.clone()
+    st.loss(work, 0, kl_coef=cfg.kl_coef, grad_scale=s, entropy_coef=eta, tok_entropy=ent)
+    H = ent[:n].cpu().numpy().astype(np.float64)
+    _, lse, _ = oracle.token_logp(z, o.pk.tok_action[:n], vocab=V, dtype=oracle.BF16)
+    hbar = 3e-5 * (1 + np.abs(lse) + np.abs(ref_e.entropy))
+    assert np.all(np.abs(H - ref_e.entropy) <= hbar)
