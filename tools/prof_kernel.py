@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--streams", action="store_true", help="also time torch in-place / copy streams")
     ap.add_argument("--dtype", default=None, choices=[None, "bf16", "f32"], help="override the config's logits dtype")
+    ap.add_argument("--vocab", type=int, default=None, help="override the config's vocabulary size")
     args = ap.parse_args()
 
     import __graft_entry__
@@ -37,6 +38,9 @@ def main():
     from paper_2508_05387_b200.step import LearnerStep
 
     cfg = synth.CONFIGS[args.config]
+    if args.vocab:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, V=args.vocab)
     dt = args.dtype or cfg.dtype
     n_roll = -(-args.rows // cfg.S)
     n_roll = -(-n_roll // cfg.G) * cfg.G
