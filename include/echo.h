@@ -63,7 +63,7 @@ enum { ECHO_FLAG_CLIPPED = 1, ECHO_FLAG_NONFINITE = 2 };
 /* Algorithm selector for echo_policy_loss_fwd_bwd_ex (tests / benchmarks). */
 enum {
   ECHO_ALGO_AUTO = 0,           /* OCT_REG for bf16 with 16384 <= vocab <= 155648, HEX_REG for bf16 up to
-                                   311296, ROW_L2 otherwise */
+                                   311296 and for fp32 up to 155648, ROW_L2 otherwise */
   ECHO_ALGO_ROW_L2 = 1,         /* one 1024-thread CTA per row, two streaming passes, the second re-reads the row
                                    from L2; bf16 or fp32, any vocab */
   ECHO_ALGO_QUAD_REG = 2,       /* 4-CTA cluster per row, each CTA a quarter-row in registers, two CTAs (two rows)
@@ -74,7 +74,8 @@ enum {
   ECHO_ALGO_OCT_REG = 4,        /* as QUAD_REG with an 8-CTA cluster per row (eighth-rows in registers) and four
                                    CTAs (four rows) per SM; the fastest on B200 for Qwen vocabularies */
   ECHO_ALGO_HEX_REG = 5         /* as OCT_REG with a 16-CTA cluster (non-portable cluster size): bf16 vocabularies
-                                   up to 311296 (Gemma / Llama-4 class) */
+                                   up to 311296 (Gemma / Llama-4 class), fp32 logits up to 155648 (the exps are
+                                   kept at full fp32 precision between the passes) */
 };
 
 /* Device-resident result of echo_pack_batch (32 bytes). */

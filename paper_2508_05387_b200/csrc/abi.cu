@@ -262,7 +262,8 @@ echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, i
   p.trace_rows = g_trace_rows;
 #endif
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (echo::hex_supports(dtype, vocab) && vocab >= 16384) return from_cuda(echo::launch_quad_logp(p, s, sms, nullptr));
+  if (echo::hex_supports(dtype, vocab) && vocab >= 16384)
+    return from_cuda(echo::launch_quad_logp(p, dtype, s, sms, nullptr));
   return from_cuda(echo::launch_row(p, dtype, s, sms, nullptr, false));
 }
 

@@ -55,13 +55,14 @@ struct LaunchShape {
 // Per-kernel launchers (policy_loss_{quad,row}.cu); with shape != nullptr: report the shape, launch nothing.
 cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape,
                        bool grad = true);
-cudaError_t launch_quad_logp(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
+cudaError_t launch_quad_logp(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms,
+                             LaunchShape* shape);
 int max_active_clusters(const void* fn, int threads, size_t smem, int cluster, int fallback);
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape);
 bool quad_supports(int32_t dtype, int32_t V);
 bool oct_supports(int32_t dtype, int32_t V);
 bool hex_supports(int32_t dtype, int32_t V);
-cudaError_t launch_hex(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
+cudaError_t launch_hex(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape);
 cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape);
 // Dispatch by algorithm; with shape != nullptr: fill in the launch shape and launch nothing.
 cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cudaStream_t stream, int num_sms,

@@ -58,7 +58,7 @@ cudaError_t launch_policy_loss(const LossParams& p, int32_t dtype, int algo, cud
   if (algo == ECHO_ALGO_QUAD_REG) return launch_quad(p, true, stream, num_sms, shape);
   if (algo == ECHO_ALGO_QUAD_REG_EXACT) return launch_quad(p, false, stream, num_sms, shape);
   if (algo == ECHO_ALGO_OCT_REG) return launch_oct(p, stream, num_sms, shape);
-  if (algo == ECHO_ALGO_HEX_REG) return launch_hex(p, stream, num_sms, shape);
+  if (algo == ECHO_ALGO_HEX_REG) return launch_hex(p, dtype, stream, num_sms, shape);
   return launch_row(p, dtype, stream, num_sms, shape);
 }
 

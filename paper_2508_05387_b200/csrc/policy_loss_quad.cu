@@ -39,13 +39,16 @@ namespace echo {
 //   QCfg<4, 8>: 4-CTA cluster, 2 CTAs (2 rows) per SM  -- ECHO_ALGO_QUAD_REG
 //   QCfg<8, 4>: 8-CTA cluster, 4 CTAs (4 rows) per SM  -- ECHO_ALGO_OCT_REG
 //   QCfg<16, 4>: 16-CTA cluster, 4 CTAs per SM          -- ECHO_ALGO_HEX_REG (vocabularies up to 311296)
-template <int kCtas_, int kWarps_>
+template <int kCtas_, int kWarps_, bool kF32_ = false>
 struct QCfg {
   static constexpr int kCtas = kCtas_;                  // CTAs per row (cluster size)
   static constexpr int kWarps = kWarps_;                // all warps compute; warp 0 also issues the TMA loads
+  static constexpr bool kF32 = kF32_;                   // fp32 logits (else bf16)
+  static constexpr int kElemBytes = kF32 ? 4 : 2;
+  static constexpr int kVecElems = 16 / kElemBytes;     // logits per 16-byte vector
   static constexpr int kThreads = kWarps * 32;
   static constexpr int kChunk = kThreads * 16;          // one 16-byte vector per thread
-  static constexpr int kChunkElems = kChunk / 2;
+  static constexpr int kChunkElems = kChunk / kElemBytes;
   static constexpr int kCtasPerSm = 16 / kWarps;
   static constexpr int kRing = kCtasPerSm == 2 ? 28 : 27;  // staging ring slots (~1.5 slices; fills the SM)
   static constexpr int kRegChunks = 19;                 // V <= kCtas * 19 * kChunkElems (155648 for 8 CTAs)
@@ -101,14 +104,15 @@ struct QuadGeom {
 template <class C>
 ECHO_DEVINL QuadGeom quad_geom(int32_t V, uint32_t rank) {
   QuadGeom g;
-  const int32_t q = ((V + C::kCtas - 1) / C::kCtas + 7) & ~7;
+  constexpr int32_t E = C::kVecElems;
+  const int32_t q = ((V + C::kCtas - 1) / C::kCtas + E - 1) & ~(E - 1);
   g.q = q;
-  // slices start on 8-column boundaries; a rank past the end gets an empty slice [V8, V8)
-  const int32_t v8 = (V + 7) & ~7;
-  g.c0 = min((int32_t)rank * q, v8);
+  // slices start on vector (16-byte) boundaries; a rank past the end gets an empty slice [V_E, V_E)
+  const int32_t vE = (V + E - 1) & ~(E - 1);
+  g.c0 = min((int32_t)rank * q, vE);
   g.c1 = max(min((int32_t)(rank + 1) * q, V), g.c0);
-  const int32_t c1r = (g.c1 + 7) & ~7;
-  g.slice_bytes = (uint32_t)(c1r - g.c0) * 2u;
+  const int32_t c1r = (g.c1 + E - 1) & ~(E - 1);
+  g.slice_bytes = (uint32_t)(c1r - g.c0) * (uint32_t)C::kElemBytes;
   g.nchunks = (int)((g.slice_bytes + C::kChunk - 1) / C::kChunk);
   return g;
 }
@@ -126,7 +130,7 @@ ECHO_DEVINL void quad_issue_chunks(const LossParams& p, const QuadGeom& g, uint3
     const uint32_t bar = full0 + 8 * (j & 3u);
     if (c == 0) mbar_arrive_expect_tx(bar, g.slice_bytes);
     const int64_t row = j == it0 ? row0 : j == it0 + 1 ? row1 : row2;
-    const uint8_t* src = p.logits + row * p.ld_bytes + (int64_t)g.c0 * 2 + (int64_t)c * C::kChunk;
+    const uint8_t* src = p.logits + row * p.ld_bytes + (int64_t)g.c0 * C::kElemBytes + (int64_t)c * C::kChunk;
     const uint32_t nb = min((uint32_t)C::kChunk, g.slice_bytes - c * C::kChunk);
     bulk_g2s(ring0 + (q % C::kRing) * C::kChunk, src, nb, bar, pol);
   }
@@ -208,9 +212,11 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
   }
 
   const float gscale = kGrad ? base_scale(p) : 0.0f;
-  const int32_t col_t = c0 + tid * 8;
+  constexpr int32_t E = C::kVecElems;
+  constexpr uint32_t kNegInf2 = C::kF32 ? 0xFF800000u : kBf16NegInf2;  // -inf in every lane of a word
+  const int32_t col_t = c0 + tid * E;
   const bool last_valid = (uint32_t)(nchunks - 1) * C::kChunk + (uint32_t)tid * 16u < g.slice_bytes;
-  const bool has_tail = (c1 & 7) && (c1 & ~7) >= col_t && ((c1 & ~7) - col_t) % C::kChunkElems == 0;
+  const bool has_tail = (c1 & (E - 1)) && (c1 & ~(E - 1)) >= col_t && ((c1 & ~(E - 1)) - col_t) % C::kChunkElems == 0;
   const int nstore = nchunks - (last_valid ? 0 : 1) - (has_tail ? 1 : 0);
   const uint64_t l2e2 = f2(kLog2e, kLog2e);
   const uint32_t my_off = (uint32_t)tid * 16u;
@@ -309,8 +315,18 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     if (nchunks > 0 && (!last_valid || has_tail)) {
       const uint32_t slot = (slot0 + (uint32_t)nchunks - 1u) % C::kRing;
       const uint32_t addr = ring0 + slot * C::kChunk + my_off;
-      const uint4 w = last_valid ? mask_tail(lds_v4(addr), c1 & 7)
-                                 : make_uint4(kBf16NegInf2, kBf16NegInf2, kBf16NegInf2, kBf16NegInf2);
+      uint4 w = make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+      if (last_valid) {
+        w = lds_v4(addr);
+        if constexpr (C::kF32) {
+          uint32_t* x = &w.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e >= (c1 & 3)) x[e] = 0xFF800000u;
+        } else {
+          w = mask_tail(w, c1 & 7);
+        }
+      }
       sts_v4(addr, w);
     }
 #pragma unroll
@@ -320,7 +336,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
         if (slot >= (uint32_t)C::kRing) slot -= C::kRing;
         v[c] = lds_v4(ring0 + slot * C::kChunk + my_off);
       } else {
-        v[c] = make_uint4(kBf16NegInf2, kBf16NegInf2, kBf16NegInf2, kBf16NegInf2);
+        v[c] = make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
       }
     }
     __syncwarp();
@@ -328,16 +344,28 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     ECHO_TRACE_MARK(p, it, 10);
 
     ECHO_TRACE_MARK(p, it, 1);
-    uint32_t mx2 = kBf16NegInf2;
+    float mx;
+    if constexpr (C::kF32) {
+      float m = -INFINITY;
 #pragma unroll
-    for (int c = 0; c < C::kRegChunks; ++c) mx2 = bmax2(mx2, bmax2(bmax2(v[c].x, v[c].y), bmax2(v[c].z, v[c].w)));
-    const float mx = fmaxf(__uint_as_float(mx2 << 16), __uint_as_float(mx2 & 0xFFFF0000u));
-    const bool own_a = a >= col_t && a < c1 && ((a - col_t) % C::kChunkElems) < 8;
+      for (int c = 0; c < C::kRegChunks; ++c)
+        m = fmaxf(m, fmaxf(fmaxf(__uint_as_float(v[c].x), __uint_as_float(v[c].y)),
+                           fmaxf(__uint_as_float(v[c].z), __uint_as_float(v[c].w))));
+      mx = m;
+    } else {
+      uint32_t mx2 = kBf16NegInf2;
+#pragma unroll
+      for (int c = 0; c < C::kRegChunks; ++c) mx2 = bmax2(mx2, bmax2(bmax2(v[c].x, v[c].y), bmax2(v[c].z, v[c].w)));
+      mx = fmaxf(__uint_as_float(mx2 << 16), __uint_as_float(mx2 & 0xFFFF0000u));
+    }
+    const bool own_a = a >= col_t && a < c1 && ((a - col_t) % C::kChunkElems) < E;
     if (tid == 0 && a >= c0 && a < c1) {  // the action's logit, straight from the ring (valid until barrier 1)
-      const uint32_t off = (uint32_t)(a - c0) * 2u;
+      const uint32_t off = (uint32_t)(a - c0) * (uint32_t)C::kElemBytes;
       uint32_t slot = slot0 + off / C::kChunk;
       if (slot >= (uint32_t)C::kRing) slot -= C::kRing;
-      sm.za = __uint_as_float((uint32_t)lds_u16(ring0 + slot * C::kChunk + off % C::kChunk) << 16);
+      const uint32_t at = ring0 + slot * C::kChunk + off % C::kChunk;
+      if constexpr (C::kF32) sm.za = __uint_as_float(lds_u32(at));
+      else sm.za = __uint_as_float((uint32_t)lds_u16(at) << 16);
     }
 
     // ---- pass 1b
@@ -349,17 +377,31 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
       if (c < nchunks) {
         uint32_t* w = &v[c].x;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < (C::kF32 ? 2 : 4); ++k) {  // two logits per step: a bf16 pair word, or two fp32 words
           // entropy: masked -inf logits are clamped to -1e30 so that e z = 0 (not NaN) here and in pass 2
-          if (kEnt) w[k] = bmax2(w[k], kBf16NegBig2);
-          const uint64_t z2 = bf2_to_f2(w[k]);
+          if constexpr (kEnt) {
+            if constexpr (C::kF32) {
+              w[2 * k] = __float_as_uint(fmaxf(__uint_as_float(w[2 * k]), -1.0e30f));
+              w[2 * k + 1] = __float_as_uint(fmaxf(__uint_as_float(w[2 * k + 1]), -1.0e30f));
+            } else {
+              w[k] = bmax2(w[k], kBf16NegBig2);
+            }
+          }
+          const uint64_t z2 = C::kF32 ? f2(__uint_as_float(w[2 * k]), __uint_as_float(w[2 * k + 1])) : bf2_to_f2(w[k]);
           float e0, e1;
           f2split(fma2(z2, l2e2, nmb2), e0, e1);
           e0 = ex2(e0);
           e1 = ex2(e1);
           s2 = add2(s2, f2(e0, e1));
           if (kEnt) t2 = fma2(f2(e0, e1), z2, t2);
-          if (kStoreExp) w[k] = pack_f16x2(e0, e1);
+          if (kStoreExp) {
+            if constexpr (C::kF32) {  // fp32 logits: the exps replace them at full precision
+              w[2 * k] = __float_as_uint(e0);
+              w[2 * k + 1] = __float_as_uint(e1);
+            } else {
+              w[k] = pack_f16x2(e0, e1);
+            }
+          }
         }
       }
     }
@@ -447,7 +489,7 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
     const uint64_t k2 = kStoreExp ? f2(kt, kt) : f2(-coef, -coef);
     const uint64_t nlse2 = f2(-lse * kLog2e, -lse * kLog2e);
     uint8_t* const row_base = p.logits + row * p.ld_bytes;
-    uint8_t* const dst = row_base + (int64_t)col_t * 2;
+    uint8_t* const dst = row_base + (int64_t)col_t * C::kElemBytes;
     uint4 vtail = make_uint4(0u, 0u, 0u, 0u);
     const uint64_t st_pol = policy_evict_normal();
 #pragma unroll
@@ -455,32 +497,49 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
       if (c < nchunks) {
         uint32_t* w = &v[c].x;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < (C::kF32 ? 2 : 4); ++k) {
           float d0, d1;
           if (kStoreExp) {
-            f2split(mul2(f2(f16lo(w[k]), f16hi(w[k])), k2), d0, d1);
-          } else if (kEnt) {
-            // d = p (e (z - lse + H) - c) = p (e z + k),  k = e (H - lse) - c
-            const uint64_t z2 = bf2_to_f2(w[k]);
+            const uint64_t e2 = C::kF32 ? f2(__uint_as_float(w[2 * k]), __uint_as_float(w[2 * k + 1]))
+                                        : f2(f16lo(w[k]), f16hi(w[k]));
+            f2split(mul2(e2, k2), d0, d1);
+          } else {
+            const uint64_t z2 = C::kF32 ? f2(__uint_as_float(w[2 * k]), __uint_as_float(w[2 * k + 1])) : bf2_to_f2(w[k]);
             float t0, t1;
             f2split(fma2(z2, l2e2, nlse2), t0, t1);
-            f2split(mul2(f2(ex2(t0), ex2(t1)), fma2(z2, ee2, ek2)), d0, d1);
-          } else {
-            float t0, t1;
-            f2split(fma2(bf2_to_f2(w[k]), l2e2, nlse2), t0, t1);
-            f2split(mul2(f2(ex2(t0), ex2(t1)), k2), d0, d1);
+            if (kEnt)  // d = p (e (z - lse + H) - c) = p (e z + k),  k = e (H - lse) - c
+              f2split(mul2(f2(ex2(t0), ex2(t1)), fma2(z2, ee2, ek2)), d0, d1);
+            else
+              f2split(mul2(f2(ex2(t0), ex2(t1)), k2), d0, d1);
           }
-          w[k] = pack_bf16x2(d0, d1);
+          if constexpr (C::kF32) {
+            w[2 * k] = __float_as_uint(d0);
+            w[2 * k + 1] = __float_as_uint(d1);
+          } else {
+            w[k] = pack_bf16x2(d0, d1);
+          }
         }
         if (c < nstore) stg_v4_hint(dst + (int64_t)c * C::kChunk, v[c], st_pol);
         if (c == nchunks - 1) vtail = v[c];
       }
     }
     // one partial store after the unrolled loop (not one copy per chunk): keeps the loop body in the I-cache
-    if (has_tail)
-      store_partial8(reinterpret_cast<__nv_bfloat16*>(dst + (int64_t)(nchunks - 1) * C::kChunk), vtail, c1 & 7);
+    if (has_tail) {
+      uint8_t* const tail = dst + (int64_t)(nchunks - 1) * C::kChunk;
+      if constexpr (C::kF32) {
+        const uint32_t tw[4] = {vtail.x, vtail.y, vtail.z, vtail.w};
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+          if (e < (c1 & 3)) reinterpret_cast<uint32_t*>(tail)[e] = tw[e];
+      } else {
+        store_partial8(reinterpret_cast<__nv_bfloat16*>(tail), vtail, c1 & 7);
+      }
+    }
     ECHO_TRACE_MARK(p, it, 5);
-    if (own_a) reinterpret_cast<__nv_bfloat16*>(row_base)[a] = __float2bfloat16_rn(sm.da);
+    if (own_a) {
+      if constexpr (C::kF32) reinterpret_cast<float*>(row_base)[a] = sm.da;
+      else reinterpret_cast<__nv_bfloat16*>(row_base)[a] = __float2bfloat16_rn(sm.da);
+    }
   }
   cluster_sync_all();
   if (tid == 0) {
@@ -495,9 +554,10 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
 
 template <class C>
 static bool supports_t(int32_t dtype, int32_t V) {
-  if (dtype != ECHO_BF16 || V < 8 * C::kCtas) return false;
-  const int32_t q = ((V + C::kCtas - 1) / C::kCtas + 7) & ~7;
-  return ((int64_t)q * 2 + C::kChunk - 1) / C::kChunk <= C::kRegChunks;
+  constexpr int32_t E = C::kVecElems;
+  if (dtype != (C::kF32 ? ECHO_F32 : ECHO_BF16) || V < E * C::kCtas) return false;
+  const int32_t q = ((V + C::kCtas - 1) / C::kCtas + E - 1) & ~(E - 1);
+  return ((int64_t)q * C::kElemBytes + C::kChunk - 1) / C::kChunk <= C::kRegChunks;
 }
 
 template <class C, int kMode>
@@ -525,10 +585,13 @@ static cudaError_t launch_t(const LossParams& p, cudaStream_t stream, int num_sm
 using Quad = QCfg<4, 8>;
 using Oct = QCfg<8, 4>;
 using Hex = QCfg<16, 4>;  // 16-CTA cluster (non-portable size): vocabularies up to 311296 (Gemma / Llama-4 class)
+using HexF = QCfg<16, 4, true>;  // 16-CTA cluster over fp32 logits: vocabularies up to 155648
 
 bool quad_supports(int32_t dtype, int32_t V) { return supports_t<Quad>(dtype, V); }
 bool oct_supports(int32_t dtype, int32_t V) { return supports_t<Oct>(dtype, V); }
-bool hex_supports(int32_t dtype, int32_t V) { return supports_t<Hex>(dtype, V); }
+bool hex_supports(int32_t dtype, int32_t V) {
+  return dtype == ECHO_F32 ? supports_t<HexF>(dtype, V) : supports_t<Hex>(dtype, V);
+}
 
 static bool wants_entropy(const LossParams& p) { return p.entropy_coef > 0.0f || p.tok_entropy != nullptr; }
 cudaError_t launch_quad(const LossParams& p, bool store_exp, cudaStream_t stream, int num_sms, LaunchShape* shape) {
@@ -540,13 +603,18 @@ cudaError_t launch_oct(const LossParams& p, cudaStream_t stream, int num_sms, La
   if (wants_entropy(p)) return launch_t<Oct, kModeEntropy>(p, stream, num_sms, shape);
   return launch_t<Oct, kModeCache>(p, stream, num_sms, shape);
 }
-cudaError_t launch_hex(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+cudaError_t launch_hex(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  if (dtype == ECHO_F32) {
+    if (wants_entropy(p)) return launch_t<HexF, kModeEntropy>(p, stream, num_sms, shape);
+    return launch_t<HexF, kModeCache>(p, stream, num_sms, shape);
+  }
   if (wants_entropy(p)) return launch_t<Hex, kModeEntropy>(p, stream, num_sms, shape);
   return launch_t<Hex, kModeCache>(p, stream, num_sms, shape);
 }
 // forward-only log-probs: the 8-CTA tile (1.93 ms vs 1.97 ms for the 4-CTA one on 32768 x 151936), the 16-CTA
 // tile past its vocabulary range
-cudaError_t launch_quad_logp(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+cudaError_t launch_quad_logp(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape) {
+  if (dtype == ECHO_F32) return launch_t<HexF, kModeLogp>(p, stream, num_sms, shape);
   if (!supports_t<Oct>(ECHO_BF16, p.V)) return launch_t<Hex, kModeLogp>(p, stream, num_sms, shape);
   return launch_t<Oct, kModeLogp>(p, stream, num_sms, shape);
 }

@@ -816,3 +816,43 @@ def test_hex_tile_large_vocabularies(V):
     _, lse, _ = oracle.token_logp(z, o.pk.tok_action[:n], vocab=V, dtype=oracle.BF16)
     hbar = 3e-5 * (1 + np.abs(lse) + np.abs(ref_e.entropy))
     assert np.all(np.abs(H - ref_e.entropy) <= hbar)
+
+
+@pytest.mark.parametrize("V", [151936, 150001, 32768])
+def test_fp32_cluster_tile(V):
+    """fp32 logits on the 16-CTA tile (AUTO for fp32, 16384 <= V <= 155648): fwd+bwd, forward-only log-probs and
+    the entropy variant against the oracle, ragged V, padding columns untouched."""
+    import dataclasses
+    from paper_2508_05387_b200 import abi
+    cfg = dataclasses.replace(synth.CONFIGS["qwen3-4b"], V=V, dtype="f32")
+    b = synth.make_batch(cfg, 0, cfg.G)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    assert abi.echo_policy_loss_launch_shape(abi.ECHO_F32, 64, V)["algo"] == abi.ECHO_ALGO_HEX_REG
+    n = 40
+    ld = (V + 3) // 4 * 4 + 4
+    logits = fill(st, cfg, 0, n, ld=ld)
+    z = logits[:, :V].cpu().numpy()
+    args = (o.pk.tok_action[:n], o.pk.tok_old[:n], o.pk.tok_ref[:n], o.pk.tok_slot[:n], o.adv)
+    N = info.n_tokens
+    lp = torch.empty(n, device="cuda")
+    abi.echo_token_logp(logits, abi.ECHO_F32, n, V, ld, st.tok_action, lp)
+    lp_ref, lse, _ = oracle.token_logp(z, o.pk.tok_action[:n], vocab=V, dtype=oracle.F32)
+    assert np.all(np.abs(lp.cpu().numpy() - lp_ref) <= 1e-5 + 1e-6 * np.abs(lp_ref))
+    ref = oracle.policy_loss(z, *args, n_global=N, kl_coef=cfg.kl_coef, grad_scale=float(N))
+    work = logits.clone()
+    st.loss(work, 0, kl_coef=cfg.kl_coef, grad_scale=float(N))
+    check_rows(d_gpu=work[:, :V].cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
+               loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref, dtype="f32",
+               old=o.pk.tok_old[:n],
+               cslack=coef_slack(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef,
+                                 float(N), N))
+    assert torch.equal(work[:, V:], logits[:, V:])
+    eta = 0.02
+    ref_e = oracle.policy_loss(z, *args, n_global=N, kl_coef=cfg.kl_coef, grad_scale=float(N), entropy_coef=eta)
+    ent = torch.empty(st.cap, device="cuda")
+    work = logits.clone()
+    st.loss(work, 0, kl_coef=cfg.kl_coef, grad_scale=float(N), entropy_coef=eta, tok_entropy=ent)
+    H = ent[:n].cpu().numpy().astype(np.float64)
+    hbar = 3e-5 * (1 + np.abs(lse) + np.abs(ref_e.entropy))
+    assert np.all(np.abs(H - ref_e.entropy) <= hbar)
