@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "echo_common.cuh"
@@ -419,10 +420,19 @@ cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n
   p.za = ws + (size_t)2 * p.n_vt * n_rows;
   const void* fn = (const void*)lmhead_tile_kernel<kPair>;
   const size_t smem = lm::smem_bytes<kPair>();
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // per device, once: the shared-memory opt-in and the resident-cluster count
+  static std::atomic<int> cached[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
+  int64_t units = dev < 64 ? (int64_t)cached[dev].load(std::memory_order_relaxed) - 1 : -1;
+  if (units < 0) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    units = kPair ? max_active_clusters(fn, lm::kThreads, smem, 2, num_sms / 2) : num_sms;
+    if (dev < 64) cached[dev].store((int)units + 1, std::memory_order_relaxed);
+  }
   const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
-  int64_t units = kPair ? max_active_clusters(fn, lm::kThreads, smem, 2, num_sms / 2) : num_sms;
   if (units > n_tiles) units = n_tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * C::kCtas));

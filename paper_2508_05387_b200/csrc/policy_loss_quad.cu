@@ -91,6 +91,7 @@ struct __align__(128) QuadSmem {
 constexpr int kSchedSlots = 256;
 __device__ unsigned long long g_row_sched[kSchedSlots][2];
 static std::atomic<uint32_t> g_next_sched_slot{0};  // shared by every tile / mode: one slot per launch
+constexpr int kMaxDevices = 64;
 constexpr int kRowAhead = 3;
   // rows are broadcast this many iterations ahead (<= 4: the table depth)
 
@@ -564,13 +565,22 @@ template <class C, int kMode>
 static cudaError_t launch_t(const LossParams& p, cudaStream_t stream, int num_sms, LaunchShape* shape) {
   const size_t smem = sizeof(QuadSmem<C>);
   const void* fn = (const void*)policy_loss_quad_kernel<C, kMode>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // function attributes and the resident-cluster count are per device and never change: set / query once
+  static std::atomic<int> cached[kMaxDevices];  // resident clusters + 1 (0: not yet known)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (C::kCtas > 8) {  // 16-CTA clusters are beyond the portable size: opt in
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  int64_t clusters = dev < kMaxDevices ? (int64_t)cached[dev].load(std::memory_order_relaxed) - 1 : -1;
+  if (clusters < 0) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    if (C::kCtas > 8) {  // 16-CTA clusters are beyond the portable size: opt in
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    clusters = max_active_clusters(fn, C::kThreads, smem, C::kCtas, num_sms * C::kCtasPerSm / C::kCtas);
+    if (dev < kMaxDevices) cached[dev].store((int)clusters + 1, std::memory_order_relaxed);
   }
-  int64_t clusters = max_active_clusters(fn, C::kThreads, smem, C::kCtas, num_sms * C::kCtasPerSm / C::kCtas);
   if (clusters > p.n_rows) clusters = p.n_rows;
   if (shape) {
     *shape = LaunchShape{(int32_t)(clusters * C::kCtas), C::kCtas, C::kThreads, (int32_t)smem};
