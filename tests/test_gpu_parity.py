@@ -856,3 +856,58 @@ def test_fp32_cluster_tile(V):
     H = ent[:n].cpu().numpy().astype(np.float64)
     hbar = 3e-5 * (1 + np.abs(lse) + np.abs(ref_e.entropy))
     assert np.all(np.abs(H - ref_e.entropy) <= hbar)
+
+
+def test_fuzz_shapes_and_tiles():
+    """Randomised shapes through every tile and dtype: V from 16 to 311296 (ragged, empty high-rank slices), row
+    counts below and above the resident clusters, ld padding; sampled rows against the oracle, padding untouched,
+    and the AUTO choice reported by echo_policy_loss_launch_shape."""
+    import dataclasses
+    from paper_2508_05387_b200 import abi
+    rng = np.random.default_rng(2026)
+    base = synth.CONFIGS["qwen3-4b"]
+    cases = []
+    for _ in range(24):
+        dtype = "f32" if rng.random() < 0.3 else "bf16"
+        vmax = 155648 if dtype == "f32" else 311296
+        V = int(np.exp(rng.uniform(np.log(16), np.log(vmax))))
+        algo = None
+        if dtype == "bf16" and rng.random() < 0.4:
+            def ok(a):
+                try:
+                    abi.echo_policy_loss_launch_shape(abi.ECHO_BF16, 8, V, abi.ALGO_NAMES[a])
+                    return True
+                except abi.EchoError:
+                    return False
+            opts = [a for a in ("quad_reg", "quad_reg_exact", "oct_reg", "hex_reg", "row_l2") if ok(a)]
+            algo = opts[int(rng.integers(0, len(opts)))]
+        cases.append((dtype, V, algo, int(rng.integers(1, 300))))
+    for dtype, V, algo_name, n in cases:
+        cfg = dataclasses.replace(base, V=V, dtype=dtype)
+        b = synth.make_batch(cfg, 0, cfg.G)
+        st, info = device_step(cfg, b)
+        o = oracle_step(cfg, b)
+        n = min(n, info.n_tokens)
+        esize = 2 if dtype == "bf16" else 4
+        ld = (V + 7) // 8 * 8 + (8 if rng.random() < 0.5 else 0)
+        logits = fill(st, cfg, 0, n, ld=ld)
+        z = as_oracle_rows(logits)[:, :V]
+        rows = np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, 6)]))
+        args = (o.pk.tok_action[rows], o.pk.tok_old[rows], o.pk.tok_ref[rows], o.pk.tok_slot[rows], o.adv)
+        N = info.n_tokens
+        ref = oracle.policy_loss(z[rows], *args, n_global=N, kl_coef=cfg.kl_coef, grad_scale=float(N))
+        work = logits.clone()
+        algo = None if algo_name is None else abi.ALGO_NAMES[algo_name]
+        try:
+            st.loss(work, 0, kl_coef=cfg.kl_coef, grad_scale=float(N), algo=algo)
+        except abi.EchoError:
+            assert algo is not None          # an explicit tile that cannot take this V; AUTO always can
+            continue
+        torch.cuda.synchronize()
+        d = work[torch.from_numpy(rows).cuda(), :V].float().cpu().numpy()
+        check_rows(d_gpu=d, logp_gpu=st.tok_logp[rows].cpu().numpy(), loss_gpu=st.tok_loss[rows].cpu().numpy(),
+                   flags_gpu=st.tok_flags[rows].cpu().numpy(), ref=ref, dtype=dtype, old=o.pk.tok_old[rows],
+                   cslack=coef_slack(ref, o.pk.tok_old[rows], o.pk.tok_ref[rows], o.adv[o.pk.tok_slot[rows]],
+                                     cfg.kl_coef, float(N), N))
+        if ld > V:
+            assert torch.equal(work[:, V:], logits[:, V:]), (dtype, V, algo_name)
