@@ -866,11 +866,12 @@ def test_fuzz_shapes_and_tiles():
     from paper_2508_05387_b200 import abi
     rng = np.random.default_rng(2026)
     base = synth.CONFIGS["qwen3-4b"]
-    cases = []
-    for _ in range(24):
+    cases, used = [], set()
+    for i in range(64):
         dtype = "f32" if rng.random() < 0.3 else "bf16"
         vmax = 155648 if dtype == "f32" else 311296
-        V = int(np.exp(rng.uniform(np.log(16), np.log(vmax))))
+        # half log-uniform over the whole range (row kernel territory below 16384), half in the cluster tiles' range
+        V = int(np.exp(rng.uniform(np.log(16), np.log(vmax)))) if i % 2 else int(rng.integers(16384, vmax + 1))
         algo = None
         if dtype == "bf16" and rng.random() < 0.4:
             def ok(a):
@@ -911,3 +912,7 @@ def test_fuzz_shapes_and_tiles():
                                      cfg.kl_coef, float(N), N))
         if ld > V:
             assert torch.equal(work[:, V:], logits[:, V:]), (dtype, V, algo_name)
+        used.add((dtype, abi.echo_policy_loss_launch_shape(abi.ECHO_BF16 if dtype == "bf16" else abi.ECHO_F32, n, V,
+                                                           algo or 0)["algo"]))
+    assert {("bf16", abi.ECHO_ALGO_OCT_REG), ("bf16", abi.ECHO_ALGO_HEX_REG), ("f32", abi.ECHO_ALGO_HEX_REG),
+            ("bf16", abi.ECHO_ALGO_ROW_L2), ("f32", abi.ECHO_ALGO_ROW_L2)} <= used, used
