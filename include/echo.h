@@ -10,10 +10,21 @@
  *                                                                  PAPER.md :170-171, :278, :376-382
  *   echo_loss_stats           fixed-order fp64 reduction of the per-token outputs (statistics)
  *
+ * SURVEY.md §8.6 NEXT rows:
+ *   echo_token_logp                   f1  forward-only log-probs (read-only pass)
+ *   echo_lmhead_logp                  f2  LM head fused with the log-prob on the tcgen05 tensor cores
+ *   echo_pack_batch_v2, echo_staleness_histogram, echo_csr_from_lengths
+ *                                     f3  per-rollout staleness filter, staleness histogram, CSR after resharding
+ *   echo_policy_loss_fwd_bwd_v2, echo_gae_advantage
+ *                                     f4  loss variants (per-token advantages / weights, k1/k2/k3, dual clip,
+ *                                         entropy bonus) and PPO-GAE
+ *
  * Conventions shared by every entry point
  *   - All array pointers are DEVICE pointers owned by the caller (e.g. torch allocations).  The library
  *     never allocates, frees, synchronises or calls NCCL; every kernel goes on `stream` (a cudaStream_t,
- *     NULL = the legacy default stream).  Calls are reentrant across streams; no global mutable state.
+ *     NULL = the legacy default stream).  Calls are reentrant across streams.  The only global state is the
+ *     row schedulers' per-launch counter slots (see echo_policy_loss_fwd_bwd) and cached per-device launch
+ *     attributes.
  *   - The returned echo_status covers ARGUMENTS only (null pointers, sizes, alignment, device is not
  *     sm_100) and launch failures (cudaGetLastError -> ECHO_ERR_CUDA).  Data-dependent errors are
  *     reported on the device (echo_pack_result.status, the non-finite counter of echo_loss_stats) so
