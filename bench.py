@@ -195,7 +195,8 @@ def reference_arm(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "prompts": cfg.P, "group_size": cfg.G, "seq_len": cfg.S,
                        "vocab": cfg.V, "max_lag": cfg.max_lag, "kl_coef": cfg.kl_coef},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -364,7 +365,10 @@ def main_echo(args):
                      "traffic": traffic, "peak_source": peak_src, "bytes_per_token": bpt,
                      "kernel": "echo_policy_loss_fwd_bwd", "kernel_ms_avg": avg_full,
                      "kernel_share_of_step": sum(kern) / sum(r["dev_ms"] for r in recs),
-                     "frac_of_8TBps_nominal": achieved / 8000.0},
+                     "frac_of_8TBps_nominal": achieved / 8000.0,
+                     "kernel_ms_p10_p50_p90": _pct(full or kern, (10, 50, 90)),
+                     "kernel_launches_timed": len(full or kern),
+                     "fwd_bwd_only_tokens_per_s": M / (statistics.median(full or kern) * 1e-3) * world},
         "nonfinite_tokens": nonfinite,
         "loss": recs[-1]["loss"],
     }
@@ -429,11 +433,28 @@ def main_echo(args):
         r = oracle_rate(cfg, b, toks_all / args.steps, args.cpu_seconds)
         line["cpu_baseline"] = {
             "value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "oracle",
+            "cpu_model": _cpu_model(),
             "sample": f"pack+advantage of the full batch + fused loss on {r['rows']} rows (a pool of 32 sampled rows, repeated) "
                       f"({r['t_loss']:.1f} s); step extrapolated as t_meta + N * t_row"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+
+
+def _pct(xs, ps):
+    xs = sorted(xs)
+    return [xs[min(len(xs) - 1, int(round(p / 100 * (len(xs) - 1))))] for p in ps]
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def _mb_sizes(N, M):
