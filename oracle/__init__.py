@@ -65,7 +65,7 @@ def lib():
         _lib.echo_ref_scaled_loss.restype = f64
         _lib.echo_ref_csr_from_lengths.argtypes = [i32, P, P, P]
         _lib.echo_ref_csr_from_lengths.restype = ctypes.c_int
-        _lib.echo_ref_lmhead_logp.argtypes = [i64, i32, i32, P, P, P, P, P]
+        _lib.echo_ref_lmhead_logp.argtypes = [i64, i32, i32, P, P, P, P, P, P]
         _lib.echo_ref_lmhead_logp.restype = ctypes.c_int
         _lib.echo_ref_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P, i32]
         _lib.echo_ref_staleness_histogram.restype = ctypes.c_int
@@ -258,8 +258,8 @@ def csr_from_lengths(lengths):
     return off, slot[:total]
 
 
-def lmhead_logp(hidden_bf16, weight_bf16, tok_action):
-    """f2: (logp, lse) of z = hidden @ weight^T (bf16 bit patterns, uint16) at the actions, fp64."""
+def lmhead_logp(hidden_bf16, weight_bf16, tok_action, want_entropy=False):
+    """f2: (logp, lse[, entropy]) of z = hidden @ weight^T (bf16 bit patterns, uint16) at the actions, fp64."""
     h = np.ascontiguousarray(hidden_bf16, np.uint16)
     w = np.ascontiguousarray(weight_bf16, np.uint16)
     n, d = h.shape
@@ -267,10 +267,11 @@ def lmhead_logp(hidden_bf16, weight_bf16, tok_action):
     assert w.shape[1] == d
     logp = np.zeros(n, np.float64)
     lse = np.zeros(n, np.float64)
-    rc = lib().echo_ref_lmhead_logp(n, d, V, _p(h), _p(w), _p(_c(tok_action, np.int32)), _p(logp), _p(lse))
+    ent = np.zeros(n, np.float64) if want_entropy else None
+    rc = lib().echo_ref_lmhead_logp(n, d, V, _p(h), _p(w), _p(_c(tok_action, np.int32)), _p(logp), _p(lse), _p(ent))
     if rc != 0:
         raise ValueError("echo_ref_lmhead_logp: invalid argument")
-    return logp, lse
+    return (logp, lse, ent) if want_entropy else (logp, lse)
 
 
 def staleness_histogram(version, resp_len, *, group_size, max_len, t_train, max_lag, n_bins, filter_mode=0):

@@ -517,9 +517,10 @@ int echo_ref_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* kept_o
  *   z[t, v] = sum_k h[t, k] W[v, k]   (bf16 inputs widened exactly to fp64, fp64 sums in k order)
  *   lse_t = m + log sum_v exp(z[t, v] - m),  m = max_v z[t, v];   logp_t = z[t, a_t] - lse_t
  * hidden: bf16 bit patterns [n_rows x d] row-major; weight: bf16 [vocab x d] row-major.
+ * tok_entropy (nullable): H_t = -sum_v p_v log p_v, p_v = exp(z[t, v] - lse_t) (the f4 entropy of the policy).
  * ====================================================================================== */
 int echo_ref_lmhead_logp(int64_t n_rows, int32_t d, int32_t vocab, const uint16_t* hidden, const uint16_t* weight,
-                         const int32_t* tok_action, double* tok_logp, double* tok_lse) {
+                         const int32_t* tok_action, double* tok_logp, double* tok_lse, double* tok_entropy) {
   if (n_rows < 0 || d < 1 || vocab < 1) return REF_ERR_INVALID_ARGUMENT;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t t = 0; t < n_rows; ++t) {
@@ -537,6 +538,11 @@ int echo_ref_lmhead_logp(int64_t n_rows, int32_t d, int32_t vocab, const uint16_
     double lse = m + log(s);
     tok_logp[t] = z[tok_action[t]] - lse;
     if (tok_lse) tok_lse[t] = lse;
+    if (tok_entropy) {
+      double H = 0.0;
+      for (int64_t v = 0; v < vocab; ++v) H = H - exp(z[v] - lse) * (z[v] - lse);
+      tok_entropy[t] = H;
+    }
     free(z);
   }
   return REF_OK;

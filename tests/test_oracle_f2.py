@@ -61,3 +61,17 @@ def test_probabilities_sum_to_one():
         lp, _ = oracle.lmhead_logp(h, w, np.full(n, a, np.int32))
         tot += np.exp(lp)
     np.testing.assert_allclose(tot, 1.0, rtol=0, atol=1e-12)
+
+
+def test_entropy_of_the_fused_head():
+    """f2 entropy: identity head = the entropy of softmax(h) (the f4 oracle on h as logits); zero head = ln V."""
+    rng = np.random.default_rng(5)
+    n, d = 7, 64
+    h = _bf16(rng.normal(size=(n, d)) * 2)
+    act = rng.integers(0, d, n).astype(np.int32)
+    _, _, ent = oracle.lmhead_logp(h, _bf16(np.eye(d)), act, want_entropy=True)
+    out = oracle.policy_loss(h, act, np.zeros(n, np.float32), None, np.zeros(n, np.int32), np.zeros(1, np.float32),
+                             n_global=n, dtype=oracle.BF16, entropy_coef=0.5)
+    np.testing.assert_allclose(ent, out.entropy, rtol=0, atol=1e-12)
+    _, _, ent0 = oracle.lmhead_logp(h, np.zeros((300, d), np.uint16), act, want_entropy=True)
+    np.testing.assert_allclose(ent0, math.log(300), rtol=0, atol=1e-12)
