@@ -326,14 +326,15 @@ ECHO_API echo_status echo_staleness_histogram(int32_t n_rollouts, int32_t group_
  * are computed without materialising z: a tcgen05 tensor-core GEMM (bf16 inputs, fp32 accumulation in TMEM) whose
  * epilogue reduces each 128 x 256 logits tile to per-row partials, then an ordered merge (deterministic).
  * hidden: device bf16 [n_rows x d] row-major; weight: device bf16 [vocab x d] row-major; both 16-byte aligned,
- * d % 8 == 0.  tok_lse nullable.  workspace: device buffer of echo_lmhead_workspace_bytes(n_rows, vocab) bytes
- * (8 B per row per 256 vocabulary columns + 4 B per row; no initialisation needed).
+ * d % 8 == 0.  tok_lse nullable.  tok_entropy (nullable): H_t = -sum_v p_v log p_v of the row (the f4 entropy),
+ * from a third per-tile partial sum z e^{z - m}.  workspace: device buffer of echo_lmhead_workspace_bytes(n_rows,
+ * vocab) bytes (12 B per row per 256 vocabulary columns + 4 B per row; no initialisation needed).
  * Launches: 2 kernels (0 when n_rows == 0).  ECHO_ERR_INVALID_ARGUMENT on bad sizes / pointers / alignment.
  */
 ECHO_API size_t echo_lmhead_workspace_bytes(int64_t n_rows, int32_t vocab);
 ECHO_API echo_status echo_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d,
                                       int32_t vocab, const int32_t* tok_action, float* tok_logp, float* tok_lse,
-                                      void* workspace, void* stream);
+                                      float* tok_entropy, void* workspace, void* stream);
 
 /* Human-readable name of a status code (static storage). */
 ECHO_API const char* echo_status_string(echo_status status);

@@ -84,7 +84,7 @@ def _load(path=LIB_PATH):
     lib.echo_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P, i32, P]
     lib.echo_lmhead_workspace_bytes.argtypes = [i64, i32]
     lib.echo_lmhead_workspace_bytes.restype = ctypes.c_size_t
-    lib.echo_lmhead_logp.argtypes = [P, P, i64, i32, i32, P, P, P, P, P]
+    lib.echo_lmhead_logp.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P]
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
                "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths", "echo_lmhead_logp",
                "echo_staleness_histogram", "echo_pack_batch_v2"):
@@ -213,9 +213,11 @@ def echo_lmhead_workspace_bytes(n_rows, vocab) -> int:
     return int(_lib.echo_lmhead_workspace_bytes(n_rows, vocab))
 
 
-def echo_lmhead_logp(hidden, weight, n_rows, d, vocab, tok_action, tok_logp, tok_lse, workspace, stream=None):
+def echo_lmhead_logp(hidden, weight, n_rows, d, vocab, tok_action, tok_logp, tok_lse, workspace, stream=None,
+                     tok_entropy=None):
     _check("echo_lmhead_logp", _lib.echo_lmhead_logp(_p(hidden), _p(weight), n_rows, d, vocab, _p(tok_action),
-                                                      _p(tok_logp), _p(tok_lse), _p(workspace), _s(stream)))
+                                                      _p(tok_logp), _p(tok_lse), _p(tok_entropy), _p(workspace),
+                                                      _s(stream)))
 
 
 def echo_loss_stats_workspace_bytes() -> int:

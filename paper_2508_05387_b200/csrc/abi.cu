@@ -297,8 +297,8 @@ size_t echo_lmhead_workspace_bytes(int64_t n_rows, int32_t vocab) {
 }
 
 echo_status echo_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab,
-                             const int32_t* tok_action, float* tok_logp, float* tok_lse, void* workspace,
-                             void* stream) {
+                             const int32_t* tok_action, float* tok_logp, float* tok_lse, float* tok_entropy,
+                             void* workspace, void* stream) {
   if (n_rows < 0 || d < 8 || d % 8 != 0 || vocab < 1) return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rows > 0 && (!hidden || !weight || !aligned16(hidden) || !aligned16(weight) || !tok_action || !tok_logp ||
                      !workspace))
@@ -308,7 +308,7 @@ echo_status echo_lmhead_logp(const void* hidden, const void* weight, int64_t n_r
   if (st != ECHO_OK) return st;
   if (n_rows == 0) return ECHO_OK;
   const cudaError_t e = echo::launch_lmhead_logp(hidden, weight, n_rows, d, vocab, tok_action, tok_logp, tok_lse,
-                                                 workspace, static_cast<cudaStream_t>(stream), sms);
+                                                 tok_entropy, workspace, static_cast<cudaStream_t>(stream), sms);
   if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
   return from_cuda(e);
 }

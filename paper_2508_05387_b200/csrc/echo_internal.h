@@ -79,8 +79,8 @@ cudaError_t launch_csr_from_lengths(int32_t n, const int32_t* lengths, int64_t* 
 
 size_t lmhead_workspace_bytes(int64_t n_rows, int32_t V);
 cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
-                               const int32_t* tok_action, float* tok_logp, float* tok_lse, void* workspace,
-                               cudaStream_t stream, int num_sms);
+                               const int32_t* tok_action, float* tok_logp, float* tok_lse, float* tok_entropy,
+                               void* workspace, cudaStream_t stream, int num_sms);
 
 size_t loss_stats_workspace_bytes();
 cudaError_t launch_loss_stats(int64_t n, const float* tok_loss, const float* tok_logp, const float* tok_old,

@@ -152,10 +152,11 @@ struct LmParams {
   const int32_t* __restrict__ tok_action;
   float* __restrict__ part_m;  // [n_vt][n_rows]
   float* __restrict__ part_s;  // [n_vt][n_rows]
+  float* __restrict__ part_t;  // [n_vt][n_rows]: sum z e^{z - m} (entropy output only)
   float* __restrict__ za;      // [n_rows]
 };
 
-template <bool kPair>
+template <bool kPair, bool kEnt>
 __global__ void __launch_bounds__(lm::kThreads, 1)
     lmhead_tile_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w,
                        const LmParams p) {
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
       const int32_t col0 = vt * kBN;
       mbar_wait_cluster(smem_u32(&sm.tfull[buf]), aph);
       tc_fence_after();
-      float m = -INFINITY, s = 0.0f, za = 0.0f;
+      float m = -INFINITY, s = 0.0f, t = 0.0f, za = 0.0f;
       bool found = false;
 #pragma unroll 1
       for (int c = 0; c < kBN / 32; ++c) {
@@ -274,8 +275,8 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
         const int32_t cb = col0 + c * 32;
         if (cb + 32 > p.V) {  // the vocabulary's last, partial chunk: columns >= V do not exist
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (cb + i >= p.V) r[i] = 0xFF800000u;  // -inf
+          for (int i = 0; i < 32; ++i)  // -inf (-1e30 with the entropy sum, so that e z is 0, not NaN)
+            if (cb + i >= p.V) r[i] = kEnt ? 0xF149F2CAu : 0xFF800000u;
         }
         if ((uint32_t)(a - cb) < 32u) {  // the action's column is in this chunk (one chunk in ~4700)
 #pragma unroll
@@ -287,22 +288,31 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
 #pragma unroll
         for (int i = 1; i < 32; ++i) cm = fmaxf(cm, __uint_as_float(r[i]));
         if (cm > m) {
-          s = (m == -INFINITY) ? 0.0f : s * ex2((m - cm) * kLog2e);
+          const float f = (m == -INFINITY) ? 0.0f : ex2((m - cm) * kLog2e);
+          s *= f;
+          if (kEnt) t *= f;
           m = cm;
         }
         if (m != -INFINITY) {
           // 2^(z log2e - m log2e), packed fp32x2 FMA / add, one MUFU per logit
           const uint64_t nmb2 = f2(-m * kLog2e, -m * kLog2e), l2e2 = f2(kLog2e, kLog2e);
-          uint64_t acc2 = f2(0.0f, 0.0f);
+          uint64_t acc2 = f2(0.0f, 0.0f), acct = f2(0.0f, 0.0f);
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
+            const uint64_t z2 = f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1]));
             float e0, e1;
-            f2split(fma2(f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), l2e2, nmb2), e0, e1);
-            acc2 = add2(acc2, f2(ex2(e0), ex2(e1)));
+            f2split(fma2(z2, l2e2, nmb2), e0, e1);
+            const uint64_t e2 = f2(ex2(e0), ex2(e1));
+            acc2 = add2(acc2, e2);
+            if (kEnt) acct = fma2(e2, z2, acct);
           }
           float lo, hi;
           f2split(acc2, lo, hi);
           s += lo + hi;
+          if (kEnt) {
+            f2split(acct, lo, hi);
+            t += lo + hi;
+          }
         }
       }
       // accumulator read out: hand it back to the MMA warp before the global writes
@@ -315,6 +325,7 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
       if (row_ok) {
         p.part_m[(int64_t)vt * p.n_rows + row] = m;
         p.part_s[(int64_t)vt * p.n_rows + row] = s;
+        if (kEnt) p.part_t[(int64_t)vt * p.n_rows + row] = t;
         if (found) p.za[row] = za;
       }
     }
@@ -333,27 +344,34 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
   }
 }
 
-// One thread per row: merge the row's vocab-tile partials in tile order (deterministic), then logp = z_a - lse.
+// One thread per row: merge the row's vocab-tile partials in tile order (deterministic), then logp = z_a - lse
+// and, with tok_entropy, H = lse - (sum z e) / (sum e).
 __global__ void __launch_bounds__(256) lmhead_finalize_kernel(int64_t n_rows, int32_t V, int32_t n_vt,
                                                               const int32_t* __restrict__ tok_action,
                                                               const float* __restrict__ part_m,
                                                               const float* __restrict__ part_s,
+                                                              const float* __restrict__ part_t,
                                                               const float* __restrict__ za, float* __restrict__ tok_logp,
-                                                              float* __restrict__ tok_lse) {
+                                                              float* __restrict__ tok_lse,
+                                                              float* __restrict__ tok_entropy) {
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (row >= n_rows) return;
-  float m = -INFINITY, s = 0.0f;
+  float m = -INFINITY, s = 0.0f, t = 0.0f;
   for (int32_t vt = 0; vt < n_vt; ++vt) {
     const float mi = part_m[(int64_t)vt * n_rows + row], si = part_s[(int64_t)vt * n_rows + row];
     const float mm = fmaxf(m, mi);
     if (mm == -INFINITY) continue;
-    s = (m == -INFINITY ? 0.0f : s * ex2((m - mm) * kLog2e)) + (mi == -INFINITY ? 0.0f : si * ex2((mi - mm) * kLog2e));
+    const float fa = m == -INFINITY ? 0.0f : ex2((m - mm) * kLog2e);
+    const float fb = mi == -INFINITY ? 0.0f : ex2((mi - mm) * kLog2e);
+    s = s * fa + si * fb;
+    if (tok_entropy) t = t * fa + part_t[(int64_t)vt * n_rows + row] * fb;
     m = mm;
   }
   const float lse = m + logf(s);
   const int32_t a = tok_action[row];
   tok_logp[row] = (a >= 0 && a < V) ? za[row] - lse : NAN;
   if (tok_lse) tok_lse[row] = lse;
+  if (tok_entropy) tok_entropy[row] = lse - t / s;
 }
 
 // ------------------------------------------------------------------------------------------------ host side
@@ -384,12 +402,12 @@ static bool make_map(CUtensorMap* map, const void* base, int64_t rows, int32_t d
 
 size_t lmhead_workspace_bytes(int64_t n_rows, int32_t V) {
   const int64_t n_vt = (V + lm::kBN - 1) / lm::kBN;
-  return (size_t)(2 * n_vt + 1) * (size_t)n_rows * sizeof(float);
+  return (size_t)(3 * n_vt + 1) * (size_t)n_rows * sizeof(float);
 }
 
 cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
-                               const int32_t* tok_action, float* tok_logp, float* tok_lse, void* workspace,
-                               cudaStream_t stream, int num_sms) {
+                               const int32_t* tok_action, float* tok_logp, float* tok_lse, float* tok_entropy,
+                               void* workspace, cudaStream_t stream, int num_sms) {
   if (n_rows == 0) return cudaSuccess;
   CUtensorMap mh, mw;
   if (!make_map(&mh, hidden, n_rows, d, lm::kBM) || !make_map(&mw, weight, V, d, lm::Cfg<
@@ -417,20 +435,22 @@ cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n
   float* ws = static_cast<float*>(workspace);
   p.part_m = ws;
   p.part_s = ws + (size_t)p.n_vt * n_rows;
-  p.za = ws + (size_t)2 * p.n_vt * n_rows;
-  const void* fn = (const void*)lmhead_tile_kernel<kPair>;
+  p.part_t = ws + (size_t)2 * p.n_vt * n_rows;
+  p.za = ws + (size_t)3 * p.n_vt * n_rows;
+  const bool ent = tok_entropy != nullptr;
+  const void* fn = ent ? (const void*)lmhead_tile_kernel<kPair, true> : (const void*)lmhead_tile_kernel<kPair, false>;
   const size_t smem = lm::smem_bytes<kPair>();
   // per device, once: the shared-memory opt-in and the resident-cluster count
-  static std::atomic<int> cached[64];
+  static std::atomic<int> cached[2][64];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  int64_t units = dev < 64 ? (int64_t)cached[dev].load(std::memory_order_relaxed) - 1 : -1;
+  int64_t units = dev < 64 ? (int64_t)cached[ent][dev].load(std::memory_order_relaxed) - 1 : -1;
   if (units < 0) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     units = kPair ? max_active_clusters(fn, lm::kThreads, smem, 2, num_sms / 2) : num_sms;
-    if (dev < 64) cached[dev].store((int)units + 1, std::memory_order_relaxed);
+    if (dev < 64) cached[ent][dev].store((int)units + 1, std::memory_order_relaxed);
   }
   const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
   if (units > n_tiles) units = n_tiles;
@@ -446,10 +466,12 @@ cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kPair>, mh, mw, p);
+  e = ent ? cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kPair, true>, mh, mw, p)
+          : cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kPair, false>, mh, mw, p);
   if (e != cudaSuccess) return e;
   lmhead_finalize_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, stream>>>(n_rows, V, p.n_vt, tok_action, p.part_m,
-                                                                              p.part_s, p.za, tok_logp, tok_lse);
+                                                                              p.part_s, p.part_t, p.za, tok_logp, tok_lse,
+                                                                              tok_entropy);
   return cudaGetLastError();
 }
 

@@ -195,7 +195,7 @@ class LearnerStep:
         return h
 
     # ------------------------------------------------------------------ f2
-    def token_logp_from_hidden(self, hidden, weight, out=None, lse=None, workspace=None):
+    def token_logp_from_hidden(self, hidden, weight, out=None, lse=None, workspace=None, entropy=None):
         """f2: log-probs of the packed actions straight from the final hidden states and the LM-head weight
         (echo_lmhead_logp: the [tokens x vocab] logits are never materialised), e.g. to recompute old_logp or the
         reference model's ref_logp.  hidden: bf16 [n x d] rows aligned with the packed tokens [0, n)."""
@@ -204,7 +204,8 @@ class LearnerStep:
         if workspace is None:
             workspace = torch.empty(abi.echo_lmhead_workspace_bytes(n, self.V) // 4 + 1, dtype=torch.float32,
                                     device=self.device)
-        abi.echo_lmhead_logp(hidden, weight, n, d, self.V, self.tok_action[:n], out, lse, workspace)
+        abi.echo_lmhead_logp(hidden, weight, n, d, self.V, self.tok_action[:n], out, lse, workspace,
+                             tok_entropy=entropy)
         self.launches += abi.LAUNCHES["echo_lmhead_logp"]
         return out
 

@@ -644,7 +644,7 @@ def test_lmhead_logp_edge_cases_and_errors():
             abi.echo_lmhead_logp(h, w, n, kw["d"], kw["vocab"], act, out, None, ws)
     with pytest.raises(abi.EchoError):                                      # misaligned hidden pointer
         abi.echo_lmhead_logp(h.view(-1)[1:].data_ptr(), w, n - 1, d, V, act, out, None, ws)
-    assert abi.echo_lmhead_workspace_bytes(n, V) == (2 * 3 + 1) * n * 4
+    assert abi.echo_lmhead_workspace_bytes(n, V) == (3 * 3 + 1) * n * 4
 
 
 @pytest.mark.parametrize("d", [2048, 3584, 5120])
@@ -916,3 +916,27 @@ def test_fuzz_shapes_and_tiles():
                                                            algo or 0)["algo"]))
     assert {("bf16", abi.ECHO_ALGO_OCT_REG), ("bf16", abi.ECHO_ALGO_HEX_REG), ("f32", abi.ECHO_ALGO_HEX_REG),
             ("bf16", abi.ECHO_ALGO_ROW_L2), ("f32", abi.ECHO_ALGO_ROW_L2)} <= used, used
+
+
+@pytest.mark.parametrize("n,d,V", [(300, 512, 1000), (257, 2560, 151936)])
+def test_lmhead_entropy(n, d, V):
+    """f2 with the entropy output (f4): H_t against the fp64 oracle; logp unchanged by asking for it."""
+    from paper_2508_05387_b200 import abi
+    h, w, act = _lmhead_case(n, d, V, seed=11 + d)
+    ws = torch.empty(abi.echo_lmhead_workspace_bytes(n, V) // 4 + 1, dtype=torch.float32, device="cuda")
+    lp = torch.empty(n, device="cuda")
+    lp0 = torch.empty(n, device="cuda")
+    ent = torch.full((n,), float("nan"), device="cuda")
+    lse = torch.empty(n, device="cuda")
+    abi.echo_lmhead_logp(h, w, n, d, V, act, lp, lse, ws, tok_entropy=ent)
+    abi.echo_lmhead_logp(h, w, n, d, V, act, lp0, None, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(lp, lp0)
+    rows = np.arange(n) if V < 10000 else np.array([0, 1, 128, 255, 256])
+    hb = h[torch.from_numpy(rows).cuda()].cpu().view(torch.int16).numpy().view(np.uint16)
+    wb = w.cpu().view(torch.int16).numpy().view(np.uint16)
+    _, lse_ref, ent_ref = oracle.lmhead_logp(hb, wb, act.cpu().numpy()[rows], want_entropy=True)
+    H = ent.cpu().numpy().astype(np.float64)[rows]
+    tol = _lmhead_tol(hb, wb, np.arange(len(rows))) + 3e-5 * (1 + np.abs(lse_ref) + np.abs(ent_ref))
+    assert np.all(np.abs(H - ent_ref) <= tol), np.max(np.abs(H - ent_ref) / tol)
+    assert np.max(np.abs(H - ent_ref)) <= 2e-4
