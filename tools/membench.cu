@@ -1,4 +1,5 @@
 // membench.cu -- memory-pipeline microbenchmarks for the fused policy-loss design (diagnostic tool, not product).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/membench tools/membench.cu
 //
 // Streams a [rows x V] bf16 buffer in the shapes the kernels use and reports GB/s of algorithmic traffic:
 //   mode 0: TMA ring read only (1 CTA/SM, producer warp + 15 consumer warps LDS + release)
