@@ -40,7 +40,10 @@ namespace echo {
 namespace lm {
 constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16;  // per-CTA token rows, tile vocab columns, K step
 constexpr int kThreads = 192;
-constexpr int kGroupM = 16;  // token tiles per rasterisation group
+#ifndef ECHO_LM_GROUP
+#define ECHO_LM_GROUP 16
+#endif
+constexpr int kGroupM = ECHO_LM_GROUP;  // token tiles per rasterisation group
 constexpr uint32_t kTmemCols = 512;
 
 template <bool kPair>
