@@ -69,6 +69,9 @@ def lib():
         _lib.echo_ref_lmhead_logp.restype = ctypes.c_int
         _lib.echo_ref_staleness_histogram.argtypes = [i32, i32, i32, i64, i32, P, P, i32, P, i32]
         _lib.echo_ref_staleness_histogram.restype = ctypes.c_int
+        _lib.echo_ref_loss_from_logp.argtypes = [i64, P, P, P, P, P, P, P, P, f64, f32, f32, f32, f32, i32, f32, f32,
+                                                 P, P, P]
+        _lib.echo_ref_loss_from_logp.restype = ctypes.c_int
     return _lib
 
 
@@ -285,3 +288,23 @@ def staleness_histogram(version, resp_len, *, group_size, max_len, t_train, max_
     if rc != 0:
         raise ValueError("echo_ref_staleness_histogram: invalid argument")
     return h
+
+
+def loss_from_logp(tok_logp, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, clip_low=0.2, clip_high=0.2,
+                   kl_coef=0.0, grad_scale=1.0, tok_adv=None, tok_weight=None, clip_dual=0.0, kl_estimator=KL_K3,
+                   entropy_coef=0.0, tok_entropy=None):
+    """(4) from fp64 log-probs (f1 / f2 outputs): (loss, flags, coef) per token."""
+    lp = np.ascontiguousarray(tok_logp, np.float64)
+    n = len(lp)
+    ent = None if tok_entropy is None else np.ascontiguousarray(tok_entropy, np.float64)
+    loss = np.zeros(n, np.float64)
+    coef = np.zeros(n, np.float64)
+    flags = np.zeros(n, np.uint8)
+    rc = lib().echo_ref_loss_from_logp(n, _p(lp), _p(ent), _p(_c(tok_old, np.float32)), _p(_c(tok_ref, np.float32)),
+                                       _p(_c(tok_slot, np.int32)), _p(_c(adv_slot, np.float32)),
+                                       _p(_c(tok_adv, np.float32)), _p(_c(tok_weight, np.float32)), float(n_global),
+                                       clip_low, clip_high, clip_dual, kl_coef, kl_estimator, grad_scale, entropy_coef,
+                                       _p(loss), _p(flags), _p(coef))
+    if rc != 0:
+        raise ValueError("echo_ref_loss_from_logp: invalid argument")
+    return loss, flags, coef

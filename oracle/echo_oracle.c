@@ -577,3 +577,49 @@ int echo_ref_staleness_histogram(int32_t n_rollouts, int32_t group_size, int32_t
   }
   return REF_OK;
 }
+
+/* ======================================================================================
+ * (4) from log-probs alone (with f1 / f2, which produce logp without the logits): the per-token surrogate, KL,
+ * entropy bonus and gradient coefficient of echo_ref_policy_loss, restated from logp (and the row entropy H when
+ * entropy_coef > 0):
+ *   rho = exp(logp - old); pg = max(-A rho, -A clip(rho, 1-lo, 1+hi)); dual clip; kl by estimator;
+ *   l_t = pg + beta kl - eta H;  c_t = grad_scale w_t ([not clipped](-A rho) + beta dkl/dlogp)
+ * flags: bit0 clipped, bit1 non-finite (logp, rho, l_t, c_t not representable in fp32).
+ * ====================================================================================== */
+int echo_ref_loss_from_logp(int64_t n, const double* tok_logp, const double* tok_entropy, const float* tok_old,
+                            const float* tok_ref, const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
+                            const float* tok_weight, double n_global, float clip_low, float clip_high, float clip_dual,
+                            float kl_coef, int32_t kl_estimator, float grad_scale, float entropy_coef,
+                            double* tok_loss, uint8_t* tok_flags, double* tok_coef) {
+  if (n < 0 || (kl_coef > 0.0f && !tok_ref) || (entropy_coef > 0.0f && !tok_entropy)) return REF_ERR_INVALID_ARGUMENT;
+  const double lo = 1.0 - (double)clip_low, hi = 1.0 + (double)clip_high;
+  const double beta = (double)kl_coef, dual = (double)clip_dual, eta = (double)entropy_coef;
+  for (int64_t t = 0; t < n; ++t) {
+    double logp = tok_logp[t];
+    double A = adv_of(tok_adv, tok_slot, adv_slot, t);
+    double rho = exp(logp - (double)tok_old[t]);
+    int clipped = (A > 0.0 && rho > hi) || (A < 0.0 && rho < lo);
+    double rho_c = rho < lo ? lo : (rho > hi ? hi : rho);
+    double un = -A * rho, cl = -A * rho_c;
+    double pg = un > cl ? un : cl;
+    if (dual > 1.0 && A < 0.0 && pg > -A * dual) {
+      pg = -A * dual;
+      clipped = 1;
+    }
+    double kl = 0.0, dkl = 0.0;
+    if (beta > 0.0) {
+      double x = (double)tok_ref[t] - logp;
+      kl = kl_value(kl_estimator, x);
+      dkl = kl_dlogp(kl_estimator, x);
+    }
+    double H = eta > 0.0 ? tok_entropy[t] : 0.0;
+    double loss = pg + beta * kl - eta * H;
+    double w = tok_weight ? (double)tok_weight[t] : 1.0 / n_global;
+    double c = (double)grad_scale * w * ((clipped ? 0.0 : -A * rho) + beta * dkl);
+    int nonfinite = !(fits_f32(logp) && fits_f32(rho) && fits_f32(loss) && fits_f32(c));
+    tok_loss[t] = loss;
+    tok_flags[t] = (uint8_t)((clipped ? 1 : 0) | (nonfinite ? 2 : 0));
+    if (tok_coef) tok_coef[t] = c;
+  }
+  return REF_OK;
+}

@@ -188,3 +188,21 @@ def test_finite_differences_entropy(seed):
         assert abs(fd - d) <= 1e-5 * abs(d), (t, v, fd, d)
         checked += 1
     assert checked >= 40
+
+
+@pytest.mark.parametrize("est,dual,eta", [(oracle.KL_K3, 0.0, 0.0), (oracle.KL_K1, 3.0, 0.02), (oracle.KL_K2, 2.0, 0.1)])
+def test_loss_from_logp_equals_the_logits_path(est, dual, eta):
+    """(4) restated from log-probs (for f1 / f2, which never hold the logits) equals echo_ref_policy_loss's loss,
+    flags and coefficient given the same rows."""
+    z, act, old, ref, slot, adv, base = _problem(7)
+    n = len(act)
+    rng = np.random.default_rng(8)
+    tok_adv = (rng.normal(size=n)).astype(np.float32)
+    w = (rng.random(n) + 0.5).astype(np.float32) / n
+    kw = dict(n_global=n, kl_coef=0.05, kl_estimator=est, clip_dual=dual, tok_adv=tok_adv, tok_weight=w,
+              grad_scale=3.0, entropy_coef=eta)
+    full = oracle.policy_loss(z, act, old, ref, slot, adv, **kw)
+    loss, flags, coef = oracle.loss_from_logp(full.logp, old, ref, slot, adv, tok_entropy=full.entropy, **kw)
+    np.testing.assert_array_equal(loss, full.loss)
+    np.testing.assert_array_equal(flags, full.flags)
+    np.testing.assert_array_equal(coef, full.coef)
