@@ -72,6 +72,8 @@ def lib():
         _lib.echo_ref_loss_from_logp.argtypes = [i64, P, P, P, P, P, P, P, P, f64, f32, f32, f32, f32, i32, f32, f32,
                                                  P, P, P]
         _lib.echo_ref_loss_from_logp.restype = ctypes.c_int
+        _lib.echo_ref_lmhead_backward.argtypes = [i64, i32, i32, P, P, P, P, P, P, P, P]
+        _lib.echo_ref_lmhead_backward.restype = ctypes.c_int
     return _lib
 
 
@@ -308,3 +310,31 @@ def loss_from_logp(tok_logp, tok_old, tok_ref, tok_slot, adv_slot, *, n_global, 
     if rc != 0:
         raise ValueError("echo_ref_loss_from_logp: invalid argument")
     return loss, flags, coef
+
+
+def _widen(x):
+    """bf16 bit patterns (uint16) -> exact fp64; float arrays -> fp64."""
+    x = np.asarray(x)
+    if x.dtype == np.uint16:
+        return (x.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return np.ascontiguousarray(x, np.float64)
+
+
+def lmhead_backward(hidden, weight, tok_action, tok_coef, tok_ecoef=None, want_dlogits=False):
+    """f2 backward: (dhidden [n x d], dweight [V x d][, dlogits [n x V]]) in fp64 for z = hidden @ weight^T, with
+    D[t, v] = c_t (delta - p) + e_t p (log p + H).  hidden / weight: bf16 bit patterns (uint16) or floats."""
+    h = np.ascontiguousarray(_widen(hidden))
+    w = np.ascontiguousarray(_widen(weight))
+    n, d = h.shape
+    V = w.shape[0]
+    assert w.shape[1] == d
+    dh = np.zeros((n, d), np.float64)
+    dw = np.zeros((V, d), np.float64)
+    dz = np.zeros((n, V), np.float64) if want_dlogits else None
+    ec = None if tok_ecoef is None else np.ascontiguousarray(tok_ecoef, np.float64)
+    rc = lib().echo_ref_lmhead_backward(n, d, V, _p(h), _p(w), _p(_c(tok_action, np.int32)),
+                                        _p(np.ascontiguousarray(tok_coef, np.float64)), _p(ec), _p(dz), _p(dh),
+                                        _p(dw))
+    if rc != 0:
+        raise ValueError("echo_ref_lmhead_backward: invalid argument")
+    return (dh, dw, dz) if want_dlogits else (dh, dw)

@@ -623,3 +623,66 @@ int echo_ref_loss_from_logp(int64_t n, const double* tok_logp, const double* tok
   }
   return REF_OK;
 }
+
+/* ======================================================================================
+ * f2 backward ("backward recomputes to give dhidden and dW"): the gradient of the step objective
+ * J = sum_t c-weighted l_t through the LM head z = h W^T (PAPER.md :254-261, the learner "performs gradient updates"
+ * on the policy; the logits gradient is (5), PAPER.md :254-256):
+ *   z[t, v] = sum_k h[t, k] W[v, k];  lse_t, p[t, v] = exp(z[t, v] - lse_t), H_t = -sum_v p log p   (as lmhead_logp)
+ *   D[t, v] = c_t (delta_{v, a_t} - p[t, v]) + e_t p[t, v] (log p[t, v] + H_t)      (the (5) row of echo_ref_policy_loss)
+ *   dhidden[t, k] = sum_v D[t, v] W[v, k]      dweight[v, k] = sum_t D[t, v] h[t, k]
+ * c_t = the token's gradient coefficient (echo_ref_loss_from_logp's tok_coef), e_t = grad_scale w_t eta (nullable:
+ * 0).  hidden / weight are fp64 (the bf16 inputs widened exactly by the caller).  dlogits [n x V], dhidden [n x d],
+ * dweight [V x d]: each nullable.  All sums in index order, fp64.
+ * ====================================================================================== */
+int echo_ref_lmhead_backward(int64_t n_rows, int32_t d, int32_t vocab, const double* hidden, const double* weight,
+                             const int32_t* tok_action, const double* tok_coef, const double* tok_ecoef,
+                             double* dlogits, double* dhidden, double* dweight) {
+  if (n_rows < 0 || d < 1 || vocab < 1) return REF_ERR_INVALID_ARGUMENT;
+  double* D = (double*)malloc(sizeof(double) * (size_t)(n_rows > 0 ? n_rows : 1) * (size_t)vocab);
+  if (!D) return REF_ERR_INVALID_ARGUMENT;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t t = 0; t < n_rows; ++t) {
+    double* z = D + t * vocab;
+    double m = -INFINITY;
+    for (int64_t v = 0; v < vocab; ++v) {
+      double acc = 0.0;
+      for (int64_t k = 0; k < d; ++k) acc = acc + hidden[t * d + k] * weight[v * d + k];
+      z[v] = acc;
+      if (acc > m) m = acc;
+    }
+    double s = 0.0;
+    for (int64_t v = 0; v < vocab; ++v) s = s + exp(z[v] - m);
+    double lse = m + log(s);
+    double H = 0.0;
+    for (int64_t v = 0; v < vocab; ++v) H = H - exp(z[v] - lse) * (z[v] - lse);
+    double c = tok_coef[t], e = tok_ecoef ? tok_ecoef[t] : 0.0;
+    for (int64_t v = 0; v < vocab; ++v) {
+      double lp = z[v] - lse, p = exp(lp);
+      double delta = (v == tok_action[t]) ? 1.0 : 0.0;
+      z[v] = c * (delta - p) + e * p * (lp + H); /* D[t, v] overwrites z[t, v] */
+    }
+  }
+  if (dlogits)
+    for (int64_t i = 0; i < n_rows * (int64_t)vocab; ++i) dlogits[i] = D[i];
+  if (dhidden) {
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < n_rows; ++t)
+      for (int64_t k = 0; k < d; ++k) {
+        double acc = 0.0;
+        for (int64_t v = 0; v < vocab; ++v) acc = acc + D[t * vocab + v] * weight[v * d + k];
+        dhidden[t * d + k] = acc;
+      }
+  }
+  if (dweight) {
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < vocab; ++v)
+      for (int64_t k = 0; k < d; ++k) {
+        double acc = 0.0;
+        for (int64_t t = 0; t < n_rows; ++t) acc = acc + D[t * vocab + v] * hidden[t * d + k];
+        dweight[v * d + k] = acc;
+      }
+  }
+  free(D);
+  return REF_OK;
+}
