@@ -52,6 +52,7 @@ def parse():
                     help="f3: token-balanced resharding of the kept rollouts after the stale filter (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-f2", action="store_true", help="skip the f2 fused LM-head measurement")
+    ap.add_argument("--no-f2-train", action="store_true", help="skip the f2 training-step measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-oracle sample duration")
     return ap.parse_args()
 
@@ -425,7 +426,51 @@ def main_echo(args):
                          "flops_per_token": 2.0 * hd * cfg.V},
             "unfused_ms": f2u_ms, "unfused": "torch.matmul (cuBLAS bf16) into the logits buffer + echo_token_logp",
             "speedup_vs_unfused": f2u_ms / f2_ms}
-        del hid, wgt, ws2
+        del ws2
+        # f2 training step through the LM head (LearnerStep.loss_from_hidden: fused forward, loss from logp, D
+        # recomputed on the tensor cores in chunks, cuBLAS dhidden / dweight) against the unfused step (cuBLAS logits,
+        # the fused policy-loss kernel in place, cuBLAS dhidden / dweight)
+        if not args.no_f2_train:
+            chunk = 8192
+            dh = torch.empty(M, hd, dtype=torch.float32, device=dev)
+            dw = torch.empty(cfg.V, hd, dtype=torch.float32, device=dev)
+            dh_u = torch.empty(M, hd, dtype=torch.bfloat16, device=dev)
+            dw_u = torch.empty(cfg.V, hd, dtype=torch.bfloat16, device=dev)
+            scratch = {}
+            kl = cfg.kl_coef
+            t2, t2u = [], []
+            for r in range(5):
+                flush.fill_(float(r))
+                a0 = ev()
+                st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
+                                    chunk_rows=chunk, scratch=scratch)
+                a1 = ev()
+                flush.fill_(float(r))
+                b0 = ev()
+                torch.matmul(hid, wgt.t(), out=logits[:, :cfg.V])
+                st.loss(logits, 0, kl_coef=kl, grad_scale=1.0)
+                torch.matmul(logits[:, :cfg.V], wgt, out=dh_u)     # dh = D W, dW = D^T h (bf16 outputs)
+                torch.matmul(logits[:, :cfg.V].t(), hid, out=dw_u)
+                b1 = ev()
+                torch.cuda.synchronize()
+                if r >= 2:
+                    t2.append(a0.elapsed_time(a1))
+                    t2u.append(b0.elapsed_time(b1))
+            t2_ms, t2u_ms = statistics.median(t2), statistics.median(t2u)
+            fl6 = 6.0 * M * hd * cfg.V
+            line["f2_train_step"] = {
+                "ms_per_micro_batch": t2_ms, "tokens_per_s_per_gpu": M / (t2_ms * 1e-3), "hidden": hd,
+                "chunk_rows": chunk,
+                "roofline": {"bound": "tensor", "achieved": fl6 / (t2_ms * 1e-3) / 1e12, "peak": pk[0],
+                             "unit": "TFLOP/s", "frac": fl6 / (t2_ms * 1e-3) / 1e12 / pk[0], "peak_source": pk[1],
+                             "flops_per_token": 6.0 * hd * cfg.V,
+                             "note": "algorithmic 6 d V flops per token (forward, dh, dW); the recompute of D adds "
+                                     "2 d V more that this figure does not count"},
+                "unfused_ms": t2u_ms,
+                "unfused": "cuBLAS logits (10 GB buffer) + echo_policy_loss_fwd_bwd in place + cuBLAS dh, dW",
+                "speedup_vs_unfused": t2u_ms / t2_ms}
+            del dh, dw, dh_u, dw_u, scratch
+        del hid, wgt
     if plans:
         line["config"]["tokens_per_rank_before"] = plans[-1]["tokens_before"]
         line["config"]["tokens_per_rank_after"] = plans[-1]["tokens_after"]

@@ -13,6 +13,9 @@
  * SURVEY.md §8.6 NEXT rows:
  *   echo_token_logp                   f1  forward-only log-probs (read-only pass)
  *   echo_lmhead_logp                  f2  LM head fused with the log-prob on the tcgen05 tensor cores
+ *   echo_loss_from_logp, echo_lmhead_dlogits, echo_lmhead_backward
+ *                                     f2  training step through the LM head: (4) from logp, D recomputed on the
+ *                                         tensor cores, dhidden / dweight
  *   echo_pack_batch_v2, echo_staleness_histogram, echo_csr_from_lengths
  *                                     f3  per-rollout staleness filter, staleness histogram, CSR after resharding
  *   echo_policy_loss_fwd_bwd_v2, echo_gae_advantage
@@ -335,6 +338,58 @@ ECHO_API size_t echo_lmhead_workspace_bytes(int64_t n_rows, int32_t vocab);
 ECHO_API echo_status echo_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d,
                                       int32_t vocab, const int32_t* tok_action, float* tok_logp, float* tok_lse,
                                       float* tok_entropy, void* workspace, void* stream);
+
+/*
+ * (4) from log-probs alone -- for paths that produce logp without the logits (f2's echo_lmhead_logp, f1): the
+ * clipped surrogate, KL and entropy bonus of echo_policy_loss_fwd_bwd_v2 (PAPER.md :278, :376-382; SPEC.md :219,
+ * :243) evaluated per token from tok_logp (and tok_entropy H_t when cfg->entropy_coef > 0), with the same fp32
+ * scalar arithmetic as the fused kernels' row epilogue:
+ *   rho = exp(logp - old); pg, dual clip, KL estimator as in echo_policy_loss_fwd_bwd_v2; l_t = pg + beta kl - eta H;
+ *   tok_coef[t]  = c_t = grad_scale * w_t * dl_t/dlogp      (the (5) coefficient: dL/dz = c_t (delta - p) + ...)
+ *   tok_ecoef[t] = e_t = grad_scale * w_t * eta              (nullable; the entropy term's factor)
+ *   w_t = tok_weight ? tok_weight[t] : 1 / *n_global.
+ * All arrays are device f32[n_rows] (tok_flags u8) offset to the micro-batch; tok_ref needed iff kl_coef > 0,
+ * tok_entropy iff entropy_coef > 0; cfg is a HOST pointer.  Launches: 1 kernel (0 when n_rows == 0).
+ */
+ECHO_API echo_status echo_loss_from_logp(int64_t n_rows, const float* tok_logp, const float* tok_entropy,
+                                         const float* tok_old, const float* tok_ref, const int32_t* tok_slot,
+                                         const float* adv_slot, const float* tok_adv, const float* tok_weight,
+                                         const double* n_global, const echo_loss_config* cfg, float* tok_loss,
+                                         uint8_t* tok_flags, float* tok_coef, float* tok_ecoef, void* stream);
+
+/*
+ * f2 backward, step 1 ("backward recomputes"): the logits gradient (5) of the LM head's output
+ * z = hidden weight^T, recomputed tile by tile on the tcgen05 tensor cores (the GEMM of echo_lmhead_logp) instead of
+ * being read back from a stored [n_rows x vocab] logits matrix:
+ *   p[t, v] = exp(z[t, v] - tok_lse[t]),
+ *   D[t, v] = tok_coef[t] (delta_{v, a_t} - p) + tok_ecoef[t] p (z[t, v] - tok_lse[t] + tok_entropy[t])
+ * (the (5) row of echo_policy_loss_fwd_bwd_v2; PAPER.md :254-256), stored as bf16 (round to nearest even) into
+ * dlogits [n_rows x ld] row-major, columns vocab..ld-1 untouched.  tok_lse / tok_entropy: echo_lmhead_logp outputs;
+ * tok_coef / tok_ecoef: echo_loss_from_logp outputs (tok_ecoef nullable: no entropy term; tok_entropy read iff
+ * tok_ecoef is set).  hidden / weight as echo_lmhead_logp; ld % 8 == 0, dlogits 16-byte aligned.
+ * Launches: 1 kernel (0 when n_rows == 0).
+ */
+ECHO_API echo_status echo_lmhead_dlogits(const void* hidden, const void* weight, int64_t n_rows, int32_t d,
+                                         int32_t vocab, const int32_t* tok_action, const float* tok_lse,
+                                         const float* tok_coef, const float* tok_ecoef, const float* tok_entropy,
+                                         void* dlogits, int64_t ld, void* stream);
+
+/*
+ * f2 backward ("backward recomputes to give dhidden and dW"; PAPER.md :254-261, the learner
+ * computes the gradients of the policy): for chunks of chunk_rows tokens,
+ *   D_chunk = echo_lmhead_dlogits(...) into dlogits_ws (bf16 [chunk_rows x ld], ld = vocab rounded up to 8)
+ *   dhidden[chunk] = D_chunk weight            (f32 [n_rows x d], overwritten)
+ *   dweight       (+)= D_chunk^T hidden[chunk] (f32 [vocab x d]; accumulate = 0 overwrites, 1 adds to it)
+ * The two products are plain bf16 GEMMs with fp32 accumulation and run in cuBLAS (cublasGemmEx) on the caller's
+ * handle (a cublasHandle_t, e.g. torch.cuda.current_blas_handle(); its stream is set to `stream`, pointer mode to
+ * host); D itself comes from this library's tensor-core kernel.  Deterministic for a fixed chunk_rows and handle.
+ * Launches: per chunk 1 kernel + 2 cuBLAS GEMMs.  With n_rows == 0: dweight zeroed (accumulate = 0) or untouched.
+ */
+ECHO_API echo_status echo_lmhead_backward(const void* hidden, const void* weight, int64_t n_rows, int32_t d,
+                                          int32_t vocab, const int32_t* tok_action, const float* tok_lse,
+                                          const float* tok_coef, const float* tok_ecoef, const float* tok_entropy,
+                                          float* dhidden, float* dweight, int32_t accumulate, void* dlogits_ws,
+                                          int64_t chunk_rows, void* cublas_handle, void* stream);
 
 /* Human-readable name of a status code (static storage). */
 ECHO_API const char* echo_status_string(echo_status status);

@@ -320,16 +320,17 @@ def _widen(x):
     return np.ascontiguousarray(x, np.float64)
 
 
-def lmhead_backward(hidden, weight, tok_action, tok_coef, tok_ecoef=None, want_dlogits=False):
+def lmhead_backward(hidden, weight, tok_action, tok_coef, tok_ecoef=None, want_dlogits=False, want_dweight=True):
     """f2 backward: (dhidden [n x d], dweight [V x d][, dlogits [n x V]]) in fp64 for z = hidden @ weight^T, with
-    D[t, v] = c_t (delta - p) + e_t p (log p + H).  hidden / weight: bf16 bit patterns (uint16) or floats."""
+    D[t, v] = c_t (delta - p) + e_t p (log p + H).  hidden / weight: bf16 bit patterns (uint16) or floats.
+    want_dweight=False skips dweight (None in its place), e.g. for a few rows at a full vocabulary."""
     h = np.ascontiguousarray(_widen(hidden))
     w = np.ascontiguousarray(_widen(weight))
     n, d = h.shape
     V = w.shape[0]
     assert w.shape[1] == d
     dh = np.zeros((n, d), np.float64)
-    dw = np.zeros((V, d), np.float64)
+    dw = np.zeros((V, d), np.float64) if want_dweight else None
     dz = np.zeros((n, V), np.float64) if want_dlogits else None
     ec = None if tok_ecoef is None else np.ascontiguousarray(tok_ecoef, np.float64)
     rc = lib().echo_ref_lmhead_backward(n, d, V, _p(h), _p(w), _p(_c(tok_action, np.int32)),

@@ -17,6 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+LIBS = ["-lcublas"]
 
 
 def sources():
@@ -42,7 +43,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
         return lib
     tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, *FLAGS, *(["-DECHO_TRACE"] if trace else []), "-I", INCLUDE, "-I", CSRC, "-o", tmp,
-           *sources()]
+           *sources(), *LIBS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed ({r.returncode}):\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -26,13 +26,16 @@ PACK_RESULT_BYTES = 32
 # kernels launched per call (for the bench's gpu_launches count)
 LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2,
             "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1, "echo_csr_from_lengths": 2,
-            "echo_lmhead_logp": 2, "echo_staleness_histogram": 1, "echo_pack_batch_v2": 3}
+            "echo_lmhead_logp": 2, "echo_staleness_histogram": 1, "echo_pack_batch_v2": 3,
+            "echo_loss_from_logp": 1, "echo_lmhead_dlogits": 1}
+# echo_lmhead_backward: per chunk 1 libecho kernel + 2 cuBLAS GEMMs (library kernels, not counted here)
+BACKWARD_LAUNCHES_PER_CHUNK = 1
 
 EXPORTS = ("echo_pack_batch", "echo_pack_batch_v2", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
            "echo_policy_loss_launch_shape", "echo_token_logp", "echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage",
            "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_csr_from_lengths",
            "echo_lmhead_workspace_bytes", "echo_lmhead_logp", "echo_staleness_histogram", "echo_status_string",
-           "echo_abi_version")
+           "echo_abi_version", "echo_loss_from_logp", "echo_lmhead_dlogits", "echo_lmhead_backward")
 
 
 ECHO_KL_K3, ECHO_KL_K1, ECHO_KL_K2 = range(3)
@@ -85,9 +88,13 @@ def _load(path=LIB_PATH):
     lib.echo_lmhead_workspace_bytes.argtypes = [i64, i32]
     lib.echo_lmhead_workspace_bytes.restype = ctypes.c_size_t
     lib.echo_lmhead_logp.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P]
+    lib.echo_loss_from_logp.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P]
+    lib.echo_lmhead_dlogits.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, i64, P]
+    lib.echo_lmhead_backward.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, P, i32, P, i64, P, P]
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
                "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths", "echo_lmhead_logp",
-               "echo_staleness_histogram", "echo_pack_batch_v2"):
+               "echo_staleness_histogram", "echo_pack_batch_v2", "echo_loss_from_logp", "echo_lmhead_dlogits",
+               "echo_lmhead_backward"):
         getattr(lib, fn).restype = ctypes.c_int
     return lib
 
@@ -218,6 +225,37 @@ def echo_lmhead_logp(hidden, weight, n_rows, d, vocab, tok_action, tok_logp, tok
     _check("echo_lmhead_logp", _lib.echo_lmhead_logp(_p(hidden), _p(weight), n_rows, d, vocab, _p(tok_action),
                                                       _p(tok_logp), _p(tok_lse), _p(tok_entropy), _p(workspace),
                                                       _s(stream)))
+
+
+def echo_loss_from_logp(n_rows, tok_logp, tok_entropy, tok_old, tok_ref, tok_slot, adv_slot, tok_adv, tok_weight,
+                        n_global, cfg: LossConfig, tok_loss, tok_flags, tok_coef, tok_ecoef=None, stream=None):
+    _check("echo_loss_from_logp", _lib.echo_loss_from_logp(
+        n_rows, _p(tok_logp), _p(tok_entropy), _p(tok_old), _p(tok_ref), _p(tok_slot), _p(adv_slot), _p(tok_adv),
+        _p(tok_weight), _p(n_global), ctypes.byref(cfg), _p(tok_loss), _p(tok_flags), _p(tok_coef), _p(tok_ecoef),
+        _s(stream)))
+
+
+def echo_lmhead_dlogits(hidden, weight, n_rows, d, vocab, tok_action, tok_lse, tok_coef, tok_ecoef, tok_entropy,
+                        dlogits, ld, stream=None):
+    _check("echo_lmhead_dlogits", _lib.echo_lmhead_dlogits(
+        _p(hidden), _p(weight), n_rows, d, vocab, _p(tok_action), _p(tok_lse), _p(tok_coef), _p(tok_ecoef),
+        _p(tok_entropy), _p(dlogits), ld, _s(stream)))
+
+
+def echo_lmhead_dlogits_ld(vocab) -> int:
+    """Row stride (elements) of echo_lmhead_backward's bf16 D chunk buffer: vocab rounded up to 8."""
+    return (vocab + 7) // 8 * 8
+
+
+def echo_lmhead_backward(hidden, weight, n_rows, d, vocab, tok_action, tok_lse, tok_coef, tok_ecoef, tok_entropy,
+                         dhidden, dweight, accumulate, dlogits_ws, chunk_rows, cublas_handle=None, stream=None):
+    if cublas_handle is None:
+        import torch
+        cublas_handle = torch.cuda.current_blas_handle()
+    _check("echo_lmhead_backward", _lib.echo_lmhead_backward(
+        _p(hidden), _p(weight), n_rows, d, vocab, _p(tok_action), _p(tok_lse), _p(tok_coef), _p(tok_ecoef),
+        _p(tok_entropy), _p(dhidden), _p(dweight), int(accumulate), _p(dlogits_ws), chunk_rows, cublas_handle,
+        _s(stream)))
 
 
 def echo_loss_stats_workspace_bytes() -> int:

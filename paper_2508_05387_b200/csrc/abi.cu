@@ -52,7 +52,7 @@ extern "C" ECHO_API void echo_trace_set(unsigned long long* buf, int32_t rows) {
 
 extern "C" {
 
-int32_t echo_abi_version(void) { return 2; }
+int32_t echo_abi_version(void) { return 3; }
 
 const char* echo_status_string(echo_status s) {
   switch (s) {
@@ -309,6 +309,85 @@ echo_status echo_lmhead_logp(const void* hidden, const void* weight, int64_t n_r
   if (n_rows == 0) return ECHO_OK;
   const cudaError_t e = echo::launch_lmhead_logp(hidden, weight, n_rows, d, vocab, tok_action, tok_logp, tok_lse,
                                                  tok_entropy, workspace, static_cast<cudaStream_t>(stream), sms);
+  if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
+  return from_cuda(e);
+}
+
+static bool valid_loss_config(const echo_loss_config* cfg) {
+  return cfg && cfg->clip_low >= 0.0f && cfg->clip_low < 1.0f && cfg->clip_high >= 0.0f && cfg->kl_coef >= 0.0f &&
+         (cfg->clip_dual == 0.0f || cfg->clip_dual > 1.0f) && cfg->kl_estimator >= ECHO_KL_K3 &&
+         cfg->kl_estimator <= ECHO_KL_K2 && cfg->entropy_coef >= 0.0f && cfg->entropy_coef <= FLT_MAX;
+}
+
+echo_status echo_loss_from_logp(int64_t n_rows, const float* tok_logp, const float* tok_entropy, const float* tok_old,
+                                const float* tok_ref, const int32_t* tok_slot, const float* adv_slot,
+                                const float* tok_adv, const float* tok_weight, const double* n_global,
+                                const echo_loss_config* cfg, float* tok_loss, uint8_t* tok_flags, float* tok_coef,
+                                float* tok_ecoef, void* stream) {
+  if (n_rows < 0 || !valid_loss_config(cfg)) return ECHO_ERR_INVALID_ARGUMENT;
+  if (!n_global && !tok_weight) return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows > 0) {
+    if (!tok_logp || !tok_old || !tok_loss || !tok_flags || !tok_coef) return ECHO_ERR_INVALID_ARGUMENT;
+    if (!tok_adv && (!tok_slot || !adv_slot)) return ECHO_ERR_INVALID_ARGUMENT;
+    if (cfg->kl_coef > 0.0f && !tok_ref) return ECHO_ERR_INVALID_ARGUMENT;
+    if (cfg->entropy_coef > 0.0f && !tok_entropy) return ECHO_ERR_INVALID_ARGUMENT;
+  }
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  return from_cuda(echo::launch_loss_from_logp(n_rows, tok_logp, tok_entropy, tok_old, tok_ref, tok_slot, adv_slot,
+                                               tok_adv, tok_weight, n_global, *cfg, tok_loss, tok_flags, tok_coef,
+                                               tok_ecoef, static_cast<cudaStream_t>(stream), sms));
+}
+
+static bool valid_lmhead_shape(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab) {
+  if (n_rows < 0 || d < 8 || d % 8 != 0 || vocab < 1) return false;
+  return n_rows == 0 || (hidden && weight && aligned16(hidden) && aligned16(weight));
+}
+
+echo_status echo_lmhead_dlogits(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab,
+                                const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
+                                const float* tok_ecoef, const float* tok_entropy, void* dlogits, int64_t ld,
+                                void* stream) {
+  if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || ld < vocab || ld % 8 != 0)
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows > 0 && (!tok_action || !tok_lse || !tok_coef || !dlogits || !aligned16(dlogits) ||
+                     (tok_ecoef && !tok_entropy)))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  if (n_rows == 0) return ECHO_OK;
+  const cudaError_t e = echo::launch_lmhead_dlogits(hidden, weight, n_rows, d, vocab, tok_action, tok_lse, tok_coef,
+                                                    tok_ecoef, tok_entropy, dlogits, ld,
+                                                    static_cast<cudaStream_t>(stream), sms);
+  if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
+  return from_cuda(e);
+}
+
+echo_status echo_lmhead_backward(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab,
+                                 const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
+                                 const float* tok_ecoef, const float* tok_entropy, float* dhidden, float* dweight,
+                                 int32_t accumulate, void* dlogits_ws, int64_t chunk_rows, void* cublas_handle,
+                                 void* stream) {
+  if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || chunk_rows < 1 || chunk_rows > INT32_MAX ||
+      !cublas_handle)
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (!dweight || (n_rows > 0 && (!tok_action || !tok_lse || !tok_coef || !dhidden || !dlogits_ws ||
+                                  !aligned16(dlogits_ws) || (tok_ecoef && !tok_entropy))))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  if (n_rows == 0) {
+    if (accumulate) return ECHO_OK;
+    return from_cuda(cudaMemsetAsync(dweight, 0, (size_t)vocab * d * sizeof(float), static_cast<cudaStream_t>(stream)));
+  }
+  int cublas_status = 0;
+  const cudaError_t e = echo::launch_lmhead_backward(hidden, weight, n_rows, d, vocab, tok_action, tok_lse, tok_coef,
+                                                     tok_ecoef, tok_entropy, dhidden, dweight, accumulate != 0,
+                                                     dlogits_ws, chunk_rows, cublas_handle,
+                                                     static_cast<cudaStream_t>(stream), sms, &cublas_status);
   if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
   return from_cuda(e);
 }

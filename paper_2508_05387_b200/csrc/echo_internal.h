@@ -82,6 +82,21 @@ cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n
                                const int32_t* tok_action, float* tok_logp, float* tok_lse, float* tok_entropy,
                                void* workspace, cudaStream_t stream, int num_sms);
 
+cudaError_t launch_lmhead_dlogits(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
+                                  const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
+                                  const float* tok_ecoef, const float* tok_entropy, void* dlogits, int64_t ld,
+                                  cudaStream_t stream, int num_sms);
+cudaError_t launch_lmhead_backward(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
+                                   const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
+                                   const float* tok_ecoef, const float* tok_entropy, float* dhidden, float* dweight,
+                                   bool accumulate, void* dlogits_ws, int64_t chunk_rows, void* cublas_handle,
+                                   cudaStream_t stream, int num_sms, int* cublas_status);
+cudaError_t launch_loss_from_logp(int64_t n, const float* tok_logp, const float* tok_entropy, const float* tok_old,
+                                  const float* tok_ref, const int32_t* tok_slot, const float* adv_slot,
+                                  const float* tok_adv, const float* tok_weight, const double* n_global,
+                                  const echo_loss_config& cfg, float* tok_loss, uint8_t* tok_flags, float* tok_coef,
+                                  float* tok_ecoef, cudaStream_t stream, int num_sms);
+
 size_t loss_stats_workspace_bytes();
 cudaError_t launch_loss_stats(int64_t n, const float* tok_loss, const float* tok_logp, const float* tok_old,
                               const float* tok_ref, const float* tok_weight, const uint8_t* tok_flags, double* ws,

@@ -157,13 +157,22 @@ struct LmParams {
   float* __restrict__ part_s;  // [n_vt][n_rows]
   float* __restrict__ part_t;  // [n_vt][n_rows]: sum z e^{z - m} (entropy output only)
   float* __restrict__ za;      // [n_rows]
+  // dlogits mode (echo_lmhead_dlogits): per-row inputs and the bf16 output D [n_rows x ld]
+  const float* __restrict__ g_lse;
+  const float* __restrict__ g_coef;
+  const float* __restrict__ g_ecoef;    // nullable: no entropy term
+  const float* __restrict__ g_entropy;  // read iff g_ecoef
+  uint16_t* __restrict__ dz;
+  int64_t ld;
 };
 
-template <bool kPair, bool kEnt>
+// kMode: 0 = logp partials, 1 = logp + entropy partials, 2 = dlogits (D written to p.dz)
+template <bool kPair, int kMode>
 __global__ void __launch_bounds__(lm::kThreads, 1)
     lmhead_tile_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w,
                        const LmParams p) {
   using namespace lm;
+  constexpr bool kEnt = kMode == 1, kGrad = kMode == 2;
   using C = Cfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -267,6 +276,54 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
       const bool row_ok = row < p.n_rows;
       const int32_t a = row_ok ? p.tok_action[row] : -1;
       const int32_t col0 = vt * kBN;
+      if constexpr (kGrad) {
+        // D[t, v] = c (delta_{v,a} - p) + e p (z - lse + H) = p (e z + k) + c delta_{v,a},  k = e (H - lse) - c
+        const float lse = row_ok ? p.g_lse[row] : 0.0f, c = row_ok ? p.g_coef[row] : 0.0f;
+        const float e = (row_ok && p.g_ecoef) ? p.g_ecoef[row] : 0.0f;
+        const float H = (row_ok && p.g_ecoef) ? p.g_entropy[row] : 0.0f;
+        const float k = fmaf(e, H - lse, -c);
+        const uint64_t l2e2 = f2(kLog2e, kLog2e), nl2 = f2(-lse * kLog2e, -lse * kLog2e), e2 = f2(e, e), k2 = f2(k, k);
+        uint16_t* drow = p.dz + (row_ok ? row : 0) * p.ld;
+        mbar_wait_cluster(smem_u32(&sm.tfull[buf]), aph);
+        tc_fence_after();
+#pragma unroll 1
+        for (int ch = 0; ch < kBN / 32; ++ch) {
+          const int32_t cb = col0 + ch * 32;
+          if (cb >= p.V) break;  // warp-uniform: nothing left of the vocabulary in this tile
+          uint32_t r[32];
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + ch * 32, r);
+          uint32_t o[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t z2 = f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+            float t0, t1;
+            f2split(fma2(z2, l2e2, nl2), t0, t1);
+            float d0, d1;
+            f2split(mul2(f2(ex2(t0), ex2(t1)), fma2(z2, e2, k2)), d0, d1);
+            if (cb + i == a) d0 += c;
+            if (cb + i + 1 == a) d1 += c;
+            o[i >> 1] = pack_bf16x2(d0, d1);
+          }
+          if (row_ok) {
+            if (cb + 32 <= p.V) {
+              uint4* dst = reinterpret_cast<uint4*>(drow + cb);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (cb + i < p.V) drow[cb + i] = (uint16_t)((i & 1) ? (o[i >> 1] >> 16) : (o[i >> 1] & 0xFFFFu));
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (kPair) mbar_arrive_cluster(tempty_leader + buf * 8u);
+          else mbar_arrive(smem_u32(&sm.tempty[buf]));
+        }
+        continue;
+      }
       mbar_wait_cluster(smem_u32(&sm.tfull[buf]), aph);
       tc_fence_after();
       float m = -INFINITY, s = 0.0f, t = 0.0f, za = 0.0f;
@@ -408,52 +465,36 @@ size_t lmhead_workspace_bytes(int64_t n_rows, int32_t V) {
   return (size_t)(3 * n_vt + 1) * (size_t)n_rows * sizeof(float);
 }
 
-cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
-                               const int32_t* tok_action, float* tok_logp, float* tok_lse, float* tok_entropy,
-                               void* workspace, cudaStream_t stream, int num_sms) {
-  if (n_rows == 0) return cudaSuccess;
+#ifdef ECHO_LMHEAD_SINGLE
+constexpr bool kLmPair = false;
+#else
+constexpr bool kLmPair = true;
+#endif
+
+// Persistent launch of lmhead_tile_kernel<kLmPair, kMode>: one (pair) cluster per resident slot, capped at the tile
+// count.  p's shape fields are filled in here.
+template <int kMode>
+static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams& p, cudaStream_t stream, int num_sms) {
+  using C = lm::Cfg<kLmPair>;
   CUtensorMap mh, mw;
-  if (!make_map(&mh, hidden, n_rows, d, lm::kBM) || !make_map(&mw, weight, V, d, lm::Cfg<
-#ifdef ECHO_LMHEAD_SINGLE
-      false
-#else
-      true
-#endif
-      >::kBRows))
+  if (!make_map(&mh, hidden, p.n_rows, p.d, lm::kBM) || !make_map(&mw, weight, p.V, p.d, C::kBRows))
     return cudaErrorInvalidValue;
-#ifdef ECHO_LMHEAD_SINGLE
-  constexpr bool kPair = false;
-#else
-  constexpr bool kPair = true;
-#endif
-  using C = lm::Cfg<kPair>;
-  LmParams p;
-  p.n_rows = n_rows;
-  p.d = d;
-  p.V = V;
-  p.n_tt = (int32_t)((n_rows + C::kTileRows - 1) / C::kTileRows);
-  p.n_vt = (V + lm::kBN - 1) / lm::kBN;
-  p.n_kb = (d + lm::kBK - 1) / lm::kBK;
-  p.tok_action = tok_action;
-  float* ws = static_cast<float*>(workspace);
-  p.part_m = ws;
-  p.part_s = ws + (size_t)p.n_vt * n_rows;
-  p.part_t = ws + (size_t)2 * p.n_vt * n_rows;
-  p.za = ws + (size_t)3 * p.n_vt * n_rows;
-  const bool ent = tok_entropy != nullptr;
-  const void* fn = ent ? (const void*)lmhead_tile_kernel<kPair, true> : (const void*)lmhead_tile_kernel<kPair, false>;
-  const size_t smem = lm::smem_bytes<kPair>();
+  p.n_tt = (int32_t)((p.n_rows + C::kTileRows - 1) / C::kTileRows);
+  p.n_vt = (p.V + lm::kBN - 1) / lm::kBN;
+  p.n_kb = (p.d + lm::kBK - 1) / lm::kBK;
+  const void* fn = (const void*)lmhead_tile_kernel<kLmPair, kMode>;
+  const size_t smem = lm::smem_bytes<kLmPair>();
   // per device, once: the shared-memory opt-in and the resident-cluster count
-  static std::atomic<int> cached[2][64];
+  static std::atomic<int> cached[64];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  int64_t units = dev < 64 ? (int64_t)cached[ent][dev].load(std::memory_order_relaxed) - 1 : -1;
+  int64_t units = dev < 64 ? (int64_t)cached[dev].load(std::memory_order_relaxed) - 1 : -1;
   if (units < 0) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    units = kPair ? max_active_clusters(fn, lm::kThreads, smem, 2, num_sms / 2) : num_sms;
-    if (dev < 64) cached[ent][dev].store((int)units + 1, std::memory_order_relaxed);
+    units = kLmPair ? max_active_clusters(fn, lm::kThreads, smem, 2, num_sms / 2) : num_sms;
+    if (dev < 64) cached[dev].store((int)units + 1, std::memory_order_relaxed);
   }
   const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
   if (units > n_tiles) units = n_tiles;
@@ -469,13 +510,50 @@ cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  e = ent ? cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kPair, true>, mh, mw, p)
-          : cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kPair, false>, mh, mw, p);
+  return cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kLmPair, kMode>, mh, mw, p);
+}
+
+cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
+                               const int32_t* tok_action, float* tok_logp, float* tok_lse, float* tok_entropy,
+                               void* workspace, cudaStream_t stream, int num_sms) {
+  if (n_rows == 0) return cudaSuccess;
+  LmParams p{};
+  p.n_rows = n_rows;
+  p.d = d;
+  p.V = V;
+  p.tok_action = tok_action;
+  const int32_t n_vt = (V + lm::kBN - 1) / lm::kBN;
+  float* ws = static_cast<float*>(workspace);
+  p.part_m = ws;
+  p.part_s = ws + (size_t)n_vt * n_rows;
+  p.part_t = ws + (size_t)2 * n_vt * n_rows;
+  p.za = ws + (size_t)3 * n_vt * n_rows;
+  const cudaError_t e = tok_entropy ? launch_tile<1>(hidden, weight, p, stream, num_sms)
+                                    : launch_tile<0>(hidden, weight, p, stream, num_sms);
   if (e != cudaSuccess) return e;
-  lmhead_finalize_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, stream>>>(n_rows, V, p.n_vt, tok_action, p.part_m,
+  lmhead_finalize_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, stream>>>(n_rows, V, n_vt, tok_action, p.part_m,
                                                                               p.part_s, p.part_t, p.za, tok_logp, tok_lse,
                                                                               tok_entropy);
   return cudaGetLastError();
+}
+
+cudaError_t launch_lmhead_dlogits(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
+                                  const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
+                                  const float* tok_ecoef, const float* tok_entropy, void* dlogits, int64_t ld,
+                                  cudaStream_t stream, int num_sms) {
+  if (n_rows == 0) return cudaSuccess;
+  LmParams p{};
+  p.n_rows = n_rows;
+  p.d = d;
+  p.V = V;
+  p.tok_action = tok_action;
+  p.g_lse = tok_lse;
+  p.g_coef = tok_coef;
+  p.g_ecoef = tok_ecoef;
+  p.g_entropy = tok_entropy;
+  p.dz = static_cast<uint16_t*>(dlogits);
+  p.ld = ld;
+  return launch_tile<2>(hidden, weight, p, stream, num_sms);
 }
 
 }  // namespace echo

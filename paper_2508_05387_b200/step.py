@@ -209,6 +209,47 @@ class LearnerStep:
         self.launches += abi.LAUNCHES["echo_lmhead_logp"]
         return out
 
+    def loss_from_hidden(self, hidden, weight, row0: int, dhidden, dweight, *, accumulate=True, clip_low=0.2,
+                         clip_high=0.2, kl_coef=0.0, grad_scale=1.0, tok_adv=None, tok_weight=None, clip_dual=0.0,
+                         kl_estimator=abi.ECHO_KL_K3, entropy_coef=0.0, chunk_rows=8192, scratch=None):
+        """f2 training step through the LM head for packed rows [row0, row0 + n): (3) echo_lmhead_logp (logp, lse,
+        entropy without the logits), (4) echo_loss_from_logp (loss, flags, gradient coefficients), (5) + backward
+        echo_lmhead_backward (D recomputed on the tensor cores; dhidden = D W into ``dhidden`` f32 [n x d],
+        dweight (+)= D^T h into ``dweight`` f32 [V x d]).  Per-token outputs land in tok_logp / tok_loss / tok_flags
+        as with ``loss``.  ``scratch``: optional dict of reusable device buffers (keyed by name)."""
+        n, d = hidden.shape
+        sl = slice(row0, row0 + n)
+        sc = {} if scratch is None else scratch
+        dev = self.device
+
+        def buf(name, numel, dtype):
+            t = sc.get(name)
+            if t is None or t.numel() < numel or t.dtype != dtype:
+                t = torch.empty(max(numel, 1), dtype=dtype, device=dev)
+                sc[name] = t
+            return t[:numel]
+
+        ent_on = entropy_coef > 0
+        lse = buf("lse", n, torch.float32)
+        ent = buf("entropy", n, torch.float32) if ent_on else None
+        coef = buf("coef", n, torch.float32)
+        ecoef = buf("ecoef", n, torch.float32) if ent_on else None
+        ws = buf("ws", abi.echo_lmhead_workspace_bytes(n, self.V) // 4 + 1, torch.float32)
+        abi.echo_lmhead_logp(hidden, weight, n, d, self.V, self.tok_action[sl], self.tok_logp[sl], lse, ws,
+                             tok_entropy=ent)
+        cfg = abi.LossConfig(clip_low, clip_high, clip_dual, kl_coef, grad_scale, kl_estimator, entropy_coef)
+        ref = self.tok_ref[sl] if (self.tok_ref is not None and kl_coef > 0) else None
+        abi.echo_loss_from_logp(n, self.tok_logp[sl], ent, self.tok_old[sl], ref, self.tok_slot[sl], self.adv_slot,
+                                None if tok_adv is None else tok_adv[sl], None if tok_weight is None else tok_weight[sl],
+                                self.stats1[0:1], cfg, self.tok_loss[sl], self.tok_flags[sl], coef, ecoef)
+        chunk = max(1, min(chunk_rows, n))
+        dz = buf("dz", chunk * abi.echo_lmhead_dlogits_ld(self.V), torch.bfloat16)
+        abi.echo_lmhead_backward(hidden, weight, n, d, self.V, self.tok_action[sl], lse, coef, ecoef, ent, dhidden,
+                                 dweight, accumulate, dz, chunk)
+        if n > 0:
+            self.launches += (abi.LAUNCHES["echo_lmhead_logp"] + abi.LAUNCHES["echo_loss_from_logp"] +
+                              abi.BACKWARD_LAUNCHES_PER_CHUNK * ((n + chunk - 1) // chunk))
+
     # ------------------------------------------------------------------ (3)-(5)
     def loss(self, logits: torch.Tensor, row0: int, *, clip_low=0.2, clip_high=0.2, kl_coef=0.0, grad_scale=1.0,
              algo=None, stream=None, tok_adv=None, tok_weight=None, clip_dual=0.0, kl_estimator=abi.ECHO_KL_K3,

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     import paper_2508_05387_b200.abi as abi
     assert set(abi.EXPORTS) == set(declared_symbols())
-    assert abi.echo_abi_version() == 2
+    assert abi.echo_abi_version() == 3
     assert abi.echo_status_string(abi.ECHO_ERR_UNSUPPORTED) == "ECHO_ERR_UNSUPPORTED"
     assert abi.echo_loss_stats_workspace_bytes() > 0
 

@@ -1,0 +1,260 @@
+"""GPU parity of the f2 training step through the LM head: echo_loss_from_logp,
+echo_lmhead_dlogits (D recomputed on the tensor cores) and echo_lmhead_backward (dhidden, dweight) against the fp64
+oracle (oracle.loss_from_logp, oracle.lmhead_backward) on the same seeded inputs, through the C ABI."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def _bits(t):
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+def _bf(t):
+    return (_bits(t).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def _case(n, d, V, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    h = torch.randn(n, d, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(V, d, generator=g, device="cuda") * (2.0 / math.sqrt(d))).to(torch.bfloat16)
+    act = torch.randint(0, V, (n,), generator=g, device="cuda", dtype=torch.int32)
+    return h, w, act
+
+
+def _coefs(n, seed, lp, eta):
+    """Seeded per-token inputs of the backward from the oracle's (4): c_t from oracle.loss_from_logp at the oracle's
+    logp with a power-of-two grad_scale putting max|c| in [0.25, 0.5) (so |D| <= 0.5 and the 2e-3 bar is meaningful),
+    e_t = grad_scale eta / n; both rounded to fp32 (the ABI's type) and fed to both sides."""
+    rng = np.random.default_rng(seed)
+    old = (lp + rng.normal(size=n) * 0.2).astype(np.float32)
+    adv = rng.normal(size=8).astype(np.float32)
+    slot = rng.integers(0, 8, n).astype(np.int32)
+    _, _, c1 = oracle.loss_from_logp(lp, old, None, slot, adv, n_global=float(n))
+    scale = 2.0 ** math.floor(math.log2(0.5 / max(np.max(np.abs(c1)), 1e-30)))
+    _, _, coef = oracle.loss_from_logp(lp, old, None, slot, adv, n_global=float(n), grad_scale=scale)
+    c32 = coef.astype(np.float32)
+    e32 = np.full(n, np.float32(scale * eta / n), np.float32) if eta > 0 else None
+    return c32, e32
+
+
+# ------------------------------------------------------------------------------------------ (4) from logp
+@pytest.mark.parametrize("kl_coef,eta,dual,est,weights", [(0.0, 0.0, 0.0, 0, False), (0.05, 0.0, 3.0, 0, False),
+                                                          (0.1, 0.01, 0.0, 1, True), (0.1, 0.02, 2.0, 2, False)])
+def test_loss_from_logp_matches_oracle(kl_coef, eta, dual, est, weights):
+    from paper_2508_05387_b200 import abi
+    n = 5000
+    rng = np.random.default_rng(11)
+    lp = (-np.abs(rng.normal(size=n)) * 3).astype(np.float32)
+    old = (lp + rng.normal(size=n) * 0.3).astype(np.float32)
+    ref = (lp + rng.normal(size=n) * 0.3).astype(np.float32)
+    ent = np.abs(rng.normal(size=n) * 2).astype(np.float32)
+    adv = rng.normal(size=64).astype(np.float32)
+    slot = rng.integers(0, 64, n).astype(np.int32)
+    wt = (rng.random(n) / n).astype(np.float32) if weights else None
+    N = float(n)
+    o_loss, o_flags, o_coef = oracle.loss_from_logp(lp.astype(np.float64), old, ref, slot, adv, n_global=N,
+                                                    kl_coef=kl_coef, grad_scale=2.0, tok_weight=wt, clip_dual=dual,
+                                                    kl_estimator=est, entropy_coef=eta,
+                                                    tok_entropy=ent.astype(np.float64))
+    c = lambda x: None if x is None else torch.from_numpy(x).cuda()
+    loss = torch.empty(n, device="cuda")
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    coef = torch.empty(n, device="cuda")
+    ecoef = torch.empty(n, device="cuda")
+    ng = torch.tensor([N], dtype=torch.float64, device="cuda")
+    cfg = abi.LossConfig(0.2, 0.2, dual, kl_coef, 2.0, est, eta)
+    abi.echo_loss_from_logp(n, c(lp), c(ent), c(old), c(ref), c(slot), c(adv), None, c(wt), ng, cfg, loss, flags,
+                            coef, ecoef)
+    torch.cuda.synchronize()
+    g_loss, g_flags, g_coef = loss.cpu().numpy(), flags.cpu().numpy(), coef.cpu().numpy()
+    # the clip decision is taken in fp32 on the GPU: allow a flip only within fp32 rounding of a clip boundary
+    rho = np.exp(lp.astype(np.float64) - old)
+    near = (np.abs(rho - 0.8) < 1e-5) | (np.abs(rho - 1.2) < 1e-5) | (dual > 0) & (np.abs(rho - dual) < 1e-5)
+    assert np.all((g_flags == o_flags) | near)
+    ok = g_flags == o_flags
+    scale = np.maximum(np.abs(o_loss), 1.0)
+    assert np.max(np.abs(g_loss - o_loss)[ok] / scale[ok]) <= 1e-5
+    cs = np.maximum(np.abs(o_coef), np.max(np.abs(o_coef)) * 1e-3)
+    assert np.max(np.abs(g_coef - o_coef)[ok] / cs[ok]) <= 1e-5
+    w_t = wt.astype(np.float64) if weights else np.full(n, 1.0 / N)
+    np.testing.assert_allclose(ecoef.cpu().numpy(), np.float32(2.0) * w_t * np.float32(eta), rtol=1e-6, atol=0)
+
+
+def test_loss_from_logp_equals_the_fused_path_bit_for_bit():
+    """Same logp in, same scalar arithmetic: the fused kernel's per-token loss and flags on bf16 logits are
+    reproduced bit for bit by echo_loss_from_logp fed the fused kernel's own tok_logp / tok_entropy."""
+    from paper_2508_05387_b200 import abi
+    n, V = 777, 4096
+    g = torch.Generator(device="cuda").manual_seed(3)
+    logits = (torch.randn(n, V, generator=g, device="cuda") * 2).to(torch.bfloat16)
+    act = torch.randint(0, V, (n,), generator=g, device="cuda", dtype=torch.int32)
+    old = torch.randn(n, generator=g, device="cuda") - 8.0
+    ref = torch.randn(n, generator=g, device="cuda") - 8.0
+    adv = torch.randn(16, generator=g, device="cuda")
+    slot = torch.randint(0, 16, (n,), generator=g, device="cuda", dtype=torch.int32)
+    ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
+    cfg = abi.LossConfig(0.2, 0.28, 3.0, 0.05, 1.0, abi.ECHO_KL_K3, 0.01)
+    lp, loss, ent = (torch.empty(n, device="cuda") for _ in range(3))
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    abi.echo_policy_loss_fwd_bwd_v2(logits, abi.ECHO_BF16, n, V, V, act, old, ref, slot, adv, None, None, ng, cfg, lp,
+                                    loss, flags, tok_entropy=ent)
+    loss2, coef = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+    flags2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    abi.echo_loss_from_logp(n, lp, ent, old, ref, slot, adv, None, None, ng, cfg, loss2, flags2, coef)
+    torch.cuda.synchronize()
+    assert torch.equal(loss.view(torch.int32), loss2.view(torch.int32))
+    assert torch.equal(flags, flags2)
+
+
+# ------------------------------------------------------------------------------------------ D on the tensor cores
+def _d_check(dz_gpu, dz_ref):
+    """bf16 output (2^-9 relative rounding) of a value whose inputs carry the fp32-accumulated logit error (~1e-5
+    relative in p): |err| <= 2^-8 |D| + 2e-5 max_v |D[t, :]| per element, and 2e-3 absolute with max|D| <= 0.5."""
+    row_max = np.max(np.abs(dz_ref), axis=1, keepdims=True)
+    err = np.abs(dz_gpu - dz_ref)
+    bound = 2.0 ** -8 * np.abs(dz_ref) + 2e-5 * row_max + 1e-30
+    assert np.all(err <= bound), np.max(err / bound)
+    assert np.max(err) <= 2e-3
+
+
+@pytest.mark.parametrize("n,d,V,eta", [(128, 64, 256, 0.0), (300, 512, 1000, 0.01), (129, 72, 257, 0.0),
+                                       (1, 2560, 4096, 0.02), (700, 256, 5003, 0.0)])
+def test_lmhead_dlogits_matches_oracle(n, d, V, eta):
+    from paper_2508_05387_b200 import abi
+    h, w, act = _case(n, d, V, seed=n * 7 + V)
+    hb, wb, a = _bits(h), _bits(w), act.cpu().numpy()
+    lp, lse, H = oracle.lmhead_logp(hb, wb, a, want_entropy=True)
+    c32, e32 = _coefs(n, n + d, lp, eta=eta)
+    _, _, dz_ref = oracle.lmhead_backward(hb, wb, a, c32, e32, want_dlogits=True)
+    ld = abi.echo_lmhead_dlogits_ld(V) + 8
+    dz = torch.full((n, ld), 7.0, dtype=torch.bfloat16, device="cuda")
+    cu = lambda x: None if x is None else torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+    abi.echo_lmhead_dlogits(h, w, n, d, V, act, cu(lse), cu(c32), cu(e32), cu(H) if eta > 0 else None, dz, ld)
+    torch.cuda.synchronize()
+    out = _bf(dz)
+    assert np.all(out[:, V:] == 7.0)                                   # columns >= vocab untouched
+    _d_check(out[:, :V], dz_ref)
+
+
+# ------------------------------------------------------------------------------------------ dhidden, dweight
+@pytest.mark.parametrize("n,d,V,chunk,eta", [(300, 128, 1000, 128, 0.0), (257, 64, 777, 300, 0.02),
+                                             (520, 256, 2048, 200, 0.01)])
+def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta):
+    """dhidden and dweight (accumulated onto a prefilled buffer) over several chunks with a ragged last chunk.
+    Bound: D is bf16 (2^-9 relative) on top of its own ~1e-5 logit error; the GEMMs accumulate in fp32:
+    |err| <= 2^-7 (|D| |W|) (resp. |D|^T |h|) + 1e-6 of the row's scale."""
+    from paper_2508_05387_b200 import abi
+    h, w, act = _case(n, d, V, seed=n + V)
+    hb, wb, a = _bits(h), _bits(w), act.cpu().numpy()
+    lp, lse, H = oracle.lmhead_logp(hb, wb, a, want_entropy=True)
+    c32, e32 = _coefs(n, 5, lp, eta=eta)
+    dh_ref, dw_ref, dz_ref = oracle.lmhead_backward(hb, wb, a, c32, e32, want_dlogits=True)
+    cu = lambda x: None if x is None else torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+    dh = torch.full((n, d), float("nan"), device="cuda")
+    prev = torch.randn(V, d, device="cuda")
+    dw = prev.clone()
+    ws = torch.empty(chunk * abi.echo_lmhead_dlogits_ld(V), dtype=torch.bfloat16, device="cuda")
+    abi.echo_lmhead_backward(h, w, n, d, V, act, cu(lse), cu(c32), cu(e32), cu(H) if eta > 0 else None, dh, dw, 1,
+                             ws, chunk)
+    torch.cuda.synchronize()
+    absD = np.abs(dz_ref)
+    bh = 2.0 ** -7 * (absD @ np.abs(_bf(w))) + 1e-6 * np.max(np.abs(dh_ref), axis=1, keepdims=True) + 1e-12
+    bw = 2.0 ** -7 * (absD.T @ np.abs(_bf(h))) + 1e-6 * np.max(np.abs(dw_ref)) + 1e-12
+    g_dh = dh.cpu().numpy().astype(np.float64)
+    g_dw = (dw - prev).cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(g_dh - dh_ref) <= bh), np.max(np.abs(g_dh - dh_ref) / bh)
+    assert np.all(np.abs(g_dw - dw_ref) <= bw + 1e-6 * np.abs(prev.cpu().numpy())), np.max(np.abs(g_dw - dw_ref) / bw)
+    # overwrite mode and determinism
+    dw2 = torch.full((V, d), float("nan"), device="cuda")
+    dh2 = torch.empty(n, d, device="cuda")
+    abi.echo_lmhead_backward(h, w, n, d, V, act, cu(lse), cu(c32), cu(e32), cu(H) if eta > 0 else None, dh2, dw2, 0,
+                             ws, chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(dh, dh2)
+    assert np.all(np.abs(dw2.cpu().numpy() - dw_ref) <= bw)
+
+
+def test_lmhead_backward_edge_cases_and_errors():
+    from paper_2508_05387_b200 import abi
+    n, d, V = 64, 64, 300
+    h, w, act = _case(n, d, V, seed=1)
+    f = lambda: torch.zeros(n, device="cuda")
+    dh, dw = torch.empty(n, d, device="cuda"), torch.full((V, d), 5.0, device="cuda")
+    ws = torch.empty(n * abi.echo_lmhead_dlogits_ld(V), dtype=torch.bfloat16, device="cuda")
+    abi.echo_lmhead_backward(h, w, 0, d, V, act, f(), f(), None, None, dh, dw, 1, ws, 16)   # n = 0, accumulate: no-op
+    torch.cuda.synchronize()
+    assert torch.all(dw == 5.0)
+    abi.echo_lmhead_backward(h, w, 0, d, V, act, f(), f(), None, None, dh, dw, 0, ws, 16)   # n = 0, overwrite: zeros
+    torch.cuda.synchronize()
+    assert torch.all(dw == 0.0)
+    with pytest.raises(abi.EchoError):
+        abi.echo_lmhead_backward(h, w, n, d, V, act, f(), f(), None, None, dh, dw, 0, ws, 0)   # chunk_rows 0
+    with pytest.raises(abi.EchoError):
+        abi.echo_lmhead_backward(h, w, n, d, V, act, f(), f(), f(), None, dh, dw, 0, ws, 16)   # ecoef without H
+    with pytest.raises(abi.EchoError):
+        abi.echo_lmhead_dlogits(h, w, n, d, V, act, f(), f(), None, None, ws, V)               # ld % 8 != 0
+    # zero coefficients give a zero gradient
+    abi.echo_lmhead_backward(h, w, n, d, V, act, f(), f(), None, None, dh, dw, 0, ws, 16)
+    torch.cuda.synchronize()
+    assert torch.all(dh == 0) and torch.all(dw == 0)
+
+
+# ------------------------------------------------------------------------------------------ the step through it
+def test_learner_step_loss_from_hidden_qwen_vocab():
+    """LearnerStep.loss_from_hidden at a Qwen vocabulary (d = 2560, V = 151936) over 512 packed tokens in two chunks:
+    per-token logp / loss against the oracle chain (lmhead_logp -> loss_from_logp), dhidden on sampled rows against
+    oracle.lmhead_backward; dweight's columns sum to ~0 (every row of D sums to zero)."""
+    from paper_2508_05387_b200.step import LearnerStep
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, cfg.G)
+    st = LearnerStep(n_rollouts=cfg.G, group_size=cfg.G, max_len=cfg.S, vocab=cfg.V, dtype=cfg.dtype)
+    st.h2d(*[torch.from_numpy(np.ascontiguousarray(x)) for x in (b.version, b.resp_len, b.reward, b.action,
+                                                                 b.old_logp, b.ref_logp)])
+    info = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
+    st.advantage()
+    st.reduce_counts()
+    n, d, V = 512, 2560, cfg.V
+    assert info.n_tokens >= n
+    g = torch.Generator(device="cuda").manual_seed(9)
+    h = torch.randn(n, d, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(V, d, generator=g, device="cuda") * (2.0 / math.sqrt(d))).to(torch.bfloat16)
+    dh = torch.empty(n, d, device="cuda")
+    dw = torch.empty(V, d, device="cuda")
+    N = info.n_tokens
+    st.loss_from_hidden(h, w, 0, dh, dw, accumulate=False, kl_coef=0.01, entropy_coef=0.01, grad_scale=float(N),
+                        chunk_rows=256)
+    torch.cuda.synchronize()
+    act = st.tok_action[:n].cpu().numpy()
+    rows = np.array([0, 1, 255, 256, 400, 511])
+    hb, wb = _bits(h[rows]), _bits(w)
+    lp, lse, H = oracle.lmhead_logp(hb, wb, act[rows], want_entropy=True)
+    slot, adv = st.tok_slot[:n].cpu().numpy()[rows], st.adv_slot.cpu().numpy()
+    old, ref = st.tok_old[:n].cpu().numpy()[rows], st.tok_ref[:n].cpu().numpy()[rows]
+    o_loss, o_flags, o_coef = oracle.loss_from_logp(lp, old, ref, slot, adv, n_global=float(N), kl_coef=0.01,
+                                                    grad_scale=float(N), entropy_coef=0.01, tok_entropy=H)
+    g_lp = st.tok_logp[:n].cpu().numpy()[rows]
+    assert np.max(np.abs(g_lp - lp)) <= 2e-4
+    assert np.max(np.abs(st.tok_loss[:n].cpu().numpy()[rows] - o_loss) / np.maximum(np.abs(o_loss), 1)) <= 1e-3
+    e = np.full(len(rows), np.float32(N) * np.float32(0.01) / N)
+    dh_ref, _ = oracle.lmhead_backward(hb, wb, act[rows], o_coef, e, want_dweight=False)
+    g_dh = dh.cpu().numpy()[rows].astype(np.float64)
+    scale = np.max(np.abs(dh_ref), axis=1, keepdims=True)
+    assert np.max(np.abs(g_dh - dh_ref) / scale) <= 1e-2, np.max(np.abs(g_dh - dh_ref) / scale)
+    col = dw.sum(dim=0).abs().max().item()
+    assert col <= 1e-2 * dw.abs().sum(dim=0).max().item()
+    assert torch.isfinite(dw).all() and torch.isfinite(dh).all()

@@ -21,6 +21,10 @@ def main():
     ap.add_argument("--vocab", type=int, default=151936)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--no-unfused", action="store_true")
+    ap.add_argument("--mode", default="logp", choices=["logp", "dlogits", "backward"],
+                    help="logp: echo_lmhead_logp; dlogits: echo_lmhead_dlogits over one chunk of --chunk rows; "
+                         "backward: echo_lmhead_backward over --rows in --chunk chunks")
+    ap.add_argument("--chunk", type=int, default=8192)
     a = ap.parse_args()
     import __graft_entry__
     __graft_entry__.build()
@@ -47,7 +51,27 @@ def main():
         ts.sort()
         return ts[len(ts) // 2]
 
-    out = {"rows": n, "d": d, "vocab": V, "gflop": flops / 1e9}
+    out = {"rows": n, "d": d, "vocab": V, "gflop": flops / 1e9, "mode": a.mode}
+    if a.mode != "logp":
+        ld = abi.echo_lmhead_dlogits_ld(V)
+        lse = torch.empty(n, device="cuda")
+        abi.echo_lmhead_logp(h, w, n, d, V, act, lp, lse, ws)
+        coef = torch.randn(n, generator=g, device="cuda") * 1e-3
+        ck = min(a.chunk, n)
+        dz = torch.empty(ck, ld, dtype=torch.bfloat16, device="cuda")
+        if a.mode == "dlogits":
+            fl = 2.0 * ck * d * V
+            ms = timed(lambda: abi.echo_lmhead_dlogits(h, w, ck, d, V, act, lse, coef, None, None, dz, ld))
+            out.update(chunk=ck, dlogits_ms=ms, dlogits_tflops=fl / ms / 1e9,
+                       dlogits_store_GBps=ck * V * 2 / ms / 1e6)
+        else:
+            dh = torch.empty(n, d, device="cuda")
+            dw = torch.empty(V, d, device="cuda")
+            ms = timed(lambda: abi.echo_lmhead_backward(h, w, n, d, V, act, lse, coef, None, None, dh, dw, 0, dz, ck))
+            out.update(chunk=ck, backward_ms=ms, backward_tflops_6dV_over_3=2 * flops / ms / 1e9,
+                       backward_tflops_executed=3 * flops / ms / 1e9)
+        print(json.dumps(out))
+        return
     ms = timed(lambda: abi.echo_lmhead_logp(h, w, n, d, V, act, lp, None, ws))
     out["fused_ms"] = ms
     out["fused_tflops"] = flops / ms / 1e9
