@@ -13,7 +13,8 @@
  * SURVEY.md §8.6 NEXT rows:
  *   echo_token_logp                   f1  forward-only log-probs (read-only pass)
  *   echo_lmhead_logp                  f2  LM head fused with the log-prob on the tcgen05 tensor cores
- *   echo_loss_from_logp, echo_lmhead_dlogits, echo_lmhead_backward
+ *   echo_loss_from_logp, echo_lmhead_dlogits, echo_lmhead_backward, echo_lmhead_logits,
+ *   echo_lmhead_policy_loss_fwd_bwd
  *                                     f2  training step through the LM head: (4) from logp, D recomputed on the
  *                                         tensor cores, dhidden / dweight
  *   echo_pack_batch_v2, echo_staleness_histogram, echo_csr_from_lengths
@@ -390,6 +391,32 @@ ECHO_API echo_status echo_lmhead_backward(const void* hidden, const void* weight
                                           const float* tok_coef, const float* tok_ecoef, const float* tok_entropy,
                                           float* dhidden, float* dweight, int32_t accumulate, void* dlogits_ws,
                                           int64_t chunk_rows, void* cublas_handle, void* stream);
+
+/*
+ * f2: the LM head's logits z[t, v] = sum_k hidden[t, k] weight[v, k] as a plain tcgen05 GEMM (the GEMM of
+ * echo_lmhead_logp, fp32 accumulation in TMEM) stored as bf16 (round to nearest even) into logits [n_rows x ld]
+ * row-major, columns vocab..ld-1 untouched; ld % 8 == 0, logits 16-byte aligned.  Launches: 1 kernel.
+ */
+ECHO_API echo_status echo_lmhead_logits(const void* hidden, const void* weight, int64_t n_rows, int32_t d,
+                                        int32_t vocab, void* logits, int64_t ld, void* stream);
+
+/*
+ * f2 training step through the LM head, chunked (PAPER.md :254-261): for each chunk of
+ * chunk_rows tokens,
+ *   echo_lmhead_logits into logits_ws (bf16 [chunk_rows x ld], ld = vocab rounded up to 8),
+ *   echo_policy_loss_fwd_bwd_v2 on that chunk ((3)-(5): tok_logp / tok_loss / tok_flags / tok_entropy of the
+ *     chunk's tokens, the chunk becomes dL/dz in place),
+ *   dhidden[chunk] = D weight, dweight (+)= D^T hidden[chunk]  (cuBLAS, as echo_lmhead_backward).
+ * Per-token arrays are full-length (offset per chunk by the library); arguments as echo_policy_loss_fwd_bwd_v2 and
+ * echo_lmhead_backward.  The logits are the bf16 rounding of the fp32-accumulated z (a bf16 model's LM-head output).
+ * Launches: per chunk 2 kernels + 2 cuBLAS GEMMs.
+ */
+ECHO_API echo_status echo_lmhead_policy_loss_fwd_bwd(
+    const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab, const int32_t* tok_action,
+    const float* tok_old, const float* tok_ref, const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
+    const float* tok_weight, const double* n_global, const echo_loss_config* cfg, float* tok_logp, float* tok_loss,
+    uint8_t* tok_flags, float* tok_entropy, float* dhidden, float* dweight, int32_t accumulate, void* logits_ws,
+    int64_t chunk_rows, void* cublas_handle, void* stream);
 
 /* Human-readable name of a status code (static storage). */
 ECHO_API const char* echo_status_string(echo_status status);

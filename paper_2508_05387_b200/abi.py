@@ -27,15 +27,18 @@ PACK_RESULT_BYTES = 32
 LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_fwd_bwd": 1, "echo_loss_stats": 2,
             "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1, "echo_csr_from_lengths": 2,
             "echo_lmhead_logp": 2, "echo_staleness_histogram": 1, "echo_pack_batch_v2": 3,
-            "echo_loss_from_logp": 1, "echo_lmhead_dlogits": 1}
+            "echo_loss_from_logp": 1, "echo_lmhead_dlogits": 1, "echo_lmhead_logits": 1}
 # echo_lmhead_backward: per chunk 1 libecho kernel + 2 cuBLAS GEMMs (library kernels, not counted here)
 BACKWARD_LAUNCHES_PER_CHUNK = 1
+# echo_lmhead_policy_loss_fwd_bwd: per chunk 2 libecho kernels (logits, fused loss) + 2 cuBLAS GEMMs
+LMHEAD_LOSS_LAUNCHES_PER_CHUNK = 2
 
 EXPORTS = ("echo_pack_batch", "echo_pack_batch_v2", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
            "echo_policy_loss_launch_shape", "echo_token_logp", "echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage",
            "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_csr_from_lengths",
            "echo_lmhead_workspace_bytes", "echo_lmhead_logp", "echo_staleness_histogram", "echo_status_string",
-           "echo_abi_version", "echo_loss_from_logp", "echo_lmhead_dlogits", "echo_lmhead_backward")
+           "echo_abi_version", "echo_loss_from_logp", "echo_lmhead_dlogits", "echo_lmhead_backward",
+           "echo_lmhead_logits", "echo_lmhead_policy_loss_fwd_bwd")
 
 
 ECHO_KL_K3, ECHO_KL_K1, ECHO_KL_K2 = range(3)
@@ -91,10 +94,13 @@ def _load(path=LIB_PATH):
     lib.echo_loss_from_logp.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P]
     lib.echo_lmhead_dlogits.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, i64, P]
     lib.echo_lmhead_backward.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, P, i32, P, i64, P, P]
+    lib.echo_lmhead_logits.argtypes = [P, P, i64, i32, i32, P, i64, P]
+    lib.echo_lmhead_policy_loss_fwd_bwd.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
+                                                    i32, P, i64, P, P]
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
                "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths", "echo_lmhead_logp",
                "echo_staleness_histogram", "echo_pack_batch_v2", "echo_loss_from_logp", "echo_lmhead_dlogits",
-               "echo_lmhead_backward"):
+               "echo_lmhead_backward", "echo_lmhead_logits", "echo_lmhead_policy_loss_fwd_bwd"):
         getattr(lib, fn).restype = ctypes.c_int
     return lib
 
@@ -256,6 +262,25 @@ def echo_lmhead_backward(hidden, weight, n_rows, d, vocab, tok_action, tok_lse, 
         _p(hidden), _p(weight), n_rows, d, vocab, _p(tok_action), _p(tok_lse), _p(tok_coef), _p(tok_ecoef),
         _p(tok_entropy), _p(dhidden), _p(dweight), int(accumulate), _p(dlogits_ws), chunk_rows, cublas_handle,
         _s(stream)))
+
+
+def echo_lmhead_logits(hidden, weight, n_rows, d, vocab, logits, ld, stream=None):
+    _check("echo_lmhead_logits", _lib.echo_lmhead_logits(_p(hidden), _p(weight), n_rows, d, vocab, _p(logits), ld,
+                                                          _s(stream)))
+
+
+def echo_lmhead_policy_loss_fwd_bwd(hidden, weight, n_rows, d, vocab, tok_action, tok_old, tok_ref, tok_slot, adv_slot,
+                                    tok_adv, tok_weight, n_global, cfg: LossConfig, tok_logp, tok_loss, tok_flags,
+                                    tok_entropy, dhidden, dweight, accumulate, logits_ws, chunk_rows,
+                                    cublas_handle=None, stream=None):
+    if cublas_handle is None:
+        import torch
+        cublas_handle = torch.cuda.current_blas_handle()
+    _check("echo_lmhead_policy_loss_fwd_bwd", _lib.echo_lmhead_policy_loss_fwd_bwd(
+        _p(hidden), _p(weight), n_rows, d, vocab, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot),
+        _p(adv_slot), _p(tok_adv), _p(tok_weight), _p(n_global), ctypes.byref(cfg), _p(tok_logp), _p(tok_loss),
+        _p(tok_flags), _p(tok_entropy), _p(dhidden), _p(dweight), int(accumulate), _p(logits_ws), chunk_rows,
+        cublas_handle, _s(stream)))
 
 
 def echo_loss_stats_workspace_bytes() -> int:

@@ -392,6 +392,57 @@ echo_status echo_lmhead_backward(const void* hidden, const void* weight, int64_t
   return from_cuda(e);
 }
 
+echo_status echo_lmhead_logits(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab,
+                               void* logits, int64_t ld, void* stream) {
+  if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || ld < vocab || ld % 8 != 0)
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows > 0 && (!logits || !aligned16(logits))) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  const cudaError_t e = echo::launch_lmhead_logits(hidden, weight, n_rows, d, vocab, logits, ld,
+                                                   static_cast<cudaStream_t>(stream), sms);
+  if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
+  return from_cuda(e);
+}
+
+echo_status echo_lmhead_policy_loss_fwd_bwd(const void* hidden, const void* weight, int64_t n_rows, int32_t d,
+                                            int32_t vocab, const int32_t* tok_action, const float* tok_old,
+                                            const float* tok_ref, const int32_t* tok_slot, const float* adv_slot,
+                                            const float* tok_adv, const float* tok_weight, const double* n_global,
+                                            const echo_loss_config* cfg, float* tok_logp, float* tok_loss,
+                                            uint8_t* tok_flags, float* tok_entropy, float* dhidden, float* dweight,
+                                            int32_t accumulate, void* logits_ws, int64_t chunk_rows,
+                                            void* cublas_handle, void* stream) {
+  if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || chunk_rows < 1 || chunk_rows > INT32_MAX ||
+      !cublas_handle || !dweight || !valid_loss_config(cfg))
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (n_rows > 0 && (!dhidden || !logits_ws || !aligned16(logits_ws))) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n_rows == 0) return accumulate ? ECHO_OK : from_cuda(cudaMemsetAsync(dweight, 0, (size_t)vocab * d * 4, s));
+  const int64_t ld = ((int64_t)vocab + 7) & ~(int64_t)7;
+  const uint16_t* hid = static_cast<const uint16_t*>(hidden);
+  for (int64_t r0 = 0; r0 < n_rows; r0 += chunk_rows) {
+    const int64_t rows = (n_rows - r0 < chunk_rows) ? n_rows - r0 : chunk_rows;
+    cudaError_t e = echo::launch_lmhead_logits(hid + r0 * d, weight, rows, d, vocab, logits_ws, ld, s, sms);
+    if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
+    if (e != cudaSuccess) return ECHO_ERR_CUDA;
+    st = echo_policy_loss_fwd_bwd_v2(logits_ws, ECHO_BF16, rows, vocab, ld, tok_action + r0, tok_old + r0,
+                                     tok_ref ? tok_ref + r0 : nullptr, tok_slot ? tok_slot + r0 : nullptr, adv_slot,
+                                     tok_adv ? tok_adv + r0 : nullptr, tok_weight ? tok_weight + r0 : nullptr,
+                                     n_global, cfg, tok_logp + r0, tok_loss + r0, tok_flags + r0,
+                                     tok_entropy ? tok_entropy + r0 : nullptr, ECHO_ALGO_AUTO, stream);
+    if (st != ECHO_OK) return st;
+    if (echo::cublas_lmhead_grads(cublas_handle, s, weight, hid + r0 * d, logits_ws, ld, rows, d, vocab,
+                                  dhidden + r0 * d, dweight, accumulate || r0 > 0) != 0)
+      return ECHO_ERR_CUDA;
+  }
+  return from_cuda(cudaGetLastError());
+}
+
 size_t echo_loss_stats_workspace_bytes(void) { return echo::loss_stats_workspace_bytes(); }
 
 echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp, const float* tok_old,

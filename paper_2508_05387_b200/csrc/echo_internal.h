@@ -86,6 +86,13 @@ cudaError_t launch_lmhead_dlogits(const void* hidden, const void* weight, int64_
                                   const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
                                   const float* tok_ecoef, const float* tok_entropy, void* dlogits, int64_t ld,
                                   cudaStream_t stream, int num_sms);
+cudaError_t launch_lmhead_logits(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
+                                 void* logits, int64_t ld, cudaStream_t stream, int num_sms);
+// dhidden[rows x d] = D W and dweight (+)= D^T hidden over one chunk of rows (cuBLAS, fp32 accumulation / output);
+// returns 0 or the cublasStatus_t
+int cublas_lmhead_grads(void* cublas_handle, cudaStream_t stream, const void* weight, const void* hidden_chunk,
+                        const void* D, int64_t ld, int64_t rows, int32_t d, int32_t V, float* dhidden_chunk,
+                        float* dweight, bool beta_one);
 cudaError_t launch_lmhead_backward(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
                                    const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
                                    const float* tok_ecoef, const float* tok_entropy, float* dhidden, float* dweight,

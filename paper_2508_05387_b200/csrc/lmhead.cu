@@ -166,13 +166,13 @@ struct LmParams {
   int64_t ld;
 };
 
-// kMode: 0 = logp partials, 1 = logp + entropy partials, 2 = dlogits (D written to p.dz)
+// kMode: 0 = logp partials, 1 = logp + entropy partials, 2 = dlogits (D written to p.dz), 3 = logits (z to p.dz)
 template <bool kPair, int kMode>
 __global__ void __launch_bounds__(lm::kThreads, 1)
     lmhead_tile_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w,
                        const LmParams p) {
   using namespace lm;
-  constexpr bool kEnt = kMode == 1, kGrad = kMode == 2;
+  constexpr bool kEnt = kMode == 1, kStore = kMode >= 2;  // 2: D, 3: the logits z themselves (bf16)
   using C = Cfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -274,13 +274,14 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
       const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
       const int64_t row = (int64_t)tt * C::kTileRows + (int64_t)rank * kBM + quad * 32 + lane;
       const bool row_ok = row < p.n_rows;
-      const int32_t a = row_ok ? p.tok_action[row] : -1;
+      const int32_t a = (row_ok && kMode != 3) ? p.tok_action[row] : -1;
       const int32_t col0 = vt * kBN;
-      if constexpr (kGrad) {
+      if constexpr (kStore) {
         // D[t, v] = c (delta_{v,a} - p) + e p (z - lse + H) = p (e z + k) + c delta_{v,a},  k = e (H - lse) - c
-        const float lse = row_ok ? p.g_lse[row] : 0.0f, c = row_ok ? p.g_coef[row] : 0.0f;
-        const float e = (row_ok && p.g_ecoef) ? p.g_ecoef[row] : 0.0f;
-        const float H = (row_ok && p.g_ecoef) ? p.g_entropy[row] : 0.0f;
+        const bool rd = row_ok && kMode == 2;
+        const float lse = rd ? p.g_lse[row] : 0.0f, c = rd ? p.g_coef[row] : 0.0f;
+        const float e = (rd && p.g_ecoef) ? p.g_ecoef[row] : 0.0f;
+        const float H = (rd && p.g_ecoef) ? p.g_entropy[row] : 0.0f;
         const float k = fmaf(e, H - lse, -c);
         const uint64_t l2e2 = f2(kLog2e, kLog2e), nl2 = f2(-lse * kLog2e, -lse * kLog2e), e2 = f2(e, e), k2 = f2(k, k);
         uint16_t* drow = p.dz + (row_ok ? row : 0) * p.ld;
@@ -295,6 +296,10 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
           uint32_t o[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
+            if constexpr (kMode == 3) {
+              o[i >> 1] = pack_bf16x2(__uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+              continue;
+            }
             const uint64_t z2 = f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1]));
             float t0, t1;
             f2split(fma2(z2, l2e2, nl2), t0, t1);
@@ -554,6 +559,18 @@ cudaError_t launch_lmhead_dlogits(const void* hidden, const void* weight, int64_
   p.dz = static_cast<uint16_t*>(dlogits);
   p.ld = ld;
   return launch_tile<2>(hidden, weight, p, stream, num_sms);
+}
+
+cudaError_t launch_lmhead_logits(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
+                                 void* logits, int64_t ld, cudaStream_t stream, int num_sms) {
+  if (n_rows == 0) return cudaSuccess;
+  LmParams p{};
+  p.n_rows = n_rows;
+  p.d = d;
+  p.V = V;
+  p.dz = static_cast<uint16_t*>(logits);
+  p.ld = ld;
+  return launch_tile<3>(hidden, weight, p, stream, num_sms);
 }
 
 }  // namespace echo

@@ -211,16 +211,40 @@ class LearnerStep:
 
     def loss_from_hidden(self, hidden, weight, row0: int, dhidden, dweight, *, accumulate=True, clip_low=0.2,
                          clip_high=0.2, kl_coef=0.0, grad_scale=1.0, tok_adv=None, tok_weight=None, clip_dual=0.0,
-                         kl_estimator=abi.ECHO_KL_K3, entropy_coef=0.0, chunk_rows=8192, scratch=None):
-        """f2 training step through the LM head for packed rows [row0, row0 + n): (3) echo_lmhead_logp (logp, lse,
-        entropy without the logits), (4) echo_loss_from_logp (loss, flags, gradient coefficients), (5) + backward
-        echo_lmhead_backward (D recomputed on the tensor cores; dhidden = D W into ``dhidden`` f32 [n x d],
-        dweight (+)= D^T h into ``dweight`` f32 [V x d]).  Per-token outputs land in tok_logp / tok_loss / tok_flags
-        as with ``loss``.  ``scratch``: optional dict of reusable device buffers (keyed by name)."""
+                         kl_estimator=abi.ECHO_KL_K3, entropy_coef=0.0, chunk_rows=8192, scratch=None,
+                         mode="chunked", tok_entropy=None):
+        """f2 training step through the LM head for packed rows [row0, row0 + n): dhidden = dL/dh into ``dhidden``
+        (f32 [n x d]) and dL/dW added to (``accumulate``) or written over ``dweight`` (f32 [V x d]); per-token outputs
+        land in tok_logp / tok_loss / tok_flags as with ``loss``.  No [n x V] logits buffer: at most a
+        [chunk_rows x V] bf16 one.  ``scratch``: optional dict of reusable device buffers (keyed by name).
+
+        mode "chunked" (default, echo_lmhead_policy_loss_fwd_bwd): per chunk, z = h W^T stored as bf16 by the tcgen05
+            GEMM, the fused (3)-(5) kernel in place, cuBLAS dhidden / dweight (6 d V flops per token).
+        mode "recompute": (3) echo_lmhead_logp (logp, lse, entropy without the logits), (4) echo_loss_from_logp,
+            (5) + backward echo_lmhead_backward with D recomputed from h and W on the tensor cores (8 d V flops per
+            token; logits never rounded to bf16)."""
         n, d = hidden.shape
         sl = slice(row0, row0 + n)
         sc = {} if scratch is None else scratch
         dev = self.device
+        if mode == "chunked":
+            chunk = max(1, min(chunk_rows, n))
+            cfg = abi.LossConfig(clip_low, clip_high, clip_dual, kl_coef, grad_scale, kl_estimator, entropy_coef)
+            ws = sc.get("zc")
+            numel = chunk * abi.echo_lmhead_dlogits_ld(self.V)
+            if ws is None or ws.numel() < numel:
+                ws = sc["zc"] = torch.empty(numel, dtype=torch.bfloat16, device=dev)
+            ref = self.tok_ref[sl] if (self.tok_ref is not None and kl_coef > 0) else None
+            abi.echo_lmhead_policy_loss_fwd_bwd(
+                hidden, weight, n, d, self.V, self.tok_action[sl], self.tok_old[sl], ref, self.tok_slot[sl],
+                self.adv_slot, None if tok_adv is None else tok_adv[sl], None if tok_weight is None else tok_weight[sl],
+                self.stats1[0:1], cfg, self.tok_logp[sl], self.tok_loss[sl], self.tok_flags[sl],
+                None if tok_entropy is None else tok_entropy[sl], dhidden, dweight, accumulate, ws, chunk)
+            if n > 0:
+                self.launches += abi.LMHEAD_LOSS_LAUNCHES_PER_CHUNK * ((n + chunk - 1) // chunk)
+            return
+        if mode != "recompute":
+            raise ValueError(f"loss_from_hidden: unknown mode {mode!r}")
 
         def buf(name, numel, dtype):
             t = sc.get(name)

@@ -215,7 +215,7 @@ def test_lmhead_backward_edge_cases_and_errors():
 
 
 # ------------------------------------------------------------------------------------------ the step through it
-def test_learner_step_loss_from_hidden_qwen_vocab():
+def test_learner_step_loss_from_hidden_recompute_qwen_vocab():
     """LearnerStep.loss_from_hidden at a Qwen vocabulary (d = 2560, V = 151936) over 512 packed tokens in two chunks:
     per-token logp / loss against the oracle chain (lmhead_logp -> loss_from_logp), dhidden on sampled rows against
     oracle.lmhead_backward; dweight's columns sum to ~0 (every row of D sums to zero)."""
@@ -237,7 +237,7 @@ def test_learner_step_loss_from_hidden_qwen_vocab():
     dw = torch.empty(V, d, device="cuda")
     N = info.n_tokens
     st.loss_from_hidden(h, w, 0, dh, dw, accumulate=False, kl_coef=0.01, entropy_coef=0.01, grad_scale=float(N),
-                        chunk_rows=256)
+                        chunk_rows=256, mode="recompute")
     torch.cuda.synchronize()
     act = st.tok_action[:n].cpu().numpy()
     rows = np.array([0, 1, 255, 256, 400, 511])
@@ -258,3 +258,121 @@ def test_learner_step_loss_from_hidden_qwen_vocab():
     col = dw.sum(dim=0).abs().max().item()
     assert col <= 1e-2 * dw.abs().sum(dim=0).max().item()
     assert torch.isfinite(dw).all() and torch.isfinite(dh).all()
+
+
+# ------------------------------------------------------------------------------------------ chunked: logits + fused loss
+def _bf16_rne(x):
+    """fp64 -> fp32 -> bf16 (round to nearest even at each step: the GPU's fp32 accumulator -> bf16 store)."""
+    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def _z_tol(hb, wb):
+    """fp32-accumulation bound of the tcgen05 GEMM per element (as _lmhead_tol in test_gpu_parity.py, not doubled)."""
+    widen = lambda b: (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    hf, wf = widen(hb), widen(wb)
+    return 4 * (hb.shape[1] / 16 + 16) * 2.0 ** -24 * (np.abs(hf) @ np.abs(wf).T), hf, wf
+
+
+@pytest.mark.parametrize("n,d,V", [(300, 128, 1000), (129, 72, 257), (64, 2560, 4096)])
+def test_lmhead_logits_bf16(n, d, V):
+    """echo_lmhead_logits: bf16(z) with z = h W^T; each element is the bf16 rounding of a value within the fp32
+    accumulation bound of the fp64 product, i.e. one of the (at most two) bf16 values that bracket z +- tol."""
+    from paper_2508_05387_b200 import abi
+    h, w, _ = _case(n, d, V, seed=V + 1)
+    hb, wb = _bits(h), _bits(w)
+    tol, hf, wf = _z_tol(hb, wb)
+    z = hf @ wf.T
+    ld = abi.echo_lmhead_dlogits_ld(V) + 8
+    out = torch.full((n, ld), 3.0, dtype=torch.bfloat16, device="cuda")
+    abi.echo_lmhead_logits(h, w, n, d, V, out, ld)
+    torch.cuda.synchronize()
+    g = _bits(out)
+    assert np.all(_bf(out)[:, V:] == 3.0)
+    lo, hi = _bf16_rne(z - tol), _bf16_rne(z + tol)
+    gv = g[:, :V]
+    ok = (gv == lo) | (gv == hi) | (gv == _bf16_rne(z))
+    assert ok.all(), np.argwhere(~ok)[:5]
+    assert (gv == _bf16_rne(z)).mean() > 0.999
+
+
+@pytest.mark.parametrize("n,d,V,chunk,eta", [(300, 128, 1000, 128, 0.0), (260, 64, 777, 100, 0.01)])
+def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta):
+    """The chunked f2 step (echo_lmhead_policy_loss_fwd_bwd) against the oracle chain on the same bf16-rounded logits:
+    oracle.policy_loss on bf16(h W^T) (fp64 from the bf16 values), then dhidden = D W and dweight = D^T h in fp64.
+    Tokens whose action logit lies within the GEMM's fp32 error of a bf16 rounding boundary are excluded from the
+    per-token comparison (their bf16 logit may legitimately differ by one ulp)."""
+    from paper_2508_05387_b200 import abi
+    h, w, act = _case(n, d, V, seed=n + 3)
+    hb, wb, a = _bits(h), _bits(w), act.cpu().numpy()
+    tol, hf, wf = _z_tol(hb, wb)
+    z = hf @ wf.T
+    zb = _bf16_rne(z)
+    amb = _bf16_rne(z - tol) != _bf16_rne(z + tol)
+    rng = np.random.default_rng(n)
+    old = (rng.normal(size=n) - 7.0).astype(np.float32)
+    ref = (rng.normal(size=n) - 7.0).astype(np.float32)
+    adv = rng.normal(size=16).astype(np.float32)
+    slot = rng.integers(0, 16, n).astype(np.int32)
+    kl = 0.05
+    o = oracle.policy_loss(zb, a, old, ref, slot, adv, n_global=float(n), dtype=oracle.BF16, kl_coef=kl,
+                           grad_scale=float(n) / 4, entropy_coef=eta)
+    dh_ref, dw_ref = o.dlogits @ wf, o.dlogits.T @ hf
+    cu = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    lp, loss, ent = (torch.empty(n, device="cuda") for _ in range(3))
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    dh = torch.empty(n, d, device="cuda")
+    dw = torch.empty(V, d, device="cuda")
+    ws = torch.empty(chunk * abi.echo_lmhead_dlogits_ld(V), dtype=torch.bfloat16, device="cuda")
+    ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
+    cfg = abi.LossConfig(0.2, 0.2, 0.0, kl, float(n) / 4, abi.ECHO_KL_K3, eta)
+    abi.echo_lmhead_policy_loss_fwd_bwd(h, w, n, d, V, act, cu(old), cu(ref), cu(slot), cu(adv), None, None, ng, cfg,
+                                        lp, loss, flags, ent, dh, dw, 0, ws, chunk)
+    torch.cuda.synchronize()
+    clean = ~amb[np.arange(n), a] & (amb.sum(axis=1) < 8)
+    assert clean.mean() > 0.9
+    g_lp = lp.cpu().numpy()
+    assert np.max(np.abs(g_lp - o.logp)[clean]) <= 1e-4
+    g_loss = loss.cpu().numpy()
+    assert np.max((np.abs(g_loss - o.loss) / np.maximum(np.abs(o.loss), 1))[clean]) <= 1e-4
+    absD = np.abs(o.dlogits)
+    bh = 2.0 ** -7 * (absD @ np.abs(wf)) + 1e-6 * np.max(np.abs(dh_ref)) + 1e-12
+    bw = 2.0 ** -7 * (absD.T @ np.abs(hf)) + 1e-6 * np.max(np.abs(dw_ref)) + 1e-12
+    g_dh = dh.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(g_dh - dh_ref)[clean] <= bh[clean]), np.max(np.abs(g_dh - dh_ref)[clean] / bh[clean])
+    assert np.mean(np.abs(dw.cpu().numpy() - dw_ref) <= bw) > 0.999
+
+
+def test_learner_step_chunked_equals_unchunked_logits_path():
+    """LearnerStep.loss_from_hidden (chunked) at a Qwen vocabulary equals, bit for bit in tok_logp / tok_loss /
+    tok_flags, the logits path on the same bf16 logits (echo_lmhead_logits for all rows, then LearnerStep.loss);
+    dhidden / dweight equal cuBLAS on that path's gradient chunk by chunk."""
+    from paper_2508_05387_b200 import abi
+    from paper_2508_05387_b200.step import LearnerStep
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, cfg.G)
+    st = LearnerStep(n_rollouts=cfg.G, group_size=cfg.G, max_len=cfg.S, vocab=cfg.V, dtype=cfg.dtype)
+    st.h2d(*[torch.from_numpy(np.ascontiguousarray(x)) for x in (b.version, b.resp_len, b.reward, b.action,
+                                                                 b.old_logp, b.ref_logp)])
+    info = st.pack(t_train=synth.T_TRAIN, max_lag=cfg.max_lag)
+    st.advantage()
+    st.reduce_counts()
+    n, d, V = 640, 1024, cfg.V
+    g = torch.Generator(device="cuda").manual_seed(4)
+    h = torch.randn(n, d, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(V, d, generator=g, device="cuda") * (2.0 / math.sqrt(d))).to(torch.bfloat16)
+    dh = torch.empty(n, d, device="cuda")
+    dw = torch.empty(V, d, device="cuda")
+    st.loss_from_hidden(h, w, 0, dh, dw, accumulate=False, kl_coef=0.01, grad_scale=float(info.n_tokens),
+                        chunk_rows=256)
+    lp1, loss1, fl1 = st.tok_logp[:n].clone(), st.tok_loss[:n].clone(), st.tok_flags[:n].clone()
+    logits = torch.empty(n, V, dtype=torch.bfloat16, device="cuda")
+    abi.echo_lmhead_logits(h, w, n, d, V, logits, V)
+    st.loss(logits, 0, kl_coef=0.01, grad_scale=float(info.n_tokens))
+    torch.cuda.synchronize()
+    assert torch.equal(lp1.view(torch.int32), st.tok_logp[:n].view(torch.int32))
+    assert torch.equal(loss1.view(torch.int32), st.tok_loss[:n].view(torch.int32))
+    assert torch.equal(fl1, st.tok_flags[:n])
+    ref_dh = logits.float() @ w.float()
+    rel = (dh - ref_dh).abs().max().item() / ref_dh.abs().max().item()
+    assert rel < 1e-3, rel
