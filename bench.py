@@ -438,13 +438,18 @@ def main_echo(args):
             dw_u = torch.empty(cfg.V, hd, dtype=torch.bfloat16, device=dev)
             scratch = {}
             kl = cfg.kl_coef
-            t2, t2u = [], []
+            t2 = {"chunked": [], "recompute": []}
+            t2u = []
             for r in range(5):
-                flush.fill_(float(r))
-                a0 = ev()
-                st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
-                                    chunk_rows=chunk, scratch=scratch)
-                a1 = ev()
+                for mode in t2:
+                    flush.fill_(float(r))
+                    a0 = ev()
+                    st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
+                                        chunk_rows=chunk, scratch=scratch, mode=mode)
+                    a1 = ev()
+                    torch.cuda.synchronize()
+                    if r >= 2:
+                        t2[mode].append(a0.elapsed_time(a1))
                 flush.fill_(float(r))
                 b0 = ev()
                 torch.matmul(hid, wgt.t(), out=logits[:, :cfg.V])
@@ -454,20 +459,23 @@ def main_echo(args):
                 b1 = ev()
                 torch.cuda.synchronize()
                 if r >= 2:
-                    t2.append(a0.elapsed_time(a1))
                     t2u.append(b0.elapsed_time(b1))
-            t2_ms, t2u_ms = statistics.median(t2), statistics.median(t2u)
+            t2_ms, t2r_ms, t2u_ms = (statistics.median(t2["chunked"]), statistics.median(t2["recompute"]),
+                                     statistics.median(t2u))
             fl6 = 6.0 * M * hd * cfg.V
             line["f2_train_step"] = {
                 "ms_per_micro_batch": t2_ms, "tokens_per_s_per_gpu": M / (t2_ms * 1e-3), "hidden": hd,
-                "chunk_rows": chunk,
+                "mode": "chunked (echo_lmhead_policy_loss_fwd_bwd)", "chunk_rows": chunk,
+                "chunk_buffer_GB": chunk * cfg.V * 2 / 1e9,
                 "roofline": {"bound": "tensor", "achieved": fl6 / (t2_ms * 1e-3) / 1e12, "peak": pk[0],
                              "unit": "TFLOP/s", "frac": fl6 / (t2_ms * 1e-3) / 1e12 / pk[0], "peak_source": pk[1],
-                             "flops_per_token": 6.0 * hd * cfg.V,
-                             "note": "algorithmic 6 d V flops per token (forward, dh, dW); the recompute of D adds "
-                                     "2 d V more that this figure does not count"},
+                             "flops_per_token": 6.0 * hd * cfg.V},
+                "recompute_ms": t2r_ms,
+                "recompute": "echo_lmhead_logp + echo_loss_from_logp + echo_lmhead_backward (D recomputed: 8 d V "
+                             "flops per token)",
                 "unfused_ms": t2u_ms,
-                "unfused": "cuBLAS logits (10 GB buffer) + echo_policy_loss_fwd_bwd in place + cuBLAS dh, dW",
+                "unfused": f"cuBLAS logits ({M * cfg.V * 2 / 1e9:.1f} GB buffer) + echo_policy_loss_fwd_bwd in place "
+                           "+ cuBLAS dh, dW",
                 "speedup_vs_unfused": t2u_ms / t2_ms}
             del dh, dw, dh_u, dw_u, scratch
         del hid, wgt

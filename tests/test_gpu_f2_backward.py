@@ -289,11 +289,18 @@ def test_lmhead_logits_bf16(n, d, V):
     torch.cuda.synchronize()
     g = _bits(out)
     assert np.all(_bf(out)[:, V:] == 3.0)
-    lo, hi = _bf16_rne(z - tol), _bf16_rne(z + tol)
-    gv = g[:, :V]
-    ok = (gv == lo) | (gv == hi) | (gv == _bf16_rne(z))
-    assert ok.all(), np.argwhere(~ok)[:5]
-    assert (gv == _bf16_rne(z)).mean() > 0.999
+    gz = _bf(out)[:, :V]
+    # |bf16(z_gpu) - z| <= half an ulp of the stored value + the accumulation error of z_gpu (bound doubled, as for logp)
+    err = np.abs(gz - z)
+    print(f"lmhead_logits n={n} d={d} V={V}: max (err - ulp/2) / tol = {np.max((err - 0.5 * _ulp(gz)) / tol):.3f}")
+    assert np.all(err <= 0.5 * _ulp(gz) + 2 * tol), np.max(err / (0.5 * _ulp(gz) + 2 * tol))
+    assert (g[:, :V] == _bf16_rne(z)).mean() > 0.99
+
+
+def _ulp(x):
+    """ulp of bf16 values (8 significant bits)."""
+    x = np.maximum(np.abs(np.asarray(x, np.float64)), 2.0 ** -126)
+    return 2.0 ** (np.floor(np.log2(x)) - 7)
 
 
 @pytest.mark.parametrize("n,d,V,chunk,eta", [(300, 128, 1000, 128, 0.0), (260, 64, 777, 100, 0.01)])
@@ -308,7 +315,7 @@ def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta):
     tol, hf, wf = _z_tol(hb, wb)
     z = hf @ wf.T
     zb = _bf16_rne(z)
-    amb = _bf16_rne(z - tol) != _bf16_rne(z + tol)
+    amb = _bf16_rne(z - 2 * tol) != _bf16_rne(z + 2 * tol)
     rng = np.random.default_rng(n)
     old = (rng.normal(size=n) - 7.0).astype(np.float32)
     ref = (rng.normal(size=n) - 7.0).astype(np.float32)
@@ -329,12 +336,23 @@ def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta):
     abi.echo_lmhead_policy_loss_fwd_bwd(h, w, n, d, V, act, cu(old), cu(ref), cu(slot), cu(adv), None, None, ng, cfg,
                                         lp, loss, flags, ent, dh, dw, 0, ws, chunk)
     torch.cuda.synchronize()
-    clean = ~amb[np.arange(n), a] & (amb.sum(axis=1) < 8)
-    assert clean.mean() > 0.9
+    # per-token bound: an element whose z lies within the GEMM's error of a bf16 rounding boundary may be stored one
+    # ulp away; that moves logp by up to ulp(z_a) at the action and lse by p_v ulp(z_v) elsewhere
+    zf = (zb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    lse = zf[np.arange(n), a] - o.logp
+    pz = np.exp(zf - lse[:, None])
+    u = _ulp(zf) * amb
+    b_lp = 2e-5 + u[np.arange(n), a] + (pz * u).sum(axis=1)
     g_lp = lp.cpu().numpy()
-    assert np.max(np.abs(g_lp - o.logp)[clean]) <= 1e-4
+    assert np.all(np.abs(g_lp - o.logp) <= b_lp), np.max(np.abs(g_lp - o.logp) / b_lp)
+    # the loss moves with logp at most by |dl/dlogp| <= |A| rho + beta (1 + e^(ref - logp)) (times e^b for rho)
     g_loss = loss.cpu().numpy()
-    assert np.max((np.abs(g_loss - o.loss) / np.maximum(np.abs(o.loss), 1))[clean]) <= 1e-4
+    A = adv[slot].astype(np.float64)
+    rho = np.exp(o.logp - old)
+    lip = np.abs(A) * rho * np.exp(b_lp) + kl * (1 + np.exp(ref - o.logp) * np.exp(b_lp))
+    b_loss = lip * b_lp + 1e-5 * np.maximum(np.abs(o.loss), 1)
+    assert np.all(np.abs(g_loss - o.loss) <= b_loss), np.max(np.abs(g_loss - o.loss) / b_loss)
+    clean = np.ones(n, bool)
     absD = np.abs(o.dlogits)
     bh = 2.0 ** -7 * (absD @ np.abs(wf)) + 1e-6 * np.max(np.abs(dh_ref)) + 1e-12
     bw = 2.0 ** -7 * (absD.T @ np.abs(hf)) + 1e-6 * np.max(np.abs(dw_ref)) + 1e-12
