@@ -23,4 +23,9 @@ if [ "${NCU_F2:-1}" = "1" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:lmhead_tile -s 1 -c 1 -o $out/${tag}_f2 \
       python tools/prof_lmhead.py --reps 1 --no-unfused > $out/${tag}_ncu_f2.log 2>&1; echo "ncu_f2=$?" >> $out/${tag}_status.txt
 fi
+if [ "${NCU_F2T:-1}" = "1" ]; then
+  timeout 300 python tools/prof_lmhead.py --mode logits --rows 8192 --reps 1 > $out/${tag}_f2t_plain.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lmhead_tile -s 2 -c 1 -o $out/${tag}_f2_logits \
+      python tools/prof_lmhead.py --mode logits --rows 8192 --reps 1 > $out/${tag}_ncu_f2t.log 2>&1; echo "ncu_f2_logits=$?" >> $out/${tag}_status.txt
+fi
 cat $out/${tag}_status.txt

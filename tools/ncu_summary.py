@@ -101,6 +101,22 @@ def main():
                                           "dram__bytes_write.sum (ncu --set full, 1 launch)"}
     json.dump(tr, open(path, "w"), indent=1)
     print(json.dumps(m, indent=1))
+    # the f2 captures (tensor-core kernels): the fused LM-head log-prob and the logits-store GEMM of the chunked step
+    for name in ("f2", "f2_logits"):
+        src = os.path.join(a.src, f"{t}_{name}.ncu-rep")
+        if not os.path.exists(src):
+            continue
+        rep = os.path.join(a.dst, f"{t}_{name}.ncu-rep")
+        shutil.copy(src, rep)
+        raw = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
+        hdr, units, vals = raw[0], raw[1], raw[2]
+        keys = METRICS + ["sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+                          "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+                          "lts__t_bytes.sum", "sm__pipe_tma_cycles_active.avg.pct_of_peak_sustained_active"]
+        mm = {w: [vals[hdr.index(w)], units[hdr.index(w)]] for w in keys if w in hdr}
+        mm.update({h: [vals[i], units[i]] for i, h in enumerate(hdr) if "tensor" in h and "pct" in h})
+        json.dump(mm, open(os.path.join(a.dst, f"{t}_ncu_{name}_metrics.json"), "w"), indent=1)
+        print(name, json.dumps(mm, indent=1))
 
 
 if __name__ == "__main__":

@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--vocab", type=int, default=151936)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--no-unfused", action="store_true")
-    ap.add_argument("--mode", default="logp", choices=["logp", "dlogits", "backward"],
+    ap.add_argument("--mode", default="logp", choices=["logp", "dlogits", "backward", "logits"],
                     help="logp: echo_lmhead_logp; dlogits: echo_lmhead_dlogits over one chunk of --chunk rows; "
                          "backward: echo_lmhead_backward over --rows in --chunk chunks")
     ap.add_argument("--chunk", type=int, default=8192)
@@ -59,7 +59,11 @@ def main():
         coef = torch.randn(n, generator=g, device="cuda") * 1e-3
         ck = min(a.chunk, n)
         dz = torch.empty(ck, ld, dtype=torch.bfloat16, device="cuda")
-        if a.mode == "dlogits":
+        if a.mode == "logits":
+            fl = 2.0 * ck * d * V
+            ms = timed(lambda: abi.echo_lmhead_logits(h, w, ck, d, V, dz, ld))
+            out.update(chunk=ck, logits_ms=ms, logits_tflops=fl / ms / 1e9, logits_store_GBps=ck * V * 2 / ms / 1e6)
+        elif a.mode == "dlogits":
             fl = 2.0 * ck * d * V
             ms = timed(lambda: abi.echo_lmhead_dlogits(h, w, ck, d, V, act, lse, coef, None, None, dz, ld))
             out.update(chunk=ck, dlogits_ms=ms, dlogits_tflops=fl / ms / 1e9,
