@@ -144,6 +144,7 @@ def oracle_rate(cfg, rank_batch, n_tokens_total, target_s, threads=None):
     os.environ["OMP_NUM_THREADS"] = str(cores)
     import oracle
     import synth
+    oracle.set_threads(cores)
     b = rank_batch
     t0 = time.perf_counter()
     pk = oracle.pack_batch(b.version, b.resp_len, b.action, b.old_logp, b.ref_logp, group_size=cfg.G, max_len=cfg.S,
@@ -156,7 +157,7 @@ def oracle_rate(cfg, rank_batch, n_tokens_total, target_s, threads=None):
     # a pool of sampled rows (numpy twin of the GPU generator; generation is not timed), evaluated repeatedly
     # until ~target_s of oracle time: the oracle's cost per row does not depend on the values
     rng = np.random.default_rng(0)
-    pool = rng.integers(0, pk.n_tokens, 32)
+    pool = rng.integers(0, pk.n_tokens, 16 * cores)   # >= one 16-row OpenMP chunk (schedule(dynamic, 16)) per thread
     z = synth.logits_rows(keys[pool], pk.tok_action[pool], cfg.V, cfg.seed, "bf16" if cfg.dtype == "bf16" else "f32")
     tr = None if pk.tok_ref is None else pk.tok_ref[pool]
     t_loss, rows = 0.0, 0
@@ -189,7 +190,7 @@ def reference_arm(args):
     v = statistics.median([r["tokens_per_s"] for r in results])
     r = results[-1]
     sample = (f"pack+advantage of the full {cfg.name} batch ({cfg.R} rollouts) + fused loss on {r['rows']} sampled rows "
-              f"(V={cfg.V}; a pool of 32 generated rows evaluated repeatedly); whole-step time extrapolated as t_meta + N * t_row")
+              f"(V={cfg.V}; a pool of {16 * r['cores']} generated rows evaluated repeatedly); whole-step time extrapolated as t_meta + N * t_row")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(
                 [x["step_s"] for x in results]), "higher_is_better": True, "scaling": args.scaling,
@@ -484,10 +485,12 @@ def main_echo(args):
         line["config"]["tokens_per_rank_after"] = plans[-1]["tokens_after"]
     if world == 1 and not args.no_cpu_baseline:
         r = oracle_rate(cfg, b, toks_all / args.steps, args.cpu_seconds)
+        r1 = oracle_rate(cfg, b, toks_all / args.steps, args.cpu_seconds / 4, threads=1)
         line["cpu_baseline"] = {
+            "single_thread_tokens_per_s": r1["tokens_per_s"],
             "value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "oracle",
             "cpu_model": _cpu_model(),
-            "sample": f"pack+advantage of the full batch + fused loss on {r['rows']} rows (a pool of 32 sampled rows, repeated) "
+            "sample": f"pack+advantage of the full batch + fused loss on {r['rows']} rows (a pool of {16 * r['cores']} sampled rows, repeated) "
                       f"({r['t_loss']:.1f} s); step extrapolated as t_meta + N * t_row"}
     print(json.dumps(line), flush=True)
     if world > 1:

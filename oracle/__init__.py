@@ -74,6 +74,8 @@ def lib():
         _lib.echo_ref_loss_from_logp.restype = ctypes.c_int
         _lib.echo_ref_lmhead_backward.argtypes = [i64, i32, i32, P, P, P, P, P, P, P, P]
         _lib.echo_ref_lmhead_backward.restype = ctypes.c_int
+        _lib.echo_ref_set_threads.argtypes = [i32]
+        _lib.echo_ref_set_threads.restype = None
     return _lib
 
 
@@ -339,3 +341,8 @@ def lmhead_backward(hidden, weight, tok_action, tok_coef, tok_ecoef=None, want_d
     if rc != 0:
         raise ValueError("echo_ref_lmhead_backward: invalid argument")
     return (dh, dw, dz) if want_dlogits else (dh, dw)
+
+
+def set_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's row loops (timing only; results do not depend on it)."""
+    lib().echo_ref_set_threads(int(n))

@@ -44,6 +44,9 @@
 #include <float.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* ---- status codes (the oracle's own copies; kept independent of include/echo.h) ---- */
 enum { REF_OK = 0, REF_ERR_INVALID_ARGUMENT = 1 };
@@ -685,4 +688,13 @@ int echo_ref_lmhead_backward(int64_t n_rows, int32_t d, int32_t vocab, const dou
   }
   free(D);
   return REF_OK;
+}
+
+/* Thread count of the OpenMP loops above (timing the oracle on one core vs all cores; no effect on results). */
+void echo_ref_set_threads(int32_t n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
 }
