@@ -1,4 +1,6 @@
-// lmhead.cu -- f2: the LM head fused with the log-softmax-and-gather of (3), forward only.
+// lmhead.cu -- f2: the LM head fused with the log-softmax-and-gather of (3), and the two epilogues of
+// the training step through the LM head (lmhead_bwd.cu, abi.cu): D = dL/dz recomputed from h and W (kMode 2,
+// echo_lmhead_dlogits) and the logits themselves stored as bf16 (kMode 3, echo_lmhead_logits).
 //
 // logp_t = z[t, a_t] - logsumexp_v z[t, v],  z = h W^T  (h: [N x d] bf16 hidden states, W: [V x d] bf16 LM-head
 // weight).  The [N x V] logits are never written to HBM: the GEMM runs on the 5th-generation tensor cores with
