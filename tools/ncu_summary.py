@@ -55,6 +55,25 @@ def launch_summary(src_csv, dst_md):
     for k, v in tot.most_common():
         mine = f"{100 * v / echo_ns:.2f}%" if "echo::" in k else "—"
         out.append(f"| `{k[:70]}` | {cnt[k]} | {v / 1e3:.1f} | {100 * v / all_ns:.2f}% | {mine} |")
+    # the learner steps alone: every launch before the first forward-only (logp-mode, `, 2>`) launch, which starts
+    # the f1 / f2 side measurements bench.py runs after its timed steps
+    ids = []
+    for r in rows:
+        if r["Metric Name"] == "gpu__time_duration.sum":
+            ids.append((int(r["ID"]), r["Kernel Name"], r["Metric Value"], r["Metric Unit"]))
+    ids.sort()
+    cut = next((i for i, (_, k, _, _) in enumerate(ids) if "policy_loss" in k and ", 2>" in k), len(ids))
+    st, sc = collections.Counter(), collections.Counter()
+    for _, k, v, u in ids[:cut]:
+        ns = float(v.replace(",", "")) * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(u, 1)
+        st[k] += ns
+        sc[k] += 1
+    step_echo = sum(v for k, v in st.items() if "echo::" in k)
+    out += ["", "## Learner steps only (launches before the post-step f1 / f2 measurements; warm-up + timed steps)", "",
+            "| kernel | launches | total us | share of libecho in the steps |", "|---|---|---|---|"]
+    for k, v in st.most_common():
+        if "echo::" in k:
+            out.append(f"| `{k[:70]}` | {sc[k]} | {v / 1e3:.1f} | {100 * v / step_echo:.2f}% |")
     open(dst_md, "w").write("\n".join(out) + "\n")
 
 
