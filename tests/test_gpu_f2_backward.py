@@ -394,3 +394,37 @@ def test_learner_step_chunked_equals_unchunked_logits_path():
     ref_dh = logits.float() @ w.float()
     rel = (dh - ref_dh).abs().max().item() / ref_dh.abs().max().item()
     assert rel < 1e-3, rel
+
+
+def test_lmhead_policy_loss_edge_cases_and_errors():
+    """n_rows = 0 (dweight zeroed or untouched), a single chunk larger than n, argument errors reported before any
+    launch."""
+    from paper_2508_05387_b200 import abi
+    n, d, V = 40, 64, 300
+    h, w, act = _case(n, d, V, seed=2)
+    z = lambda: torch.zeros(n, device="cuda")
+    slot = torch.zeros(n, dtype=torch.int32, device="cuda")
+    adv = torch.ones(1, device="cuda")
+    ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
+    cfg = abi.LossConfig(0.2, 0.2, 0.0, 0.0, 1.0, abi.ECHO_KL_K3, 0.0)
+    lp, loss = z(), z()
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    dh = torch.empty(n, d, device="cuda")
+    dw = torch.full((V, d), 2.0, device="cuda")
+    ws = torch.empty(4 * n * abi.echo_lmhead_dlogits_ld(V), dtype=torch.bfloat16, device="cuda")
+    args = lambda rows, acc, chunk, c=cfg: (h, w, rows, d, V, act, z(), None, slot, adv, None, None, ng, c, lp, loss,
+                                            flags, None, dh, dw, acc, ws, chunk)
+    abi.echo_lmhead_policy_loss_fwd_bwd(*args(0, 1, 16))
+    torch.cuda.synchronize()
+    assert torch.all(dw == 2.0)
+    abi.echo_lmhead_policy_loss_fwd_bwd(*args(0, 0, 16))
+    torch.cuda.synchronize()
+    assert torch.all(dw == 0.0)
+    abi.echo_lmhead_policy_loss_fwd_bwd(*args(n, 0, 4 * n))          # one chunk covering everything
+    torch.cuda.synchronize()
+    assert torch.isfinite(dh).all() and torch.isfinite(dw).all() and torch.isfinite(lp).all()
+    for bad in (args(n, 0, 0), args(n, 0, 16, abi.LossConfig(1.5, 0.2, 0.0, 0.0, 1.0, abi.ECHO_KL_K3, 0.0))):
+        with pytest.raises(abi.EchoError):
+            abi.echo_lmhead_policy_loss_fwd_bwd(*bad)
+    with pytest.raises(abi.EchoError):                                  # ld not a multiple of 8
+        abi.echo_lmhead_logits(h, w, n, d, V, ws, V)
