@@ -439,14 +439,15 @@ def main_echo(args):
             dw_u = torch.empty(cfg.V, hd, dtype=torch.bfloat16, device=dev)
             scratch = {}
             kl = cfg.kl_coef
-            t2 = {"chunked": [], "recompute": []}
+            t2 = {"chunked": [], "recompute": [], "chunked_cublas": []}
             t2u = []
             for r in range(5):
                 for mode in t2:
                     flush.fill_(float(r))
                     a0 = ev()
                     st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
-                                        chunk_rows=chunk, scratch=scratch, mode=mode)
+                                        chunk_rows=chunk, scratch=scratch, mode=mode.split("_")[0],
+                                        blas="torch" if mode.endswith("cublas") else None)
                     a1 = ev()
                     torch.cuda.synchronize()
                     if r >= 2:
@@ -471,6 +472,8 @@ def main_echo(args):
                 "roofline": {"bound": "tensor", "achieved": fl6 / (t2_ms * 1e-3) / 1e12, "peak": pk[0],
                              "unit": "TFLOP/s", "frac": fl6 / (t2_ms * 1e-3) / 1e12 / pk[0], "peak_source": pk[1],
                              "flops_per_token": 6.0 * hd * cfg.V},
+                "gemms": "dhidden / dweight on libecho's tcgen05 GEMM (2-CTA UMMA, MN-major operands)",
+                "chunked_cublas_ms": statistics.median(t2["chunked_cublas"]),
                 "recompute_ms": t2r_ms,
                 "recompute": "echo_lmhead_logp + echo_loss_from_logp + echo_lmhead_backward (D recomputed: 8 d V "
                              "flops per token)",

@@ -28,10 +28,10 @@ LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_f
             "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1, "echo_csr_from_lengths": 2,
             "echo_lmhead_logp": 2, "echo_staleness_histogram": 1, "echo_pack_batch_v2": 3,
             "echo_loss_from_logp": 1, "echo_lmhead_dlogits": 1, "echo_lmhead_logits": 1}
-# echo_lmhead_backward: per chunk 1 libecho kernel + 2 cuBLAS GEMMs (library kernels, not counted here)
-BACKWARD_LAUNCHES_PER_CHUNK = 1
-# echo_lmhead_policy_loss_fwd_bwd: per chunk 2 libecho kernels (logits, fused loss) + 2 cuBLAS GEMMs
-LMHEAD_LOSS_LAUNCHES_PER_CHUNK = 2
+# echo_lmhead_backward: per chunk 3 libecho kernels (D, dhidden, dweight), or 1 + 2 cuBLAS GEMMs with a handle
+BACKWARD_LAUNCHES_PER_CHUNK = 3
+# echo_lmhead_policy_loss_fwd_bwd: per chunk 4 libecho kernels (logits, fused loss, dhidden, dweight), or 2 + 2 cuBLAS
+LMHEAD_LOSS_LAUNCHES_PER_CHUNK = 4
 
 EXPORTS = ("echo_pack_batch", "echo_pack_batch_v2", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
            "echo_policy_loss_launch_shape", "echo_token_logp", "echo_policy_loss_fwd_bwd_v2", "echo_gae_advantage",
@@ -255,7 +255,8 @@ def echo_lmhead_dlogits_ld(vocab) -> int:
 
 def echo_lmhead_backward(hidden, weight, n_rows, d, vocab, tok_action, tok_lse, tok_coef, tok_ecoef, tok_entropy,
                          dhidden, dweight, accumulate, dlogits_ws, chunk_rows, cublas_handle=None, stream=None):
-    if cublas_handle is None:
+    """cublas_handle: None = this library's tcgen05 GEMMs for dhidden / dweight; "torch" = torch's cuBLAS handle."""
+    if isinstance(cublas_handle, str):
         import torch
         cublas_handle = torch.cuda.current_blas_handle()
     _check("echo_lmhead_backward", _lib.echo_lmhead_backward(
@@ -273,7 +274,8 @@ def echo_lmhead_policy_loss_fwd_bwd(hidden, weight, n_rows, d, vocab, tok_action
                                     tok_adv, tok_weight, n_global, cfg: LossConfig, tok_logp, tok_loss, tok_flags,
                                     tok_entropy, dhidden, dweight, accumulate, logits_ws, chunk_rows,
                                     cublas_handle=None, stream=None):
-    if cublas_handle is None:
+    """cublas_handle: None = this library's tcgen05 GEMMs for dhidden / dweight; "torch" = torch's cuBLAS handle."""
+    if isinstance(cublas_handle, str):
         import torch
         cublas_handle = torch.cuda.current_blas_handle()
     _check("echo_lmhead_policy_loss_fwd_bwd", _lib.echo_lmhead_policy_loss_fwd_bwd(

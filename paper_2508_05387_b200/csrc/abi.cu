@@ -370,8 +370,7 @@ echo_status echo_lmhead_backward(const void* hidden, const void* weight, int64_t
                                  const float* tok_ecoef, const float* tok_entropy, float* dhidden, float* dweight,
                                  int32_t accumulate, void* dlogits_ws, int64_t chunk_rows, void* cublas_handle,
                                  void* stream) {
-  if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || chunk_rows < 1 || chunk_rows > INT32_MAX ||
-      !cublas_handle)
+  if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || chunk_rows < 1 || chunk_rows > INT32_MAX)
     return ECHO_ERR_INVALID_ARGUMENT;
   if (!dweight || (n_rows > 0 && (!tok_action || !tok_lse || !tok_coef || !dhidden || !dlogits_ws ||
                                   !aligned16(dlogits_ws) || (tok_ecoef && !tok_entropy))))
@@ -415,7 +414,7 @@ echo_status echo_lmhead_policy_loss_fwd_bwd(const void* hidden, const void* weig
                                             int32_t accumulate, void* logits_ws, int64_t chunk_rows,
                                             void* cublas_handle, void* stream) {
   if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || chunk_rows < 1 || chunk_rows > INT32_MAX ||
-      !cublas_handle || !dweight || !valid_loss_config(cfg))
+      !dweight || !valid_loss_config(cfg))
     return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rows > 0 && (!dhidden || !logits_ws || !aligned16(logits_ws))) return ECHO_ERR_INVALID_ARGUMENT;
   int sms = 0;
@@ -436,9 +435,15 @@ echo_status echo_lmhead_policy_loss_fwd_bwd(const void* hidden, const void* weig
                                      n_global, cfg, tok_logp + r0, tok_loss + r0, tok_flags + r0,
                                      tok_entropy ? tok_entropy + r0 : nullptr, ECHO_ALGO_AUTO, stream);
     if (st != ECHO_OK) return st;
-    if (echo::cublas_lmhead_grads(cublas_handle, s, weight, hid + r0 * d, logits_ws, ld, rows, d, vocab,
-                                  dhidden + r0 * d, dweight, accumulate || r0 > 0) != 0)
+    if (!cublas_handle) {
+      e = echo::tc_lmhead_grads(s, sms, weight, hid + r0 * d, logits_ws, ld, rows, d, vocab, dhidden + r0 * d, dweight,
+                                accumulate || r0 > 0);
+      if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
+      if (e != cudaSuccess) return ECHO_ERR_CUDA;
+    } else if (echo::cublas_lmhead_grads(cublas_handle, s, weight, hid + r0 * d, logits_ws, ld, rows, d, vocab,
+                                         dhidden + r0 * d, dweight, accumulate || r0 > 0) != 0) {
       return ECHO_ERR_CUDA;
+    }
   }
   return from_cuda(cudaGetLastError());
 }

@@ -93,6 +93,10 @@ cudaError_t launch_lmhead_logits(const void* hidden, const void* weight, int64_t
 int cublas_lmhead_grads(void* cublas_handle, cudaStream_t stream, const void* weight, const void* hidden_chunk,
                         const void* D, int64_t ld, int64_t rows, int32_t d, int32_t V, float* dhidden_chunk,
                         float* dweight, bool beta_one);
+// the same two products on this library's tcgen05 GEMM (gemm.cu)
+cudaError_t tc_lmhead_grads(cudaStream_t stream, int num_sms, const void* weight, const void* hidden_chunk,
+                            const void* D, int64_t ld, int64_t rows, int32_t d, int32_t V, float* dhidden_chunk,
+                            float* dweight, bool beta_one);
 cudaError_t launch_lmhead_backward(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
                                    const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
                                    const float* tok_ecoef, const float* tok_entropy, float* dhidden, float* dweight,

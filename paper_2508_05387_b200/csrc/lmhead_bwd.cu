@@ -1,6 +1,7 @@
 // lmhead_bwd.cu -- f2 backward: dhidden = D W and dweight (+)= D^T h through the LM head, where
 // D = dL/dz of a chunk of tokens is a bf16 [rows x ld] buffer produced by this library's kernels, and the two products
-// are plain cuBLAS bf16 GEMMs (fp32 accumulation and output) on the caller's handle and stream.  Chunks of chunk_rows
+// run on this library's tcgen05 GEMM (gemm.cu; cublas_handle NULL) or as cuBLAS bf16 GEMMs on the caller's handle
+// and stream, both with fp32 accumulation and output.  Chunks of chunk_rows
 // tokens bound the buffer (chunk_rows x ld x 2 bytes).  Two ways to get D:
 //   launch_lmhead_backward  D recomputed from h and W on the tensor cores (lmhead_tile_kernel<.., 2>), given the
 //                           forward's lse / entropy and echo_loss_from_logp's coefficients
@@ -44,6 +45,12 @@ cudaError_t launch_lmhead_backward(const void* hidden, const void* weight, int64
                                           tok_coef + r0, tok_ecoef ? tok_ecoef + r0 : nullptr,
                                           tok_ecoef ? tok_entropy + r0 : nullptr, dlogits_ws, ld, stream, num_sms);
     if (e != cudaSuccess) return e;
+    if (!cublas_handle) {
+      e = tc_lmhead_grads(stream, num_sms, weight, hid + r0 * d, dlogits_ws, ld, rows, d, V, dhidden + r0 * d, dweight,
+                          accumulate || r0 > 0);
+      if (e != cudaSuccess) return e;
+      continue;
+    }
     *cublas_status = cublas_lmhead_grads(cublas_handle, stream, weight, hid + r0 * d, dlogits_ws, ld, rows, d, V,
                                          dhidden + r0 * d, dweight, accumulate || r0 > 0);
     if (*cublas_status != 0) return cudaErrorUnknown;

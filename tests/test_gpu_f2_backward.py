@@ -152,9 +152,10 @@ def test_lmhead_dlogits_matches_oracle(n, d, V, eta):
 
 
 # ------------------------------------------------------------------------------------------ dhidden, dweight
+@pytest.mark.parametrize("blas", [None, "torch"], ids=["tcgen05", "cublas"])
 @pytest.mark.parametrize("n,d,V,chunk,eta", [(300, 128, 1000, 128, 0.0), (257, 64, 777, 300, 0.02),
-                                             (520, 256, 2048, 200, 0.01)])
-def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta):
+                                             (520, 256, 2048, 200, 0.01), (700, 200, 1500, 700, 0.0)])
+def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta, blas):
     """dhidden and dweight (accumulated onto a prefilled buffer) over several chunks with a ragged last chunk.
     Bound: D is bf16 (2^-9 relative) on top of its own ~1e-5 logit error; the GEMMs accumulate in fp32:
     |err| <= 2^-7 (|D| |W|) (resp. |D|^T |h|) + 1e-6 of the row's scale."""
@@ -170,7 +171,7 @@ def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta):
     dw = prev.clone()
     ws = torch.empty(chunk * abi.echo_lmhead_dlogits_ld(V), dtype=torch.bfloat16, device="cuda")
     abi.echo_lmhead_backward(h, w, n, d, V, act, cu(lse), cu(c32), cu(e32), cu(H) if eta > 0 else None, dh, dw, 1,
-                             ws, chunk)
+                             ws, chunk, cublas_handle=blas)
     torch.cuda.synchronize()
     absD = np.abs(dz_ref)
     bh = 2.0 ** -7 * (absD @ np.abs(_bf(w))) + 1e-6 * np.max(np.abs(dh_ref), axis=1, keepdims=True) + 1e-12
@@ -183,7 +184,7 @@ def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta):
     dw2 = torch.full((V, d), float("nan"), device="cuda")
     dh2 = torch.empty(n, d, device="cuda")
     abi.echo_lmhead_backward(h, w, n, d, V, act, cu(lse), cu(c32), cu(e32), cu(H) if eta > 0 else None, dh2, dw2, 0,
-                             ws, chunk)
+                             ws, chunk, cublas_handle=blas)
     torch.cuda.synchronize()
     assert torch.equal(dh, dh2)
     assert np.all(np.abs(dw2.cpu().numpy() - dw_ref) <= bw)
@@ -303,8 +304,9 @@ def _ulp(x):
     return 2.0 ** (np.floor(np.log2(x)) - 7)
 
 
+@pytest.mark.parametrize("blas", [None, "torch"], ids=["tcgen05", "cublas"])
 @pytest.mark.parametrize("n,d,V,chunk,eta", [(300, 128, 1000, 128, 0.0), (260, 64, 777, 100, 0.01)])
-def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta):
+def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta, blas):
     """The chunked f2 step (echo_lmhead_policy_loss_fwd_bwd) against the oracle chain on the same bf16-rounded logits:
     oracle.policy_loss on bf16(h W^T) (fp64 from the bf16 values), then dhidden = D W and dweight = D^T h in fp64.
     Tokens whose action logit lies within the GEMM's fp32 error of a bf16 rounding boundary are excluded from the
@@ -334,7 +336,7 @@ def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta):
     ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
     cfg = abi.LossConfig(0.2, 0.2, 0.0, kl, float(n) / 4, abi.ECHO_KL_K3, eta)
     abi.echo_lmhead_policy_loss_fwd_bwd(h, w, n, d, V, act, cu(old), cu(ref), cu(slot), cu(adv), None, None, ng, cfg,
-                                        lp, loss, flags, ent, dh, dw, 0, ws, chunk)
+                                        lp, loss, flags, ent, dh, dw, 0, ws, chunk, cublas_handle=blas)
     torch.cuda.synchronize()
     # per-token bound: an element whose z lies within the GEMM's error of a bf16 rounding boundary may be stored one
     # ulp away; that moves logp by up to ulp(z_a) at the action and lse by p_v ulp(z_v) elsewhere
