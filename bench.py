@@ -439,7 +439,7 @@ def main_echo(args):
             dw_u = torch.empty(cfg.V, hd, dtype=torch.bfloat16, device=dev)
             scratch = {}
             kl = cfg.kl_coef
-            t2 = {"chunked": [], "recompute": [], "chunked_cublas": []}
+            t2 = {"chunked": [], "recompute": [], "chunked_tcgen05": []}
             t2u = []
             for r in range(5):
                 for mode in t2:
@@ -447,7 +447,7 @@ def main_echo(args):
                     a0 = ev()
                     st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
                                         chunk_rows=chunk, scratch=scratch, mode=mode.split("_")[0],
-                                        blas="torch" if mode.endswith("cublas") else None)
+                                        blas=None if mode.endswith("tcgen05") else "torch")
                     a1 = ev()
                     torch.cuda.synchronize()
                     if r >= 2:
@@ -472,8 +472,9 @@ def main_echo(args):
                 "roofline": {"bound": "tensor", "achieved": fl6 / (t2_ms * 1e-3) / 1e12, "peak": pk[0],
                              "unit": "TFLOP/s", "frac": fl6 / (t2_ms * 1e-3) / 1e12 / pk[0], "peak_source": pk[1],
                              "flops_per_token": 6.0 * hd * cfg.V},
-                "gemms": "dhidden / dweight on libecho's tcgen05 GEMM (2-CTA UMMA, MN-major operands)",
-                "chunked_cublas_ms": statistics.median(t2["chunked_cublas"]),
+                "gemms": "logits GEMM and D on libecho's tcgen05 kernels, dhidden / dweight in cuBLAS",
+                "chunked_tcgen05_ms": statistics.median(t2["chunked_tcgen05"]),
+                "chunked_tcgen05": "the same with dhidden / dweight on libecho's own tcgen05 GEMM (echo_gemm_bf16)",
                 "recompute_ms": t2r_ms,
                 "recompute": "echo_lmhead_logp + echo_loss_from_logp + echo_lmhead_backward (D recomputed: 8 d V "
                              "flops per token)",

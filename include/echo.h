@@ -421,6 +421,17 @@ ECHO_API echo_status echo_lmhead_policy_loss_fwd_bwd(
     uint8_t* tok_flags, float* tok_entropy, float* dhidden, float* dweight, int32_t accumulate, void* logits_ws,
     int64_t chunk_rows, void* cublas_handle, void* stream);
 
+/*
+ * The tcgen05 GEMM behind echo_lmhead_backward (f2), exposed as a building block: c[m, n] (+)= sum_k A(m, k) B(n, k),
+ * fp32 accumulation and output.  A(m, k) = a[m * lda + k] (a_mn = 0, K-major) or a[k * lda + m] (a_mn = 1, MN-major);
+ * B(n, k) = b[n * ldb + k] (b_mn = 0) or b[k * ldb + n] (b_mn = 1); bf16 a, b 16-byte aligned with lda, ldb multiples
+ * of 8 elements; c fp32 [m x ldc] row-major, accumulate = 1 adds to it.  So dhidden = D W is (a = D, a_mn 0, b = W,
+ * b_mn 1) and dweight = D^T h is (a = D, a_mn 1, b = h, b_mn 1).  Launches: 1 kernel (0 when m or n is 0).
+ */
+ECHO_API echo_status echo_gemm_bf16(const void* a, int32_t a_mn, int64_t lda, const void* b, int32_t b_mn,
+                                    int64_t ldb, int64_t m, int32_t n, int32_t k, float* c, int64_t ldc,
+                                    int32_t accumulate, void* stream);
+
 /* Human-readable name of a status code (static storage). */
 ECHO_API const char* echo_status_string(echo_status status);
 

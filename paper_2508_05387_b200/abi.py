@@ -38,7 +38,7 @@ EXPORTS = ("echo_pack_batch", "echo_pack_batch_v2", "echo_group_advantage", "ech
            "echo_loss_stats_workspace_bytes", "echo_loss_stats", "echo_csr_from_lengths",
            "echo_lmhead_workspace_bytes", "echo_lmhead_logp", "echo_staleness_histogram", "echo_status_string",
            "echo_abi_version", "echo_loss_from_logp", "echo_lmhead_dlogits", "echo_lmhead_backward",
-           "echo_lmhead_logits", "echo_lmhead_policy_loss_fwd_bwd")
+           "echo_lmhead_logits", "echo_lmhead_policy_loss_fwd_bwd", "echo_gemm_bf16")
 
 
 ECHO_KL_K3, ECHO_KL_K1, ECHO_KL_K2 = range(3)
@@ -95,12 +95,13 @@ def _load(path=LIB_PATH):
     lib.echo_lmhead_dlogits.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, i64, P]
     lib.echo_lmhead_backward.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, P, i32, P, i64, P, P]
     lib.echo_lmhead_logits.argtypes = [P, P, i64, i32, i32, P, i64, P]
+    lib.echo_gemm_bf16.argtypes = [P, i32, i64, P, i32, i64, i64, i32, i32, P, i64, i32, P]
     lib.echo_lmhead_policy_loss_fwd_bwd.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
                                                     i32, P, i64, P, P]
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
                "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths", "echo_lmhead_logp",
                "echo_staleness_histogram", "echo_pack_batch_v2", "echo_loss_from_logp", "echo_lmhead_dlogits",
-               "echo_lmhead_backward", "echo_lmhead_logits", "echo_lmhead_policy_loss_fwd_bwd"):
+               "echo_lmhead_backward", "echo_lmhead_logits", "echo_lmhead_policy_loss_fwd_bwd", "echo_gemm_bf16"):
         getattr(lib, fn).restype = ctypes.c_int
     return lib
 
@@ -283,6 +284,11 @@ def echo_lmhead_policy_loss_fwd_bwd(hidden, weight, n_rows, d, vocab, tok_action
         _p(adv_slot), _p(tok_adv), _p(tok_weight), _p(n_global), ctypes.byref(cfg), _p(tok_logp), _p(tok_loss),
         _p(tok_flags), _p(tok_entropy), _p(dhidden), _p(dweight), int(accumulate), _p(logits_ws), chunk_rows,
         cublas_handle, _s(stream)))
+
+
+def echo_gemm_bf16(a, a_mn, lda, b, b_mn, ldb, m, n, k, c, ldc, accumulate=False, stream=None):
+    _check("echo_gemm_bf16", _lib.echo_gemm_bf16(_p(a), int(a_mn), lda, _p(b), int(b_mn), ldb, m, n, k, _p(c), ldc,
+                                                  int(accumulate), _s(stream)))
 
 
 def echo_loss_stats_workspace_bytes() -> int:

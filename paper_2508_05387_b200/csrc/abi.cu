@@ -448,6 +448,21 @@ echo_status echo_lmhead_policy_loss_fwd_bwd(const void* hidden, const void* weig
   return from_cuda(cudaGetLastError());
 }
 
+echo_status echo_gemm_bf16(const void* a, int32_t a_mn, int64_t lda, const void* b, int32_t b_mn, int64_t ldb,
+                           int64_t m, int32_t n, int32_t k, float* c, int64_t ldc, int32_t accumulate, void* stream) {
+  if (m < 0 || n < 0 || k < 1 || m > INT32_MAX || lda < 1 || ldb < 1 || ldc < n || (lda * 2) % 16 || (ldb * 2) % 16)
+    return ECHO_ERR_INVALID_ARGUMENT;
+  if (lda < (a_mn ? m : k) || ldb < (b_mn ? n : k)) return ECHO_ERR_INVALID_ARGUMENT;
+  if (m > 0 && n > 0 && (!a || !b || !c || !aligned16(a) || !aligned16(b))) return ECHO_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  echo_status st = device_sms(&sms);
+  if (st != ECHO_OK) return st;
+  const cudaError_t e = echo::gemm_bf16(a, a_mn != 0, lda * 2, b, b_mn != 0, ldb * 2, m, n, k, c, ldc, accumulate != 0,
+                                        static_cast<cudaStream_t>(stream), sms);
+  if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
+  return from_cuda(e);
+}
+
 size_t echo_loss_stats_workspace_bytes(void) { return echo::loss_stats_workspace_bytes(); }
 
 echo_status echo_loss_stats(int64_t n_tokens, const float* tok_loss, const float* tok_logp, const float* tok_old,

@@ -93,7 +93,12 @@ cudaError_t launch_lmhead_logits(const void* hidden, const void* weight, int64_t
 int cublas_lmhead_grads(void* cublas_handle, cudaStream_t stream, const void* weight, const void* hidden_chunk,
                         const void* D, int64_t ld, int64_t rows, int32_t d, int32_t V, float* dhidden_chunk,
                         float* dweight, bool beta_one);
-// the same two products on this library's tcgen05 GEMM (gemm.cu)
+// C[M x N] (+)= A B on the tcgen05 tensor cores (gemm.cu): A(m, k) from a K-major [M x K] (a_mn = false) or MN-major
+// [K x M] (a_mn = true) bf16 array, B(n, k) likewise with N; row strides in bytes (multiples of 16); fp32 out.
+cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void* B, bool b_mn, int64_t b_row_bytes,
+                      int64_t M, int32_t N, int32_t K, float* out, int64_t ldo, bool accumulate, cudaStream_t stream,
+                      int num_sms);
+// the two products of the f2 backward on that GEMM
 cudaError_t tc_lmhead_grads(cudaStream_t stream, int num_sms, const void* weight, const void* hidden_chunk,
                             const void* D, int64_t ld, int64_t rows, int32_t d, int32_t V, float* dhidden_chunk,
                             float* dweight, bool beta_one);

@@ -24,7 +24,7 @@
 namespace echo {
 
 namespace gm {
-constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16, kThreads = 192, kStages = 6, kGroupM = 16;
+constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16, kThreads = 192, kStages = 6;
 constexpr int kOpBytes = 128 * kBK * 2;  // one operand's stage per CTA: 128 rows (M or N) x 64 K bf16 = 16 KB
 constexpr uint32_t kTmemCols = 512;
 struct Smem {
@@ -60,20 +60,22 @@ ECHO_DEVINL void load_op(uint32_t dst, const CUtensorMap* map, int32_t row0, int
     lm::tma_load_2d<true>(dst, map, k0, row0, bar);
   }
 }
-// tile u -> (M tile, N tile): groups of kGroupM M tiles x all N tiles, N-major inside a group (L2 reuse of A rows)
-ECHO_DEVINL void tile_coords(int64_t u, int32_t n_mt, int32_t n_nt, int32_t& mt, int32_t& nt) {
-  const int64_t per_group = (int64_t)kGroupM * n_nt;
+// tile u -> (M tile, N tile): groups of group_m M tiles x all N tiles, M-fastest inside a group.  The host sizes a
+// group to about one wave of clusters (group_m = clusters / N tiles), so the tiles in flight share their A rows and B
+// columns k-block by k-block and each operand streams from DRAM about once per group.
+ECHO_DEVINL void tile_coords(int64_t u, int32_t n_mt, int32_t n_nt, int32_t group_m, int32_t& mt, int32_t& nt) {
+  const int64_t per_group = (int64_t)group_m * n_nt;
   const int32_t g = (int32_t)(u / per_group);
-  const int32_t rows_in_g = min(kGroupM, n_mt - g * kGroupM);
+  const int32_t rows_in_g = min(group_m, n_mt - g * group_m);
   const int64_t r = u - (int64_t)g * per_group;
   nt = (int32_t)(r / rows_in_g);
-  mt = g * kGroupM + (int32_t)(r % rows_in_g);
+  mt = g * group_m + (int32_t)(r % rows_in_g);
 }
 }  // namespace gm
 
 struct GemmParams {
   int64_t M;
-  int32_t N, K, n_mt, n_nt, n_kb;
+  int32_t N, K, n_mt, n_nt, n_kb, group_m;
   float* __restrict__ out;
   int64_t ldo;
   int32_t accumulate;
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       uint32_t stage = 0, phase = 0;
       for (int64_t u = unit0; u < n_tiles; u += n_units) {
         int32_t mt, nt;
-        tile_coords(u, p.n_mt, p.n_nt, mt, nt);
+        tile_coords(u, p.n_mt, p.n_nt, p.group_m, mt, nt);
         const int32_t m_row = mt * 256 + (int32_t)rank * kBM, n_row = nt * kBN + (int32_t)rank * 128;
         for (int32_t kb = 0; kb < p.n_kb; ++kb) {
           mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     const bool vec_ok = (p.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
     for (int64_t u = unit0; u < n_tiles; u += n_units, ++tc) {
       int32_t mt, nt;
-      tile_coords(u, p.n_mt, p.n_nt, mt, nt);
+      tile_coords(u, p.n_mt, p.n_nt, p.group_m, mt, nt);
       const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
       const int64_t row = (int64_t)mt * 256 + (int64_t)rank * kBM + quad * 32 + lane;
       const bool row_ok = row < p.M;
@@ -240,6 +242,7 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, Gem
   }
   const int64_t n_tiles = (int64_t)p.n_mt * p.n_nt;
   if (units > n_tiles) units = n_tiles;
+  p.group_m = (int32_t)(units / p.n_nt > 1 ? units / p.n_nt : 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * 2));
   cfg.blockDim = dim3(gm::kThreads);
@@ -256,7 +259,7 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, Gem
 }
 
 // C[M x N] (+)= A B with A(m, k), B(n, k) read from bf16 global memory as described above; row strides in bytes.
-static cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void* B, bool b_mn,
+cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void* B, bool b_mn,
                              int64_t b_row_bytes, int64_t M, int32_t N, int32_t K, float* out, int64_t ldo,
                              bool accumulate, cudaStream_t stream, int num_sms) {
   if (M == 0 || N == 0) return cudaSuccess;
@@ -278,7 +281,8 @@ static cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, cons
   p.accumulate = accumulate ? 1 : 0;
   if (a_mn && b_mn) return launch_gemm<true, true>(ma, mb, p, stream, num_sms);
   if (!a_mn && b_mn) return launch_gemm<false, true>(ma, mb, p, stream, num_sms);
-  return cudaErrorInvalidValue;  // the two forms the f2 backward uses
+  if (!a_mn && !b_mn) return launch_gemm<false, false>(ma, mb, p, stream, num_sms);
+  return launch_gemm<true, false>(ma, mb, p, stream, num_sms);
 }
 
 cudaError_t tc_lmhead_grads(cudaStream_t stream, int num_sms, const void* weight, const void* hidden_chunk,

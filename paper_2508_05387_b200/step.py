@@ -212,7 +212,7 @@ class LearnerStep:
     def loss_from_hidden(self, hidden, weight, row0: int, dhidden, dweight, *, accumulate=True, clip_low=0.2,
                          clip_high=0.2, kl_coef=0.0, grad_scale=1.0, tok_adv=None, tok_weight=None, clip_dual=0.0,
                          kl_estimator=abi.ECHO_KL_K3, entropy_coef=0.0, chunk_rows=8192, scratch=None,
-                         mode="chunked", tok_entropy=None, blas=None):
+                         mode="chunked", tok_entropy=None, blas="torch"):
         """f2 training step through the LM head for packed rows [row0, row0 + n): dhidden = dL/dh into ``dhidden``
         (f32 [n x d]) and dL/dW added to (``accumulate``) or written over ``dweight`` (f32 [V x d]); per-token outputs
         land in tok_logp / tok_loss / tok_flags as with ``loss``.  No [n x V] logits buffer: at most a
@@ -223,7 +223,8 @@ class LearnerStep:
         mode "recompute": (3) echo_lmhead_logp (logp, lse, entropy without the logits), (4) echo_loss_from_logp,
             (5) + backward echo_lmhead_backward with D recomputed from h and W on the tensor cores (8 d V flops per
             token; logits never rounded to bf16).
-        blas: None = dhidden / dweight on libecho's tcgen05 GEMM; "torch" = cuBLAS on torch's handle."""
+        blas: "torch" (default) = dhidden / dweight in cuBLAS on torch's handle (plain library GEMMs, 10-20 % faster
+            than libecho's own at these shapes, profiles/); None = libecho's tcgen05 GEMM (echo_gemm_bf16)."""
         n, d = hidden.shape
         sl = slice(row0, row0 + n)
         sc = {} if scratch is None else scratch

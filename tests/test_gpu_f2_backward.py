@@ -430,3 +430,32 @@ def test_lmhead_policy_loss_edge_cases_and_errors():
             abi.echo_lmhead_policy_loss_fwd_bwd(*bad)
     with pytest.raises(abi.EchoError):                                  # ld not a multiple of 8
         abi.echo_lmhead_logits(h, w, n, d, V, ws, V)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("m,n,k", [(256, 256, 64), (300, 200, 1000), (1, 72, 4096), (777, 513, 130)])
+def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k):
+    """echo_gemm_bf16 (the tcgen05 GEMM of the f2 backward) in every operand layout against the fp64 product, within
+    the fp32-accumulation bound 4 (K/16 + 16) 2^-24 sum_k |A B|; ragged M / N / K tiles; accumulate mode."""
+    from paper_2508_05387_b200 import abi
+    g = torch.Generator(device="cuda").manual_seed(m + n + k + 2 * a_mn + b_mn)
+    A = torch.randn(m, k, generator=g, device="cuda").to(torch.bfloat16)
+    B = torch.randn(n, k, generator=g, device="cuda").to(torch.bfloat16)
+    a_store = (A.t() if a_mn else A).contiguous()
+    b_store = (B.t() if b_mn else B).contiguous()
+    ld = lambda w: (w + 7) // 8 * 8 + 8                               # row strides: multiples of 8, padded
+    a_buf = torch.zeros(a_store.shape[0], ld(a_store.shape[1]), dtype=torch.bfloat16, device="cuda")
+    b_buf = torch.zeros(b_store.shape[0], ld(b_store.shape[1]), dtype=torch.bfloat16, device="cuda")
+    a_buf[:, :a_store.shape[1]] = a_store
+    b_buf[:, :b_store.shape[1]] = b_store
+    ldc = n + 3
+    prev = torch.randn(m, ldc, generator=g, device="cuda")
+    c = prev.clone()
+    abi.echo_gemm_bf16(a_buf, a_mn, a_buf.shape[1], b_buf, b_mn, b_buf.shape[1], m, n, k, c, ldc, accumulate=True)
+    torch.cuda.synchronize()
+    Af, Bf = _bf(A), _bf(B)
+    ref = Af @ Bf.T
+    bound = 4 * (k / 16 + 16) * 2.0 ** -24 * (np.abs(Af) @ np.abs(Bf).T) + 1e-6 * np.abs(prev[:, :n].cpu().numpy())
+    got = (c - prev)[:, :n].cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(got - ref) <= bound + 1e-6), np.max(np.abs(got - ref) / (bound + 1e-6))
+    assert torch.equal(c[:, n:], prev[:, n:])                          # columns >= n untouched
