@@ -52,12 +52,12 @@ constexpr uint32_t idesc() {
 }
 // stage one operand's 128 rows (M or N) x 64 K of this CTA
 template <bool kMN>
-ECHO_DEVINL void load_op(uint32_t dst, const CUtensorMap* map, int32_t row0, int32_t k0, uint32_t bar) {
+ECHO_DEVINL void load_op(uint32_t dst, const CUtensorMap* map, int32_t row0, int32_t k0, uint32_t bar, uint64_t pol) {
   if constexpr (kMN) {  // global [K x rows]: two boxes {64 rows, 64 K}
-    lm::tma_load_2d<true>(dst, map, row0, k0, bar);
-    lm::tma_load_2d<true>(dst + 8192, map, row0 + 64, k0, bar);
+    lm::tma_load_2d_pair_hint(dst, map, row0, k0, bar, pol);
+    lm::tma_load_2d_pair_hint(dst + 8192, map, row0 + 64, k0, bar, pol);
   } else {              // global [rows x K]: one box {64 K, 128 rows}
-    lm::tma_load_2d<true>(dst, map, k0, row0, bar);
+    lm::tma_load_2d_pair_hint(dst, map, k0, row0, bar, pol);
   }
 }
 // tile u -> (M tile, N tile): groups of group_m M tiles x all N tiles, M-fastest inside a group.  The host sizes a
@@ -76,6 +76,8 @@ ECHO_DEVINL void tile_coords(int64_t u, int32_t n_mt, int32_t n_nt, int32_t grou
 struct GemmParams {
   int64_t M;
   int32_t N, K, n_mt, n_nt, n_kb, group_m;
+  int32_t pol_a, pol_b;  // L2 policy per operand: 2 = evict_last (small, re-read by every tile), 1 = evict_first
+                         // (streamed past a kept operand), 0 = evict_normal
   float* __restrict__ out;
   int64_t ldo;
   int32_t accumulate;
@@ -123,6 +125,10 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      const uint64_t pol_a = p.pol_a == 2 ? policy_evict_last() : p.pol_a == 1 ? policy_evict_first()
+                                                                                : policy_evict_normal();
+      const uint64_t pol_b = p.pol_b == 2 ? policy_evict_last() : p.pol_b == 1 ? policy_evict_first()
+                                                                                : policy_evict_normal();
       for (int64_t u = unit0; u < n_tiles; u += n_units) {
         int32_t mt, nt;
         tile_coords(u, p.n_mt, p.n_nt, p.group_m, mt, nt);
@@ -131,8 +137,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
           mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
           const uint32_t bar = mapa(smem_u32(&sm.full[stage]), 0);
           if (leader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), 4 * kOpBytes);
-          load_op<kAMN>(smem_u32(sm.a[stage]), &map_a, m_row, kb * kBK, bar);
-          load_op<kBMN>(smem_u32(sm.b[stage]), &map_b, n_row, kb * kBK, bar);
+          load_op<kAMN>(smem_u32(sm.a[stage]), &map_a, m_row, kb * kBK, bar, pol_a);
+          load_op<kBMN>(smem_u32(sm.b[stage]), &map_b, n_row, kb * kBK, bar, pol_b);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
@@ -279,6 +285,13 @@ cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void*
   p.out = out;
   p.ldo = ldo;
   p.accumulate = accumulate ? 1 : 0;
+  // an operand small enough to stay in L2 (<= 48 MB, e.g. h of a chunk for dweight) is kept there while the large one
+  // streams through with evict_first; with both large, both load with evict_normal (grouped tiles share k-blocks)
+  const int64_t a_bytes = M * (int64_t)K * 2, b_bytes = (int64_t)N * K * 2;
+  const bool keep_a = a_bytes <= (48ll << 20) && a_bytes < b_bytes;
+  const bool keep_b = !keep_a && b_bytes <= (48ll << 20) && b_bytes <= a_bytes;
+  p.pol_a = keep_a ? 2 : keep_b ? 1 : 0;
+  p.pol_b = keep_b ? 2 : keep_a ? 1 : 0;
   if (a_mn && b_mn) return launch_gemm<true, true>(ma, mb, p, stream, num_sms);
   if (!a_mn && b_mn) return launch_gemm<false, true>(ma, mb, p, stream, num_sms);
   if (!a_mn && !b_mn) return launch_gemm<false, false>(ma, mb, p, stream, num_sms);

@@ -31,6 +31,16 @@ ECHO_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t x, in
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
         : "memory");
 }
+// Same (pair form) with an L2 cache policy (createpolicy: evict_first for a streamed operand, evict_last for one that
+// every tile re-reads).
+ECHO_DEVINL void tma_load_2d_pair_hint(uint32_t dst, const CUtensorMap* map, int32_t x, int32_t y, uint32_t bar,
+                                       uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
+      : "memory");
+}
 // Arrive on `bar` when the MMAs issued so far have completed: this CTA's barrier, or (pair) the barrier at the
 // same offset in both CTAs of the pair.
 template <bool kPair>
