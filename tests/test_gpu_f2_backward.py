@@ -459,3 +459,37 @@ def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k):
     got = (c - prev)[:, :n].cpu().numpy().astype(np.float64)
     assert np.all(np.abs(got - ref) <= bound + 1e-6), np.max(np.abs(got - ref) / (bound + 1e-6))
     assert torch.equal(c[:, n:], prev[:, n:])                          # columns >= n untouched
+
+
+def test_chunked_f4_options_equal_the_logits_path():
+    """The chunked step offsets every per-token array per chunk: with per-token advantages and weights, the k2 KL,
+    the dual clip and the entropy bonus, its tok_logp / tok_loss / tok_flags / tok_entropy equal (bit for bit) the
+    logits path's (echo_lmhead_logits for all rows, then echo_policy_loss_fwd_bwd_v2)."""
+    from paper_2508_05387_b200 import abi
+    n, d, V, chunk = 1000, 256, 4099, 384
+    h, w, act = _case(n, d, V, seed=11)
+    g = torch.Generator(device="cuda").manual_seed(12)
+    old = torch.randn(n, generator=g, device="cuda") - 8.0
+    ref = torch.randn(n, generator=g, device="cuda") - 8.0
+    tadv = torch.randn(n, generator=g, device="cuda")
+    twt = torch.rand(n, generator=g, device="cuda") / n
+    cfg = abi.LossConfig(0.2, 0.28, 3.0, 0.05, 2.0, abi.ECHO_KL_K2, 0.01)
+    outs = []
+    for path in ("chunked", "logits"):
+        lp, loss, ent = (torch.empty(n, device="cuda") for _ in range(3))
+        flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+        if path == "chunked":
+            ws = torch.empty(chunk * abi.echo_lmhead_dlogits_ld(V), dtype=torch.bfloat16, device="cuda")
+            dh, dw = torch.empty(n, d, device="cuda"), torch.empty(V, d, device="cuda")
+            abi.echo_lmhead_policy_loss_fwd_bwd(h, w, n, d, V, act, old, ref, None, None, tadv, twt, None, cfg, lp,
+                                                loss, flags, ent, dh, dw, 0, ws, chunk)
+        else:
+            ld = abi.echo_lmhead_dlogits_ld(V)
+            z = torch.empty(n, ld, dtype=torch.bfloat16, device="cuda")
+            abi.echo_lmhead_logits(h, w, n, d, V, z, ld)
+            abi.echo_policy_loss_fwd_bwd_v2(z, abi.ECHO_BF16, n, V, ld, act, old, ref, None, None, tadv, twt, None,
+                                            cfg, lp, loss, flags, tok_entropy=ent)
+        torch.cuda.synchronize()
+        outs.append((lp, loss, flags, ent))
+    for a, b in zip(*outs):
+        assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
