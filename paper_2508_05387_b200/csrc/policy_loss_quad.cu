@@ -39,7 +39,8 @@ namespace echo {
 //   QCfg<4, 8>: 4-CTA cluster, 2 CTAs (2 rows) per SM  -- ECHO_ALGO_QUAD_REG
 //   QCfg<8, 4>: 8-CTA cluster, 4 CTAs (4 rows) per SM  -- ECHO_ALGO_OCT_REG
 //   QCfg<16, 4>: 16-CTA cluster, 4 CTAs per SM          -- ECHO_ALGO_HEX_REG (vocabularies up to 311296)
-template <int kCtas_, int kWarps_, bool kF32_ = false>
+//   QCfg<16, 4, false, 10, 8>: logp mode only -- 16-CTA cluster, 8 CTAs per SM (32 warps), 10 vectors per thread
+template <int kCtas_, int kWarps_, bool kF32_ = false, int kRegChunks_ = 19, int kCtasPerSm_ = 16 / kWarps_>
 struct QCfg {
   static constexpr int kCtas = kCtas_;                  // CTAs per row (cluster size)
   static constexpr int kWarps = kWarps_;                // all warps compute; warp 0 also issues the TMA loads
@@ -49,9 +50,10 @@ struct QCfg {
   static constexpr int kThreads = kWarps * 32;
   static constexpr int kChunk = kThreads * 16;          // one 16-byte vector per thread
   static constexpr int kChunkElems = kChunk / kElemBytes;
-  static constexpr int kCtasPerSm = 16 / kWarps;
-  static constexpr int kRing = kCtasPerSm == 2 ? 28 : 27;  // staging ring slots (~1.5 slices; fills the SM)
-  static constexpr int kRegChunks = 19;                 // V <= kCtas * 19 * kChunkElems (155648 for 8 CTAs)
+  static constexpr int kCtasPerSm = kCtasPerSm_;
+  // staging ring slots (~1.5 slices; fills the SM's shared memory)
+  static constexpr int kRing = kCtasPerSm == 2 ? 28 : kCtasPerSm == 4 ? 27 : 13;
+  static constexpr int kRegChunks = kRegChunks_;        // V <= kCtas * kRegChunks * kChunkElems (155648 for 8 x 19)
 };
 constexpr int kQBar = 1;                                // named barrier id
 
@@ -623,8 +625,14 @@ cudaError_t launch_hex(const LossParams& p, int32_t dtype, cudaStream_t stream, 
 }
 // forward-only log-probs: the 8-CTA tile (1.93 ms vs 1.97 ms for the 4-CTA one on 32768 x 151936), the 16-CTA
 // tile past its vocabulary range
+#ifdef ECHO_LOGP_HEX8
+using HexLogp = QCfg<16, 4, false, 10, 8>;
+#endif
 cudaError_t launch_quad_logp(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape) {
   if (dtype == ECHO_F32) return launch_t<HexF, kModeLogp>(p, stream, num_sms, shape);
+#ifdef ECHO_LOGP_HEX8
+  if (supports_t<HexLogp>(ECHO_BF16, p.V)) return launch_t<HexLogp, kModeLogp>(p, stream, num_sms, shape);
+#endif
   if (!supports_t<Oct>(ECHO_BF16, p.V)) return launch_t<Hex, kModeLogp>(p, stream, num_sms, shape);
   return launch_t<Oct, kModeLogp>(p, stream, num_sms, shape);
 }

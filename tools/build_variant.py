@@ -14,7 +14,7 @@ spec.loader.exec_module(b)
 name, defs = sys.argv[1], sys.argv[2:]
 os.makedirs(os.path.join(ROOT, "ab_libs"), exist_ok=True)
 out = os.path.join(ROOT, "ab_libs", f"libecho_{name}.so")
-cmd = [b.NVCC, *b.ARCH, *b.FLAGS, *defs, "-I", b.INCLUDE, "-I", b.CSRC, "-o", out, *b.sources()]
+cmd = [b.NVCC, *b.ARCH, *b.FLAGS, *defs, "-I", b.INCLUDE, "-I", b.CSRC, "-o", out, *b.sources(), *b.LIBS]
 r = subprocess.run(cmd, capture_output=True, text=True)
 if r.returncode:
     sys.exit(r.stderr)
