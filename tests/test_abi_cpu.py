@@ -55,7 +55,7 @@ def test_quad_kernel_uses_tma_bulk_copies_and_dsmem():
     blocks = re.split(r"\n\s*Function : ", sass)
     quad = [b for b in blocks if "policy_loss_quad_kernel" in b.split("\n", 1)[0]]
     assert len(quad) == 12          # 4-CTA cache / exact / entropy; 8- and 16-CTA (bf16, fp32) cache / logp / entropy
-    for tag in ("QCfgILi8ELi4ELb0EEELi1E", "QCfgILi4ELi8ELb0EEELi1E"):   # 8-CTA (AUTO) and 4-CTA, fp16-cache mode
+    for tag in ("QCfgILi8ELi4ELb0ELi19ELi4EEELi1E", "QCfgILi4ELi8ELb0ELi19ELi2EEELi1E"):   # 8-CTA (AUTO) and 4-CTA, fp16-cache mode
         body = [b for b in quad if tag in b.split("\n", 1)[0]][0]
         assert "UBLKCP.S.G" in body      # cp.async.bulk global->shared (TMA engine)
         assert "SYNCS" in body           # mbarrier phase / tx tracking
