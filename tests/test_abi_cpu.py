@@ -93,3 +93,17 @@ def test_missing_library_fails_loudly(tmp_path):
     r = subprocess.run([sys.executable, "-c", "import paper_2508_05387_b200"], cwd=tmp_path, capture_output=True,
                        text=True)
     assert r.returncode != 0 and "not built" in r.stderr
+
+
+def test_tensor_core_kernels_use_tcgen05_and_tma():
+    """f2's LM-head kernels (every epilogue mode) and the backward GEMM (every operand layout) are 2-CTA tcgen05
+    kernels fed by TMA tensor loads: UTCHMMA.2CTA (tcgen05.mma cta_group::2), UTMALDG.2D.2CTA, TMEM loads (LDTM),
+    no legacy HMMA and no register spills."""
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", os.path.join(PKG, "libecho.so")],
+                          capture_output=True, text=True, check=True).stdout
+    blocks = re.split(r"\n\s*Function : ", sass)
+    tc = [b for b in blocks if re.search(r"(lmhead_tile_kernel|gemm_tile_kernel)", b.split("\n", 1)[0])]
+    assert len(tc) == 8          # lmhead modes 0..3, gemm (A, B) in {K, MN}-major
+    for body in tc:
+        assert "UTCHMMA.2CTA" in body and "UTMALDG.2D.2CTA" in body and "LDTM" in body
+        assert " HMMA" not in body and "LDL" not in body and "STL" not in body
