@@ -493,3 +493,42 @@ def test_chunked_f4_options_equal_the_logits_path():
         outs.append((lp, loss, flags, ent))
     for a, b in zip(*outs):
         assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+
+
+def test_chunked_step_deterministic_and_graph_capturable():
+    """The chunked f2 step on libecho's own kernels (no cuBLAS) is bitwise repeatable, and a CUDA graph of it replays
+    to the same bits (the fused kernel's row scheduler resets its own counter slot)."""
+    from paper_2508_05387_b200 import abi
+    n, d, V, chunk = 700, 192, 3001, 256
+    h, w, act = _case(n, d, V, seed=21)
+    g = torch.Generator(device="cuda").manual_seed(22)
+    old = torch.randn(n, generator=g, device="cuda") - 7.0
+    slot = torch.zeros(n, dtype=torch.int32, device="cuda")
+    adv = torch.randn(1, generator=g, device="cuda")
+    ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
+    cfg = abi.LossConfig(0.2, 0.2, 0.0, 0.0, 4.0, abi.ECHO_KL_K3, 0.0)
+    ws = torch.empty(chunk * abi.echo_lmhead_dlogits_ld(V), dtype=torch.bfloat16, device="cuda")
+
+    def bufs():
+        return ([torch.empty(n, device="cuda") for _ in range(2)] + [torch.empty(n, dtype=torch.uint8, device="cuda")]
+                + [torch.empty(n, d, device="cuda"), torch.empty(V, d, device="cuda")])
+
+    def run(b, stream=None):
+        lp, loss, flags, dh, dw = b
+        abi.echo_lmhead_policy_loss_fwd_bwd(h, w, n, d, V, act, old, None, slot, adv, None, None, ng, cfg, lp, loss,
+                                            flags, None, dh, dw, 0, ws, chunk, stream=stream)
+
+    b1, b2, b3 = bufs(), bufs(), bufs()
+    run(b1)
+    run(b2)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            run(b3, stream=s)
+    graph.replay()
+    torch.cuda.synchronize()
+    for x, y, z in zip(b1, b2, b3):
+        assert torch.equal(x.view(torch.uint8), y.view(torch.uint8))
+        assert torch.equal(x.view(torch.uint8), z.view(torch.uint8))
