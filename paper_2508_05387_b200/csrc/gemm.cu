@@ -27,12 +27,17 @@ namespace gm {
 constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16, kThreads = 192, kStages = 6;
 constexpr int kOpBytes = 128 * kBK * 2;  // one operand's stage per CTA: 128 rows (M or N) x 64 K bf16 = 16 KB
 constexpr uint32_t kTmemCols = 512;
+constexpr int kTidRing = 4;  // tile ids in flight between the scheduler (leader producer) and the other roles
 struct Smem {
   uint8_t a[kStages][kOpBytes];
   uint8_t b[kStages][kOpBytes];
   uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  uint64_t tid_full[kTidRing], tid_empty[kTidRing];
+  uint32_t tile_id[kTidRing];
   uint32_t tmem_base;
 };
+// consumers of a tile id: the leader's MMA thread and 4 epilogue warps, the peer's producer thread and 4 epilogue warps
+constexpr uint32_t kTidConsumers = 10;
 constexpr size_t smem_bytes() { return sizeof(Smem) + 1024; }
 
 // MN-major SWIZZLE_128B descriptor: start >> 4 | LBO 8192 B (>> 4) | SBO 1024 B (>> 4) | version 1 | layout 2
@@ -73,9 +78,16 @@ ECHO_DEVINL void tile_coords(int64_t u, int32_t n_mt, int32_t n_nt, int32_t grou
 }
 }  // namespace gm
 
+// In-order dynamic tile scheduler: per-launch counter slots (round robin over kGemmSlots, each reset to zero by its
+// launch's last CTA), so that clusters that start late or run slow take fewer tiles -- no wave-quantisation tail.
+constexpr int kGemmSlots = 64;
+__device__ unsigned int g_gemm_sched[kGemmSlots][2];
+static std::atomic<unsigned> g_gemm_next_slot{0};
+
 struct GemmParams {
   int64_t M;
   int32_t N, K, n_mt, n_nt, n_kb, group_m;
+  unsigned int* sched;  // this launch's {tile counter, finished CTAs} (reset by the last CTA)
   int32_t pol_a, pol_b;  // L2 policy per operand: 2 = evict_last (small, re-read by every tile), 1 = evict_first
                          // (streamed past a kept operand), 0 = evict_normal
   float* __restrict__ out;
@@ -94,8 +106,18 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_tiles = (int64_t)p.n_mt * p.n_nt;
   const uint32_t rank = cluster_ctarank();
-  const int64_t unit0 = (int64_t)cluster_id_x(), n_units = (int64_t)nclusters_x();
   const bool leader = rank == 0;
+  // tile id of the `use`-th tile of this cluster (every role walks the same sequence); n_tiles marks the end
+  auto next_tile = [&](uint32_t use) -> int64_t {
+    const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
+    mbar_wait_cluster(smem_u32(&sm.tid_full[r]), ph);
+    return (int64_t)sm.tile_id[r];
+  };
+  auto release_tile = [&](uint32_t use) {  // one arrival per consumer (thread or warp lane 0) on the leader
+    const uint32_t r = use % kTidRing;
+    if (leader) mbar_arrive(smem_u32(&sm.tid_empty[r]));
+    else lm::mbar_arrive_cluster(mapa(smem_u32(&sm.tid_empty[r]), 0));
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -105,6 +127,10 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.tfull[b]), 1);
       mbar_init(smem_u32(&sm.tempty[b]), 8);  // one arrival per epilogue warp of both CTAs
+    }
+    for (int r = 0; r < kTidRing; ++r) {
+      mbar_init(smem_u32(&sm.tid_full[r]), 1);
+      mbar_init(smem_u32(&sm.tid_empty[r]), kTidConsumers);  // used on the leader only
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -129,7 +155,23 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
                                                                                 : policy_evict_normal();
       const uint64_t pol_b = p.pol_b == 2 ? policy_evict_last() : p.pol_b == 1 ? policy_evict_first()
                                                                                 : policy_evict_normal();
-      for (int64_t u = unit0; u < n_tiles; u += n_units) {
+      for (uint32_t use = 0;; ++use) {
+        int64_t u;
+        if (leader) {  // the scheduler: grab the next tile, publish it to this CTA and the peer
+          const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
+          mbar_wait(smem_u32(&sm.tid_empty[r]), ph ^ 1u);
+          u = (int64_t)atomicAdd(&p.sched[0], 1u);
+          if (u > n_tiles) u = n_tiles;
+          sm.tile_id[r] = (uint32_t)u;
+          mbar_arrive(smem_u32(&sm.tid_full[r]));
+          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa(smem_u32(&sm.tile_id[r]), 1)), "r"((uint32_t)u)
+                       : "memory");
+          lm::mbar_arrive_cluster(mapa(smem_u32(&sm.tid_full[r]), 1));
+        } else {
+          u = next_tile(use);
+          release_tile(use);
+        }
+        if (u >= n_tiles) break;
         int32_t mt, nt;
         tile_coords(u, p.n_mt, p.n_nt, p.group_m, mt, nt);
         const int32_t m_row = mt * 256 + (int32_t)rank * kBM, n_row = nt * kBN + (int32_t)rank * 128;
@@ -150,7 +192,10 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     // ---------------------------------------------------------------- MMA issuer (the leader's lane 0)
     if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, tc = 0;
-      for (int64_t u = unit0; u < n_tiles; u += n_units, ++tc) {
+      for (;; ++tc) {
+        const int64_t u = next_tile(tc);
+        release_tile(tc);
+        if (u >= n_tiles) break;
         const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
         mbar_wait_cluster(smem_u32(&sm.tempty[buf]), aph ^ 1u);
         lm::tc_fence_after();
@@ -178,7 +223,11 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     uint32_t tc = 0;
     const uint32_t tempty_leader = mapa(smem_u32(&sm.tempty[0]), 0);
     const bool vec_ok = (p.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
-    for (int64_t u = unit0; u < n_tiles; u += n_units, ++tc) {
+    for (;; ++tc) {
+      const int64_t u = next_tile(tc);
+      __syncwarp();
+      if (lane == 0) release_tile(tc);
+      if (u >= n_tiles) break;
       int32_t mt, nt;
       tile_coords(u, p.n_mt, p.n_nt, p.group_m, mt, nt);
       const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
@@ -228,6 +277,14 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     lm::tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
   }
+  if (threadIdx.x == 0) {  // every scheduler of this launch is done once all CTAs are here: reset the slot
+    __threadfence();
+    if (atomicAdd(&p.sched[1], 1u) == gridDim.x - 1) {
+      p.sched[0] = 0u;
+      p.sched[1] = 0u;
+      __threadfence();
+    }
+  }
 }
 
 template <bool kAMN, bool kBMN>
@@ -249,6 +306,10 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, Gem
   const int64_t n_tiles = (int64_t)p.n_mt * p.n_nt;
   if (units > n_tiles) units = n_tiles;
   p.group_m = (int32_t)(units / p.n_nt > 1 ? units / p.n_nt : 1);
+  unsigned int* slots = nullptr;
+  e = cudaGetSymbolAddress((void**)&slots, g_gemm_sched);
+  if (e != cudaSuccess) return e;
+  p.sched = slots + 2 * (g_gemm_next_slot.fetch_add(1, std::memory_order_relaxed) % kGemmSlots);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * 2));
   cfg.blockDim = dim3(gm::kThreads);
