@@ -82,12 +82,18 @@ ECHO_DEVINL void tile_coords(int64_t u, int32_t n_mt, int32_t n_nt, int32_t grou
 // launch's last CTA), so that clusters that start late or run slow take fewer tiles -- no wave-quantisation tail.
 constexpr int kGemmSlots = 64;
 __device__ unsigned int g_gemm_sched[kGemmSlots][2];
+// split-K: per output tile, the number of epilogue warps (8) that have stored the lower K half (zeroed at teardown); the
+// upper half of tile t has id n_out + t, so it is handed out after every lower half (in-order scheduler: no deadlock)
+constexpr int kMaxSplitTiles = 4096;
+__device__ unsigned int g_gemm_flags[kGemmSlots][kMaxSplitTiles];
 static std::atomic<unsigned> g_gemm_next_slot{0};
 
 struct GemmParams {
   int64_t M;
   int32_t N, K, n_mt, n_nt, n_kb, group_m;
   unsigned int* sched;  // this launch's {tile counter, finished CTAs} (reset by the last CTA)
+  unsigned int* flags;  // split-K: this launch's per-output-tile counters
+  int32_t split;        // 1 or 2: K halves per output tile (ids t, n_out + t: the second pass adds onto the first)
   int32_t pol_a, pol_b;  // L2 policy per operand: 2 = evict_last (small, re-read by every tile), 1 = evict_first
                          // (streamed past a kept operand), 0 = evict_normal
   float* __restrict__ out;
@@ -104,7 +110,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
   const uint32_t raw = smem_u32(smem_raw);
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n_tiles = (int64_t)p.n_mt * p.n_nt;
+  const int64_t n_out = (int64_t)p.n_mt * p.n_nt, n_tiles = n_out * p.split;
+  const int32_t kb_half = p.n_kb / 2;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   // tile id of the `use`-th tile of this cluster (every role walks the same sequence); n_tiles marks the end
@@ -173,9 +180,12 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         }
         if (u >= n_tiles) break;
         int32_t mt, nt;
-        tile_coords(u, p.n_mt, p.n_nt, p.group_m, mt, nt);
+        const bool upper = u >= n_out;  // split-K: the second pass over the upper K half
+        tile_coords(upper ? u - n_out : u, p.n_mt, p.n_nt, p.group_m, mt, nt);
         const int32_t m_row = mt * 256 + (int32_t)rank * kBM, n_row = nt * kBN + (int32_t)rank * 128;
-        for (int32_t kb = 0; kb < p.n_kb; ++kb) {
+        const int32_t kb0 = upper ? kb_half : 0;
+        const int32_t kb1 = (p.split == 1 || upper) ? p.n_kb : kb_half;
+        for (int32_t kb = kb0; kb < kb1; ++kb) {
           mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
           const uint32_t bar = mapa(smem_u32(&sm.full[stage]), 0);
           if (leader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), 4 * kOpBytes);
@@ -200,14 +210,17 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         mbar_wait_cluster(smem_u32(&sm.tempty[buf]), aph ^ 1u);
         lm::tc_fence_after();
         const uint32_t d_tmem = tmem + buf * kBN;
-        for (int32_t kb = 0; kb < p.n_kb; ++kb) {
+        const bool upper = u >= n_out;
+        const int32_t kb0 = upper ? kb_half : 0;
+        const int32_t kb1 = (p.split == 1 || upper) ? p.n_kb : kb_half;
+        for (int32_t kb = kb0; kb < kb1; ++kb) {
           mbar_wait_cluster(smem_u32(&sm.full[stage]), phase);
           lm::tc_fence_after();
           const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
 #pragma unroll
           for (int k = 0; k < kBK / kUmmaK; ++k)
             lm::umma_f16<true>(d_tmem, op_desc<kAMN>(a0, k), op_desc<kBMN>(b0, k), idesc<kAMN, kBMN>(),
-                               (kb > 0 || k > 0) ? 1u : 0u);
+                               (kb > kb0 || k > 0) ? 1u : 0u);
           lm::umma_commit<true>(smem_u32(&sm.empty[stage]));
           if (++stage == kStages) {
             stage = 0;
@@ -229,13 +242,27 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       if (lane == 0) release_tile(tc);
       if (u >= n_tiles) break;
       int32_t mt, nt;
-      tile_coords(u, p.n_mt, p.n_nt, p.group_m, mt, nt);
+      const int64_t ot = u >= n_out ? u - n_out : u;  // output tile
+      tile_coords(ot, p.n_mt, p.n_nt, p.group_m, mt, nt);
       const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
       const int64_t row = (int64_t)mt * 256 + (int64_t)rank * kBM + quad * 32 + lane;
       const bool row_ok = row < p.M;
       float* orow = p.out + (row_ok ? row : 0) * p.ldo;
+      // split-K: the second half adds onto the first half's stores (fixed order: deterministic)
+      const bool second = u >= n_out;
+      const bool acc = p.accumulate || second;
       mbar_wait_cluster(smem_u32(&sm.tfull[buf]), aph);
       lm::tc_fence_after();
+      if (second) {
+        if (lane == 0) {
+          uint32_t v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.flags + ot) : "memory");
+          } while (v < 8u);
+        }
+        __syncwarp();
+        __threadfence();
+      }
 #pragma unroll 1
       for (int ch = 0; ch < kBN / 32; ++ch) {
         const int32_t cb = nt * kBN + ch * 32;
@@ -249,8 +276,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
           for (int j = 0; j < 8; ++j) {
             float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            if (p.accumulate) {
-              const float4 o = dst[j];
+            if (acc) {
+              const float4 o = __ldcg(dst + j);
               v.x += o.x;
               v.y += o.y;
               v.z += o.z;
@@ -261,8 +288,13 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (cb + i < p.N) orow[cb + i] = __uint_as_float(r[i]) + (p.accumulate ? orow[cb + i] : 0.0f);
+            if (cb + i < p.N) orow[cb + i] = __uint_as_float(r[i]) + (acc ? __ldcg(orow + cb + i) : 0.0f);
         }
+      }
+      if (p.split == 2 && !second) {  // publish this warp's rows of the first half
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.flags + ot, 1u);
       }
       lm::tc_fence_before();
       __syncwarp();
@@ -282,6 +314,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     if (atomicAdd(&p.sched[1], 1u) == gridDim.x - 1) {
       p.sched[0] = 0u;
       p.sched[1] = 0u;
+      if (p.split == 2)
+        for (int64_t t = 0; t < n_out; ++t) p.flags[t] = 0u;
       __threadfence();
     }
   }
@@ -304,12 +338,25 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, Gem
     if (dev < 64) cached[dev].store((int)units + 1, std::memory_order_relaxed);
   }
   const int64_t n_tiles = (int64_t)p.n_mt * p.n_nt;
-  if (units > n_tiles) units = n_tiles;
+  // split the K loop in two when that fills the last wave better (e.g. dhidden: 320 tiles on 74 clusters, 86 % -> 96 %)
+  // and both halves stay long (>= 64 k-blocks)
+  p.split = 1;
+  if (n_tiles <= kMaxSplitTiles && p.n_kb >= 128) {
+    const int64_t U = units;
+    auto eff = [U](int64_t t) { const int64_t w = (t + U - 1) / U; return (double)t / (double)(w * U); };
+    if (eff(2 * n_tiles) > eff(n_tiles) + 0.05) p.split = 2;  // (a second pass costs a little: only for a clear gain)
+  }
+  if (units > n_tiles * p.split) units = n_tiles * p.split;
   p.group_m = (int32_t)(units / p.n_nt > 1 ? units / p.n_nt : 1);
   unsigned int* slots = nullptr;
   e = cudaGetSymbolAddress((void**)&slots, g_gemm_sched);
   if (e != cudaSuccess) return e;
-  p.sched = slots + 2 * (g_gemm_next_slot.fetch_add(1, std::memory_order_relaxed) % kGemmSlots);
+  unsigned int* flags = nullptr;
+  e = cudaGetSymbolAddress((void**)&flags, g_gemm_flags);
+  if (e != cudaSuccess) return e;
+  const unsigned slot = g_gemm_next_slot.fetch_add(1, std::memory_order_relaxed) % kGemmSlots;
+  p.sched = slots + 2 * slot;
+  p.flags = flags + (size_t)slot * kMaxSplitTiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * 2));
   cfg.blockDim = dim3(gm::kThreads);

@@ -433,7 +433,8 @@ def test_lmhead_policy_loss_edge_cases_and_errors():
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("m,n,k", [(256, 256, 64), (300, 200, 1000), (1, 72, 4096), (777, 513, 130)])
+@pytest.mark.parametrize("m,n,k", [(256, 256, 64), (300, 200, 1000), (1, 72, 4096), (777, 513, 130),
+                                   (300, 200, 16384), (513, 300, 9000)])   # the last two split K in halves
 def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k):
     """echo_gemm_bf16 (the tcgen05 GEMM of the f2 backward) in every operand layout against the fp64 product, within
     the fp32-accumulation bound 4 (K/16 + 16) 2^-24 sum_k |A B|; ragged M / N / K tiles; accumulate mode."""
@@ -459,6 +460,10 @@ def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k):
     got = (c - prev)[:, :n].cpu().numpy().astype(np.float64)
     assert np.all(np.abs(got - ref) <= bound + 1e-6), np.max(np.abs(got - ref) / (bound + 1e-6))
     assert torch.equal(c[:, n:], prev[:, n:])                          # columns >= n untouched
+    c2 = prev.clone()                                                  # deterministic (split-K halves in fixed order)
+    abi.echo_gemm_bf16(a_buf, a_mn, a_buf.shape[1], b_buf, b_mn, b_buf.shape[1], m, n, k, c2, ldc, accumulate=True)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
 
 
 def test_chunked_f4_options_equal_the_logits_path():
