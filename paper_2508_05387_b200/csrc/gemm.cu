@@ -11,7 +11,10 @@
 // [K x M], M contiguous: two boxes of 64 M x 64 K per stage; UMMA canonical MN-major SW128 layout with 1024-B atoms of
 // 64 MN x 8 K, LBO = 8 KB between the two 64-wide MN atoms, SBO = 1 KB between 8-row K groups, +2 KB per K = 16
 // step).  Epilogue: thread = output row (TMEM lane), 32 fp32 columns per tcgen05.ld, 16-byte stores (+ loads when
-// accumulating).
+// accumulating).  Tiles are handed out in order by a dynamic scheduler (the leader's producer thread owns a per-launch
+// counter and broadcasts tile ids to its MMA / epilogue warps and to the peer CTA through a 4-deep ring); a poorly
+// filled last wave with a long K loop is avoided by a deterministic two-pass split-K (lower K halves first, the upper
+// half's epilogue adds onto the lower half's stores after a per-tile counter says they are complete).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
