@@ -18,8 +18,8 @@
 //                      exp2 over the tile's valid columns, z[t, a_t] when the action falls in the tile; partials
 //                      to the workspace; the accumulator is released as soon as it has been read, so the MMA of
 //                      the next tile overlaps this epilogue
-// Tiles are rasterised in groups of 16 token tiles x all vocab tiles (column-major inside a group), so the CTAs in
-// flight share a few MB of A and B in L2.
+// Tiles are rasterised in groups of 32 token tiles x all vocab tiles (column-major inside a group), so the CTAs in
+// flight share a few vocab tiles of B and the group's A rows (32 pair tiles x 256 x 2560 bf16 = 42 MB, L2-resident).
 //
 // kPair (ECHO_LMHEAD_PAIR, the default): a 2-CTA cluster shares one 256 x 256 tile with tcgen05.mma.cta_group::2
 // (M = 256): each CTA stages its own 128 token rows of A and HALF of the 256 vocab rows of B, the leader CTA's one
@@ -44,7 +44,7 @@ namespace lm {
 constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16;  // per-CTA token rows, tile vocab columns, K step
 constexpr int kThreads = 192;
 #ifndef ECHO_LM_GROUP
-#define ECHO_LM_GROUP 16
+#define ECHO_LM_GROUP 32  // 16 / 32 / 64 / 128 A/B'd on the 32768-row logp launch: 32 fastest
 #endif
 constexpr int kGroupM = ECHO_LM_GROUP;  // token tiles per rasterisation group
 constexpr uint32_t kTmemCols = 512;
