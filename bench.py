@@ -12,8 +12,12 @@ value      = kept tokens of all ranks / max-over-ranks device time of the path (
 e2e.value  = the same through the public step API with pinned host inputs copied H2D and the statistics read
              back inside the timed region (generator time subtracted, it is not part of the method)
 
-  python bench.py [--gpus N --steps K --warmup W] [--config qwen3-4b] [--algo auto|quad_reg|quad_reg_exact|row_l2]
+  python bench.py [--gpus N --steps K --warmup W] [--config qwen3-32b] [--algo auto|quad_reg|quad_reg_exact|row_l2]
   python bench.py --impl reference ...      # the CPU oracle arm (rank 0 only)
+
+With --gpus N > 1 and no torchrun environment (WORLD_SIZE unset) the script re-executes itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL).  N > 1 defaults to strong scaling
+(BASELINE.json configs[4]: one Qwen3-32B-shaped batch split by rollout group over the ranks).
 """
 from __future__ import annotations
 
@@ -32,7 +36,8 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "policy-loss fwd+bwd tokens/sec and % HBM roofline at 1/2/4/8 B200"
-DEFAULT_CONFIG = "qwen3-4b"      # BASELINE.json configs[1]: the single-GPU configuration the metric is quoted on
+DEFAULT_CONFIG = "qwen3-32b"     # BASELINE.json configs[4]: the north_star's target batch (fits one GPU: 8.4 M tokens
+                                 # streamed in 32768-row micro-batches), swept over 1/2/4/8 GPUs by strong scaling
 L2_FLUSH_BYTES = 256 << 20
 # LM-head hidden sizes of the BASELINE.json models (f2: the fused LM-head log-prob is measured at this shape)
 HIDDEN = {"tiny": 64, "qwen3-4b": 2560, "qwen2.5-7b": 3584, "qwen3-30b-a3b": 2048, "qwen3-32b": 5120}
@@ -47,7 +52,9 @@ def parse():
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--algo", default="auto", choices=["auto", "row_l2", "quad_reg", "quad_reg_exact", "oct_reg", "hex_reg"])
     ap.add_argument("--micro-batch", type=int, default=32768)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong = one batch split over the ranks (default, BASELINE.json configs[4]); "
+                         "weak = one batch per rank")
     ap.add_argument("--balance", action="store_true",
                     help="f3: token-balanced resharding of the kept rollouts after the stale filter (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -174,33 +181,58 @@ def oracle_rate(cfg, rank_batch, n_tokens_total, target_s, threads=None):
 
 
 def reference_arm(args):
-    """--impl reference: the CPU oracle on the box's host cores, rank 0 only."""
+    """--impl reference: the CPU oracle on the box's host cores, rank 0 only.  Loads oracle/ and synth/ only (never
+    the product library).  Each step is one bounded sample of the workload: pack + advantage of the whole batch and
+    the fused loss on a row sample of ~--cpu-seconds; ms_per_step is that sample's measured wall time, `value` the
+    whole-batch rate it implies (N / (t_meta + N t_row)), and the extrapolated full-batch step is reported apart."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import synth
-    cfg = synth.CONFIGS[args.config]
+    cfg, config = run_config(synth.CONFIGS[args.config], args, args.gpus)
     b = synth.make_batch(cfg)
+    n_tok = _kept_tokens(cfg, b)
     budget = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
     results = []
     for i in range(args.warmup + args.steps):
-        r = oracle_rate(cfg, b, _kept_tokens(cfg, b), budget)
+        r = oracle_rate(cfg, b, n_tok, budget)
         if i >= args.warmup:
             results.append(r)
     v = statistics.median([r["tokens_per_s"] for r in results])
     r = results[-1]
-    sample = (f"pack+advantage of the full {cfg.name} batch ({cfg.R} rollouts) + fused loss on {r['rows']} sampled rows "
-              f"(V={cfg.V}; a pool of {16 * r['cores']} generated rows evaluated repeatedly); whole-step time extrapolated as t_meta + N * t_row")
+    sample = (f"pack+advantage of the full {cfg.name} batch ({cfg.R} rollouts) + fused loss on {r['rows']} sampled "
+              f"rows (V={cfg.V}; a pool of {16 * r['cores']} generated rows evaluated repeatedly, ~{budget:.0f} s); "
+              f"value = N / (t_meta + N * t_row)")
+    sample_ms = [1e3 * (x["t_meta"] + x["t_loss"]) for x in results]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(
-                [x["step_s"] for x in results]), "higher_is_better": True, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "prompts": cfg.P, "group_size": cfg.G, "seq_len": cfg.S,
-                       "vocab": cfg.V, "max_lag": cfg.max_lag, "kl_coef": cfg.kl_coef},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(sample_ms),
+            "ms_per_step_is": "measured wall time of one bounded oracle sample (pack + advantage of the full batch, "
+                              "fused loss on the sampled rows)",
+            "extrapolated_full_step_ms": 1e3 * statistics.median([x["step_s"] for x in results]),
+            "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "oracle", "sample": sample,
                              "cpu_model": _cpu_model()},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_config(base, args, world):
+    """The workload as both arms report it (identical dicts: the driver compares them)."""
+    cfg = scaled_config(base, args, world)
+    return cfg, {"workload": cfg.name, "prompts": cfg.P, "group_size": cfg.G, "seq_len": cfg.S, "vocab": cfg.V,
+                 "max_lag": cfg.max_lag, "kl_coef": cfg.kl_coef, "parallelism": f"dp{world}",
+                 "scaling": args.scaling if world > 1 else "n/a (1 GPU)", "micro_batch_rows": args.micro_batch,
+                 "l2": "inputs >> L2 (10 GB micro-batches) + 256 MB L2 flush after each generator launch"}
+
+
+def scaled_config(base, args, world):
+    """Weak scaling: one BASELINE batch per rank (global batch world x P prompts); strong: one batch in total."""
+    import synth
+    if args.scaling == "weak" and world > 1:
+        return synth.Config(base.name, base.P * world, base.G, base.S, base.V, base.dtype, base.max_lag, base.kl_coef,
+                            base.lag_mode, base.index, base.stale_groups * world, base.fixed_lags, base.lengths)
+    return base
 
 
 def _kept_tokens(cfg, b):
@@ -225,12 +257,11 @@ def main_echo(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch with torchrun, or let bench.py "
+                         f"re-execute itself under torchrun by leaving WORLD_SIZE unset)")
     base = synth.CONFIGS[args.config]
-    if args.scaling == "weak" and world > 1:
-        cfg = synth.Config(base.name, base.P * world, base.G, base.S, base.V, base.dtype, base.max_lag, base.kl_coef,
-                           base.lag_mode, base.index, base.stale_groups * world, base.fixed_lags, base.lengths)
-    else:
-        cfg = base
+    cfg, config = run_config(base, args, world)
     g0, g1 = shard_groups(cfg.P, world, rank)
     r0, r1 = g0 * cfg.G, g1 * cfg.G
     b = synth.make_batch(cfg, r0, r1)
@@ -309,7 +340,8 @@ def main_echo(args):
         return {"e2e_ms": el(t0, t5) - gen_ms - waits, "dev_ms": el(t1, ta) + el(tb, t2) + sum(ker) + el(t3b, t4),
                 "kernel_ms": ker,
                 "n_tokens": N, "h2d": h2d, "d2h": abi.PACK_RESULT_BYTES + st.stats_host.numel() * 8,
-                "nonfinite": float(st.stats_host[9 + 4]), "loss": float(st.stats_host[9]) / max(N, 1)}
+                "nonfinite": float(st.stats_host[9 + 4]),
+                "loss": float(st.stats_host[9]) / max(float(st.stats_host[0]), 1.0)}   # sum l (all ranks) / N_global
 
     for _ in range(args.warmup):
         one_step(False)
@@ -354,11 +386,8 @@ def main_echo(args):
         "metric": METRIC, "value": toks_all / (dev_ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
-        "config": {"workload": cfg.name, "prompts": cfg.P, "group_size": cfg.G, "seq_len": cfg.S, "vocab": cfg.V,
-                   "max_lag": cfg.max_lag, "kl_coef": cfg.kl_coef, "tokens_per_step": int(toks_all / args.steps),
-                   "micro_batch_rows": M, "algo": args.algo, "parallelism": f"dp{world}",
-                   "balance": bool(args.balance),
-                   "l2": "inputs >> L2 (10 GB micro-batches) + 256 MB L2 flush after each generator launch"},
+        "config": config,
+        "run": {"tokens_per_step": int(toks_all / args.steps), "algo": args.algo, "balance": bool(args.balance)},
         "clocks": clk,
         "e2e": {"value": toks_all / (e2e_ms * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": recs[0]["h2d"], "d2h_bytes_per_step": recs[0]["d2h"]},
@@ -392,6 +421,38 @@ def main_echo(args):
     line["f1_token_logp"] = {"ms_per_micro_batch": f1_ms, "tokens_per_s_per_gpu": M / (f1_ms * 1e-3),
                              "achieved_GBps": f1_bpt * M / (f1_ms * 1e-3) / 1e9, "bytes_per_token": f1_bpt,
                              "frac": f1_bpt * M / (f1_ms * 1e-3) / 1e9 / peak}
+    # SURVEY.md §8.6 f4 loss variants on the same micro-batch: the entropy bonus (eta = 0.01, per-token entropies
+    # written) and per-token advantages + sequence-mean weights (PPO-GAE style advantages, w_t = 1 / (n_seq L_i))
+    ent = torch.empty(M, dtype=torch.float32, device=dev)
+    gen4 = torch.Generator(device=dev).manual_seed(cfg.seed + 4)
+    tok_adv = torch.randn(st.cap, generator=gen4, device=dev)
+    n_seq = max(1, st.pack_info.n_rollouts_kept)
+    tok_w = torch.full((st.cap,), 1.0 / (n_seq * cfg.S), dtype=torch.float32, device=dev)
+    legs = {"f4_entropy": (dict(entropy_coef=0.01, tok_entropy=ent), bpt + 4,
+                           "entropy bonus eta = 0.01 with tok_entropy written (+4 B/token)"),
+            "f4_weights_adv": (dict(tok_adv=tok_adv, tok_weight=tok_w), bpt + 4,
+                               "per-token advantages + sequence-mean weights (tok_adv and tok_weight read instead "
+                               "of tok_slot: +4 B/token)")}
+    plain_gbps = achieved
+    for key, (kw, leg_bpt, what) in legs.items():
+        ts = []
+        for r in range(6):
+            sgpu.fill_logits(logits, dtype=cfg.dtype, vocab=cfg.V, row0=0, tok_slot=st.tok_slot,
+                             tok_action=st.tok_action, kept_rollout=st.kept_rollout, kept_offset=st.kept_offset,
+                             max_len=cfg.S, seed=cfg.seed)
+            flush.fill_(float(r))
+            a0 = ev()
+            st.loss(logits, 0, kl_coef=cfg.kl_coef, grad_scale=1.0, algo=algo, **kw)
+            a1 = ev()
+            torch.cuda.synchronize()
+            if r >= 2:
+                ts.append(a0.elapsed_time(a1))
+        ms = statistics.median(ts)
+        gbps = leg_bpt * M / (ms * 1e-3) / 1e9
+        line[key] = {"ms_per_micro_batch": ms, "tokens_per_s_per_gpu": M / (ms * 1e-3), "achieved_GBps": gbps,
+                     "bytes_per_token": leg_bpt, "frac": gbps / peak, "vs_plain_fused_GBps": gbps / plain_gbps,
+                     "variant": what}
+    del ent, tok_adv, tok_w
     # the LM head fused with the log-prob (tensor-core bound), same micro-batch of tokens, against
     # the unfused path (cuBLAS GEMM into the logits buffer, then echo_token_logp)
     if cfg.dtype == "bf16" and not args.no_f2:
@@ -485,8 +546,8 @@ def main_echo(args):
             del dh, dw, dh_u, dw_u, scratch
         del hid, wgt
     if plans:
-        line["config"]["tokens_per_rank_before"] = plans[-1]["tokens_before"]
-        line["config"]["tokens_per_rank_after"] = plans[-1]["tokens_after"]
+        line["run"]["tokens_per_rank_before"] = plans[-1]["tokens_before"]
+        line["run"]["tokens_per_rank_after"] = plans[-1]["tokens_after"]
     if world == 1 and not args.no_cpu_baseline:
         r = oracle_rate(cfg, b, toks_all / args.steps, args.cpu_seconds)
         r1 = oracle_rate(cfg, b, toks_all / args.steps, args.cpu_seconds / 4, threads=1)
@@ -535,13 +596,33 @@ def _ncu_traffic(args):
         return None
 
 
+def _reexec_under_torchrun(args):
+    """--gpus N > 1 without a torchrun environment: run N ranks (one per GPU) of this same command line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: re-executing under torchrun ({args.gpus} ranks)", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
-    import __graft_entry__
-    __graft_entry__.build()
     if args.impl == "reference":
+        # the oracle arm builds and loads oracle/ and synth/ only -- never the product library
+        import oracle
+        oracle.build()
         reference_arm(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _reexec_under_torchrun(args)
+    # rank count visible in the NCCL init log (the driver counts ranks from it)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    import __graft_entry__
+    __graft_entry__.build()
     main_echo(args)
     try:
         import torch.distributed as dist

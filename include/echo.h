@@ -116,7 +116,9 @@ typedef struct {
  *   (position j of rollout i at i*S + j; positions >= resp_len[i] are never read).  ref_logp may be
  *   NULL (then tok_ref must be NULL too).  aux [R x S] is an optional per-token payload packed like old_logp
  *   into tok_aux (e.g. the PPO-GAE advantages of echo_gae_advantage; both NULL or both set).
- *   rollout_base = global id of local rollout 0.
+ *   rollout_base = global id of local rollout 0; it must be a multiple of group_size (a shard holds whole
+ *   groups: pack groups rollouts by local index and echo_group_advantage by global id / G), else
+ *   ECHO_ERR_INVALID_ARGUMENT.
  * Outputs (ascending, stable compaction; tokens rollout-major):
  *   kept_rollout[R]   global ids of kept rollouts (first n_rollouts_kept entries written)
  *   kept_offset[R+1]  CSR offsets into the token arrays (first n_rollouts_kept + 1 entries written)
@@ -175,7 +177,8 @@ ECHO_API echo_status echo_gae_advantage(int32_t n_rollouts, int32_t max_len, con
  *   mean = (sum r)/n_g, std = sqrt(sum (r - mean)^2 / n_g) (population), A = (r - mean)/(std + eps),
  *   rounded to fp32.  Every token of rollout i receives A_i through tok_slot (SPEC.md :209).
  * reward[R]: per-rollout return (sum of its per-step rewards, PAPER.md :164), indexed by local id.
- * kept_rollout / pack: outputs of echo_pack_batch on the same shard.
+ * kept_rollout / pack: outputs of echo_pack_batch on the same shard; rollout_base the same value as there (a
+ *   multiple of group_size, else ECHO_ERR_INVALID_ARGUMENT).
  * Outputs: adv_slot[R] (first n_rollouts_kept written), adv_stats[6] fp64 partial sums
  *   {sum A, sum A^2, sum r, sum r^2, n_zero_std_groups, n_rollouts_kept} (A as fp32 values; per-group
  *   partials summed in ascending group order).  Bit-identical to a sequential fp64 evaluation.
@@ -205,10 +208,11 @@ ECHO_API echo_status echo_group_advantage(int32_t n_rollouts, int32_t group_size
  * Arithmetic: fp32 accumulation over the bf16/fp32 logits, gradient stored with round-to-nearest-even.
  *   Deterministic: a row's reduction order depends only on vocab and the kernel, never on the grid, the stream,
  *   the micro-batch split or which cluster the row is scheduled on.
- * Concurrency: the kernels hand rows out from a per-launch counter slot (256 slots, round robin, each reset by its
- *   launch's last CTA), so calls may run concurrently on different streams (up to 256 launches in flight) and are
- *   capturable in CUDA graphs; a captured graph keeps its slot, so one graph must not be replayed concurrently
- *   with itself.
+ * Concurrency: the kernels hand rows out from a per-launch counter slot (256 slots, each reset by its launch's last
+ *   CTA).  Eager launches take slots 0..191 round robin, so up to 192 may be in flight at once on different
+ *   streams; launches captured into a CUDA graph keep their slot for the graph's lifetime and take slots 192..255,
+ *   so a replay never shares a counter with an eager launch.  Unsupported (rows would be skipped or done twice,
+ *   silently): replaying one graph concurrently with itself, or more than 64 captured launches running at once.
  * Launches: 1 kernel (0 when n_rows == 0).
  */
 ECHO_API echo_status echo_policy_loss_fwd_bwd(void* logits, int32_t dtype, int64_t n_rows, int32_t vocab, int64_t ld,
@@ -238,7 +242,9 @@ ECHO_API echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t 
 
 /* f4 loss variants ("PPO, KL-constrained PPO, GRPO ... or emerging variants", PAPER.md :278). */
 enum { ECHO_KL_K3 = 0, /* exp(ref - logp) - (ref - logp) - 1: unbiased, non-negative (the default, reading R5) */
-       ECHO_KL_K1 = 1, /* logp - ref (SPEC.md :244's estimator, here against pi_ref)                           */
+       ECHO_KL_K1 = 1, /* logp - ref: the Schulman k1 estimator of KL(pi_theta || pi_ref), d/dlogp = +1. NOT the
+                        * sign of SPEC.md :244's k1 (logprob_old - logprob_new, against pi_old): passing old_logp as
+                        * tok_ref does not reproduce that term -- its gradient has the opposite sign.             */
        ECHO_KL_K2 = 2  /* (logp - ref)^2 / 2                                                                   */ };
 
 typedef struct {

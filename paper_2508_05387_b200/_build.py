@@ -48,7 +48,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed ({r.returncode}):\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     if not trace:
-        with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+        os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)    # git-ignored: register / spill report per build
+        with open(os.path.join(ROOT, "build", "ptxas_info.txt"), "w") as f:
             f.write(r.stderr)
     if verbose:
         print(r.stderr)

@@ -87,6 +87,8 @@ echo_status echo_pack_batch_v2(int32_t n_rollouts, int32_t group_size, int32_t m
   if (filter_mode != ECHO_FILTER_GROUP && filter_mode != ECHO_FILTER_ROLLOUT) return ECHO_ERR_INVALID_ARGUMENT;
   if (n_rollouts % group_size != 0) return ECHO_ERR_INVALID_ARGUMENT;
   if (rollout_base < 0 || rollout_base + (int64_t)n_rollouts > INT32_MAX) return ECHO_ERR_INVALID_ARGUMENT;
+  // pack groups rollouts by local index, (2) by global id / G: the two agree only on a group boundary
+  if (rollout_base % group_size != 0) return ECHO_ERR_INVALID_ARGUMENT;
   if (!result || !kept_offset || (n_rollouts > 0 && (!version || !resp_len || !action || !old_logp || !kept_rollout)))
     return ECHO_ERR_INVALID_ARGUMENT;
   if (token_capacity > 0 && (!tok_slot || !tok_action || !tok_old)) return ECHO_ERR_INVALID_ARGUMENT;
@@ -119,6 +121,7 @@ echo_status echo_group_advantage(int32_t n_rollouts, int32_t group_size, float e
                                  float* adv_slot, double* adv_stats, void* stream) {
   if (n_rollouts < 0 || group_size < 2 || n_rollouts % group_size != 0 || !(eps >= 0.0f))
     return ECHO_ERR_INVALID_ARGUMENT;
+  if (rollout_base < 0 || rollout_base % group_size != 0) return ECHO_ERR_INVALID_ARGUMENT;
   if (!pack || !adv_stats || (n_rollouts > 0 && (!reward || !kept_rollout || !adv_slot)))
     return ECHO_ERR_INVALID_ARGUMENT;
   int sms = 0;

@@ -6,7 +6,23 @@
 
 #include "echo.h"
 
+#include <atomic>
+
 namespace echo {
+
+// Row / tile scheduler counter slot of one launch (each slot reset by its launch's last CTA).  Launches captured into
+// a CUDA graph keep their slot for the graph's lifetime, so they draw from the top quarter of the slots and eager
+// launches from the rest: an eager launch never shares a counter with a graph replay, whatever the launch count.
+// Collisions remain possible only between more than n_slots / 4 captured launches replayed concurrently, or more
+// than 3 n_slots / 4 eager launches in flight at once (include/echo.h "Concurrency").
+inline uint32_t next_sched_slot(std::atomic<uint32_t>& eager, std::atomic<uint32_t>& captured, cudaStream_t stream,
+                                uint32_t n_slots) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  const uint32_t n_graph = n_slots / 4, n_eager = n_slots - n_graph;
+  if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    return n_eager + captured.fetch_add(1, std::memory_order_relaxed) % n_graph;
+  return eager.fetch_add(1, std::memory_order_relaxed) % n_eager;
+}
 
 // Parameter block of the fused policy-loss kernels (passed by value as a kernel argument).
 struct LossParams {

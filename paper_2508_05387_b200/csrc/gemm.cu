@@ -89,7 +89,7 @@ __device__ unsigned int g_gemm_sched[kGemmSlots][2];
 // upper half of tile t has id n_out + t, so it is handed out after every lower half (in-order scheduler: no deadlock)
 constexpr int kMaxSplitTiles = 4096;
 __device__ unsigned int g_gemm_flags[kGemmSlots][kMaxSplitTiles];
-static std::atomic<unsigned> g_gemm_next_slot{0};
+static std::atomic<uint32_t> g_gemm_next_slot{0}, g_gemm_next_slot_graph{0};
 
 struct GemmParams {
   int64_t M;
@@ -359,7 +359,7 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, Gem
   unsigned int* flags = nullptr;
   e = cudaGetSymbolAddress((void**)&flags, g_gemm_flags);
   if (e != cudaSuccess) return e;
-  const unsigned slot = g_gemm_next_slot.fetch_add(1, std::memory_order_relaxed) % kGemmSlots;
+  const unsigned slot = next_sched_slot(g_gemm_next_slot, g_gemm_next_slot_graph, stream, kGemmSlots);
   p.sched = slots + 2 * slot;
   p.flags = flags + (size_t)slot * kMaxSplitTiles;
   cudaLaunchConfig_t cfg = {};

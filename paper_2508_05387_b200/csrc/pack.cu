@@ -210,6 +210,11 @@ cudaError_t launch_staleness_hist(int32_t R, int32_t G, int32_t S, int64_t t_tra
                                   const int64_t* version, const int32_t* resp_len, int32_t n_bins, int64_t* hist,
                                   int32_t filter_mode, cudaStream_t stream) {
   const size_t smem = (size_t)4 * (n_bins + 2) * sizeof(unsigned long long);
+  if (smem > 48 * 1024) {  // n_bins > 1534: past the default dynamic shared-memory limit (ABI allows 4096 bins)
+    cudaError_t e = cudaFuncSetAttribute(staleness_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   staleness_hist_kernel<<<1, 1024, smem, stream>>>(R, G, S, t_train, max_lag, version, resp_len, n_bins,
                                                    reinterpret_cast<long long*>(hist), filter_mode);
   return cudaGetLastError();

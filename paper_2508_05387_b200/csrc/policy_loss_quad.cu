@@ -92,7 +92,7 @@ struct __align__(128) QuadSmem {
 // a launch takes the next slot round-robin and its last CTA resets the pair, so no memset is needed.
 constexpr int kSchedSlots = 256;
 __device__ unsigned long long g_row_sched[kSchedSlots][2];
-static std::atomic<uint32_t> g_next_sched_slot{0};  // shared by every tile / mode: one slot per launch
+static std::atomic<uint32_t> g_next_sched_slot{0}, g_next_sched_slot_graph{0};  // shared by every tile / mode
 constexpr int kMaxDevices = 64;
 constexpr int kRowAhead = 3;
   // rows are broadcast this many iterations ahead (<= 4: the table depth)
@@ -589,7 +589,7 @@ static cudaError_t launch_t(const LossParams& p, cudaStream_t stream, int num_sm
     return cudaSuccess;
   }
   LossParams q = p;
-  q.sched_slot = (int32_t)(g_next_sched_slot.fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
+  q.sched_slot = (int32_t)next_sched_slot(g_next_sched_slot, g_next_sched_slot_graph, stream, kSchedSlots);
   policy_loss_quad_kernel<C, kMode><<<(unsigned)(clusters * C::kCtas), C::kThreads, smem, stream>>>(q);
   return cudaGetLastError();
 }

@@ -203,9 +203,9 @@ cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, 
     *shape = LaunchShape{(int32_t)grid, 1, kRThreads, 0};
     return cudaSuccess;
   }
-  static std::atomic<uint32_t> next_slot{0};
+  static std::atomic<uint32_t> next_slot{0}, next_slot_graph{0};
   LossParams q = p;
-  q.sched_slot = (int32_t)(next_slot.fetch_add(1, std::memory_order_relaxed) % kRowSchedSlots);
+  q.sched_slot = (int32_t)next_sched_slot(next_slot, next_slot_graph, stream, kRowSchedSlots);
   const bool ent = grad && (p.entropy_coef > 0.0f || p.tok_entropy != nullptr);
   if (dtype == ECHO_BF16) {
     if (ent)

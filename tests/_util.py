@@ -46,31 +46,55 @@ def host_rows(cfg: synth.Config, keys, actions):
     return synth.logits_rows(keys, actions, cfg.V, cfg.seed, "bf16" if cfg.dtype == "bf16" else "f32")
 
 
-def coef_slack(ref: oracle.LossOut, old, tok_ref, adv_tok, kl_coef, grad_scale, n_global):
-    """Bound on |c_gpu - c_ref| from the fp32 log-prob alone: dc/dlogp = s/N (-A rho [unclipped] - beta e^x),
-    x = ref - logp, times |d logp| <= 1e-6 (1 + |logp|) (fp32 log-sum-exp over the row), plus fp32 rounding."""
-    rho = np.exp(ref.logp - np.asarray(old, np.float64))
-    sens = np.abs(np.asarray(adv_tok, np.float64)) * rho
+def coef_sens(ref: oracle.LossOut, old, tok_ref, adv_tok, kl_coef, grad_scale, n_global=None, tok_weight=None,
+              kl_estimator=oracle.KL_K3):
+    """(|dc/dlogp|, cmag) per row, from the oracle's fp64 values.
+
+    c_t = s w_t ([unclipped] (-A rho) + beta dkl/dlogp), rho = e^(logp - old)  (echo_ref_policy_loss, SPEC.md :219)
+      dc/dlogp = s w_t ([unclipped] (-A rho) + beta d2kl/dlogp2),  d2kl/dlogp2 = e^(ref - logp) (k3), 0 (k1), 1 (k2)
+    On a clipped row (oracle flags bit 0: PPO clip or dual clip) the surrogate contributes no gradient, so its term is
+    dropped.  cmag = s w_t (|A| rho [unclipped] + beta |dkl/dlogp|) >= |c_t| bounds the terms the fp32 epilogue adds
+    (its rounding error is <= 2^-20 cmag)."""
+    logp = ref.logp
+    rho = np.exp(logp - np.asarray(old, np.float64))
+    uncl = (ref.flags & 1) == 0
+    A = np.abs(np.asarray(adv_tok, np.float64))
+    w = (1.0 / float(n_global)) if tok_weight is None else np.asarray(tok_weight, np.float64)
+    sens = np.where(uncl, A * rho, 0.0)
+    mag = sens.copy()
     if kl_coef > 0:
-        sens = sens + kl_coef * np.exp(np.asarray(tok_ref, np.float64) - ref.logp)
-    return grad_scale / n_global * sens * 1e-6 * (1 + np.abs(ref.logp)) + 1e-6 * np.abs(ref.coef)
+        x = np.asarray(tok_ref, np.float64) - logp
+        if kl_estimator == oracle.KL_K3:
+            sens = sens + kl_coef * np.exp(x)
+            mag = mag + kl_coef * np.abs(1.0 - np.exp(x))
+        elif kl_estimator == oracle.KL_K2:
+            sens = sens + kl_coef
+            mag = mag + kl_coef * np.abs(x)
+        else:
+            mag = mag + kl_coef
+    return grad_scale * w * sens, grad_scale * w * mag
 
 
 def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dtype: str, clip=(0.2, 0.2),
-               old=None, cslack=None, eslack=None, loss_atol=1e-6):
-    """Element-wise parity of a set of rows; returns number of gradient rows compared.
+               old=None, sens=None, eslack=None, loss_atol=1e-6, p=None, action=None, label=""):
+    """Element-wise parity of a set of rows (SURVEY.md §8.3 tolerances); returns (rows compared, max |err| / |c_t|).
 
-    logp: |d| <= 1e-5 + 1e-6 |logp|; l_t: rtol 1e-5 (+1e-6 abs); dlogits (bf16): |d| <= ulp_bf16(d_ref) + 4e-6 |c_t|
-    + slack_t (faithful rounding: one of the two bf16 neighbours of the exact value) and the
-    north_star bar max|d| <= 2e-3 (checked by the callers at max|d_ref| in [0.25, 0.5));
-    (fp32): |d| <= 1e-5 |d_ref| + 4e-6 |c_t| + slack_t, where slack_t (coef_slack) bounds the error the fp32
-    log-prob propagates into c_t.  Rows whose reference ratio sits within 1e-5 of a clip boundary decide
-    "clipped" in different precisions (fp64 vs fp32): only logp is compared there.  eslack (per element, the
-    entropy term's fp32 error bound) and loss_atol widen the bars for the entropy variant.
-    """
+    logp: |d| <= 1e-5 + 1e-6 |logp|;  l_t: rtol 1e-5 (+ loss_atol);  flags equal.
+    dlogits, per element (d_ref = c_t (delta_{v,a} - p_v), p_v = exp(z_v - lse) in fp64):
+        |d_gpu - d_ref| <= base(d_ref) + 2^-20 cmag_t + dc_t |delta_{v,a} - p_v| + |c_t| p_v dlse_t (+ eslack)
+      base = 1 bf16 ulp(d_ref) (faithful rounding: one of the two bf16 neighbours of the exact value) or 1e-5 |d_ref|
+      (fp32 logits); dlse_t = |logp_gpu - logp_ref| + 2^-22 (1 + |logp|) is the row's measured log-sum-exp error (z_a
+      is exact, so lse errs by what logp errs) and moves p_v by p_v dlse_t; dc_t = sens_t dlse_t is what that error
+      does to c_t through the ratio and the KL term (coef_sens), reaching column v through |delta_{v,a} - p_v| only.
+    Consistency (the a5 pin -d/c = exp(z - lse); rows with c_t != 0 and no entropy term): for v != a_t
+      with p_v >= 2^-14 max_v p_v,   |(-d_v / c_t) - p_v| <= (2^-7 + dc_t / |c_t| + dlse_t) p_v.
+    p / action: the rows' fp64 probabilities and actions; without them (no entropy term) they are recovered from the
+    oracle's own gradient, -d_ref / c_t = p_v (v != a) or p_a - 1 (v = a); rows with c_t = 0 take |delta - p| <= 1.
+    Rows whose reference ratio sits within 1e-5 of a clip boundary decide "clipped" in different precisions (fp64 vs
+    fp32): only logp is compared there.  eslack (per element) widens the bar for the entropy term."""
     logp_gpu = np.asarray(logp_gpu, np.float64)
-    assert np.all(np.abs(logp_gpu - ref.logp) <= 1e-5 + 1e-6 * np.abs(ref.logp)), \
-        f"logp max err {np.max(np.abs(logp_gpu - ref.logp))}"
+    lerr = np.abs(logp_gpu - ref.logp)
+    assert np.all(lerr <= 1e-5 + 1e-6 * np.abs(ref.logp)), f"logp max err {np.max(lerr)}"
     rho = np.exp(ref.logp - np.asarray(old, np.float64))
     near = (np.abs(rho - (1 - clip[0])) < 1e-5) | (np.abs(rho - (1 + clip[1])) < 1e-5)
     ok = ~near & ((ref.flags & 2) == 0)
@@ -81,12 +105,32 @@ def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dty
         f"loss max err {np.max(np.abs(loss_gpu - ref.loss)[ok])}"
     d = np.asarray(d_gpu, np.float64)[ok]
     dr = ref.dlogits[ok]
-    c = np.abs(ref.coef[ok])[:, None]
-    slack = 0.0 if cslack is None else np.asarray(cslack)[ok][:, None]
-    base = bf16_ulp(dr) if dtype == "bf16" else 1e-5 * np.abs(dr)      # faithful bf16 rounding: within 1 ulp
+    if d.size == 0:
+        return 0, 0.0
+    c = ref.coef[ok][:, None]
+    ca = np.abs(c)
+    has_c = ca > 0
+    cs = np.where(has_c, c, 1.0)
+    dlse = (lerr + 2.0 ** -22 * (1 + np.abs(ref.logp)))[ok][:, None]
+    if sens is None:
+        sens_t, cmag = np.zeros_like(ca), ca
+    else:
+        sens_t, cmag = (np.asarray(x, np.float64)[ok][:, None] for x in sens)
+    dc = sens_t * dlse
+    if p is None:
+        q = -dr / cs
+        onehot = has_c & (q < 0)
+        pv = np.where(has_c, np.where(onehot, q + 1.0, q), 0.0)
+        dist = np.where(has_c, np.abs(onehot - pv), 1.0)
+    else:
+        pv = np.asarray(p, np.float64)[ok]
+        onehot = np.zeros(pv.shape, bool)
+        onehot[np.arange(pv.shape[0]), np.asarray(action)[ok]] = True
+        dist = np.abs(onehot - pv)
+    base = bf16_ulp(dr) if dtype == "bf16" else 1e-5 * np.abs(dr)
+    tol = base + 2.0 ** -20 * cmag + dc * dist + ca * pv * dlse
     if eslack is not None:
-        slack = slack + np.asarray(eslack)[ok]
-    tol = np.broadcast_to(base + 4e-6 * c + slack, d.shape)
+        tol = tol + np.asarray(eslack)[ok]
     err = np.abs(d - dr)
     bad = err > tol + 1e-30
     if bad.any():
@@ -94,4 +138,18 @@ def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dty
         i = np.argmax(err[bad] / tol[bad])
         raise AssertionError(f"dlogits: {bad.sum()} elements out of tolerance; worst row {r[i]} col {v[i]}: "
                              f"gpu {d[r[i], v[i]]!r} ref {dr[r[i], v[i]]!r} c {c[r[i], 0]!r} tol {tol[r[i], v[i]]!r}")
-    return int(ok.sum()), float(err.max()) if err.size else 0.0
+    n_cons = 0
+    if eslack is None:
+        pmax = np.max(pv, axis=1, keepdims=True)
+        sel = has_c & ~onehot & (pv > 0) & (pv >= 2.0 ** -14 * pmax)
+        n_cons = int(sel.sum())
+        if n_cons:
+            ratio = -d / cs
+            ctol = (2.0 ** -7 + dc / np.where(has_c, ca, 1.0) + dlse) * pv
+            cbad = sel & (np.abs(ratio - pv) > ctol)
+            assert not cbad.any(), (f"consistency -d/c vs p: {cbad.sum()} elements off; worst relative "
+                                    f"{np.max(np.abs(ratio - pv)[cbad] / pv[cbad]):.3e}")
+    rel = float(np.max(np.where(has_c, err / np.where(has_c, ca, 1.0), 0.0)))
+    print(f"[check_rows{(' ' + label) if label else ''}] rows {int(ok.sum())}  max|err| {err.max():.3e}  "
+          f"max|err|/|c_t| {rel:.3e}  consistency-checked {n_cons}")
+    return int(ok.sum()), rel

@@ -107,3 +107,18 @@ def test_tensor_core_kernels_use_tcgen05_and_tma():
     for body in tc:
         assert "UTCHMMA.2CTA" in body and "UTMALDG.2D.2CTA" in body and "LDTM" in body
         assert " HMMA" not in body and "LDL" not in body and "STL" not in body
+
+
+def test_shard_base_must_be_a_group_boundary():
+    """echo_pack_batch groups rollouts by local index and echo_group_advantage by global id / G, so a
+    rollout_base that is not a multiple of group_size is rejected synchronously (argument check, no device work)."""
+    import ctypes
+    import paper_2508_05387_b200.abi as abi
+    lib = abi._lib
+    res = ctypes.create_string_buffer(abi.PACK_RESULT_BYTES)
+    off = (ctypes.c_int64 * 1)()
+    st = lib.echo_pack_batch_v2(0, 4, 8, 16, 10, 1, 6, None, None, None, None, None, None, 0, None, off, None, None,
+                                None, None, None, res, 0, None)
+    assert st == abi.ECHO_ERR_INVALID_ARGUMENT
+    st = lib.echo_group_advantage(0, 4, ctypes.c_float(1e-8), None, None, 2, res, None, off, None)
+    assert st == abi.ECHO_ERR_INVALID_ARGUMENT

@@ -12,7 +12,7 @@ import torch
 
 import oracle
 import synth
-from _util import check_rows, coef_slack, host_rows, oracle_step, pow2_scale_for
+from _util import check_rows, coef_sens, host_rows, oracle_step, pow2_scale_for
 
 pytestmark = pytest.mark.gpu
 
@@ -175,7 +175,7 @@ def test_tiny_full_step(kl_coef):
     check_rows(d_gpu=logits.cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
                loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
                dtype="f32", old=o.pk.tok_old,
-               cslack=coef_slack(ref, o.pk.tok_old, o.pk.tok_ref, o.adv[o.pk.tok_slot], kl_coef, s, n))
+               sens=coef_sens(ref, o.pk.tok_old, o.pk.tok_ref, o.adv[o.pk.tok_slot], kl_coef, s, n))
     L_ref = ref.loss.sum() / n
     assert abs(out["loss"] - L_ref) <= 1e-5 * max(abs(L_ref), np.abs(ref.loss).mean())
     for k, i in (("loss/n_clipped", 3), ("loss/n_nonfinite", 4), ("loss/n_tokens", 8)):
@@ -293,7 +293,8 @@ def test_full_config_sampled_rows(name, algo_name):
         d = logits[idx].float().cpu().numpy()
         check_rows(d_gpu=d, logp_gpu=st.tok_logp[gl].cpu().numpy(), loss_gpu=st.tok_loss[gl].cpu().numpy(),
                    flags_gpu=st.tok_flags[gl].cpu().numpy(), ref=ref, dtype=cfg.dtype, old=o.pk.tok_old[gl],
-                   cslack=coef_slack(ref, o.pk.tok_old[gl], tr, o.adv[o.pk.tok_slot[gl]], cfg.kl_coef, s, N))
+                   sens=coef_sens(ref, o.pk.tok_old[gl], tr, o.adv[o.pk.tok_slot[gl]], cfg.kl_coef, s, N),
+                   label=f"{name} {algo_name} row0={row0}")
         assert np.max(np.abs(d - ref.dlogits)) <= 2e-3                 # the north_star bar
         # every row of the micro-batch: |sum_v d| <= 2^-8 |c| (bf16 RNE) + fp32 slack
         rows_sum = logits.float().sum(dim=1).abs()
@@ -308,6 +309,38 @@ def test_full_config_sampled_rows(name, algo_name):
         del logits
     torch.cuda.empty_cache()
 
+
+
+def test_check_rows_rejects_dropped_small_gradients():
+    """Mutation test of the dlogits bar: the AUTO kernel's output on sampled Qwen3-4B rows passes check_rows; the same
+    output with every entry whose p_v < 1e-5 zeroed (the bulk of a 152k-column row) must fail it, and so must an
+    all-zero gradient and one whose entries with p_v >= 1e-4 (non-action) are off by a relative 2^-6 (> 1 bf16 ulp)."""
+    cfg = synth.CONFIGS["qwen3-4b"]
+    b = synth.make_batch(cfg, 0, 2 * cfg.G)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    n = 64
+    logits = fill(st, cfg, 0, n)
+    z = host_rows(cfg, o.keys[:n], o.pk.tok_action[:n])
+    args = (o.pk.tok_action[:n], o.pk.tok_old[:n], o.pk.tok_ref[:n], o.pk.tok_slot[:n], o.adv)
+    N = info.n_tokens
+    probe = oracle.policy_loss(z, *args, n_global=N, kl_coef=cfg.kl_coef)
+    s = pow2_scale_for(np.abs(probe.dlogits).max())
+    ref = oracle.policy_loss(z, *args, n_global=N, kl_coef=cfg.kl_coef, grad_scale=s)
+    st.loss(logits, 0, kl_coef=cfg.kl_coef, grad_scale=s)                 # AUTO
+    d = logits.float().cpu().numpy()
+    kw = dict(logp_gpu=st.tok_logp[:n].cpu().numpy(), loss_gpu=st.tok_loss[:n].cpu().numpy(),
+              flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref, dtype="bf16", old=o.pk.tok_old[:n],
+              sens=coef_sens(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef, s, N))
+    check_rows(d_gpu=d, label="AUTO unmutated", **kw)
+    c = ref.coef[:, None]
+    pv = np.where(c != 0, np.abs(ref.dlogits / np.where(c != 0, c, 1.0)), 0.0)
+    small = pv < 1e-5
+    assert small.mean() > 0.5                                             # the bulk of every row
+    for name, mutated in (("p<1e-5 zeroed", np.where(small, 0.0, d)), ("all zero", np.zeros_like(d)),
+                          ("x(1+2^-6) where p>=1e-4", np.where((pv >= 1e-4) & (pv < 0.5), d * (1 + 2.0 ** -6), d))):
+        with pytest.raises(AssertionError):
+            check_rows(d_gpu=mutated, label=name, **kw)
 
 def test_nonfinite_rows_flagged():
     from paper_2508_05387_b200 import abi
@@ -361,7 +394,7 @@ def test_ragged_vocab_and_padding_untouched(V, ld, algo):
     assert torch.equal(out[:, V:].view(torch.int16), zb[:, V:].view(torch.int16))
     check_rows(d_gpu=out[:, :V].float().numpy(), logp_gpu=logp.cpu().numpy(), loss_gpu=loss.cpu().numpy(),
                flags_gpu=flags.cpu().numpy(), ref=ref, dtype="bf16", old=old,
-               cslack=coef_slack(ref, old, None, adv[slot], 0.0, float(n), n))
+               sens=coef_sens(ref, old, None, adv[slot], 0.0, float(n), n))
 
 
 def test_abi_argument_errors():
@@ -478,8 +511,7 @@ def test_loss_variants_v2(name, algo, est, dual):
             tok_weight=torch.from_numpy(w).cuda(), clip_dual=dual, kl_estimator=est)
     rho = np.exp(ref.logp - old[:n].astype(np.float64))
     keep = np.abs(rho - dual) > 1e-5 if dual else np.ones(n, bool)
-    sens = (np.abs(tok_adv[:n]) * rho + kl * np.maximum(1.0, np.exp(o.pk.tok_ref[:n] - ref.logp))) * s * w[:n]
-    cs = sens * 1e-6 * (1 + np.abs(ref.logp)) + 1e-6 * np.abs(ref.coef)
+    sens, cmag = coef_sens(ref, old[:n], o.pk.tok_ref[:n], tok_adv[:n], kl, s, tok_weight=w[:n], kl_estimator=est)
     sub = lambda x: x[keep]
     import copy
     r2 = copy.copy(ref)
@@ -487,7 +519,8 @@ def test_loss_variants_v2(name, algo, est, dual):
                                                        ref.dlogits[keep])
     check_rows(d_gpu=logits.float().cpu().numpy()[keep], logp_gpu=sub(st.tok_logp[:n].cpu().numpy()),
                loss_gpu=sub(st.tok_loss[:n].cpu().numpy()), flags_gpu=sub(st.tok_flags[:n].cpu().numpy()), ref=r2,
-               dtype=cfg.dtype, old=sub(old[:n]), cslack=sub(cs))
+               dtype=cfg.dtype, old=sub(old[:n]), sens=(sub(sens), sub(cmag)),
+               label=f"v2 {name} algo={algo} est={est} dual={dual}")
     if dual:
         assert (ref.flags & 1).any()
 
@@ -533,7 +566,9 @@ def test_entropy_bonus_v2(name, algo):
     es = e * p * (np.abs(zf) + np.abs(lse)[:, None] + np.abs(ref.entropy)[:, None] + 1) * 3e-5
     check_rows(d_gpu=logits.float().cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
                loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
-               dtype=cfg.dtype, old=o.pk.tok_old[:n], eslack=es, loss_atol=1e-6 + eta * hbar)
+               dtype=cfg.dtype, old=o.pk.tok_old[:n], eslack=es, loss_atol=1e-6 + eta * hbar,
+               sens=coef_sens(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], kl, s, info.n_tokens),
+               p=p, action=o.pk.tok_action[:n], label=f"entropy {name} algo={algo}")
     # masked columns: exactly zero gradient
     assert torch.all(logits[:8, :V][masked] == 0)
 
@@ -688,7 +723,7 @@ def test_fp32_logits_qwen_vocab():
     check_rows(d_gpu=logits.cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
                loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
                dtype="f32", old=o.pk.tok_old[:n],
-               cslack=coef_slack(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef,
+               sens=coef_sens(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef,
                                  float(N), N))
 
 
@@ -804,7 +839,7 @@ def test_hex_tile_large_vocabularies(V):
     check_rows(d_gpu=work[:, :V].float().cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
                loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref,
                dtype="bf16", old=o.pk.tok_old[:n],
-               cslack=coef_slack(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef, s, N))
+               sens=coef_sens(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef, s, N))
     assert torch.equal(work[:, V:], logits[:, V:])                      # padding untouched
     # entropy variant on the same rows
     eta = 0.01
@@ -845,7 +880,7 @@ def test_fp32_cluster_tile(V):
     check_rows(d_gpu=work[:, :V].cpu().numpy(), logp_gpu=st.tok_logp[:n].cpu().numpy(),
                loss_gpu=st.tok_loss[:n].cpu().numpy(), flags_gpu=st.tok_flags[:n].cpu().numpy(), ref=ref, dtype="f32",
                old=o.pk.tok_old[:n],
-               cslack=coef_slack(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef,
+               sens=coef_sens(ref, o.pk.tok_old[:n], o.pk.tok_ref[:n], o.adv[o.pk.tok_slot[:n]], cfg.kl_coef,
                                  float(N), N))
     assert torch.equal(work[:, V:], logits[:, V:])
     eta = 0.02
@@ -908,7 +943,7 @@ def test_fuzz_shapes_and_tiles():
         d = work[torch.from_numpy(rows).cuda(), :V].float().cpu().numpy()
         check_rows(d_gpu=d, logp_gpu=st.tok_logp[rows].cpu().numpy(), loss_gpu=st.tok_loss[rows].cpu().numpy(),
                    flags_gpu=st.tok_flags[rows].cpu().numpy(), ref=ref, dtype=dtype, old=o.pk.tok_old[rows],
-                   cslack=coef_slack(ref, o.pk.tok_old[rows], o.pk.tok_ref[rows], o.adv[o.pk.tok_slot[rows]],
+                   sens=coef_sens(ref, o.pk.tok_old[rows], o.pk.tok_ref[rows], o.adv[o.pk.tok_slot[rows]],
                                      cfg.kl_coef, float(N), N))
         if ld > V:
             assert torch.equal(work[:, V:], logits[:, V:]), (dtype, V, algo_name)

@@ -2,7 +2,7 @@
 
 (3) closed forms: uniform rows give logp = -ln V (SPEC.md :202; golden logp_closed_forms.json); a single
     spike Delta gives logp = Delta - ln(e^Delta + V - 1) and p > 0.999 at Delta = 20 (SPEC.md :203);
-    softmax normalisation to 1e-12 (SPEC.md :204); row-shift invariance.
+    softmax normalisation to 1e-12 (SPEC.md :204); row-shift invariance; column-permutation equivariance.
 (4) old == new => rho = 1 and pg = -A; clip saturation => zero gradient (SPEC.md :219 objective with
     eps 0.2, :243); ref == logp => kl = 0; linearity in beta and grad_scale.
 (5) central finite differences of the loss (h = 1e-4) on >= 200 sampled (t, v) of the tiny config,
@@ -82,6 +82,37 @@ def test_softmax_normalises_and_row_shift_invariance():
     np.testing.assert_allclose(o1.logp, o2.logp, rtol=0, atol=1e-12)
     np.testing.assert_allclose(o1.dlogits, o2.dlogits, rtol=0, atol=1e-15)
 
+
+
+def test_column_permutation_equivariance():
+    """(3)-(5) do not depend on the vocabulary's column order (SURVEY.md §8.3 a3 pin): permuting the columns of a row
+    (and mapping the action with it) leaves logp, l_t, c_t and the flags unchanged up to the fp64 summation order
+    (V u relative) and permutes the gradient the same way.  A kernel or oracle that indexes a column by its tile
+    position instead of its vocabulary id (e.g. a wrong action column, an off-by-one tail) breaks this."""
+    rng = np.random.default_rng(11)
+    n, V = 6, 1031
+    z = (rng.normal(size=(n, V)) * 2).astype(np.float32)
+    act = rng.integers(0, V, n).astype(np.int32)
+    z[np.arange(n), act] += 6.0
+    old = (rng.normal(size=n) * 0.3 - 1.0).astype(np.float32)
+    ref = (rng.normal(size=n) * 0.3 - 1.0).astype(np.float32)
+    slot = np.arange(n, dtype=np.int32) % 3
+    adv = np.array([1.25, -0.5, 0.0], np.float32)
+    kw = dict(n_global=float(n), kl_coef=0.3, grad_scale=2.0)
+    o1 = oracle.policy_loss(z, act, old, ref, slot, adv, **kw)
+    for trial in range(3):
+        perm = rng.permutation(V)                 # new column j holds old column perm[j]
+        inv = np.argsort(perm)
+        o2 = oracle.policy_loss(np.ascontiguousarray(z[:, perm]), inv[act].astype(np.int32), old, ref, slot, adv, **kw)
+        tol = V * 2.0 ** -53 * 8
+        np.testing.assert_allclose(o2.logp, o1.logp, rtol=tol, atol=tol)
+        np.testing.assert_allclose(o2.loss, o1.loss, rtol=tol, atol=tol)
+        np.testing.assert_allclose(o2.coef, o1.coef, rtol=tol, atol=1e-300)
+        np.testing.assert_array_equal(o2.flags, o1.flags)
+        np.testing.assert_allclose(o2.dlogits, o1.dlogits[:, perm], rtol=tol, atol=tol * np.abs(o1.coef).max())
+    # a wrong action column is visible: the permuted rows with the UNmapped action give different log-probs
+    o3 = oracle.policy_loss(np.ascontiguousarray(z[:, perm]), act, old, ref, slot, adv, **kw)
+    assert np.max(np.abs(o3.logp - o1.logp)) > 1.0
 
 def test_old_equals_new_gives_unit_ratio():
     cfg = synth.CONFIGS["tiny"]

@@ -49,12 +49,21 @@ def _step_stats(cfg, r0, r1, n_global=None):
     return pk, adv, stats1
 
 
+# 16 groups of 4 (f32, V = 1024) with the 7B config's async staleness: 5 of 16 groups dropped, so ranks at W = 4 and 8
+# keep uneven token counts (the north_star's 8-GPU split; PAPER.md :224 drops whole groups)
+ASYNC16 = synth.Config("async16", 16, 4, 64, 1024, "f32", 2, 0.001, "async", 0, stale_groups=5, lengths="ragged")
+
+
+def _cfg(name):
+    return ASYNC16 if name == "async16" else synth.CONFIGS[name]
+
+
 def _worker(rank, world, port, cfg_name, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        cfg = synth.CONFIGS[cfg_name]
+        cfg = _cfg(cfg_name)
         g0, g1 = shard_groups(cfg.P, world, rank)
         pk, adv, stats1 = _step_stats(cfg, g0 * cfg.G, g1 * cfg.G)
         s1 = torch.tensor(stats1, dtype=torch.float64)
@@ -72,12 +81,14 @@ def _worker(rank, world, port, cfg_name, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_two_rank_step_equals_single_rank(world):
-    cfg = synth.CONFIGS["tiny"]
+@pytest.mark.parametrize("world,name", [(2, "tiny"), (4, "async16"), (8, "async16"), (8, "tiny")])
+def test_multi_rank_step_equals_single_rank(world, name):
+    """W gloo ranks (W = 8: the north_star's 8-GPU split; with "tiny" at W = 8 half the ranks own no group) give
+    the single-rank step's all-reduced counts, loss statistics and per-token coefficients."""
+    cfg = _cfg(name)
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), "tiny", out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), name, out), nprocs=world, join=True)
     # single-rank reference
     pk, adv, stats1 = _step_stats(cfg, 0, cfg.R)
     keys = (pk.kept_rollout[pk.tok_slot].astype(np.int64) * cfg.S
@@ -92,6 +103,8 @@ def test_two_rank_step_equals_single_rank(world):
     np.testing.assert_allclose(st[[0, 1, 2, 7, 9]], lo.stats[[0, 1, 2, 7, 9]], rtol=1e-12, atol=1e-12)
     np.testing.assert_array_equal(st[[3, 4, 8]], lo.stats[[3, 4, 8]])
     assert st[5] == lo.stats[5] and st[6] == lo.stats[6]      # min / max exact
+    if name == "async16":
+        assert stats1[8] == 5 and len({out[r][2].size for r in range(world)}) > 1   # uneven ranks
     # the union of rank outputs is the single-rank output (global ids, W-invariant per-token coefficients)
     np.testing.assert_array_equal(np.concatenate([out[r][2] for r in range(world)]), pk.kept_rollout)
     np.testing.assert_array_equal(np.concatenate([out[r][3] for r in range(world)]), lo.coef)
@@ -142,7 +155,7 @@ def _rebalance_worker(rank, world, port, cfg_name, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        cfg = synth.CONFIGS[cfg_name]
+        cfg = _cfg(cfg_name)
         g0, g1 = shard_groups(cfg.P, world, rank)
         pk, adv, stats1 = _step_stats(cfg, g0 * cfg.G, g1 * cfg.G)
         s1 = torch.tensor(stats1, dtype=torch.float64)
@@ -168,14 +181,14 @@ def _rebalance_worker(rank, world, port, cfg_name, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_rebalanced_step_equals_single_rank(world):
+@pytest.mark.parametrize("world,name", [(2, "tiny"), (3, "tiny"), (4, "async16"), (8, "async16")])
+def test_rebalanced_step_equals_single_rank(world, name):
     """f3: after the exchange every rank holds a contiguous, token-balanced range of the global kept sequence,
-    and the per-token results and step statistics equal the single-rank step's."""
-    cfg = synth.CONFIGS["tiny"]
+    and the per-token results and step statistics equal the single-rank step's (W up to 8, uneven ranks)."""
+    cfg = _cfg(name)
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_rebalance_worker, args=(world, _free_port(), "tiny", out), nprocs=world, join=True)
+    mp.spawn(_rebalance_worker, args=(world, _free_port(), name, out), nprocs=world, join=True)
     pk, adv, stats1 = _step_stats(cfg, 0, cfg.R)
     keys = (pk.kept_rollout[pk.tok_slot].astype(np.int64) * cfg.S
             + (np.arange(pk.n_tokens, dtype=np.int64) - pk.kept_offset[pk.tok_slot]))
