@@ -489,42 +489,55 @@ def main_echo(args):
             "unfused_ms": f2u_ms, "unfused": "torch.matmul (cuBLAS bf16) into the logits buffer + echo_token_logp",
             "speedup_vs_unfused": f2u_ms / f2_ms}
         del ws2
-        # f2 training step through the LM head (LearnerStep.loss_from_hidden: fused forward, loss from logp, D
-        # recomputed on the tensor cores in chunks, cuBLAS dhidden / dweight) against the unfused step (cuBLAS logits,
-        # the fused policy-loss kernel in place, cuBLAS dhidden / dweight)
+        # f2 training step through the LM head (LearnerStep.loss_from_hidden), every GEMM on libecho's tcgen05 kernels,
+        # against two comparison arms that call cuBLAS from this script (bench tooling only, not the library): the
+        # chunked step with cuBLAS dhidden / dweight (fp32 out, dweight accumulated -- what the library did in round
+        # 1) and the unfused step (cuBLAS logits into a full buffer, the fused loss kernel in place, cuBLAS backward)
         if not args.no_f2_train:
             chunk = 8192
+            ldz = abi.echo_lmhead_dlogits_ld(cfg.V)
             dh = torch.empty(M, hd, dtype=torch.float32, device=dev)
             dw = torch.empty(cfg.V, hd, dtype=torch.float32, device=dev)
             dh_u = torch.empty(M, hd, dtype=torch.bfloat16, device=dev)
             dw_u = torch.empty(cfg.V, hd, dtype=torch.bfloat16, device=dev)
+            zc = torch.empty(chunk, ldz, dtype=torch.bfloat16, device=dev)
             scratch = {}
             kl = cfg.kl_coef
-            t2 = {"chunked": [], "recompute": [], "chunked_tcgen05": []}
-            t2u = []
+
+            def chunked_cublas_backward():
+                for r0 in range(0, M, chunk):
+                    rows = min(chunk, M - r0)
+                    z = zc[:rows]
+                    abi.echo_lmhead_logits(hid[r0:r0 + rows], wgt, rows, hd, cfg.V, z, ldz)
+                    st.loss(z, r0, kl_coef=kl, grad_scale=1.0)
+                    D = z[:, :cfg.V]
+                    torch.mm(D, wgt, out_dtype=torch.float32, out=dh[r0:r0 + rows])
+                    if r0 == 0:
+                        torch.mm(D.t(), hid[r0:r0 + rows], out_dtype=torch.float32, out=dw)
+                    else:
+                        torch.addmm(dw, D.t(), hid[r0:r0 + rows], out_dtype=torch.float32, out=dw)
+
+            t2 = {"chunked": [], "recompute": [], "chunked_cublas_backward": [], "unfused_cublas": []}
             for r in range(5):
                 for mode in t2:
                     flush.fill_(float(r))
                     a0 = ev()
-                    st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
-                                        chunk_rows=chunk, scratch=scratch, mode=mode.split("_")[0],
-                                        blas=None if mode.endswith("tcgen05") else "torch")
+                    if mode in ("chunked", "recompute"):
+                        st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
+                                            chunk_rows=chunk, scratch=scratch, mode=mode)
+                    elif mode == "chunked_cublas_backward":
+                        chunked_cublas_backward()
+                    else:
+                        torch.matmul(hid, wgt.t(), out=logits[:, :cfg.V])
+                        st.loss(logits, 0, kl_coef=kl, grad_scale=1.0)
+                        torch.matmul(logits[:, :cfg.V], wgt, out=dh_u)     # dh = D W, dW = D^T h (bf16 outputs)
+                        torch.matmul(logits[:, :cfg.V].t(), hid, out=dw_u)
                     a1 = ev()
                     torch.cuda.synchronize()
                     if r >= 2:
                         t2[mode].append(a0.elapsed_time(a1))
-                flush.fill_(float(r))
-                b0 = ev()
-                torch.matmul(hid, wgt.t(), out=logits[:, :cfg.V])
-                st.loss(logits, 0, kl_coef=kl, grad_scale=1.0)
-                torch.matmul(logits[:, :cfg.V], wgt, out=dh_u)     # dh = D W, dW = D^T h (bf16 outputs)
-                torch.matmul(logits[:, :cfg.V].t(), hid, out=dw_u)
-                b1 = ev()
-                torch.cuda.synchronize()
-                if r >= 2:
-                    t2u.append(b0.elapsed_time(b1))
-            t2_ms, t2r_ms, t2u_ms = (statistics.median(t2["chunked"]), statistics.median(t2["recompute"]),
-                                     statistics.median(t2u))
+            ms = {k: statistics.median(v) for k, v in t2.items()}
+            t2_ms = ms["chunked"]
             fl6 = 6.0 * M * hd * cfg.V
             line["f2_train_step"] = {
                 "ms_per_micro_batch": t2_ms, "tokens_per_s_per_gpu": M / (t2_ms * 1e-3), "hidden": hd,
@@ -532,18 +545,21 @@ def main_echo(args):
                 "chunk_buffer_GB": chunk * cfg.V * 2 / 1e9,
                 "roofline": {"bound": "tensor", "achieved": fl6 / (t2_ms * 1e-3) / 1e12, "peak": pk[0],
                              "unit": "TFLOP/s", "frac": fl6 / (t2_ms * 1e-3) / 1e12 / pk[0], "peak_source": pk[1],
+                             "frac_of_sustained": fl6 / (t2_ms * 1e-3) / 1e12 / measured_bf16_peak(sustained=True)[0],
                              "flops_per_token": 6.0 * hd * cfg.V},
-                "gemms": "logits GEMM and D on libecho's tcgen05 kernels, dhidden / dweight in cuBLAS",
-                "chunked_tcgen05_ms": statistics.median(t2["chunked_tcgen05"]),
-                "chunked_tcgen05": "the same with dhidden / dweight on libecho's own tcgen05 GEMM (echo_gemm_bf16)",
-                "recompute_ms": t2r_ms,
+                "gemms": "logits GEMM, fused loss, dhidden and dweight all on libecho's kernels (tcgen05, no cuBLAS)",
+                "recompute_ms": ms["recompute"],
                 "recompute": "echo_lmhead_logp + echo_loss_from_logp + echo_lmhead_backward (D recomputed: 8 d V "
                              "flops per token)",
-                "unfused_ms": t2u_ms,
-                "unfused": f"cuBLAS logits ({M * cfg.V * 2 / 1e9:.1f} GB buffer) + echo_policy_loss_fwd_bwd in place "
-                           "+ cuBLAS dh, dW",
-                "speedup_vs_unfused": t2u_ms / t2_ms}
-            del dh, dw, dh_u, dw_u, scratch
+                "chunked_cublas_backward_ms": ms["chunked_cublas_backward"],
+                "chunked_cublas_backward": "comparison: the same chunked step with dhidden / dweight in cuBLAS "
+                                           "(torch.mm / addmm, fp32 out, dweight accumulated)",
+                "vs_chunked_cublas_backward": ms["chunked_cublas_backward"] / t2_ms,
+                "unfused_ms": ms["unfused_cublas"],
+                "unfused": f"comparison: cuBLAS logits ({M * cfg.V * 2 / 1e9:.1f} GB buffer) + echo_policy_loss_fwd_bwd "
+                           "in place + cuBLAS dh, dW (bf16 out)",
+                "speedup_vs_unfused": ms["unfused_cublas"] / t2_ms}
+            del dh, dw, dh_u, dw_u, scratch, zc
         del hid, wgt
     if plans:
         line["run"]["tokens_per_rank_before"] = plans[-1]["tokens_before"]

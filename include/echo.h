@@ -387,18 +387,16 @@ ECHO_API echo_status echo_lmhead_dlogits(const void* hidden, const void* weight,
  *   D_chunk = echo_lmhead_dlogits(...) into dlogits_ws (bf16 [chunk_rows x ld], ld = vocab rounded up to 8)
  *   dhidden[chunk] = D_chunk weight            (f32 [n_rows x d], overwritten)
  *   dweight       (+)= D_chunk^T hidden[chunk] (f32 [vocab x d]; accumulate = 0 overwrites, 1 adds to it)
- * The two products are plain bf16 GEMMs with fp32 accumulation: with cublas_handle == NULL on this library's tcgen05
- * GEMM (2-CTA UMMA, K-major D / MN-major W for dhidden, MN-major D and hidden for dweight), else in cuBLAS
- * (cublasGemmEx) on the caller's handle (a cublasHandle_t, e.g. torch.cuda.current_blas_handle(); its stream is set
- * to `stream`, pointer mode to host).  D itself always comes from this library's tensor-core kernel.  Deterministic
- * for a fixed chunk_rows (and handle).  Launches: per chunk 3 kernels (or 1 kernel + 2 cuBLAS GEMMs).  With
- * n_rows == 0: dweight zeroed (accumulate = 0) or untouched.
+ * The two products are bf16 GEMMs with fp32 accumulation on this library's tcgen05 GEMM (echo_gemm_bf16: 2-CTA
+ * UMMA with multicast 4-CTA clusters, K-major D / MN-major W for dhidden, MN-major D and hidden for dweight, the
+ * output written by TMA stores or added in L2).  Deterministic for a fixed chunk_rows.  Launches: per chunk 3
+ * kernels.  With n_rows == 0: dweight zeroed (accumulate = 0) or untouched.
  */
 ECHO_API echo_status echo_lmhead_backward(const void* hidden, const void* weight, int64_t n_rows, int32_t d,
                                           int32_t vocab, const int32_t* tok_action, const float* tok_lse,
                                           const float* tok_coef, const float* tok_ecoef, const float* tok_entropy,
                                           float* dhidden, float* dweight, int32_t accumulate, void* dlogits_ws,
-                                          int64_t chunk_rows, void* cublas_handle, void* stream);
+                                          int64_t chunk_rows, void* stream);
 
 /*
  * f2: the LM head's logits z[t, v] = sum_k hidden[t, k] weight[v, k] as a plain tcgen05 GEMM (the GEMM of
@@ -414,18 +412,17 @@ ECHO_API echo_status echo_lmhead_logits(const void* hidden, const void* weight, 
  *   echo_lmhead_logits into logits_ws (bf16 [chunk_rows x ld], ld = vocab rounded up to 8),
  *   echo_policy_loss_fwd_bwd_v2 on that chunk ((3)-(5): tok_logp / tok_loss / tok_flags / tok_entropy of the
  *     chunk's tokens, the chunk becomes dL/dz in place),
- *   dhidden[chunk] = D weight, dweight (+)= D^T hidden[chunk]  (tcgen05 GEMMs, or cuBLAS with a handle, as
- *     echo_lmhead_backward).
+ *   dhidden[chunk] = D weight, dweight (+)= D^T hidden[chunk]  (the tcgen05 GEMMs of echo_lmhead_backward).
  * Per-token arrays are full-length (offset per chunk by the library); arguments as echo_policy_loss_fwd_bwd_v2 and
  * echo_lmhead_backward.  The logits are the bf16 rounding of the fp32-accumulated z (a bf16 model's LM-head output).
- * Launches: per chunk 4 kernels (2 + 2 cuBLAS GEMMs with a handle).
+ * Launches: per chunk 4 kernels.
  */
 ECHO_API echo_status echo_lmhead_policy_loss_fwd_bwd(
     const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab, const int32_t* tok_action,
     const float* tok_old, const float* tok_ref, const int32_t* tok_slot, const float* adv_slot, const float* tok_adv,
     const float* tok_weight, const double* n_global, const echo_loss_config* cfg, float* tok_logp, float* tok_loss,
     uint8_t* tok_flags, float* tok_entropy, float* dhidden, float* dweight, int32_t accumulate, void* logits_ws,
-    int64_t chunk_rows, void* cublas_handle, void* stream);
+    int64_t chunk_rows, void* stream);
 
 /*
  * The tcgen05 GEMM behind echo_lmhead_backward (f2), exposed as a building block: c[m, n] (+)= sum_k A(m, k) B(n, k),

@@ -180,6 +180,7 @@ class LossOut:
     dlogits: np.ndarray | None
     stats: np.ndarray
     entropy: np.ndarray
+    lse: np.ndarray | None = None    # log-sum-exp of the row = z_a - logp (z_a decoded exactly from the input row)
 
 
 KL_K3, KL_K1, KL_K2 = 0, 1, 2
@@ -219,7 +220,9 @@ def policy_loss(logits, tok_action, tok_old, tok_ref, tok_slot, adv_slot, *, n_g
                                     _p(logp), _p(loss), _p(flags), _p(coef), _p(ent), _p(d), _p(stats))
     if rc != 0:
         raise ValueError("echo_ref_policy_loss: invalid argument")
-    return LossOut(logp, loss, flags, coef, d, stats, ent)
+    za = logits[np.arange(n), np.clip(tok_action, 0, V - 1)] if n else logits[:0, 0]
+    za = za.astype(np.float64) if dtype == F32 else (za.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return LossOut(logp, loss, flags, coef, d, stats, ent, za - logp)
 
 
 def token_logp(logits, tok_action, *, vocab=None, dtype=None):

@@ -28,9 +28,9 @@ LAUNCHES = {"echo_pack_batch": 3, "echo_group_advantage": 1, "echo_policy_loss_f
             "echo_token_logp": 1, "echo_policy_loss_fwd_bwd_v2": 1, "echo_gae_advantage": 1, "echo_csr_from_lengths": 2,
             "echo_lmhead_logp": 2, "echo_staleness_histogram": 1, "echo_pack_batch_v2": 3,
             "echo_loss_from_logp": 1, "echo_lmhead_dlogits": 1, "echo_lmhead_logits": 1}
-# echo_lmhead_backward: per chunk 3 libecho kernels (D, dhidden, dweight), or 1 + 2 cuBLAS GEMMs with a handle
+# echo_lmhead_backward: per chunk 3 libecho kernels (D, dhidden, dweight)
 BACKWARD_LAUNCHES_PER_CHUNK = 3
-# echo_lmhead_policy_loss_fwd_bwd: per chunk 4 libecho kernels (logits, fused loss, dhidden, dweight), or 2 + 2 cuBLAS
+# echo_lmhead_policy_loss_fwd_bwd: per chunk 4 libecho kernels (logits, fused loss, dhidden, dweight)
 LMHEAD_LOSS_LAUNCHES_PER_CHUNK = 4
 
 EXPORTS = ("echo_pack_batch", "echo_pack_batch_v2", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
@@ -93,11 +93,11 @@ def _load(path=LIB_PATH):
     lib.echo_lmhead_logp.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P]
     lib.echo_loss_from_logp.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P]
     lib.echo_lmhead_dlogits.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, i64, P]
-    lib.echo_lmhead_backward.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, P, i32, P, i64, P, P]
+    lib.echo_lmhead_backward.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, P, i32, P, i64, P]
     lib.echo_lmhead_logits.argtypes = [P, P, i64, i32, i32, P, i64, P]
     lib.echo_gemm_bf16.argtypes = [P, i32, i64, P, i32, i64, i64, i32, i32, P, i64, i32, P]
     lib.echo_lmhead_policy_loss_fwd_bwd.argtypes = [P, P, i64, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
-                                                    i32, P, i64, P, P]
+                                                    i32, P, i64, P]
     for fn in ("echo_pack_batch", "echo_group_advantage", "echo_policy_loss_fwd_bwd", "echo_policy_loss_fwd_bwd_ex",
                "echo_loss_stats", "echo_policy_loss_fwd_bwd_v2", "echo_csr_from_lengths", "echo_lmhead_logp",
                "echo_staleness_histogram", "echo_pack_batch_v2", "echo_loss_from_logp", "echo_lmhead_dlogits",
@@ -255,15 +255,10 @@ def echo_lmhead_dlogits_ld(vocab) -> int:
 
 
 def echo_lmhead_backward(hidden, weight, n_rows, d, vocab, tok_action, tok_lse, tok_coef, tok_ecoef, tok_entropy,
-                         dhidden, dweight, accumulate, dlogits_ws, chunk_rows, cublas_handle=None, stream=None):
-    """cublas_handle: None = this library's tcgen05 GEMMs for dhidden / dweight; "torch" = torch's cuBLAS handle."""
-    if isinstance(cublas_handle, str):
-        import torch
-        cublas_handle = torch.cuda.current_blas_handle()
+                         dhidden, dweight, accumulate, dlogits_ws, chunk_rows, stream=None):
     _check("echo_lmhead_backward", _lib.echo_lmhead_backward(
         _p(hidden), _p(weight), n_rows, d, vocab, _p(tok_action), _p(tok_lse), _p(tok_coef), _p(tok_ecoef),
-        _p(tok_entropy), _p(dhidden), _p(dweight), int(accumulate), _p(dlogits_ws), chunk_rows, cublas_handle,
-        _s(stream)))
+        _p(tok_entropy), _p(dhidden), _p(dweight), int(accumulate), _p(dlogits_ws), chunk_rows, _s(stream)))
 
 
 def echo_lmhead_logits(hidden, weight, n_rows, d, vocab, logits, ld, stream=None):
@@ -273,17 +268,12 @@ def echo_lmhead_logits(hidden, weight, n_rows, d, vocab, logits, ld, stream=None
 
 def echo_lmhead_policy_loss_fwd_bwd(hidden, weight, n_rows, d, vocab, tok_action, tok_old, tok_ref, tok_slot, adv_slot,
                                     tok_adv, tok_weight, n_global, cfg: LossConfig, tok_logp, tok_loss, tok_flags,
-                                    tok_entropy, dhidden, dweight, accumulate, logits_ws, chunk_rows,
-                                    cublas_handle=None, stream=None):
-    """cublas_handle: None = this library's tcgen05 GEMMs for dhidden / dweight; "torch" = torch's cuBLAS handle."""
-    if isinstance(cublas_handle, str):
-        import torch
-        cublas_handle = torch.cuda.current_blas_handle()
+                                    tok_entropy, dhidden, dweight, accumulate, logits_ws, chunk_rows, stream=None):
     _check("echo_lmhead_policy_loss_fwd_bwd", _lib.echo_lmhead_policy_loss_fwd_bwd(
         _p(hidden), _p(weight), n_rows, d, vocab, _p(tok_action), _p(tok_old), _p(tok_ref), _p(tok_slot),
         _p(adv_slot), _p(tok_adv), _p(tok_weight), _p(n_global), ctypes.byref(cfg), _p(tok_logp), _p(tok_loss),
         _p(tok_flags), _p(tok_entropy), _p(dhidden), _p(dweight), int(accumulate), _p(logits_ws), chunk_rows,
-        cublas_handle, _s(stream)))
+        _s(stream)))
 
 
 def echo_gemm_bf16(a, a_mn, lda, b, b_mn, ldb, m, n, k, c, ldc, accumulate=False, stream=None):

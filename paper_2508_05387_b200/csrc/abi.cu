@@ -52,7 +52,7 @@ extern "C" ECHO_API void echo_trace_set(unsigned long long* buf, int32_t rows) {
 
 extern "C" {
 
-int32_t echo_abi_version(void) { return 3; }
+int32_t echo_abi_version(void) { return 4; }  // 4: the f2 backward lost its cuBLAS handle
 
 const char* echo_status_string(echo_status s) {
   switch (s) {
@@ -371,8 +371,7 @@ echo_status echo_lmhead_dlogits(const void* hidden, const void* weight, int64_t 
 echo_status echo_lmhead_backward(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t vocab,
                                  const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
                                  const float* tok_ecoef, const float* tok_entropy, float* dhidden, float* dweight,
-                                 int32_t accumulate, void* dlogits_ws, int64_t chunk_rows, void* cublas_handle,
-                                 void* stream) {
+                                 int32_t accumulate, void* dlogits_ws, int64_t chunk_rows, void* stream) {
   if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || chunk_rows < 1 || chunk_rows > INT32_MAX)
     return ECHO_ERR_INVALID_ARGUMENT;
   if (!dweight || (n_rows > 0 && (!tok_action || !tok_lse || !tok_coef || !dhidden || !dlogits_ws ||
@@ -385,11 +384,9 @@ echo_status echo_lmhead_backward(const void* hidden, const void* weight, int64_t
     if (accumulate) return ECHO_OK;
     return from_cuda(cudaMemsetAsync(dweight, 0, (size_t)vocab * d * sizeof(float), static_cast<cudaStream_t>(stream)));
   }
-  int cublas_status = 0;
   const cudaError_t e = echo::launch_lmhead_backward(hidden, weight, n_rows, d, vocab, tok_action, tok_lse, tok_coef,
                                                      tok_ecoef, tok_entropy, dhidden, dweight, accumulate != 0,
-                                                     dlogits_ws, chunk_rows, cublas_handle,
-                                                     static_cast<cudaStream_t>(stream), sms, &cublas_status);
+                                                     dlogits_ws, chunk_rows, static_cast<cudaStream_t>(stream), sms);
   if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
   return from_cuda(e);
 }
@@ -415,7 +412,7 @@ echo_status echo_lmhead_policy_loss_fwd_bwd(const void* hidden, const void* weig
                                             const echo_loss_config* cfg, float* tok_logp, float* tok_loss,
                                             uint8_t* tok_flags, float* tok_entropy, float* dhidden, float* dweight,
                                             int32_t accumulate, void* logits_ws, int64_t chunk_rows,
-                                            void* cublas_handle, void* stream) {
+                                            void* stream) {
   if (!valid_lmhead_shape(hidden, weight, n_rows, d, vocab) || chunk_rows < 1 || chunk_rows > INT32_MAX ||
       !dweight || !valid_loss_config(cfg))
     return ECHO_ERR_INVALID_ARGUMENT;
@@ -438,15 +435,10 @@ echo_status echo_lmhead_policy_loss_fwd_bwd(const void* hidden, const void* weig
                                      n_global, cfg, tok_logp + r0, tok_loss + r0, tok_flags + r0,
                                      tok_entropy ? tok_entropy + r0 : nullptr, ECHO_ALGO_AUTO, stream);
     if (st != ECHO_OK) return st;
-    if (!cublas_handle) {
-      e = echo::tc_lmhead_grads(s, sms, weight, hid + r0 * d, logits_ws, ld, rows, d, vocab, dhidden + r0 * d, dweight,
-                                accumulate || r0 > 0);
-      if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
-      if (e != cudaSuccess) return ECHO_ERR_CUDA;
-    } else if (echo::cublas_lmhead_grads(cublas_handle, s, weight, hid + r0 * d, logits_ws, ld, rows, d, vocab,
-                                         dhidden + r0 * d, dweight, accumulate || r0 > 0) != 0) {
-      return ECHO_ERR_CUDA;
-    }
+    e = echo::tc_lmhead_grads(s, sms, weight, hid + r0 * d, logits_ws, ld, rows, d, vocab, dhidden + r0 * d, dweight,
+                              accumulate || r0 > 0);
+    if (e == cudaErrorInvalidValue) return ECHO_ERR_INVALID_ARGUMENT;
+    if (e != cudaSuccess) return ECHO_ERR_CUDA;
   }
   return from_cuda(cudaGetLastError());
 }

@@ -104,11 +104,6 @@ cudaError_t launch_lmhead_dlogits(const void* hidden, const void* weight, int64_
                                   cudaStream_t stream, int num_sms);
 cudaError_t launch_lmhead_logits(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
                                  void* logits, int64_t ld, cudaStream_t stream, int num_sms);
-// dhidden[rows x d] = D W and dweight (+)= D^T hidden over one chunk of rows (cuBLAS, fp32 accumulation / output);
-// returns 0 or the cublasStatus_t
-int cublas_lmhead_grads(void* cublas_handle, cudaStream_t stream, const void* weight, const void* hidden_chunk,
-                        const void* D, int64_t ld, int64_t rows, int32_t d, int32_t V, float* dhidden_chunk,
-                        float* dweight, bool beta_one);
 // C[M x N] (+)= A B on the tcgen05 tensor cores (gemm.cu): A(m, k) from a K-major [M x K] (a_mn = false) or MN-major
 // [K x M] (a_mn = true) bf16 array, B(n, k) likewise with N; row strides in bytes (multiples of 16); fp32 out.
 cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void* B, bool b_mn, int64_t b_row_bytes,
@@ -121,8 +116,8 @@ cudaError_t tc_lmhead_grads(cudaStream_t stream, int num_sms, const void* weight
 cudaError_t launch_lmhead_backward(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
                                    const int32_t* tok_action, const float* tok_lse, const float* tok_coef,
                                    const float* tok_ecoef, const float* tok_entropy, float* dhidden, float* dweight,
-                                   bool accumulate, void* dlogits_ws, int64_t chunk_rows, void* cublas_handle,
-                                   cudaStream_t stream, int num_sms, int* cublas_status);
+                                   bool accumulate, void* dlogits_ws, int64_t chunk_rows, cudaStream_t stream,
+                                   int num_sms);
 cudaError_t launch_loss_from_logp(int64_t n, const float* tok_logp, const float* tok_entropy, const float* tok_old,
                                   const float* tok_ref, const int32_t* tok_slot, const float* adv_slot,
                                   const float* tok_adv, const float* tok_weight, const double* n_global,

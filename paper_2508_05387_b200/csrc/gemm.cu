@@ -13,10 +13,22 @@
 // step).  Epilogue: thread = output row (TMEM lane), 32 fp32 columns per tcgen05.ld, 16-byte stores (+ loads when
 // accumulating).  Tiles are handed out in order by a dynamic scheduler (the leader's producer thread owns a per-launch
 // counter and broadcasts tile ids to its MMA / epilogue warps and to the peer CTA through a 4-deep ring); a poorly
-// filled last wave with a long K loop is avoided by a deterministic two-pass split-K (lower K halves first, the upper
-// half's epilogue adds onto the lower half's stores after a per-tile counter says they are complete).
+// filled last wave with a long K loop is avoided by a deterministic S-piece split-K (S <= 8 chosen so that n_tiles * S
+// fills whole waves: every piece j of every tile is handed out before any piece j + 1, and piece j's epilogue adds onto
+// piece j - 1's stores after a per-tile counter says they are complete -- a fixed fold order, so results do not depend
+// on the schedule).
+//
+// kMc (multicast): a 4-CTA cluster of two pairs computes the two N-neighbouring tiles (m, 2j) and (m, 2j + 1) in
+// lockstep, and the A operand they share is loaded once: CTA (pair p, role r) loads half p of role r's 128 A rows and
+// multicasts it to role r of both pairs (cp.async.bulk.tensor .multicast::cluster, each destination signalling its own
+// pair leader's full barrier).  A's L2 reads halve (per CTA and k-block 24 KB instead of 32 KB), which is what the
+// power-capped tensor cores turn into clock.  A CTA's ring slot is then written by both pairs, so every MMA commit
+// of a stage arrives on the empty barrier of all four CTAs (count 2).
 #include <cuda.h>
 #include <cuda_bf16.h>
+
+#include <stdlib.h>
+#include <string.h>
 
 #include <atomic>
 
@@ -31,16 +43,22 @@ constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16, kThreads = 192, kStag
 constexpr int kOpBytes = 128 * kBK * 2;  // one operand's stage per CTA: 128 rows (M or N) x 64 K bf16 = 16 KB
 constexpr uint32_t kTmemCols = 512;
 constexpr int kTidRing = 4;  // tile ids in flight between the scheduler (leader producer) and the other roles
+template <bool kMc>
+struct Geo {
+  static constexpr int kCl = kMc ? 4 : 2;  // CTAs per cluster
+  // consumers of a tile id: every producer except the scheduler's, each pair leader's MMA thread, 4 epilogue warps
+  // per CTA
+  static constexpr uint32_t kTidConsumers = (kCl - 1) + kCl / 2 + 4 * kCl;
+};
 struct Smem {
   uint8_t a[kStages][kOpBytes];
   uint8_t b[kStages][kOpBytes];
+  uint8_t ostage[4][32 * 128];  // epilogue staging per TMEM lane quadrant: 32 rows x 32 fp32, SWIZZLE_128B layout
   uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
   uint64_t tid_full[kTidRing], tid_empty[kTidRing];
   uint32_t tile_id[kTidRing];
   uint32_t tmem_base;
 };
-// consumers of a tile id: the leader's MMA thread and 4 epilogue warps, the peer's producer thread and 4 epilogue warps
-constexpr uint32_t kTidConsumers = 10;
 constexpr size_t smem_bytes() { return sizeof(Smem) + 1024; }
 
 // MN-major SWIZZLE_128B descriptor: start >> 4 | LBO 8192 B (>> 4) | SBO 1024 B (>> 4) | version 1 | layout 2
@@ -57,6 +75,13 @@ template <bool kAMN, bool kBMN>
 constexpr uint32_t idesc() {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)kAMN << 15) | ((uint32_t)kBMN << 16) |
          ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+// stage half `h` (64 rows) of one operand's 128 rows, multicast to the CTAs of `mask`
+template <bool kMN>
+ECHO_DEVINL void load_half_mc(uint32_t dst, const CUtensorMap* map, int32_t row0, int32_t k0, uint32_t bar, int h,
+                              uint16_t mask, uint64_t pol) {
+  if constexpr (kMN) lm::tma_load_2d_pair_mc(dst + h * 8192, map, row0 + 64 * h, k0, bar, mask, pol);
+  else lm::tma_load_2d_pair_mc(dst + h * 8192, map, k0, row0 + 64 * h, bar, mask, pol);  // box {64 K, 64 rows}
 }
 // stage one operand's 128 rows (M or N) x 64 K of this CTA
 template <bool kMN>
@@ -85,66 +110,87 @@ ECHO_DEVINL void tile_coords(int64_t u, int32_t n_mt, int32_t n_nt, int32_t grou
 // launch's last CTA), so that clusters that start late or run slow take fewer tiles -- no wave-quantisation tail.
 constexpr int kGemmSlots = 64;
 __device__ unsigned int g_gemm_sched[kGemmSlots][2];
-// split-K: per output tile, the number of epilogue warps (8) that have stored the lower K half (zeroed at teardown); the
-// upper half of tile t has id n_out + t, so it is handed out after every lower half (in-order scheduler: no deadlock)
+// split-K: per output tile, the number of epilogue-warp completions (8 per finished piece; zeroed at teardown).  Piece j
+// of tile t has id j n_out + t, so it is handed out after every piece j - 1 (in-order scheduler: no deadlock -- a
+// cluster walks its ids in increasing order, so the piece it waits for is always held by another, earlier cluster)
 constexpr int kMaxSplitTiles = 4096;
+constexpr int kMaxSplit = 8;
 __device__ unsigned int g_gemm_flags[kGemmSlots][kMaxSplitTiles];
 static std::atomic<uint32_t> g_gemm_next_slot{0}, g_gemm_next_slot_graph{0};
 
 struct GemmParams {
   int64_t M;
   int32_t N, K, n_mt, n_nt, n_kb, group_m;
+  int32_t n_nu;         // N units: N tiles (pair clusters) or N-tile pairs (kMc); scheduling unit = (M tile, N unit)
   unsigned int* sched;  // this launch's {tile counter, finished CTAs} (reset by the last CTA)
   unsigned int* flags;  // split-K: this launch's per-output-tile counters
-  int32_t split;        // 1 or 2: K halves per output tile (ids t, n_out + t: the second pass adds onto the first)
+  int32_t split;        // 1..kMaxSplit: K pieces per output tile (id j n_out + t: piece j adds onto piece j - 1)
   int32_t pol_a, pol_b;  // L2 policy per operand: 2 = evict_last (small, re-read by every tile), 1 = evict_first
                          // (streamed past a kept operand), 0 = evict_normal
   float* __restrict__ out;
   int64_t ldo;
   int32_t accumulate;
+  int32_t tma_out;  // output 16-B aligned with ldo % 4 == 0: the epilogue writes through map_c (TMA store / L2 add)
 };
 
-template <bool kAMN, bool kBMN>
+template <bool kAMN, bool kBMN, bool kMc>
 __global__ void __launch_bounds__(gm::kThreads, 1)
     gemm_tile_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                     const GemmParams p) {
+                     const __grid_constant__ CUtensorMap map_c, const GemmParams p) {
   using namespace gm;
+  using G = Geo<kMc>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n_out = (int64_t)p.n_mt * p.n_nt, n_tiles = n_out * p.split;
-  const int32_t kb_half = p.n_kb / 2;
+  const int64_t n_units = (int64_t)p.n_mt * p.n_nu, n_tiles = n_units * p.split;
+  // k-block range of piece j: [j n_kb / S, (j + 1) n_kb / S)
+  auto kb_begin = [&](int32_t j) { return (int32_t)(((int64_t)j * p.n_kb) / p.split); };
   const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
+  const uint32_t role = rank & 1u, pair = rank >> 1;  // role in the pair (0 = pair leader), pair in the cluster
+  const uint32_t pl = rank & ~1u;                      // this CTA's pair leader
+  const bool sched = rank == 0, pleader = role == 0;
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pair));
   // tile id of the `use`-th tile of this cluster (every role walks the same sequence); n_tiles marks the end
   auto next_tile = [&](uint32_t use) -> int64_t {
     const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
     mbar_wait_cluster(smem_u32(&sm.tid_full[r]), ph);
     return (int64_t)sm.tile_id[r];
   };
-  auto release_tile = [&](uint32_t use) {  // one arrival per consumer (thread or warp lane 0) on the leader
+  auto next_tile_warp = [&](uint32_t use) -> int64_t {  // a whole warp: lane 0 polls, every lane then acquires
+    const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
+    mbar_wait_cluster_warp(smem_u32(&sm.tid_full[r]), ph, lane);
+    return (int64_t)sm.tile_id[r];
+  };
+  auto release_tile = [&](uint32_t use) {  // one arrival per consumer (thread or warp lane 0) on the scheduler CTA
     const uint32_t r = use % kTidRing;
-    if (leader) mbar_arrive(smem_u32(&sm.tid_empty[r]));
+    if (sched) mbar_arrive(smem_u32(&sm.tid_empty[r]));
     else lm::mbar_arrive_cluster(mapa(smem_u32(&sm.tid_empty[r]), 0));
+  };
+  // unit -> this pair's output tile (kMc: the pairs take N tiles 2j and 2j + 1)
+  auto coords = [&](int64_t unit, int32_t& mt, int32_t& nt) {
+    int32_t nu;
+    tile_coords(unit, p.n_mt, p.n_nu, p.group_m, mt, nu);
+    nt = kMc ? 2 * nu + (int32_t)pair : nu;
   };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(smem_u32(&sm.full[s]), 1);
-      mbar_init(smem_u32(&sm.empty[s]), 1);
+      mbar_init(smem_u32(&sm.empty[s]), kMc ? 2 : 1);  // kMc: both pairs' MMAs read data this slot receives
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.tfull[b]), 1);
-      mbar_init(smem_u32(&sm.tempty[b]), 8);  // one arrival per epilogue warp of both CTAs
+      mbar_init(smem_u32(&sm.tempty[b]), 8);  // one arrival per epilogue warp of both CTAs of the pair
     }
     for (int r = 0; r < kTidRing; ++r) {
       mbar_init(smem_u32(&sm.tid_full[r]), 1);
-      mbar_init(smem_u32(&sm.tid_empty[r]), kTidConsumers);  // used on the leader only
+      mbar_init(smem_u32(&sm.tid_empty[r]), G::kTidConsumers);  // used on the scheduler CTA only
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    if (p.tma_out) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
@@ -165,34 +211,41 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
                                                                                 : policy_evict_normal();
       const uint64_t pol_b = p.pol_b == 2 ? policy_evict_last() : p.pol_b == 1 ? policy_evict_first()
                                                                                 : policy_evict_normal();
+      const uint16_t role_mask = (uint16_t)((1u << role) | (1u << (role + 2)));  // kMc: role r of both pairs
       for (uint32_t use = 0;; ++use) {
         int64_t u;
-        if (leader) {  // the scheduler: grab the next tile, publish it to this CTA and the peer
+        if (sched) {  // the scheduler: grab the next unit, publish it to this CTA and the others
           const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
           mbar_wait(smem_u32(&sm.tid_empty[r]), ph ^ 1u);
           u = (int64_t)atomicAdd(&p.sched[0], 1u);
           if (u > n_tiles) u = n_tiles;
           sm.tile_id[r] = (uint32_t)u;
           mbar_arrive(smem_u32(&sm.tid_full[r]));
-          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa(smem_u32(&sm.tile_id[r]), 1)), "r"((uint32_t)u)
-                       : "memory");
-          lm::mbar_arrive_cluster(mapa(smem_u32(&sm.tid_full[r]), 1));
+#pragma unroll
+          for (uint32_t q = 1; q < (uint32_t)G::kCl; ++q) {
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa(smem_u32(&sm.tile_id[r]), q)), "r"((uint32_t)u)
+                         : "memory");
+            lm::mbar_arrive_cluster(mapa(smem_u32(&sm.tid_full[r]), q));
+          }
         } else {
           u = next_tile(use);
           release_tile(use);
         }
         if (u >= n_tiles) break;
         int32_t mt, nt;
-        const bool upper = u >= n_out;  // split-K: the second pass over the upper K half
-        tile_coords(upper ? u - n_out : u, p.n_mt, p.n_nt, p.group_m, mt, nt);
-        const int32_t m_row = mt * 256 + (int32_t)rank * kBM, n_row = nt * kBN + (int32_t)rank * 128;
-        const int32_t kb0 = upper ? kb_half : 0;
-        const int32_t kb1 = (p.split == 1 || upper) ? p.n_kb : kb_half;
+        const int32_t piece = (int32_t)(u / n_units);  // split-K piece
+        coords(u - (int64_t)piece * n_units, mt, nt);
+        const int32_t m_row = mt * 256 + (int32_t)role * kBM, n_row = nt * kBN + (int32_t)role * 128;
+        const int32_t kb0 = kb_begin(piece), kb1 = kb_begin(piece + 1);
+        const uint32_t bar0 = mapa(smem_u32(&sm.full[0]), pl);
         for (int32_t kb = kb0; kb < kb1; ++kb) {
           mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
-          const uint32_t bar = mapa(smem_u32(&sm.full[stage]), 0);
-          if (leader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), 4 * kOpBytes);
-          load_op<kAMN>(smem_u32(sm.a[stage]), &map_a, m_row, kb * kBK, bar, pol_a);
+          const uint32_t bar = bar0 + 8u * stage;
+          if (pleader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), 4 * kOpBytes);
+          if constexpr (kMc)
+            load_half_mc<kAMN>(smem_u32(sm.a[stage]), &map_a, m_row, kb * kBK, bar, (int)pair, role_mask, pol_a);
+          else
+            load_op<kAMN>(smem_u32(sm.a[stage]), &map_a, m_row, kb * kBK, bar, pol_a);
           load_op<kBMN>(smem_u32(sm.b[stage]), &map_b, n_row, kb * kBK, bar, pol_b);
           if (++stage == kStages) {
             stage = 0;
@@ -202,8 +255,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer (the leader's lane 0)
-    if (lane == 0 && leader) {
+    // ---------------------------------------------------------------- MMA issuer (each pair leader's lane 0)
+    if (lane == 0 && pleader) {
       uint32_t stage = 0, phase = 0, tc = 0;
       for (;; ++tc) {
         const int64_t u = next_tile(tc);
@@ -213,9 +266,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         mbar_wait_cluster(smem_u32(&sm.tempty[buf]), aph ^ 1u);
         lm::tc_fence_after();
         const uint32_t d_tmem = tmem + buf * kBN;
-        const bool upper = u >= n_out;
-        const int32_t kb0 = upper ? kb_half : 0;
-        const int32_t kb1 = (p.split == 1 || upper) ? p.n_kb : kb_half;
+        const int32_t piece = (int32_t)(u / n_units);
+        const int32_t kb0 = kb_begin(piece), kb1 = kb_begin(piece + 1);
         for (int32_t kb = kb0; kb < kb1; ++kb) {
           mbar_wait_cluster(smem_u32(&sm.full[stage]), phase);
           lm::tc_fence_after();
@@ -224,44 +276,57 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
           for (int k = 0; k < kBK / kUmmaK; ++k)
             lm::umma_f16<true>(d_tmem, op_desc<kAMN>(a0, k), op_desc<kBMN>(b0, k), idesc<kAMN, kBMN>(),
                                (kb > kb0 || k > 0) ? 1u : 0u);
-          lm::umma_commit<true>(smem_u32(&sm.empty[stage]));
+          // the slot is free once this pair (and, kMc, the other pair) have read it: arrive on every CTA that
+          // receives data into it
+          lm::umma_commit_mask(smem_u32(&sm.empty[stage]), kMc ? (uint16_t)0xF : pair_mask);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        lm::umma_commit<true>(smem_u32(&sm.tfull[buf]));
+        lm::umma_commit_mask(smem_u32(&sm.tfull[buf]), pair_mask);
       }
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5 = TMEM lane quadrants)
+    // thread = output row (TMEM lane), 32 fp32 columns per tcgen05.ld.  TMA path: the warp's 32 x 32 block goes to
+    // its shared-memory staging box (16-byte granule j of row r at j ^ (r & 7): the SWIZZLE_128B layout) and one lane
+    // writes it with a tensor-map store, or with an add performed in L2 (cp.reduce.async.bulk .add) when
+    // accumulating -- no global loads, full-line writes, a few instructions per 1024 outputs.
     const int quad = warp & 3;
     uint32_t tc = 0;
-    const uint32_t tempty_leader = mapa(smem_u32(&sm.tempty[0]), 0);
+    const uint32_t tempty_leader = mapa(smem_u32(&sm.tempty[0]), pl);
     const bool vec_ok = (p.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
+    const uint32_t ostage = smem_u32(sm.ostage[quad]);
     for (;; ++tc) {
-      const int64_t u = next_tile(tc);
+      const int64_t u = next_tile_warp(tc);
       __syncwarp();
       if (lane == 0) release_tile(tc);
       if (u >= n_tiles) break;
       int32_t mt, nt;
-      const int64_t ot = u >= n_out ? u - n_out : u;  // output tile
-      tile_coords(ot, p.n_mt, p.n_nt, p.group_m, mt, nt);
+      const int32_t piece = (int32_t)(u / n_units);
+      const int64_t unit = u - (int64_t)piece * n_units;
+      coords(unit, mt, nt);
+      const int64_t ot = unit * (G::kCl / 2) + pair;  // this pair's output tile (split-K counter index)
       const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
-      const int64_t row = (int64_t)mt * 256 + (int64_t)rank * kBM + quad * 32 + lane;
+      const int64_t row0 = (int64_t)mt * 256 + (int64_t)role * kBM + quad * 32;  // this warp's 32 output rows
+      const int64_t row = row0 + lane;
       const bool row_ok = row < p.M;
       float* orow = p.out + (row_ok ? row : 0) * p.ldo;
-      // split-K: the second half adds onto the first half's stores (fixed order: deterministic)
-      const bool second = u >= n_out;
+      // split-K: piece j > 0 adds onto piece j - 1's stores (fixed order: deterministic)
+      const bool second = piece > 0;
       const bool acc = p.accumulate || second;
-      mbar_wait_cluster(smem_u32(&sm.tfull[buf]), aph);
+      mbar_wait_cluster_warp(smem_u32(&sm.tfull[buf]), aph, lane);
       lm::tc_fence_after();
       if (second) {
         if (lane == 0) {
           uint32_t v;
-          do {
+          for (;;) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.flags + ot) : "memory");
-          } while (v < 8u);
+            if (v >= 8u * (uint32_t)piece) break;
+            __nanosleep(256);
+          }
+          if (p.tma_out) lm::fence_proxy_async_all();  // the L2 adds below are ordered after the acquire
         }
         __syncwarp();
         __threadfence();
@@ -272,6 +337,23 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         if (cb >= p.N) break;  // warp-uniform
         uint32_t r[32];
         lm::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + ch * 32, r);
+        if (p.tma_out) {
+          if (row0 >= p.M) continue;  // warp-uniform: the whole 32-row block is past the end
+          if (lane == 0) lm::bulk_wait_read0();  // the staging box has been read by the previous chunk's TMA
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            sts_v4(ostage + (uint32_t)lane * 128u + ((uint32_t)(j ^ (lane & 7)) << 4),
+                   make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
+          lm::fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            if (acc) lm::tma_reduce_add_2d(&map_c, ostage, cb, (int32_t)row0);
+            else lm::tma_store_2d(&map_c, ostage, cb, (int32_t)row0);
+            lm::bulk_commit();
+          }
+          continue;
+        }
         if (!row_ok) continue;
         if (vec_ok && cb + 32 <= p.N) {
           float4* dst = reinterpret_cast<float4*>(orow + cb);
@@ -294,15 +376,21 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
             if (cb + i < p.N) orow[cb + i] = __uint_as_float(r[i]) + (acc ? __ldcg(orow + cb + i) : 0.0f);
         }
       }
-      if (p.split == 2 && !second) {  // publish this warp's rows of the first half
+      // the accumulator has been read: release it to the MMA of the tile after next
+      lm::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) lm::mbar_arrive_cluster(tempty_leader + buf * 8u);
+      if (piece + 1 < p.split) {  // publish this warp's rows of piece j (complete in global memory)
+        if (p.tma_out && lane == 0) {
+          lm::bulk_wait0();
+          lm::fence_proxy_async_all();
+        }
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(p.flags + ot, 1u);
       }
-      lm::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) lm::mbar_arrive_cluster(tempty_leader + buf * 8u);
     }
+    if (p.tma_out && lane == 0) lm::bulk_wait0();  // staging boxes read and writes done before the CTA retires
   }
 
   __syncwarp();
@@ -317,42 +405,53 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     if (atomicAdd(&p.sched[1], 1u) == gridDim.x - 1) {
       p.sched[0] = 0u;
       p.sched[1] = 0u;
-      if (p.split == 2)
-        for (int64_t t = 0; t < n_out; ++t) p.flags[t] = 0u;
+      if (p.split > 1)
+        for (int64_t t = 0; t < n_units * (G::kCl / 2); ++t) p.flags[t] = 0u;
       __threadfence();
     }
   }
 }
 
-template <bool kAMN, bool kBMN>
-static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams& p, cudaStream_t stream,
-                               int num_sms) {
-  const void* fn = (const void*)gemm_tile_kernel<kAMN, kBMN>;
+template <bool kAMN, bool kBMN, bool kMc>
+static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, GemmParams& p,
+                               cudaStream_t stream, int num_sms) {
+  constexpr int kCl = gm::Geo<kMc>::kCl;
+  const void* fn = (const void*)gemm_tile_kernel<kAMN, kBMN, kMc>;
   const size_t smem = gm::smem_bytes();
   static std::atomic<int> cached[64];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  int64_t units = dev < 64 ? (int64_t)cached[dev].load(std::memory_order_relaxed) - 1 : -1;
+  int64_t units = dev < 64 ? (int64_t)cached[dev].load(std::memory_order_relaxed) - 1 : -1;  // resident clusters
   if (units < 0) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    units = max_active_clusters(fn, gm::kThreads, smem, 2, num_sms / 2);
+    units = max_active_clusters(fn, gm::kThreads, smem, kCl, num_sms / kCl);
     if (dev < 64) cached[dev].store((int)units + 1, std::memory_order_relaxed);
   }
-  const int64_t n_tiles = (int64_t)p.n_mt * p.n_nt;
-  // split the K loop in two when that fills the last wave better (e.g. dhidden: 320 tiles on 74 clusters, 86 % -> 96 %)
-  // and both halves stay long (>= 64 k-blocks)
+  p.n_nu = kMc ? (p.n_nt + 1) / 2 : p.n_nt;
+  const int64_t n_work = (int64_t)p.n_mt * p.n_nu;
+  // split the K loop into S pieces when that fills the last wave better (dhidden at 8192 rows: 320 tiles on 74
+  // clusters fill 86 % of 5 waves; S = 3 fills 99.8 % of 13) and every piece stays long (>= 64 k-blocks).  Each extra
+  // piece costs one add-onto-the-output epilogue pass, hence the small per-piece penalty.
   p.split = 1;
-  if (n_tiles <= kMaxSplitTiles && p.n_kb >= 128) {
+  if (n_work * (kCl / 2) <= kMaxSplitTiles) {
     const int64_t U = units;
     auto eff = [U](int64_t t) { const int64_t w = (t + U - 1) / U; return (double)t / (double)(w * U); };
-    if (eff(2 * n_tiles) > eff(n_tiles) + 0.05) p.split = 2;  // (a second pass costs a little: only for a clear gain)
+    double best = eff(n_work);
+    for (int32_t sp = 2; sp <= kMaxSplit && p.n_kb / sp >= 64; ++sp) {
+      const double e2 = eff(sp * n_work) - 0.01 * (sp - 1);
+      if (e2 > best + 0.02) {
+        best = e2;
+        p.split = sp;
+      }
+    }
   }
-  if (units > n_tiles * p.split) units = n_tiles * p.split;
+  if (units > n_work * p.split) units = n_work * p.split;
   // half a wave of clusters per group: measured better than a full wave (dweight at 8192 rows 5.99 -> 5.24 ms,
   // 32768 rows 22.3 -> 21.8 ms; dhidden equal or better; 7 stages or a doubled group: no gain)
-  p.group_m = (int32_t)(units / (2 * p.n_nt) > 1 ? units / (2 * p.n_nt) : 1);
+  p.group_m = (int32_t)(units / (2 * p.n_nu) > 1 ? units / (2 * p.n_nu) : 1);
+  if (const char* env = getenv("ECHO_GEMM_GROUP")) p.group_m = atoi(env) > 0 ? atoi(env) : p.group_m;  // A/B knob
   unsigned int* slots = nullptr;
   e = cudaGetSymbolAddress((void**)&slots, g_gemm_sched);
   if (e != cudaSuccess) return e;
@@ -363,18 +462,27 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, Gem
   p.sched = slots + 2 * slot;
   p.flags = flags + (size_t)slot * kMaxSplitTiles;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(units * 2));
+  cfg.gridDim = dim3((unsigned)(units * kCl));
   cfg.blockDim = dim3(gm::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = 2;
+  attr.val.clusterDim.x = kCl;
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_tile_kernel<kAMN, kBMN>, ma, mb, p);
+  return cudaLaunchKernelEx(&cfg, gemm_tile_kernel<kAMN, kBMN, kMc>, ma, mb, mc, p);
+}
+
+template <bool kMc>
+static cudaError_t launch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
+                                 const CUtensorMap& mc, GemmParams& p, cudaStream_t stream, int num_sms) {
+  if (a_mn && b_mn) return launch_gemm<true, true, kMc>(ma, mb, mc, p, stream, num_sms);
+  if (!a_mn && b_mn) return launch_gemm<false, true, kMc>(ma, mb, mc, p, stream, num_sms);
+  if (!a_mn && !b_mn) return launch_gemm<false, false, kMc>(ma, mb, mc, p, stream, num_sms);
+  return launch_gemm<true, false, kMc>(ma, mb, mc, p, stream, num_sms);
 }
 
 // C[M x N] (+)= A B with A(m, k), B(n, k) read from bf16 global memory as described above; row strides in bytes.
@@ -382,9 +490,16 @@ cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void*
                              int64_t b_row_bytes, int64_t M, int32_t N, int32_t K, float* out, int64_t ldo,
                              bool accumulate, cudaStream_t stream, int num_sms) {
   if (M == 0 || N == 0) return cudaSuccess;
+  // multicast clusters: off by default -- interleaved A/B on one box measured them 7-13 % slower than plain pairs at
+  // the f2 shapes (profiles/r2h_ab_mc.jsonl; L2 already merges the pairs' concurrent reads of the shared operand);
+  // ECHO_GEMM_MC=1 selects them (N tiles must pair up: >= 2)
+  bool mc = false;
+  if (const char* env = getenv("ECHO_GEMM_MC")) mc = atoi(env) != 0 && (N + gm::kBN - 1) / gm::kBN >= 2;
   CUtensorMap ma, mb;
+  // a K-major A is loaded in 64-row halves when multicast (one half per pair)
+  const uint32_t a_box_rows = mc ? 64 : 128;
   const bool ok_a = a_mn ? make_tensor_map_bf16(&ma, A, (uint64_t)M, (uint64_t)K, (uint64_t)a_row_bytes, 64, 64)
-                         : make_tensor_map_bf16(&ma, A, (uint64_t)K, (uint64_t)M, (uint64_t)a_row_bytes, 64, 128);
+                         : make_tensor_map_bf16(&ma, A, (uint64_t)K, (uint64_t)M, (uint64_t)a_row_bytes, 64, a_box_rows);
   const bool ok_b = b_mn ? make_tensor_map_bf16(&mb, B, (uint64_t)N, (uint64_t)K, (uint64_t)b_row_bytes, 64, 64)
                          : make_tensor_map_bf16(&mb, B, (uint64_t)K, (uint64_t)N, (uint64_t)b_row_bytes, 64, 128);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
@@ -398,17 +513,26 @@ cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void*
   p.out = out;
   p.ldo = ldo;
   p.accumulate = accumulate ? 1 : 0;
-  // an operand small enough to stay in L2 (<= 48 MB, e.g. h of a chunk for dweight) is kept there while the large one
-  // streams through with evict_first; with both large, both load with evict_normal (grouped tiles share k-blocks)
+  // output through a tensor map (box 32 columns x 32 rows of fp32, SWIZZLE_128B) when its layout allows
+  // (N % 4: a tensor-map store writes whole 16-byte granules, so a ragged last granule would spill past column N)
+  CUtensorMap mc_map;
+  memset(&mc_map, 0, sizeof(mc_map));
+  p.tma_out = (ldo % 4 == 0 && N % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+               make_tensor_map_f32(&mc_map, out, (uint64_t)N, (uint64_t)M, (uint64_t)ldo * 4, 32, 32))
+                  ? 1
+                  : 0;
+  // an operand small enough to stay in L2 (<= 48 MB, e.g. h of an 8192-row chunk for dweight) is kept there while the
+  // large one streams through with evict_first; with both large, both load with evict_normal (grouped tiles share
+  // k-blocks)
   const int64_t a_bytes = M * (int64_t)K * 2, b_bytes = (int64_t)N * K * 2;
-  const bool keep_a = a_bytes <= (48ll << 20) && a_bytes < b_bytes;
-  const bool keep_b = !keep_a && b_bytes <= (48ll << 20) && b_bytes <= a_bytes;
+  int64_t keep_max = 48ll << 20;
+  if (const char* env = getenv("ECHO_GEMM_KEEP_MB")) keep_max = (int64_t)atoi(env) << 20;  // A/B knob
+  const bool keep_a = a_bytes <= keep_max && a_bytes < b_bytes;
+  const bool keep_b = !keep_a && b_bytes <= keep_max && b_bytes <= a_bytes;
   p.pol_a = keep_a ? 2 : keep_b ? 1 : 0;
   p.pol_b = keep_b ? 2 : keep_a ? 1 : 0;
-  if (a_mn && b_mn) return launch_gemm<true, true>(ma, mb, p, stream, num_sms);
-  if (!a_mn && b_mn) return launch_gemm<false, true>(ma, mb, p, stream, num_sms);
-  if (!a_mn && !b_mn) return launch_gemm<false, false>(ma, mb, p, stream, num_sms);
-  return launch_gemm<true, false>(ma, mb, p, stream, num_sms);
+  return mc ? launch_majors<true>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms)
+            : launch_majors<false>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms);
 }
 
 cudaError_t tc_lmhead_grads(cudaStream_t stream, int num_sms, const void* weight, const void* hidden_chunk,

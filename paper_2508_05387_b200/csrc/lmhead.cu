@@ -18,8 +18,9 @@
 //                      exp2 over the tile's valid columns, z[t, a_t] when the action falls in the tile; partials
 //                      to the workspace; the accumulator is released as soon as it has been read, so the MMA of
 //                      the next tile overlaps this epilogue
-// Tiles are rasterised in groups of 32 token tiles x all vocab tiles (column-major inside a group), so the CTAs in
-// flight share a few vocab tiles of B and the group's A rows (32 pair tiles x 256 x 2560 bf16 = 42 MB, L2-resident).
+// Tiles are rasterised in groups of G token tiles x all vocab tiles (column-major inside a group), so the CTAs in
+// flight share a few vocab tiles of B and the group's A rows; G is sized so that the group's A rows take ~42 MB of L2
+// (G = 32 pair tiles x 256 x 2560 bf16 at d = 2560, 16 at d = 5120; the env var ECHO_LM_GROUP overrides it for A/B).
 //
 // kPair (ECHO_LMHEAD_PAIR, the default): a 2-CTA cluster shares one 256 x 256 tile with tcgen05.mma.cta_group::2
 // (M = 256): each CTA stages its own 128 token rows of A and HALF of the 256 vocab rows of B, the leader CTA's one
@@ -30,6 +31,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+
+#include <stdlib.h>
 
 #include <atomic>
 #include <mutex>
@@ -43,10 +46,6 @@ namespace echo {
 namespace lm {
 constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16;  // per-CTA token rows, tile vocab columns, K step
 constexpr int kThreads = 192;
-#ifndef ECHO_LM_GROUP
-#define ECHO_LM_GROUP 32  // 16 / 32 / 64 / 128 A/B'd on the 32768-row logp launch: 32 fastest
-#endif
-constexpr int kGroupM = ECHO_LM_GROUP;  // token tiles per rasterisation group
 constexpr uint32_t kTmemCols = 512;
 
 template <bool kPair>
@@ -79,20 +78,22 @@ template <bool kPair>
 ECHO_DEVINL void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
   umma_f16<kPair>(tmem_d, adesc, bdesc, idesc<kPair>(), accumulate);
 }
-// tile u -> (token tile, vocab tile): groups of kGroupM token tiles, vocab-major inside a group
-ECHO_DEVINL void tile_coords(int64_t u, int32_t n_tt, int32_t n_vt, int32_t& tt, int32_t& vt) {
-  const int64_t per_group = (int64_t)kGroupM * n_vt;
+// tile u -> (token tile, vocab tile): groups of group_m token tiles, vocab-major inside a group
+ECHO_DEVINL void tile_coords(int64_t u, int32_t n_tt, int32_t n_vt, int32_t group_m, int32_t& tt, int32_t& vt) {
+  const int64_t per_group = (int64_t)group_m * n_vt;
   const int32_t g = (int32_t)(u / per_group);
-  const int32_t rows_in_g = min(kGroupM, n_tt - g * kGroupM);
+  const int32_t rows_in_g = min(group_m, n_tt - g * group_m);
   const int64_t r = u - (int64_t)g * per_group;
   vt = (int32_t)(r / rows_in_g);
-  tt = g * kGroupM + (int32_t)(r % rows_in_g);
+  tt = g * group_m + (int32_t)(r % rows_in_g);
 }
 }  // namespace lm
 
 struct LmParams {
   int64_t n_rows;
   int32_t d, V, n_tt, n_vt, n_kb;
+  int32_t group_m;  // token tiles per rasterisation group (launch_tile)
+  int32_t n_vu;     // vocab units: vocab tiles, or (kMc) pairs of neighbouring vocab tiles
   const int32_t* __restrict__ tok_action;
   float* __restrict__ part_m;  // [n_vt][n_rows]
   float* __restrict__ part_s;  // [n_vt][n_rows]
@@ -108,27 +109,39 @@ struct LmParams {
 };
 
 // kMode: 0 = logp partials, 1 = logp + entropy partials, 2 = dlogits (D written to p.dz), 3 = logits (z to p.dz)
-template <bool kPair, int kMode>
+// kMc (with kPair): 4-CTA clusters of two pairs on the vocab tiles 2j and 2j + 1 of the same token tile; the token
+// rows of A (h) they share are loaded once and multicast (each CTA loads half of its role's 128 rows for both pairs),
+// which cuts A's L2 reads in half -- see gemm.cu.
+template <bool kPair, int kMode, bool kMc = false>
 __global__ void __launch_bounds__(lm::kThreads, 1)
     lmhead_tile_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w,
                        const LmParams p) {
   using namespace lm;
+  static_assert(kPair || !kMc, "multicast clusters are made of CTA pairs");
   constexpr bool kEnt = kMode == 1, kStore = kMode >= 2;  // 2: D, 3: the logits z themselves (bf16)
   using C = Cfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   Smem<kPair>& sm = *reinterpret_cast<Smem<kPair>*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
-  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vu;   // scheduling units
+  const uint32_t crank = kPair ? cluster_ctarank() : 0u;
+  const uint32_t rank = crank & 1u;                    // role in the pair (0 = leader)
+  const uint32_t pair = kMc ? crank >> 1 : 0u, pl = crank & ~1u;
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pair));
   const int64_t unit0 = kPair ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
   const int64_t n_units = kPair ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
   const bool leader = rank == 0;
+  auto coords = [&](int64_t u, int32_t& tt, int32_t& vt) {
+    int32_t vu;
+    tile_coords(u, p.n_tt, p.n_vu, p.group_m, tt, vu);
+    vt = kMc ? 2 * vu + (int32_t)pair : vu;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(smem_u32(&sm.full[s]), 1);
-      mbar_init(smem_u32(&sm.empty[s]), 1);
+      mbar_init(smem_u32(&sm.empty[s]), kMc ? 2 : 1);  // kMc: both pairs' MMAs read data this slot receives
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.tfull[b]), 1);
@@ -161,15 +174,21 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      const uint64_t pol = policy_evict_normal();
+      const uint16_t role_mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));  // kMc: this role in both pairs
       for (int64_t u = unit0; u < n_tiles; u += n_units) {
         int32_t tt, vt;
-        tile_coords(u, p.n_tt, p.n_vt, tt, vt);
+        coords(u, tt, vt);
         for (int32_t kb = 0; kb < p.n_kb; ++kb) {
           mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
-          // both CTAs' bytes complete on the leader's full barrier; only the leader arms it (with both halves)
-          const uint32_t bar = kPair ? mapa(smem_u32(&sm.full[stage]), 0) : smem_u32(&sm.full[stage]);
+          // both CTAs' bytes complete on the pair leader's full barrier; only it arms it (with both halves)
+          const uint32_t bar = kPair ? mapa(smem_u32(&sm.full[stage]), pl) : smem_u32(&sm.full[stage]);
           if (leader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), C::kStageBytes * C::kCtas);
-          tma_load_2d<kPair>(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * C::kTileRows + (int32_t)rank * kBM, bar);
+          if constexpr (kMc)  // half `pair` of this role's 128 token rows, to this role of both pairs
+            tma_load_2d_pair_mc(smem_u32(sm.a[stage]) + pair * 8192u, &map_h, kb * kBK,
+                                tt * C::kTileRows + (int32_t)rank * kBM + (int32_t)pair * 64, bar, role_mask, pol);
+          else
+            tma_load_2d<kPair>(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * C::kTileRows + (int32_t)rank * kBM, bar);
           tma_load_2d<kPair>(smem_u32(sm.b[stage]), &map_w, kb * kBK, vt * kBN + (int32_t)rank * C::kBRows, bar);
           if (++stage == C::kStages) {
             stage = 0;
@@ -195,23 +214,26 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
           for (int k = 0; k < kBK / kUmmaK; ++k)
             umma_bf16<kPair>(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2),
                              (kb > 0 || k > 0) ? 1u : 0u);
-          umma_commit<kPair>(smem_u32(&sm.empty[stage]));  // the stage's smem is free once these MMAs have read it
+          // the stage's smem is free once these MMAs (kMc: and the other pair's) have read it
+          if constexpr (kMc) umma_commit_mask(smem_u32(&sm.empty[stage]), 0xF);
+          else umma_commit<kPair>(smem_u32(&sm.empty[stage]));
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit<kPair>(smem_u32(&sm.tfull[buf]));  // accumulator complete
+        if constexpr (kMc) umma_commit_mask(smem_u32(&sm.tfull[buf]), pair_mask);  // accumulator complete
+        else umma_commit<kPair>(smem_u32(&sm.tfull[buf]));
       }
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5 = TMEM lane quadrants)
     const int quad = warp & 3;
     uint32_t tc = 0;
-    const uint32_t tempty_leader = kPair ? mapa(smem_u32(&sm.tempty[0]), 0) : smem_u32(&sm.tempty[0]);
+    const uint32_t tempty_leader = kPair ? mapa(smem_u32(&sm.tempty[0]), pl) : smem_u32(&sm.tempty[0]);
     for (int64_t u = unit0; u < n_tiles; u += n_units, ++tc) {
       int32_t tt, vt;
-      tile_coords(u, p.n_tt, p.n_vt, tt, vt);
+      coords(u, tt, vt);
       const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
       const int64_t row = (int64_t)tt * C::kTileRows + (int64_t)rank * kBM + quad * 32 + lane;
       const bool row_ok = row < p.n_rows;
@@ -226,7 +248,7 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
         const float k = fmaf(e, H - lse, -c);
         const uint64_t l2e2 = f2(kLog2e, kLog2e), nl2 = f2(-lse * kLog2e, -lse * kLog2e), e2 = f2(e, e), k2 = f2(k, k);
         uint16_t* drow = p.dz + (row_ok ? row : 0) * p.ld;
-        mbar_wait_cluster(smem_u32(&sm.tfull[buf]), aph);
+        mbar_wait_cluster_warp(smem_u32(&sm.tfull[buf]), aph, lane);
         tc_fence_after();
 #pragma unroll 1
         for (int ch = 0; ch < kBN / 32; ++ch) {
@@ -270,7 +292,7 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
         }
         continue;
       }
-      mbar_wait_cluster(smem_u32(&sm.tfull[buf]), aph);
+      mbar_wait_cluster_warp(smem_u32(&sm.tfull[buf]), aph, lane);
       tc_fence_after();
       float m = -INFINITY, s = 0.0f, t = 0.0f, za = 0.0f;
       bool found = false;
@@ -328,7 +350,7 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
         if (kPair) mbar_arrive_cluster(tempty_leader + buf * 8u);
         else mbar_arrive(smem_u32(&sm.tempty[buf]));
       }
-      if (row_ok) {
+      if (row_ok && vt < p.n_vt) {  // (kMc with an odd tile count: the last pair's second tile does not exist)
         p.part_m[(int64_t)vt * p.n_rows + row] = m;
         p.part_s[(int64_t)vt * p.n_rows + row] = s;
         if (kEnt) p.part_t[(int64_t)vt * p.n_rows + row] = t;
@@ -409,6 +431,19 @@ bool make_tensor_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, ui
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_tensor_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                         uint32_t box_inner, uint32_t box_outer) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static bool make_map(CUtensorMap* map, const void* base, int64_t rows, int32_t d, uint32_t box_rows) {
   return make_tensor_map_bf16(map, base, (uint64_t)d, (uint64_t)rows, (uint64_t)d * 2, (uint32_t)lm::kBK, box_rows);
 }
@@ -426,16 +461,23 @@ constexpr bool kLmPair = true;
 
 // Persistent launch of lmhead_tile_kernel<kLmPair, kMode>: one (pair) cluster per resident slot, capped at the tile
 // count.  p's shape fields are filled in here.
-template <int kMode>
-static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams& p, cudaStream_t stream, int num_sms) {
+template <int kMode, bool kMc>
+static cudaError_t launch_tile_mc(const void* hidden, const void* weight, LmParams& p, cudaStream_t stream,
+                                  int num_sms) {
   using C = lm::Cfg<kLmPair>;
+  constexpr int kCl = kMc ? 4 : C::kCtas;
   CUtensorMap mh, mw;
-  if (!make_map(&mh, hidden, p.n_rows, p.d, lm::kBM) || !make_map(&mw, weight, p.V, p.d, C::kBRows))
+  if (!make_map(&mh, hidden, p.n_rows, p.d, kMc ? 64 : lm::kBM) || !make_map(&mw, weight, p.V, p.d, C::kBRows))
     return cudaErrorInvalidValue;
   p.n_tt = (int32_t)((p.n_rows + C::kTileRows - 1) / C::kTileRows);
   p.n_vt = (p.V + lm::kBN - 1) / lm::kBN;
+  p.n_vu = kMc ? (p.n_vt + 1) / 2 : p.n_vt;
   p.n_kb = (p.d + lm::kBK - 1) / lm::kBK;
-  const void* fn = (const void*)lmhead_tile_kernel<kLmPair, kMode>;
+  // group A rows ~42 MB: 16 / 32 / 64 / 128 pair tiles A/B'd at d = 2560 on the 32768-row logp launch, 32 fastest
+  p.group_m = (int32_t)((42ll << 20) / ((int64_t)C::kTileRows * p.d * 2));
+  if (const char* env = getenv("ECHO_LM_GROUP")) p.group_m = atoi(env);
+  p.group_m = p.group_m < 2 ? 2 : p.group_m > 128 ? 128 : p.group_m;
+  const void* fn = (const void*)lmhead_tile_kernel<kLmPair, kMode, kMc>;
   const size_t smem = lm::smem_bytes<kLmPair>();
   // per device, once: the shared-memory opt-in and the resident-cluster count
   static std::atomic<int> cached[64];
@@ -446,24 +488,34 @@ static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams&
   if (units < 0) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    units = kLmPair ? max_active_clusters(fn, lm::kThreads, smem, 2, num_sms / 2) : num_sms;
+    units = kLmPair ? max_active_clusters(fn, lm::kThreads, smem, kCl, num_sms / kCl) : num_sms;
     if (dev < 64) cached[dev].store((int)units + 1, std::memory_order_relaxed);
   }
-  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
+  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vu;
   if (units > n_tiles) units = n_tiles;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(units * C::kCtas));
+  cfg.gridDim = dim3((unsigned)(units * kCl));
   cfg.blockDim = dim3(lm::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = C::kCtas;
+  attr.val.clusterDim.x = kCl;
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kLmPair, kMode>, mh, mw, p);
+  return cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kLmPair, kMode, kMc>, mh, mw, p);
+}
+
+// multicast 4-CTA clusters (pairs of vocab tiles sharing their token rows) with ECHO_LM_MC=1: measured 3-4 % slower
+// than plain pairs (profiles/r2h_ab_mc.jsonl), so off by default
+template <int kMode>
+static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams& p, cudaStream_t stream, int num_sms) {
+  bool mc = false;
+  if (const char* env = getenv("ECHO_LM_MC")) mc = kLmPair && atoi(env) != 0;
+  return mc ? launch_tile_mc<kMode, kLmPair>(hidden, weight, p, stream, num_sms)
+            : launch_tile_mc<kMode, false>(hidden, weight, p, stream, num_sms);
 }
 
 cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,

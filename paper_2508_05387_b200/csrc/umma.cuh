@@ -41,6 +41,24 @@ ECHO_DEVINL void tma_load_2d_pair_hint(uint32_t dst, const CUtensorMap* map, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
       : "memory");
 }
+// Pair form with TMA multicast: the box lands at the same offset in every CTA of `mask` (a 4-CTA cluster of two
+// pairs), and each destination signals its own pair leader's barrier at bar's offset (bar: this CTA's pair leader's
+// barrier, i.e. peer bit 0).
+ECHO_DEVINL void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int32_t x, int32_t y, uint32_t bar,
+                                     uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "h"(mask), "l"(policy)
+      : "memory");
+}
+// Arrive on `bar` (same offset) in every CTA of `mask` when the MMAs issued so far have completed (pair MMA).
+ECHO_DEVINL void umma_commit_mask(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
 // Arrive on `bar` when the MMAs issued so far have completed: this CTA's barrier, or (pair) the barrier at the
 // same offset in both CTAs of the pair.
 template <bool kPair>
@@ -88,10 +106,32 @@ ECHO_DEVINL void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint3
         : "memory");
 }
 
+// Shared -> global tensor-map writes of a box (fp32): a plain store, or an add performed in L2 (cp.reduce.async.bulk),
+// tracked by the issuing thread's bulk async-groups.
+ECHO_DEVINL void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+ECHO_DEVINL void tma_reduce_add_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+ECHO_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+ECHO_DEVINL void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+ECHO_DEVINL void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+ECHO_DEVINL void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+ECHO_DEVINL void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
 }  // namespace lm
 
-// Host: 2-D bf16 tensor map with SWIZZLE_128B boxes (lmhead.cu).
+// Host: 2-D bf16 / fp32 tensor maps with SWIZZLE_128B boxes (lmhead.cu).
 bool make_tensor_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                           uint32_t box_inner, uint32_t box_outer);
+bool make_tensor_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                         uint32_t box_inner, uint32_t box_outer);
 
 }  // namespace echo

@@ -212,19 +212,18 @@ class LearnerStep:
     def loss_from_hidden(self, hidden, weight, row0: int, dhidden, dweight, *, accumulate=True, clip_low=0.2,
                          clip_high=0.2, kl_coef=0.0, grad_scale=1.0, tok_adv=None, tok_weight=None, clip_dual=0.0,
                          kl_estimator=abi.ECHO_KL_K3, entropy_coef=0.0, chunk_rows=8192, scratch=None,
-                         mode="chunked", tok_entropy=None, blas="torch"):
+                         mode="chunked", tok_entropy=None):
         """f2 training step through the LM head for packed rows [row0, row0 + n): dhidden = dL/dh into ``dhidden``
         (f32 [n x d]) and dL/dW added to (``accumulate``) or written over ``dweight`` (f32 [V x d]); per-token outputs
         land in tok_logp / tok_loss / tok_flags as with ``loss``.  No [n x V] logits buffer: at most a
         [chunk_rows x V] bf16 one.  ``scratch``: optional dict of reusable device buffers (keyed by name).
 
         mode "chunked" (default, echo_lmhead_policy_loss_fwd_bwd): per chunk, z = h W^T stored as bf16 by the tcgen05
-            GEMM, the fused (3)-(5) kernel in place, cuBLAS dhidden / dweight (6 d V flops per token).
+            GEMM, the fused (3)-(5) kernel in place, dhidden / dweight on libecho's tcgen05 GEMM (6 d V flops per
+            token).
         mode "recompute": (3) echo_lmhead_logp (logp, lse, entropy without the logits), (4) echo_loss_from_logp,
             (5) + backward echo_lmhead_backward with D recomputed from h and W on the tensor cores (8 d V flops per
-            token; logits never rounded to bf16).
-        blas: "torch" (default) = dhidden / dweight in cuBLAS on torch's handle (plain library GEMMs, 10-20 % faster
-            than libecho's own at these shapes, profiles/); None = libecho's tcgen05 GEMM (echo_gemm_bf16)."""
+            token; logits never rounded to bf16)."""
         n, d = hidden.shape
         sl = slice(row0, row0 + n)
         sc = {} if scratch is None else scratch
@@ -241,8 +240,7 @@ class LearnerStep:
                 hidden, weight, n, d, self.V, self.tok_action[sl], self.tok_old[sl], ref, self.tok_slot[sl],
                 self.adv_slot, None if tok_adv is None else tok_adv[sl], None if tok_weight is None else tok_weight[sl],
                 self.stats1[0:1], cfg, self.tok_logp[sl], self.tok_loss[sl], self.tok_flags[sl],
-                None if tok_entropy is None else tok_entropy[sl], dhidden, dweight, accumulate, ws, chunk,
-                cublas_handle=blas)
+                None if tok_entropy is None else tok_entropy[sl], dhidden, dweight, accumulate, ws, chunk)
             if n > 0:
                 self.launches += abi.LMHEAD_LOSS_LAUNCHES_PER_CHUNK * ((n + chunk - 1) // chunk)
             return
@@ -272,7 +270,7 @@ class LearnerStep:
         chunk = max(1, min(chunk_rows, n))
         dz = buf("dz", chunk * abi.echo_lmhead_dlogits_ld(self.V), torch.bfloat16)
         abi.echo_lmhead_backward(hidden, weight, n, d, self.V, self.tok_action[sl], lse, coef, ecoef, ent, dhidden,
-                                 dweight, accumulate, dz, chunk, cublas_handle=blas)
+                                 dweight, accumulate, dz, chunk)
         if n > 0:
             self.launches += (abi.LAUNCHES["echo_lmhead_logp"] + abi.LAUNCHES["echo_loss_from_logp"] +
                               abi.BACKWARD_LAUNCHES_PER_CHUNK * ((n + chunk - 1) // chunk))

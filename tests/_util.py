@@ -83,8 +83,9 @@ def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dty
     dlogits, per element (d_ref = c_t (delta_{v,a} - p_v), p_v = exp(z_v - lse) in fp64):
         |d_gpu - d_ref| <= base(d_ref) + 2^-20 cmag_t + dc_t |delta_{v,a} - p_v| + |c_t| p_v dlse_t (+ eslack)
       base = 1 bf16 ulp(d_ref) (faithful rounding: one of the two bf16 neighbours of the exact value) or 1e-5 |d_ref|
-      (fp32 logits); dlse_t = |logp_gpu - logp_ref| + 2^-22 (1 + |logp|) is the row's measured log-sum-exp error (z_a
-      is exact, so lse errs by what logp errs) and moves p_v by p_v dlse_t; dc_t = sens_t dlse_t is what that error
+      (fp32 logits); dlse_t = |logp_gpu - logp_ref| + 2^-22 (1 + |lse|) is the row's measured log-sum-exp error (z_a
+      is exact, so lse errs by what logp errs) plus the rounding of the fp32 exponent arguments (z - lse) log2e, whose
+      terms are |lse|-sized; it moves p_v by p_v dlse_t; dc_t = sens_t dlse_t is what that error
       does to c_t through the ratio and the KL term (coef_sens), reaching column v through |delta_{v,a} - p_v| only.
     Consistency (the a5 pin -d/c = exp(z - lse); rows with c_t != 0 and no entropy term): for v != a_t
       with p_v >= 2^-14 max_v p_v,   |(-d_v / c_t) - p_v| <= (2^-7 + dc_t / |c_t| + dlse_t) p_v.
@@ -111,7 +112,10 @@ def check_rows(*, d_gpu, logp_gpu, loss_gpu, flags_gpu, ref: oracle.LossOut, dty
     ca = np.abs(c)
     has_c = ca > 0
     cs = np.where(has_c, c, 1.0)
-    dlse = (lerr + 2.0 ** -22 * (1 + np.abs(ref.logp)))[ok][:, None]
+    # fp32 exponent arguments (z - lse) log2e are formed from |lse|-sized terms: 2^-22 (1 + |lse|) bounds their rounding
+    lse_mag = np.abs(ref.lse) if ref.lse is not None else np.abs(ref.logp)
+    lse_mag = np.where(np.isfinite(lse_mag), lse_mag, 0.0)
+    dlse = (lerr + 2.0 ** -22 * (1 + lse_mag))[ok][:, None]
     if sens is None:
         sens_t, cmag = np.zeros_like(ca), ca
     else:

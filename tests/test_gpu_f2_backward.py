@@ -134,7 +134,9 @@ def _d_check(dz_gpu, dz_ref):
 
 @pytest.mark.parametrize("n,d,V,eta", [(128, 64, 256, 0.0), (300, 512, 1000, 0.01), (129, 72, 257, 0.0),
                                        (1, 2560, 4096, 0.02), (700, 256, 5003, 0.0)])
-def test_lmhead_dlogits_matches_oracle(n, d, V, eta):
+@pytest.mark.parametrize("mc", ["0", "1"])
+def test_lmhead_dlogits_matches_oracle(n, d, V, eta, mc, monkeypatch):
+    monkeypatch.setenv("ECHO_LM_MC", mc)
     from paper_2508_05387_b200 import abi
     h, w, act = _case(n, d, V, seed=n * 7 + V)
     hb, wb, a = _bits(h), _bits(w), act.cpu().numpy()
@@ -152,10 +154,9 @@ def test_lmhead_dlogits_matches_oracle(n, d, V, eta):
 
 
 # ------------------------------------------------------------------------------------------ dhidden, dweight
-@pytest.mark.parametrize("blas", [None, "torch"], ids=["tcgen05", "cublas"])
 @pytest.mark.parametrize("n,d,V,chunk,eta", [(300, 128, 1000, 128, 0.0), (257, 64, 777, 300, 0.02),
                                              (520, 256, 2048, 200, 0.01), (700, 200, 1500, 700, 0.0)])
-def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta, blas):
+def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta):
     """dhidden and dweight (accumulated onto a prefilled buffer) over several chunks with a ragged last chunk.
     Bound: D is bf16 (2^-9 relative) on top of its own ~1e-5 logit error; the GEMMs accumulate in fp32:
     |err| <= 2^-7 (|D| |W|) (resp. |D|^T |h|) + 1e-6 of the row's scale."""
@@ -171,7 +172,7 @@ def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta, blas):
     dw = prev.clone()
     ws = torch.empty(chunk * abi.echo_lmhead_dlogits_ld(V), dtype=torch.bfloat16, device="cuda")
     abi.echo_lmhead_backward(h, w, n, d, V, act, cu(lse), cu(c32), cu(e32), cu(H) if eta > 0 else None, dh, dw, 1,
-                             ws, chunk, cublas_handle=blas)
+                             ws, chunk)
     torch.cuda.synchronize()
     absD = np.abs(dz_ref)
     bh = 2.0 ** -7 * (absD @ np.abs(_bf(w))) + 1e-6 * np.max(np.abs(dh_ref), axis=1, keepdims=True) + 1e-12
@@ -184,7 +185,7 @@ def test_lmhead_backward_matches_oracle(n, d, V, chunk, eta, blas):
     dw2 = torch.full((V, d), float("nan"), device="cuda")
     dh2 = torch.empty(n, d, device="cuda")
     abi.echo_lmhead_backward(h, w, n, d, V, act, cu(lse), cu(c32), cu(e32), cu(H) if eta > 0 else None, dh2, dw2, 0,
-                             ws, chunk, cublas_handle=blas)
+                             ws, chunk)
     torch.cuda.synchronize()
     assert torch.equal(dh, dh2)
     assert np.all(np.abs(dw2.cpu().numpy() - dw_ref) <= bw)
@@ -304,9 +305,8 @@ def _ulp(x):
     return 2.0 ** (np.floor(np.log2(x)) - 7)
 
 
-@pytest.mark.parametrize("blas", [None, "torch"], ids=["tcgen05", "cublas"])
 @pytest.mark.parametrize("n,d,V,chunk,eta", [(300, 128, 1000, 128, 0.0), (260, 64, 777, 100, 0.01)])
-def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta, blas):
+def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta):
     """The chunked f2 step (echo_lmhead_policy_loss_fwd_bwd) against the oracle chain on the same bf16-rounded logits:
     oracle.policy_loss on bf16(h W^T) (fp64 from the bf16 values), then dhidden = D W and dweight = D^T h in fp64.
     Tokens whose action logit lies within the GEMM's fp32 error of a bf16 rounding boundary are excluded from the
@@ -336,7 +336,7 @@ def test_lmhead_policy_loss_chunked_matches_oracle(n, d, V, chunk, eta, blas):
     ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
     cfg = abi.LossConfig(0.2, 0.2, 0.0, kl, float(n) / 4, abi.ECHO_KL_K3, eta)
     abi.echo_lmhead_policy_loss_fwd_bwd(h, w, n, d, V, act, cu(old), cu(ref), cu(slot), cu(adv), None, None, ng, cfg,
-                                        lp, loss, flags, ent, dh, dw, 0, ws, chunk, cublas_handle=blas)
+                                        lp, loss, flags, ent, dh, dw, 0, ws, chunk)
     torch.cuda.synchronize()
     # per-token bound: an element whose z lies within the GEMM's error of a bf16 rounding boundary may be stored one
     # ulp away; that moves logp by up to ulp(z_a) at the action and lse by p_v ulp(z_v) elsewhere
@@ -434,10 +434,16 @@ def test_lmhead_policy_loss_edge_cases_and_errors():
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("m,n,k", [(256, 256, 64), (300, 200, 1000), (1, 72, 4096), (777, 513, 130),
-                                   (300, 200, 16384), (513, 300, 9000)])   # the last two split K in halves
-def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k):
+                                   (300, 200, 16384), (513, 300, 9000)])   # the last two split K (4 and 2 pieces)
+@pytest.mark.parametrize("tma_out", [False, True])
+@pytest.mark.parametrize("mc", ["0", "1"])
+def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k, tma_out, mc, monkeypatch):
     """echo_gemm_bf16 (the tcgen05 GEMM of the f2 backward) in every operand layout against the fp64 product, within
-    the fp32-accumulation bound 4 (K/16 + 16) 2^-24 sum_k |A B|; ragged M / N / K tiles; accumulate mode."""
+    the fp32-accumulation bound 4 (K/16 + 16) 2^-24 sum_k |A B|; ragged M / N / K tiles; accumulate and overwrite
+    modes; an output row stride that is a multiple of 4 floats takes the TMA store / L2-add epilogue, any other the
+    per-thread one.  mc = 1: 4-CTA clusters whose two pairs share (multicast) the A operand (N tiles paired up, an odd
+    last one computed against zero-filled B and not stored)."""
+    monkeypatch.setenv("ECHO_GEMM_MC", mc)
     from paper_2508_05387_b200 import abi
     g = torch.Generator(device="cuda").manual_seed(m + n + k + 2 * a_mn + b_mn)
     A = torch.randn(m, k, generator=g, device="cuda").to(torch.bfloat16)
@@ -449,7 +455,7 @@ def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k):
     b_buf = torch.zeros(b_store.shape[0], ld(b_store.shape[1]), dtype=torch.bfloat16, device="cuda")
     a_buf[:, :a_store.shape[1]] = a_store
     b_buf[:, :b_store.shape[1]] = b_store
-    ldc = n + 3
+    ldc = (n + 3) // 4 * 4 + 4 if tma_out else n + 3
     prev = torch.randn(m, ldc, generator=g, device="cuda")
     c = prev.clone()
     abi.echo_gemm_bf16(a_buf, a_mn, a_buf.shape[1], b_buf, b_mn, b_buf.shape[1], m, n, k, c, ldc, accumulate=True)
@@ -460,10 +466,17 @@ def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k):
     got = (c - prev)[:, :n].cpu().numpy().astype(np.float64)
     assert np.all(np.abs(got - ref) <= bound + 1e-6), np.max(np.abs(got - ref) / (bound + 1e-6))
     assert torch.equal(c[:, n:], prev[:, n:])                          # columns >= n untouched
-    c2 = prev.clone()                                                  # deterministic (split-K halves in fixed order)
+    c2 = prev.clone()                                                  # deterministic (split-K pieces in fixed order)
     abi.echo_gemm_bf16(a_buf, a_mn, a_buf.shape[1], b_buf, b_mn, b_buf.shape[1], m, n, k, c2, ldc, accumulate=True)
     torch.cuda.synchronize()
     assert torch.equal(c, c2)
+    c3 = prev.clone()                                                  # overwrite mode
+    abi.echo_gemm_bf16(a_buf, a_mn, a_buf.shape[1], b_buf, b_mn, b_buf.shape[1], m, n, k, c3, ldc, accumulate=False)
+    torch.cuda.synchronize()
+    got3 = c3[:, :n].cpu().numpy().astype(np.float64)
+    bound3 = 4 * (k / 16 + 16) * 2.0 ** -24 * (np.abs(Af) @ np.abs(Bf).T)
+    assert np.all(np.abs(got3 - ref) <= bound3 + 1e-6), np.max(np.abs(got3 - ref) / (bound3 + 1e-6))
+    assert torch.equal(c3[:, n:], prev[:, n:])
 
 
 def test_chunked_f4_options_equal_the_logits_path():

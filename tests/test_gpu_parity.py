@@ -621,8 +621,11 @@ def _lmhead_tol(hb, wb, rows):
 
 @pytest.mark.parametrize("n,d,V", [(128, 64, 256), (300, 512, 1000), (129, 72, 257), (1, 2560, 4096),
                                    (700, 256, 5000)])
-def test_lmhead_logp_small(n, d, V):
-    """f2: the fused LM-head log-prob against the fp64 oracle (every row), ragged token / vocab / K tiles."""
+@pytest.mark.parametrize("mc", ["0", "1"])
+def test_lmhead_logp_small(n, d, V, mc, monkeypatch):
+    """f2: the fused LM-head log-prob against the fp64 oracle (every row), ragged token / vocab / K tiles; 2-CTA pairs
+    (mc 0) or 4-CTA clusters multicasting the token rows (mc 1; V = 257 / 5000 give an odd vocab-tile count)."""
+    monkeypatch.setenv("ECHO_LM_MC", mc)
     h, w, act = _lmhead_case(n, d, V, seed=n + d + V)
     lp, lse = _lmhead_run(h, w, act)
     hb = h.cpu().view(torch.int16).numpy().view(np.uint16)

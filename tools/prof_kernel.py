@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--streams", action="store_true", help="also time torch in-place / copy streams")
     ap.add_argument("--dtype", default=None, choices=[None, "bf16", "f32"], help="override the config's logits dtype")
     ap.add_argument("--vocab", type=int, default=None, help="override the config's vocabulary size")
+    ap.add_argument("--entropy", type=float, default=0.0, help="f4 entropy bonus eta (> 0: the entropy variant)")
     args = ap.parse_args()
 
     import __graft_entry__
@@ -58,6 +59,7 @@ def main():
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     bpt = 2 * cfg.V * esize + 21 + (4 if cfg.kl_coef > 0 else 0)
     names = abi.ALGO_NAMES
+    ent = torch.empty(M, dtype=torch.float32, device="cuda")
     out = {"config": cfg.name, "rows": M, "bytes_per_token": bpt, "algos": {}}
 
     def regen():
@@ -73,7 +75,10 @@ def main():
             regen()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            st.loss(logits, 0, kl_coef=cfg.kl_coef, algo=algo)
+            if args.entropy > 0:
+                st.loss(logits, 0, kl_coef=cfg.kl_coef, algo=algo, entropy_coef=args.entropy, tok_entropy=ent)
+            else:
+                st.loss(logits, 0, kl_coef=cfg.kl_coef, algo=algo)
             e1.record()
             torch.cuda.synchronize()
             if r >= args.warmup:

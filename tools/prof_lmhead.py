@@ -25,7 +25,6 @@ def main():
                     help="logp: echo_lmhead_logp; dlogits: echo_lmhead_dlogits over one chunk of --chunk rows; "
                          "backward: echo_lmhead_backward over --rows in --chunk chunks")
     ap.add_argument("--chunk", type=int, default=8192)
-    ap.add_argument("--blas", default=None, choices=[None, "torch"], help="backward GEMMs: libecho tcgen05 / cuBLAS")
     a = ap.parse_args()
     import __graft_entry__
     __graft_entry__.build()
@@ -72,9 +71,8 @@ def main():
         else:
             dh = torch.empty(n, d, device="cuda")
             dw = torch.empty(V, d, device="cuda")
-            ms = timed(lambda: abi.echo_lmhead_backward(h, w, n, d, V, act, lse, coef, None, None, dh, dw, 0, dz, ck,
-                                                          cublas_handle=a.blas))
-            out.update(chunk=ck, blas=a.blas or "tcgen05", backward_ms=ms, backward_tflops_6dV_over_3=2 * flops / ms / 1e9,
+            ms = timed(lambda: abi.echo_lmhead_backward(h, w, n, d, V, act, lse, coef, None, None, dh, dw, 0, dz, ck))
+            out.update(chunk=ck, backward_ms=ms, backward_tflops_6dV_over_3=2 * flops / ms / 1e9,
                        backward_tflops_executed=3 * flops / ms / 1e9)
         print(json.dumps(out))
         return
