@@ -3,6 +3,8 @@
 
 #include <cuda_bf16.h>
 
+#include <stdlib.h>
+
 #include "echo_internal.h"
 
 namespace {
@@ -265,6 +267,11 @@ echo_status echo_token_logp(const void* logits, int32_t dtype, int64_t n_rows, i
   p.trace_rows = g_trace_rows;
 #endif
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // bf16: one warp per row (token_logp.cu); ECHO_LOGP_CLUSTER=1 selects the fused kernel's cluster tile in logp mode
+  const char* env = getenv("ECHO_LOGP_CLUSTER");
+  const bool cluster = env && atoi(env) != 0;
+  if (!cluster && echo::token_logp_warp_supports(dtype, vocab))
+    return from_cuda(echo::launch_token_logp_warp(p, s, sms));
   if (echo::hex_supports(dtype, vocab) && vocab >= 16384)
     return from_cuda(echo::launch_quad_logp(p, dtype, s, sms, nullptr));
   return from_cuda(echo::launch_row(p, dtype, s, sms, nullptr, false));

@@ -80,31 +80,6 @@ ECHO_DEVINL float ex2(float x) {
 }
 
 // ---------------------------------------------------------------- L2 cache policies
-// 2^x for two fp32 lanes on the FMA pipe (no MUFU): x clamped to >= -126, x = j + f with j = rint(x) (the 1.5 2^23
-// magic add) and |f| <= 1/2, 2^f by a degree-5 polynomial (coefficients fitted to the relative error on [-1/2, 1/2]:
-// max 3.4e-7, against ~2.4e-7 for ex2.approx), then j added to the exponent field.  Used where the MUFU pipe, not
-// issue, is the limiter (the entropy variant's second exponential per logit).
-ECHO_DEVINL uint64_t ex2_poly2(uint64_t x2) {
-  float x0, x1;
-  f2split(x2, x0, x1);
-  x0 = fmaxf(x0, -126.0f);
-  x1 = fmaxf(x1, -126.0f);
-  const uint64_t magic = f2(12582912.0f, 12582912.0f);
-  const uint64_t xr = add2(f2(x0, x1), magic);              // rint(x) in the low mantissa bits
-  const uint64_t j = add2(xr, f2(-12582912.0f, -12582912.0f));
-  const uint64_t f = fma2(j, f2(-1.0f, -1.0f), f2(x0, x1)); // x - j
-  uint64_t p = fma2(f2(1.2915669940412045e-3f, 1.2915669940412045e-3f), f, f2(9.668530896306038e-3f, 9.668530896306038e-3f));
-  p = fma2(p, f, f2(5.5516887456178665e-2f, 5.5516887456178665e-2f));
-  p = fma2(p, f, f2(2.4022264778614044e-1f, 2.4022264778614044e-1f));
-  p = fma2(p, f, f2(6.931464672088623e-1f, 6.931464672088623e-1f));
-  p = fma2(p, f, f2(1.0f, 1.0f));
-  float p0, p1, r0, r1;
-  f2split(p, p0, p1);
-  f2split(xr, r0, r1);
-  // exponent += j: the low bits of xr hold j (two's complement in the mantissa of 1.5 2^23)
-  return f2(__int_as_float(__float_as_int(p0) + (__float_as_int(r0) << 23)),
-            __int_as_float(__float_as_int(p1) + (__float_as_int(r1) << 23)));
-}
 ECHO_DEVINL uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -210,7 +185,8 @@ ECHO_DEVINL void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
   }
 }
 // A whole warp waits on one barrier: lane 0 polls it, then every lane takes its own (now immediate) acquire.
-// (A try_wait suspend-time hint here made the tensor-core kernels 5-25 % slower: the woken epilogue is late.)
+// (try_wait suspend-time hints on the tensor-core kernels' waits were neutral to 25 % slower in interleaved A/B:
+// profiles/r2j_ab_cublas.jsonl, r2l_ab_cublas.jsonl.)
 ECHO_DEVINL void mbar_wait_cluster_warp(uint32_t bar, uint32_t parity, int lane) {
   if (lane == 0) mbar_wait_cluster(bar, parity);
   __syncwarp();

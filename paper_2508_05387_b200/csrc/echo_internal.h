@@ -71,6 +71,9 @@ struct LaunchShape {
 // Per-kernel launchers (policy_loss_{quad,row}.cu); with shape != nullptr: report the shape, launch nothing.
 cudaError_t launch_row(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms, LaunchShape* shape,
                        bool grad = true);
+// f1: forward-only log-probs, one warp per row (token_logp.cu)
+bool token_logp_warp_supports(int32_t dtype, int32_t V);
+cudaError_t launch_token_logp_warp(const LossParams& p, cudaStream_t stream, int num_sms);
 cudaError_t launch_quad_logp(const LossParams& p, int32_t dtype, cudaStream_t stream, int num_sms,
                              LaunchShape* shape);
 int max_active_clusters(const void* fn, int threads, size_t smem, int cluster, int fallback);

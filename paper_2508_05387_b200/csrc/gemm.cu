@@ -448,9 +448,12 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, con
     }
   }
   if (units > n_work * p.split) units = n_work * p.split;
-  // half a wave of clusters per group: measured better than a full wave (dweight at 8192 rows 5.99 -> 5.24 ms,
-  // 32768 rows 22.3 -> 21.8 ms; dhidden equal or better; 7 stages or a doubled group: no gain)
+  // raster group: half a wave of clusters (measured better than a full wave at d = 2560: dweight at 8192 rows 5.99 ->
+  // 5.24 ms), but 16 M tiles once there are >= 16 N units -- the tiles in flight then span ~16 M x 4.6 N tiles instead
+  // of ~4 x 20, cutting the DRAM re-reads of the N-side operand (interleaved A/B at d = 5120, 8192 rows: dhidden
+  // 11.81 -> 10.66 ms, dweight 11.28 -> 10.51 ms; profiles/r2i_ab_knobs.jsonl)
   p.group_m = (int32_t)(units / (2 * p.n_nu) > 1 ? units / (2 * p.n_nu) : 1);
+  if (p.n_nu >= 16) p.group_m = 16;
   if (const char* env = getenv("ECHO_GEMM_GROUP")) p.group_m = atoi(env) > 0 ? atoi(env) : p.group_m;  // A/B knob
   unsigned int* slots = nullptr;
   e = cudaGetSymbolAddress((void**)&slots, g_gemm_sched);

@@ -56,14 +56,20 @@ struct Cfg {
   static constexpr int kStages = kPair ? 6 : 4;
   static constexpr int kTileRows = kBM * kCtas;          // token rows of a (pair) tile
 };
+constexpr int kTidRing = 4;  // tile ids in flight between the scheduler (leader producer) and the other roles
 template <bool kPair>
 struct Smem {
   using C = Cfg<kPair>;
   uint8_t a[C::kStages][C::kABytes];
   uint8_t b[C::kStages][C::kBBytes];
   uint64_t full[C::kStages], empty[C::kStages], tfull[2], tempty[2];
+  uint64_t tid_full[kTidRing], tid_empty[kTidRing];
+  uint32_t tile_id[kTidRing];
   uint32_t tmem_base;
 };
+// consumers of a tile id: the leader's MMA thread, 4 epilogue warps per CTA, the peer's producer thread
+template <bool kPair>
+constexpr uint32_t tid_consumers() { return kPair ? 10u : 5u; }
 template <bool kPair>
 constexpr size_t smem_bytes() { return sizeof(Smem<kPair>) + 1024; }  // + SWIZZLE_128B 1024-B alignment slack
 
@@ -93,7 +99,7 @@ struct LmParams {
   int64_t n_rows;
   int32_t d, V, n_tt, n_vt, n_kb;
   int32_t group_m;  // token tiles per rasterisation group (launch_tile)
-  int32_t n_vu;     // vocab units: vocab tiles, or (kMc) pairs of neighbouring vocab tiles
+  unsigned int* sched;  // this launch's {tile counter, finished CTAs} (in-order dynamic scheduler; reset by the last CTA)
   const int32_t* __restrict__ tok_action;
   float* __restrict__ part_m;  // [n_vt][n_rows]
   float* __restrict__ part_s;  // [n_vt][n_rows]
@@ -109,43 +115,53 @@ struct LmParams {
 };
 
 // kMode: 0 = logp partials, 1 = logp + entropy partials, 2 = dlogits (D written to p.dz), 3 = logits (z to p.dz)
-// kMc (with kPair): 4-CTA clusters of two pairs on the vocab tiles 2j and 2j + 1 of the same token tile; the token
-// rows of A (h) they share are loaded once and multicast (each CTA loads half of its role's 128 rows for both pairs),
-// which cuts A's L2 reads in half -- see gemm.cu.
-template <bool kPair, int kMode, bool kMc = false>
+// Tiles are handed out in order by a dynamic scheduler (as in gemm.cu): the leader's producer thread takes the next
+// tile from a per-launch counter and broadcasts it to its MMA / epilogue warps and to the peer CTA through a 4-deep
+// ring, so all clusters work inside one compact window of tiles.  (A static stride lets clusters drift apart over the
+// ~1000 waves of a 32768-row launch, and the raster group's operands stop being shared in L2.)
+template <bool kPair, int kMode>
 __global__ void __launch_bounds__(lm::kThreads, 1)
     lmhead_tile_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w,
                        const LmParams p) {
   using namespace lm;
-  static_assert(kPair || !kMc, "multicast clusters are made of CTA pairs");
   constexpr bool kEnt = kMode == 1, kStore = kMode >= 2;  // 2: D, 3: the logits z themselves (bf16)
   using C = Cfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   Smem<kPair>& sm = *reinterpret_cast<Smem<kPair>*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vu;   // scheduling units
-  const uint32_t crank = kPair ? cluster_ctarank() : 0u;
-  const uint32_t rank = crank & 1u;                    // role in the pair (0 = leader)
-  const uint32_t pair = kMc ? crank >> 1 : 0u, pl = crank & ~1u;
-  const uint16_t pair_mask = (uint16_t)(3u << (2 * pair));
-  const int64_t unit0 = kPair ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
-  const int64_t n_units = kPair ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
+  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
-  auto coords = [&](int64_t u, int32_t& tt, int32_t& vt) {
-    int32_t vu;
-    tile_coords(u, p.n_tt, p.n_vu, p.group_m, tt, vu);
-    vt = kMc ? 2 * vu + (int32_t)pair : vu;
+  // tile id of the `use`-th tile of this cluster (every role walks the same sequence); n_tiles marks the end
+  auto next_tile = [&](uint32_t use) -> int64_t {
+    const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
+    mbar_wait_cluster(smem_u32(&sm.tid_full[r]), ph);
+    return (int64_t)sm.tile_id[r];
+  };
+  auto next_tile_warp = [&](uint32_t use) -> int64_t {  // a whole warp: lane 0 polls, every lane then acquires
+    const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
+    mbar_wait_cluster_warp(smem_u32(&sm.tid_full[r]), ph, lane);
+    return (int64_t)sm.tile_id[r];
+  };
+  auto release_tile = [&](uint32_t use) {  // one arrival per consumer (thread or warp lane 0) on the leader
+    const uint32_t r = use % kTidRing;
+    if (leader) mbar_arrive(smem_u32(&sm.tid_empty[r]));
+    else mbar_arrive_cluster(mapa(smem_u32(&sm.tid_empty[r]), 0));
   };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(smem_u32(&sm.full[s]), 1);
-      mbar_init(smem_u32(&sm.empty[s]), kMc ? 2 : 1);  // kMc: both pairs' MMAs read data this slot receives
+      mbar_init(smem_u32(&sm.empty[s]), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.tfull[b]), 1);
       mbar_init(smem_u32(&sm.tempty[b]), 4 * C::kCtas);  // one arrival per epilogue warp (of both CTAs)
+    }
+    for (int r = 0; r < kTidRing; ++r) {
+      mbar_init(smem_u32(&sm.tid_full[r]), 1);
+      mbar_init(smem_u32(&sm.tid_empty[r]), tid_consumers<kPair>());  // used on the leader only
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_h)) : "memory");
@@ -171,24 +187,36 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
+    // ---------------------------------------------------------------- TMA producer (the leader's is the scheduler)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      const uint64_t pol = policy_evict_normal();
-      const uint16_t role_mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));  // kMc: this role in both pairs
-      for (int64_t u = unit0; u < n_tiles; u += n_units) {
+      for (uint32_t use = 0;; ++use) {
+        int64_t u;
+        if (leader) {
+          const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
+          mbar_wait(smem_u32(&sm.tid_empty[r]), ph ^ 1u);
+          u = (int64_t)atomicAdd(&p.sched[0], 1u);
+          if (u > n_tiles) u = n_tiles;
+          sm.tile_id[r] = (uint32_t)u;
+          mbar_arrive(smem_u32(&sm.tid_full[r]));
+          if constexpr (kPair) {
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa(smem_u32(&sm.tile_id[r]), 1)), "r"((uint32_t)u)
+                         : "memory");
+            mbar_arrive_cluster(mapa(smem_u32(&sm.tid_full[r]), 1));
+          }
+        } else {
+          u = next_tile(use);
+          release_tile(use);
+        }
+        if (u >= n_tiles) break;
         int32_t tt, vt;
-        coords(u, tt, vt);
+        tile_coords(u, p.n_tt, p.n_vt, p.group_m, tt, vt);
         for (int32_t kb = 0; kb < p.n_kb; ++kb) {
           mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
-          // both CTAs' bytes complete on the pair leader's full barrier; only it arms it (with both halves)
-          const uint32_t bar = kPair ? mapa(smem_u32(&sm.full[stage]), pl) : smem_u32(&sm.full[stage]);
+          // both CTAs' bytes complete on the leader's full barrier; only the leader arms it (with both halves)
+          const uint32_t bar = kPair ? mapa(smem_u32(&sm.full[stage]), 0) : smem_u32(&sm.full[stage]);
           if (leader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), C::kStageBytes * C::kCtas);
-          if constexpr (kMc)  // half `pair` of this role's 128 token rows, to this role of both pairs
-            tma_load_2d_pair_mc(smem_u32(sm.a[stage]) + pair * 8192u, &map_h, kb * kBK,
-                                tt * C::kTileRows + (int32_t)rank * kBM + (int32_t)pair * 64, bar, role_mask, pol);
-          else
-            tma_load_2d<kPair>(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * C::kTileRows + (int32_t)rank * kBM, bar);
+          tma_load_2d<kPair>(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * C::kTileRows + (int32_t)rank * kBM, bar);
           tma_load_2d<kPair>(smem_u32(sm.b[stage]), &map_w, kb * kBK, vt * kBN + (int32_t)rank * C::kBRows, bar);
           if (++stage == C::kStages) {
             stage = 0;
@@ -200,8 +228,11 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0 && leader) {  // pair: the leader's thread issues for both CTAs
-      uint32_t stage = 0, phase = 0, tc = 0;
-      for (int64_t u = unit0; u < n_tiles; u += n_units, ++tc) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t tc = 0;; ++tc) {
+        const int64_t u = next_tile(tc);
+        release_tile(tc);
+        if (u >= n_tiles) break;
         const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
         mbar_wait_cluster(smem_u32(&sm.tempty[buf]), aph ^ 1u);
         tc_fence_after();
@@ -214,26 +245,27 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
           for (int k = 0; k < kBK / kUmmaK; ++k)
             umma_bf16<kPair>(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2),
                              (kb > 0 || k > 0) ? 1u : 0u);
-          // the stage's smem is free once these MMAs (kMc: and the other pair's) have read it
-          if constexpr (kMc) umma_commit_mask(smem_u32(&sm.empty[stage]), 0xF);
-          else umma_commit<kPair>(smem_u32(&sm.empty[stage]));
+          umma_commit<kPair>(smem_u32(&sm.empty[stage]));  // the stage's smem is free once these MMAs have read it
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        if constexpr (kMc) umma_commit_mask(smem_u32(&sm.tfull[buf]), pair_mask);  // accumulator complete
-        else umma_commit<kPair>(smem_u32(&sm.tfull[buf]));
+        umma_commit<kPair>(smem_u32(&sm.tfull[buf]));  // accumulator complete
       }
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5 = TMEM lane quadrants)
     const int quad = warp & 3;
     uint32_t tc = 0;
-    const uint32_t tempty_leader = kPair ? mapa(smem_u32(&sm.tempty[0]), pl) : smem_u32(&sm.tempty[0]);
-    for (int64_t u = unit0; u < n_tiles; u += n_units, ++tc) {
+    const uint32_t tempty_leader = kPair ? mapa(smem_u32(&sm.tempty[0]), 0) : smem_u32(&sm.tempty[0]);
+    for (;; ++tc) {
+      const int64_t u = next_tile_warp(tc);
+      __syncwarp();
+      if (lane == 0) release_tile(tc);
+      if (u >= n_tiles) break;
       int32_t tt, vt;
-      coords(u, tt, vt);
+      tile_coords(u, p.n_tt, p.n_vt, p.group_m, tt, vt);
       const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
       const int64_t row = (int64_t)tt * C::kTileRows + (int64_t)rank * kBM + quad * 32 + lane;
       const bool row_ok = row < p.n_rows;
@@ -350,7 +382,7 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
         if (kPair) mbar_arrive_cluster(tempty_leader + buf * 8u);
         else mbar_arrive(smem_u32(&sm.tempty[buf]));
       }
-      if (row_ok && vt < p.n_vt) {  // (kMc with an odd tile count: the last pair's second tile does not exist)
+      if (row_ok) {
         p.part_m[(int64_t)vt * p.n_rows + row] = m;
         p.part_s[(int64_t)vt * p.n_rows + row] = s;
         if (kEnt) p.part_t[(int64_t)vt * p.n_rows + row] = t;
@@ -369,6 +401,14 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+  }
+  if (threadIdx.x == 0) {  // every scheduler of this launch is done once all CTAs are here: reset the slot
+    __threadfence();
+    if (atomicAdd(&p.sched[1], 1u) == gridDim.x - 1) {
+      p.sched[0] = 0u;
+      p.sched[1] = 0u;
+      __threadfence();
+    }
   }
 }
 
@@ -459,25 +499,29 @@ constexpr bool kLmPair = false;
 constexpr bool kLmPair = true;
 #endif
 
+// In-order dynamic tile scheduler slots (as in gemm.cu): one {counter, finished CTAs} pair per launch, reset by the
+// launch's last CTA; graph-captured launches keep theirs (next_sched_slot).
+constexpr int kLmSlots = 64;
+__device__ unsigned int g_lm_sched[kLmSlots][2];
+static std::atomic<uint32_t> g_lm_next_slot{0}, g_lm_next_slot_graph{0};
+
 // Persistent launch of lmhead_tile_kernel<kLmPair, kMode>: one (pair) cluster per resident slot, capped at the tile
 // count.  p's shape fields are filled in here.
-template <int kMode, bool kMc>
-static cudaError_t launch_tile_mc(const void* hidden, const void* weight, LmParams& p, cudaStream_t stream,
-                                  int num_sms) {
+template <int kMode>
+static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams& p, cudaStream_t stream, int num_sms) {
   using C = lm::Cfg<kLmPair>;
-  constexpr int kCl = kMc ? 4 : C::kCtas;
   CUtensorMap mh, mw;
-  if (!make_map(&mh, hidden, p.n_rows, p.d, kMc ? 64 : lm::kBM) || !make_map(&mw, weight, p.V, p.d, C::kBRows))
+  if (!make_map(&mh, hidden, p.n_rows, p.d, lm::kBM) || !make_map(&mw, weight, p.V, p.d, C::kBRows))
     return cudaErrorInvalidValue;
   p.n_tt = (int32_t)((p.n_rows + C::kTileRows - 1) / C::kTileRows);
   p.n_vt = (p.V + lm::kBN - 1) / lm::kBN;
-  p.n_vu = kMc ? (p.n_vt + 1) / 2 : p.n_vt;
   p.n_kb = (p.d + lm::kBK - 1) / lm::kBK;
-  // group A rows ~42 MB: 16 / 32 / 64 / 128 pair tiles A/B'd at d = 2560 on the 32768-row logp launch, 32 fastest
+  // group A rows ~42 MB: 16 / 32 / 64 / 128 pair tiles A/B'd at d = 2560 on the 32768-row logp launch, 32 fastest;
+  // 4 / 8 / 16 / 32 at d = 5120: 16 fastest (profiles/r2i_ab_knobs.jsonl)
   p.group_m = (int32_t)((42ll << 20) / ((int64_t)C::kTileRows * p.d * 2));
   if (const char* env = getenv("ECHO_LM_GROUP")) p.group_m = atoi(env);
   p.group_m = p.group_m < 2 ? 2 : p.group_m > 128 ? 128 : p.group_m;
-  const void* fn = (const void*)lmhead_tile_kernel<kLmPair, kMode, kMc>;
+  const void* fn = (const void*)lmhead_tile_kernel<kLmPair, kMode>;
   const size_t smem = lm::smem_bytes<kLmPair>();
   // per device, once: the shared-memory opt-in and the resident-cluster count
   static std::atomic<int> cached[64];
@@ -488,34 +532,28 @@ static cudaError_t launch_tile_mc(const void* hidden, const void* weight, LmPara
   if (units < 0) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    units = kLmPair ? max_active_clusters(fn, lm::kThreads, smem, kCl, num_sms / kCl) : num_sms;
+    units = kLmPair ? max_active_clusters(fn, lm::kThreads, smem, C::kCtas, num_sms / C::kCtas) : num_sms;
     if (dev < 64) cached[dev].store((int)units + 1, std::memory_order_relaxed);
   }
-  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vu;
+  const int64_t n_tiles = (int64_t)p.n_tt * p.n_vt;
   if (units > n_tiles) units = n_tiles;
+  unsigned int* slots = nullptr;
+  e = cudaGetSymbolAddress((void**)&slots, g_lm_sched);
+  if (e != cudaSuccess) return e;
+  p.sched = slots + 2 * next_sched_slot(g_lm_next_slot, g_lm_next_slot_graph, stream, kLmSlots);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(units * kCl));
+  cfg.gridDim = dim3((unsigned)(units * C::kCtas));
   cfg.blockDim = dim3(lm::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = kCl;
+  attr.val.clusterDim.x = C::kCtas;
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kLmPair, kMode, kMc>, mh, mw, p);
-}
-
-// multicast 4-CTA clusters (pairs of vocab tiles sharing their token rows) with ECHO_LM_MC=1: measured 3-4 % slower
-// than plain pairs (profiles/r2h_ab_mc.jsonl), so off by default
-template <int kMode>
-static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams& p, cudaStream_t stream, int num_sms) {
-  bool mc = false;
-  if (const char* env = getenv("ECHO_LM_MC")) mc = kLmPair && atoi(env) != 0;
-  return mc ? launch_tile_mc<kMode, kLmPair>(hidden, weight, p, stream, num_sms)
-            : launch_tile_mc<kMode, false>(hidden, weight, p, stream, num_sms);
+  return cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kLmPair, kMode>, mh, mw, p);
 }
 
 cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,

@@ -26,6 +26,8 @@
 // which cluster a row is scheduled on.
 #include <cuda_bf16.h>
 
+#include <stdlib.h>
+
 #include <atomic>
 
 #include "echo_common.cuh"
@@ -511,10 +513,9 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
             float t0, t1;
             f2split(fma2(z2, l2e2, nlse2), t0, t1);
             if (kEnt) {  // d = p (e (z - lse + H) - c) = p (e z + k),  k = e (H - lse) - c
-              // this variant needs a second exponential per logit, which makes the MUFU pipe the limiter: the odd
-              // chunks take it on the FMA pipe instead (ex2_poly2), balancing the two
-              const uint64_t p2 = (c & 1) ? ex2_poly2(f2(t0, t1)) : f2(ex2(t0), ex2(t1));
-              f2split(mul2(p2, fma2(z2, ee2, ek2)), d0, d1);
+              // (the odd chunks' exponential on an FMA-pipe polynomial instead of MUFU was 17 % slower, interleaved
+              // A/B: profiles/r2j_ab_ent.jsonl)
+              f2split(mul2(f2(ex2(t0), ex2(t1)), fma2(z2, ee2, ek2)), d0, d1);
             }
             else
               f2split(mul2(f2(ex2(t0), ex2(t1)), k2), d0, d1);

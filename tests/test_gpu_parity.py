@@ -444,9 +444,11 @@ def test_token_logp_forward_only(name):
     assert np.max(np.abs(logp.cpu().numpy() - ref_logp)) <= 1e-5 + 1e-6 * np.abs(ref_logp).max()
     assert np.max(np.abs(lse.cpu().numpy() - ref_lse)) <= 1e-5 + 1e-6 * np.abs(ref_lse).max()
     np.testing.assert_array_equal(flags.cpu().numpy(), ref_flags)
-    # consistency with the fused kernel's logp on the same rows
+    # consistency with the fused kernel's logp on the same rows (a different reduction tree: one warp per row here,
+    # so the two agree within the sum of their oracle bounds)
     st.loss(logits, 0, kl_coef=0.0)
-    assert torch.equal(st.tok_logp[:n], logp) or name == "tiny"   # same reduction tree on the quad path
+    lf = st.tok_logp[:n].double()
+    assert torch.all((lf - logp.double()).abs() <= 2e-5 + 2e-6 * lf.abs())
 
 
 # ---------------------------------------------------------------------------------------------- f4: variants
@@ -621,11 +623,8 @@ def _lmhead_tol(hb, wb, rows):
 
 @pytest.mark.parametrize("n,d,V", [(128, 64, 256), (300, 512, 1000), (129, 72, 257), (1, 2560, 4096),
                                    (700, 256, 5000)])
-@pytest.mark.parametrize("mc", ["0", "1"])
-def test_lmhead_logp_small(n, d, V, mc, monkeypatch):
-    """f2: the fused LM-head log-prob against the fp64 oracle (every row), ragged token / vocab / K tiles; 2-CTA pairs
-    (mc 0) or 4-CTA clusters multicasting the token rows (mc 1; V = 257 / 5000 give an odd vocab-tile count)."""
-    monkeypatch.setenv("ECHO_LM_MC", mc)
+def test_lmhead_logp_small(n, d, V):
+    """f2: the fused LM-head log-prob against the fp64 oracle (every row), ragged token / vocab / K tiles."""
     h, w, act = _lmhead_case(n, d, V, seed=n + d + V)
     lp, lse = _lmhead_run(h, w, act)
     hb = h.cpu().view(torch.int16).numpy().view(np.uint16)
