@@ -50,7 +50,7 @@ def launch_summary(src_csv, dst_md):
         cnt[r["Kernel Name"]] += 1
     all_ns = sum(tot.values())
     echo_ns = sum(v for k, v in tot.items() if "echo::" in k)
-    out = ["# ncu launch list (bench.py --steps 1 --warmup 3, cold/serialised per-launch times, us)", "",
+    out = ["# ncu launch list (bench.py --steps 1 --warmup 1 --no-cpu-baseline, cold/serialised per-launch times, us)", "",
            "| kernel | launches | total us | share of all | share of libecho |", "|---|---|---|---|---|"]
     for k, v in tot.most_common():
         mine = f"{100 * v / echo_ns:.2f}%" if "echo::" in k else "—"
@@ -62,7 +62,8 @@ def launch_summary(src_csv, dst_md):
         if r["Metric Name"] == "gpu__time_duration.sum":
             ids.append((int(r["ID"]), r["Kernel Name"], r["Metric Value"], r["Metric Unit"]))
     ids.sort()
-    cut = next((i for i, (_, k, _, _) in enumerate(ids) if "policy_loss" in k and ", 2>" in k), len(ids))
+    cut = next((i for i, (_, k, _, _) in enumerate(ids)
+                if "token_logp_warp" in k or ("policy_loss" in k and ", 2>" in k)), len(ids))
     st, sc = collections.Counter(), collections.Counter()
     for _, k, v, u in ids[:cut]:
         ns = float(v.replace(",", "")) * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(u, 1)
@@ -100,7 +101,7 @@ def main():
     ap.add_argument("tag")
     ap.add_argument("--src", default="gpurun_out")
     ap.add_argument("--dst", default="profiles")
-    ap.add_argument("--workload", default="qwen3-4b")
+    ap.add_argument("--workload", default="qwen3-32b")
     ap.add_argument("--rows", type=int, default=32768)
     a = ap.parse_args()
     t = a.tag
@@ -121,7 +122,7 @@ def main():
     json.dump(tr, open(path, "w"), indent=1)
     print(json.dumps(m, indent=1))
     # the f2 captures (tensor-core kernels): the fused LM-head log-prob and the logits-store GEMM of the chunked step
-    for name in ("f2", "f2_logits"):
+    for name in ("f1", "f2", "f2_logits", "gemm_dh", "gemm_dw"):
         src = os.path.join(a.src, f"{t}_{name}.ncu-rep")
         if not os.path.exists(src):
             continue
