@@ -517,12 +517,16 @@ def main_echo(args):
                     else:
                         torch.addmm(dw, D.t(), hid[r0:r0 + rows], out_dtype=torch.float32, out=dw)
 
-            t2 = {"chunked": [], "recompute": [], "chunked_cublas_backward": [], "unfused_cublas": []}
+            t2 = {"chunked": [], "chunked_16384": [], "chunked_32768": [], "recompute": [],
+                  "chunked_cublas_backward": [], "unfused_cublas": []}
             for r in range(5):
                 for mode in t2:
                     flush.fill_(float(r))
                     a0 = ev()
-                    if mode in ("chunked", "recompute"):
+                    if mode.startswith("chunked_") and mode[8:].isdigit():   # larger chunks: bigger GEMMs, bigger buffer
+                        st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
+                                            chunk_rows=int(mode[8:]), scratch=scratch, mode="chunked")
+                    elif mode in ("chunked", "recompute"):
                         st.loss_from_hidden(hid, wgt, 0, dh, dw, accumulate=False, kl_coef=kl, grad_scale=1.0,
                                             chunk_rows=chunk, scratch=scratch, mode=mode)
                     elif mode == "chunked_cublas_backward":
@@ -548,6 +552,7 @@ def main_echo(args):
                              "frac_of_sustained": fl6 / (t2_ms * 1e-3) / 1e12 / measured_bf16_peak(sustained=True)[0],
                              "flops_per_token": 6.0 * hd * cfg.V},
                 "gemms": "logits GEMM, fused loss, dhidden and dweight all on libecho's kernels (tcgen05, no cuBLAS)",
+                "chunk_rows_sweep_ms": {"8192": t2_ms, "16384": ms["chunked_16384"], "32768": ms["chunked_32768"]},
                 "recompute_ms": ms["recompute"],
                 "recompute": "echo_lmhead_logp + echo_loss_from_logp + echo_lmhead_backward (D recomputed: 8 d V "
                              "flops per token)",
@@ -634,9 +639,11 @@ def main():
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         _reexec_under_torchrun(args)
-    # rank count visible in the NCCL init log (the driver counts ranks from it)
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    # rank count visible in the NCCL init log (the driver counts ranks from it), on stderr so stdout keeps the JSON
+    if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        os.environ["NCCL_DEBUG"] = "INFO"
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import __graft_entry__
     __graft_entry__.build()
     main_echo(args)
