@@ -1,15 +1,10 @@
 #!/bin/bash
-# Weak scaling of the default workload at 2..NGPU GPUs with the current build (bench.py under torchrun, NCCL).
-# Usage (under gpurun --gpus N): NGPU=4 bash tools/scale_check.sh <tag>
-tag=${1:-rX}
-out=gpurun_out
-mkdir -p $out
-python -c "import __graft_entry__ as g; g.build()" > $out/${tag}_scale_build.log 2>&1
-n=2
-while [ $n -le ${NGPU:-2} ]; do
-  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
-      --master-port $((29600 + n)) bench.py --gpus $n > $out/${tag}_scale${n}.json 2> $out/${tag}_scale${n}.err
-  echo "scale${n}=$?" >> $out/${tag}_scale_status.txt
-  n=$((n * 2))
-done
-cat $out/${tag}_scale_status.txt
+# Multi-GPU check of the bench contract (under gpurun --gpus N): the default command with --gpus N re-executes itself
+# under torchrun; the reference arm under torchrun prints from rank 0 only.  Usage: bash tools/scale_check.sh N TAG
+n=${1:-2}; tag=${2:-s$n}
+mkdir -p gpurun_out
+timeout 1200 python bench.py --gpus $n > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err; echo "bench=$?"
+grep -c "NCCL INFO" gpurun_out/${tag}_bench.err
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29533 \
+    bench.py --gpus $n --impl reference --steps 1 --warmup 0 > gpurun_out/${tag}_ref.json 2> gpurun_out/${tag}_ref.err
+echo "ref=$?"
