@@ -18,12 +18,11 @@
 // piece j - 1's stores after a per-tile counter says they are complete -- a fixed fold order, so results do not depend
 // on the schedule).
 //
-// kMc (multicast): a 4-CTA cluster of two pairs computes the two N-neighbouring tiles (m, 2j) and (m, 2j + 1) in
-// lockstep, and the A operand they share is loaded once: CTA (pair p, role r) loads half p of role r's 128 A rows and
-// multicasts it to role r of both pairs (cp.async.bulk.tensor .multicast::cluster, each destination signalling its own
-// pair leader's full barrier).  A's L2 reads halve (per CTA and k-block 24 KB instead of 32 KB), which is what the
-// power-capped tensor cores turn into clock.  A CTA's ring slot is then written by both pairs, so every MMA commit
-// of a stage arrives on the empty barrier of all four CTAs (count 2).
+// kWide: a unit is the 256 x 512 block of two N-neighbouring tiles, computed by one pair with its two TMEM
+// accumulators side by side (512 columns) instead of double-buffering: each k-block loads A once for both tiles (per CTA
+// and k-block 48 KB of L2 reads for 2 x 128 x 256 x 64 MACs instead of 2 x 32 KB), and the A operand's DRAM
+// re-reads across N halve.  The price is an epilogue that no longer overlaps the next unit's K loop, so it is chosen
+// for long K loops only.  (Round 2 also tried 4-CTA clusters multicasting A to two pairs: 7-13 % slower.)
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -43,23 +42,22 @@ constexpr int kBM = 128, kBN = 256, kBK = 64, kUmmaK = 16, kThreads = 192, kStag
 constexpr int kOpBytes = 128 * kBK * 2;  // one operand's stage per CTA: 128 rows (M or N) x 64 K bf16 = 16 KB
 constexpr uint32_t kTmemCols = 512;
 constexpr int kTidRing = 4;  // tile ids in flight between the scheduler (leader producer) and the other roles
-template <bool kMc>
-struct Geo {
-  static constexpr int kCl = kMc ? 4 : 2;  // CTAs per cluster
-  // consumers of a tile id: every producer except the scheduler's, each pair leader's MMA thread, 4 epilogue warps
-  // per CTA
-  static constexpr uint32_t kTidConsumers = (kCl - 1) + kCl / 2 + 4 * kCl;
-};
+template <bool kWide>
 struct Smem {
-  uint8_t a[kStages][kOpBytes];
-  uint8_t b[kStages][kOpBytes];
+  static constexpr int kSt = kWide ? 4 : kStages;    // ring depth (48 KB stages when wide)
+  static constexpr int kNB = kWide ? 2 : 1;          // B tiles per stage
+  uint8_t a[kSt][kOpBytes];
+  uint8_t b[kSt][kNB][kOpBytes];
   uint8_t ostage[4][32 * 128];  // epilogue staging per TMEM lane quadrant: 32 rows x 32 fp32, SWIZZLE_128B layout
-  uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  uint64_t full[kSt], empty[kSt], tfull[2], tempty[2];
   uint64_t tid_full[kTidRing], tid_empty[kTidRing];
   uint32_t tile_id[kTidRing];
   uint32_t tmem_base;
 };
-constexpr size_t smem_bytes() { return sizeof(Smem) + 1024; }
+// consumers of a tile id: the leader's MMA thread and 4 epilogue warps, the peer's producer thread and 4 epilogue warps
+constexpr uint32_t kTidConsumers = 10;
+template <bool kWide>
+constexpr size_t smem_bytes() { return sizeof(Smem<kWide>) + 1024; }
 
 // MN-major SWIZZLE_128B descriptor: start >> 4 | LBO 8192 B (>> 4) | SBO 1024 B (>> 4) | version 1 | layout 2
 ECHO_DEVINL uint64_t sw128_mn_desc(uint32_t smem_addr) {
@@ -75,13 +73,6 @@ template <bool kAMN, bool kBMN>
 constexpr uint32_t idesc() {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)kAMN << 15) | ((uint32_t)kBMN << 16) |
          ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-}
-// stage half `h` (64 rows) of one operand's 128 rows, multicast to the CTAs of `mask`
-template <bool kMN>
-ECHO_DEVINL void load_half_mc(uint32_t dst, const CUtensorMap* map, int32_t row0, int32_t k0, uint32_t bar, int h,
-                              uint16_t mask, uint64_t pol) {
-  if constexpr (kMN) lm::tma_load_2d_pair_mc(dst + h * 8192, map, row0 + 64 * h, k0, bar, mask, pol);
-  else lm::tma_load_2d_pair_mc(dst + h * 8192, map, k0, row0 + 64 * h, bar, mask, pol);  // box {64 K, 64 rows}
 }
 // stage one operand's 128 rows (M or N) x 64 K of this CTA
 template <bool kMN>
@@ -121,7 +112,7 @@ static std::atomic<uint32_t> g_gemm_next_slot{0}, g_gemm_next_slot_graph{0};
 struct GemmParams {
   int64_t M;
   int32_t N, K, n_mt, n_nt, n_kb, group_m;
-  int32_t n_nu;         // N units: N tiles (pair clusters) or N-tile pairs (kMc); scheduling unit = (M tile, N unit)
+  int32_t n_nu;         // N units: N tiles, or (kWide) pairs of N tiles; scheduling unit = (M tile, N unit)
   unsigned int* sched;  // this launch's {tile counter, finished CTAs} (reset by the last CTA)
   unsigned int* flags;  // split-K: this launch's per-output-tile counters
   int32_t split;        // 1..kMaxSplit: K pieces per output tile (id j n_out + t: piece j adds onto piece j - 1)
@@ -133,24 +124,22 @@ struct GemmParams {
   int32_t tma_out;  // output 16-B aligned with ldo % 4 == 0: the epilogue writes through map_c (TMA store / L2 add)
 };
 
-template <bool kAMN, bool kBMN, bool kMc>
+template <bool kAMN, bool kBMN, bool kWide>
 __global__ void __launch_bounds__(gm::kThreads, 1)
     gemm_tile_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ CUtensorMap map_c, const GemmParams p) {
   using namespace gm;
-  using G = Geo<kMc>;
+  using S = Smem<kWide>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
+  S& sm = *reinterpret_cast<S*>(smem_raw + (((raw + 1023u) & ~1023u) - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_units = (int64_t)p.n_mt * p.n_nu, n_tiles = n_units * p.split;
   // k-block range of piece j: [j n_kb / S, (j + 1) n_kb / S)
   auto kb_begin = [&](int32_t j) { return (int32_t)(((int64_t)j * p.n_kb) / p.split); };
   const uint32_t rank = cluster_ctarank();
-  const uint32_t role = rank & 1u, pair = rank >> 1;  // role in the pair (0 = pair leader), pair in the cluster
-  const uint32_t pl = rank & ~1u;                      // this CTA's pair leader
-  const bool sched = rank == 0, pleader = role == 0;
-  const uint16_t pair_mask = (uint16_t)(3u << (2 * pair));
+  const bool leader = rank == 0;
+  constexpr int kUnitN = kWide ? 2 * kBN : kBN;  // output columns of a unit
   // tile id of the `use`-th tile of this cluster (every role walks the same sequence); n_tiles marks the end
   auto next_tile = [&](uint32_t use) -> int64_t {
     const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
@@ -162,30 +151,27 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     mbar_wait_cluster_warp(smem_u32(&sm.tid_full[r]), ph, lane);
     return (int64_t)sm.tile_id[r];
   };
-  auto release_tile = [&](uint32_t use) {  // one arrival per consumer (thread or warp lane 0) on the scheduler CTA
+  auto release_tile = [&](uint32_t use) {  // one arrival per consumer (thread or warp lane 0) on the leader
     const uint32_t r = use % kTidRing;
-    if (sched) mbar_arrive(smem_u32(&sm.tid_empty[r]));
+    if (leader) mbar_arrive(smem_u32(&sm.tid_empty[r]));
     else lm::mbar_arrive_cluster(mapa(smem_u32(&sm.tid_empty[r]), 0));
   };
-  // unit -> this pair's output tile (kMc: the pairs take N tiles 2j and 2j + 1)
-  auto coords = [&](int64_t unit, int32_t& mt, int32_t& nt) {
-    int32_t nu;
-    tile_coords(unit, p.n_mt, p.n_nu, p.group_m, mt, nu);
-    nt = kMc ? 2 * nu + (int32_t)pair : nu;
-  };
+  // accumulator of the tc-th unit: double-buffered, or (kWide) both 256-column halves of TMEM, one unit at a time
+  auto acc_buf = [&](uint32_t tc) -> uint32_t { return kWide ? 0u : (tc & 1u); };
+  auto acc_phase = [&](uint32_t tc) -> uint32_t { return kWide ? (tc & 1u) : ((tc >> 1) & 1u); };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < S::kSt; ++s) {
       mbar_init(smem_u32(&sm.full[s]), 1);
-      mbar_init(smem_u32(&sm.empty[s]), kMc ? 2 : 1);  // kMc: both pairs' MMAs read data this slot receives
+      mbar_init(smem_u32(&sm.empty[s]), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&sm.tfull[b]), 1);
-      mbar_init(smem_u32(&sm.tempty[b]), 8);  // one arrival per epilogue warp of both CTAs of the pair
+      mbar_init(smem_u32(&sm.tempty[b]), 8);  // one arrival per epilogue warp of both CTAs
     }
     for (int r = 0; r < kTidRing; ++r) {
       mbar_init(smem_u32(&sm.tid_full[r]), 1);
-      mbar_init(smem_u32(&sm.tid_empty[r]), G::kTidConsumers);  // used on the scheduler CTA only
+      mbar_init(smem_u32(&sm.tid_empty[r]), kTidConsumers);  // used on the leader only
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -211,43 +197,37 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
                                                                                 : policy_evict_normal();
       const uint64_t pol_b = p.pol_b == 2 ? policy_evict_last() : p.pol_b == 1 ? policy_evict_first()
                                                                                 : policy_evict_normal();
-      const uint16_t role_mask = (uint16_t)((1u << role) | (1u << (role + 2)));  // kMc: role r of both pairs
       for (uint32_t use = 0;; ++use) {
         int64_t u;
-        if (sched) {  // the scheduler: grab the next unit, publish it to this CTA and the others
+        if (leader) {  // the scheduler: grab the next unit, publish it to this CTA and the peer
           const uint32_t r = use % kTidRing, ph = (use / kTidRing) & 1u;
           mbar_wait(smem_u32(&sm.tid_empty[r]), ph ^ 1u);
           u = (int64_t)atomicAdd(&p.sched[0], 1u);
           if (u > n_tiles) u = n_tiles;
           sm.tile_id[r] = (uint32_t)u;
           mbar_arrive(smem_u32(&sm.tid_full[r]));
-#pragma unroll
-          for (uint32_t q = 1; q < (uint32_t)G::kCl; ++q) {
-            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa(smem_u32(&sm.tile_id[r]), q)), "r"((uint32_t)u)
-                         : "memory");
-            lm::mbar_arrive_cluster(mapa(smem_u32(&sm.tid_full[r]), q));
-          }
+          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa(smem_u32(&sm.tile_id[r]), 1)), "r"((uint32_t)u)
+                       : "memory");
+          lm::mbar_arrive_cluster(mapa(smem_u32(&sm.tid_full[r]), 1));
         } else {
           u = next_tile(use);
           release_tile(use);
         }
         if (u >= n_tiles) break;
-        int32_t mt, nt;
+        int32_t mt, nu;
         const int32_t piece = (int32_t)(u / n_units);  // split-K piece
-        coords(u - (int64_t)piece * n_units, mt, nt);
-        const int32_t m_row = mt * 256 + (int32_t)role * kBM, n_row = nt * kBN + (int32_t)role * 128;
+        tile_coords(u - (int64_t)piece * n_units, p.n_mt, p.n_nu, p.group_m, mt, nu);
+        const int32_t m_row = mt * 256 + (int32_t)rank * kBM, n_row = nu * kUnitN + (int32_t)rank * 128;
         const int32_t kb0 = kb_begin(piece), kb1 = kb_begin(piece + 1);
-        const uint32_t bar0 = mapa(smem_u32(&sm.full[0]), pl);
         for (int32_t kb = kb0; kb < kb1; ++kb) {
           mbar_wait(smem_u32(&sm.empty[stage]), phase ^ 1u);
-          const uint32_t bar = bar0 + 8u * stage;
-          if (pleader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), 4 * kOpBytes);
-          if constexpr (kMc)
-            load_half_mc<kAMN>(smem_u32(sm.a[stage]), &map_a, m_row, kb * kBK, bar, (int)pair, role_mask, pol_a);
-          else
-            load_op<kAMN>(smem_u32(sm.a[stage]), &map_a, m_row, kb * kBK, bar, pol_a);
-          load_op<kBMN>(smem_u32(sm.b[stage]), &map_b, n_row, kb * kBK, bar, pol_b);
-          if (++stage == kStages) {
+          const uint32_t bar = mapa(smem_u32(&sm.full[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), 2 * (1 + S::kNB) * kOpBytes);
+          load_op<kAMN>(smem_u32(sm.a[stage]), &map_a, m_row, kb * kBK, bar, pol_a);
+#pragma unroll
+          for (int j = 0; j < S::kNB; ++j)  // kWide: the second N tile's half, 256 columns further
+            load_op<kBMN>(smem_u32(sm.b[stage][j]), &map_b, n_row + j * kBN, kb * kBK, bar, pol_b);
+          if (++stage == S::kSt) {
             stage = 0;
             phase ^= 1u;
           }
@@ -255,14 +235,14 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer (each pair leader's lane 0)
-    if (lane == 0 && pleader) {
+    // ---------------------------------------------------------------- MMA issuer (the leader's lane 0)
+    if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, tc = 0;
       for (;; ++tc) {
         const int64_t u = next_tile(tc);
         release_tile(tc);
         if (u >= n_tiles) break;
-        const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
+        const uint32_t buf = acc_buf(tc), aph = acc_phase(tc);
         mbar_wait_cluster(smem_u32(&sm.tempty[buf]), aph ^ 1u);
         lm::tc_fence_after();
         const uint32_t d_tmem = tmem + buf * kBN;
@@ -271,20 +251,21 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         for (int32_t kb = kb0; kb < kb1; ++kb) {
           mbar_wait_cluster(smem_u32(&sm.full[stage]), phase);
           lm::tc_fence_after();
-          const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b[stage]);
+          const uint32_t a0 = smem_u32(sm.a[stage]);
 #pragma unroll
-          for (int k = 0; k < kBK / kUmmaK; ++k)
-            lm::umma_f16<true>(d_tmem, op_desc<kAMN>(a0, k), op_desc<kBMN>(b0, k), idesc<kAMN, kBMN>(),
-                               (kb > kb0 || k > 0) ? 1u : 0u);
-          // the slot is free once this pair (and, kMc, the other pair) have read it: arrive on every CTA that
-          // receives data into it
-          lm::umma_commit_mask(smem_u32(&sm.empty[stage]), kMc ? (uint16_t)0xF : pair_mask);
-          if (++stage == kStages) {
+          for (int k = 0; k < kBK / kUmmaK; ++k) {
+#pragma unroll
+            for (int j = 0; j < S::kNB; ++j)
+              lm::umma_f16<true>(d_tmem + j * kBN, op_desc<kAMN>(a0, k), op_desc<kBMN>(smem_u32(sm.b[stage][j]), k),
+                                 idesc<kAMN, kBMN>(), (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          lm::umma_commit<true>(smem_u32(&sm.empty[stage]));  // the stage is free once these MMAs have read it
+          if (++stage == S::kSt) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        lm::umma_commit_mask(smem_u32(&sm.tfull[buf]), pair_mask);
+        lm::umma_commit<true>(smem_u32(&sm.tfull[buf]));
       }
     }
   } else {
@@ -295,7 +276,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     // accumulating -- no global loads, full-line writes, a few instructions per 1024 outputs.
     const int quad = warp & 3;
     uint32_t tc = 0;
-    const uint32_t tempty_leader = mapa(smem_u32(&sm.tempty[0]), pl);
+    const uint32_t tempty_leader = mapa(smem_u32(&sm.tempty[0]), 0);
     const bool vec_ok = (p.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
     const uint32_t ostage = smem_u32(sm.ostage[quad]);
     for (;; ++tc) {
@@ -303,13 +284,12 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       __syncwarp();
       if (lane == 0) release_tile(tc);
       if (u >= n_tiles) break;
-      int32_t mt, nt;
+      int32_t mt, nu;
       const int32_t piece = (int32_t)(u / n_units);
-      const int64_t unit = u - (int64_t)piece * n_units;
-      coords(unit, mt, nt);
-      const int64_t ot = unit * (G::kCl / 2) + pair;  // this pair's output tile (split-K counter index)
-      const uint32_t buf = tc & 1u, aph = (tc >> 1) & 1u;
-      const int64_t row0 = (int64_t)mt * 256 + (int64_t)role * kBM + quad * 32;  // this warp's 32 output rows
+      const int64_t ot = u - (int64_t)piece * n_units;  // output unit (split-K counter index)
+      tile_coords(ot, p.n_mt, p.n_nu, p.group_m, mt, nu);
+      const uint32_t buf = acc_buf(tc), aph = acc_phase(tc);
+      const int64_t row0 = (int64_t)mt * 256 + (int64_t)rank * kBM + quad * 32;  // this warp's 32 output rows
       const int64_t row = row0 + lane;
       const bool row_ok = row < p.M;
       float* orow = p.out + (row_ok ? row : 0) * p.ldo;
@@ -332,8 +312,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         __threadfence();
       }
 #pragma unroll 1
-      for (int ch = 0; ch < kBN / 32; ++ch) {
-        const int32_t cb = nt * kBN + ch * 32;
+      for (int ch = 0; ch < kUnitN / 32; ++ch) {
+        const int32_t cb = nu * kUnitN + ch * 32;
         if (cb >= p.N) break;  // warp-uniform
         uint32_t r[32];
         lm::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + ch * 32, r);
@@ -406,18 +386,17 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       p.sched[0] = 0u;
       p.sched[1] = 0u;
       if (p.split > 1)
-        for (int64_t t = 0; t < n_units * (G::kCl / 2); ++t) p.flags[t] = 0u;
+        for (int64_t t = 0; t < n_units; ++t) p.flags[t] = 0u;
       __threadfence();
     }
   }
 }
 
-template <bool kAMN, bool kBMN, bool kMc>
+template <bool kAMN, bool kBMN, bool kWide>
 static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, GemmParams& p,
                                cudaStream_t stream, int num_sms) {
-  constexpr int kCl = gm::Geo<kMc>::kCl;
-  const void* fn = (const void*)gemm_tile_kernel<kAMN, kBMN, kMc>;
-  const size_t smem = gm::smem_bytes();
+  const void* fn = (const void*)gemm_tile_kernel<kAMN, kBMN, kWide>;
+  const size_t smem = gm::smem_bytes<kWide>();
   static std::atomic<int> cached[64];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -426,16 +405,16 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, con
   if (units < 0) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    units = max_active_clusters(fn, gm::kThreads, smem, kCl, num_sms / kCl);
+    units = max_active_clusters(fn, gm::kThreads, smem, 2, num_sms / 2);
     if (dev < 64) cached[dev].store((int)units + 1, std::memory_order_relaxed);
   }
-  p.n_nu = kMc ? (p.n_nt + 1) / 2 : p.n_nt;
+  p.n_nu = kWide ? (p.n_nt + 1) / 2 : p.n_nt;
   const int64_t n_work = (int64_t)p.n_mt * p.n_nu;
   // split the K loop into S pieces when that fills the last wave better (dhidden at 8192 rows: 320 tiles on 74
   // clusters fill 86 % of 5 waves; S = 3 fills 99.8 % of 13) and every piece stays long (>= 64 k-blocks).  Each extra
   // piece costs one add-onto-the-output epilogue pass, hence the small per-piece penalty.
   p.split = 1;
-  if (n_work * (kCl / 2) <= kMaxSplitTiles) {
+  if (n_work <= kMaxSplitTiles) {
     const int64_t U = units;
     auto eff = [U](int64_t t) { const int64_t w = (t + U - 1) / U; return (double)t / (double)(w * U); };
     double best = eff(n_work);
@@ -465,27 +444,27 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, con
   p.sched = slots + 2 * slot;
   p.flags = flags + (size_t)slot * kMaxSplitTiles;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(units * kCl));
+  cfg.gridDim = dim3((unsigned)(units * 2));
   cfg.blockDim = dim3(gm::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = kCl;
+  attr.val.clusterDim.x = 2;
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_tile_kernel<kAMN, kBMN, kMc>, ma, mb, mc, p);
+  return cudaLaunchKernelEx(&cfg, gemm_tile_kernel<kAMN, kBMN, kWide>, ma, mb, mc, p);
 }
 
-template <bool kMc>
+template <bool kWide>
 static cudaError_t launch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
                                  const CUtensorMap& mc, GemmParams& p, cudaStream_t stream, int num_sms) {
-  if (a_mn && b_mn) return launch_gemm<true, true, kMc>(ma, mb, mc, p, stream, num_sms);
-  if (!a_mn && b_mn) return launch_gemm<false, true, kMc>(ma, mb, mc, p, stream, num_sms);
-  if (!a_mn && !b_mn) return launch_gemm<false, false, kMc>(ma, mb, mc, p, stream, num_sms);
-  return launch_gemm<true, false, kMc>(ma, mb, mc, p, stream, num_sms);
+  if (a_mn && b_mn) return launch_gemm<true, true, kWide>(ma, mb, mc, p, stream, num_sms);
+  if (!a_mn && b_mn) return launch_gemm<false, true, kWide>(ma, mb, mc, p, stream, num_sms);
+  if (!a_mn && !b_mn) return launch_gemm<false, false, kWide>(ma, mb, mc, p, stream, num_sms);
+  return launch_gemm<true, false, kWide>(ma, mb, mc, p, stream, num_sms);
 }
 
 // C[M x N] (+)= A B with A(m, k), B(n, k) read from bf16 global memory as described above; row strides in bytes.
@@ -493,16 +472,18 @@ cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void*
                              int64_t b_row_bytes, int64_t M, int32_t N, int32_t K, float* out, int64_t ldo,
                              bool accumulate, cudaStream_t stream, int num_sms) {
   if (M == 0 || N == 0) return cudaSuccess;
-  // multicast clusters: off by default -- interleaved A/B on one box measured them 7-13 % slower than plain pairs at
-  // the f2 shapes (profiles/r2h_ab_mc.jsonl; L2 already merges the pairs' concurrent reads of the shared operand);
-  // ECHO_GEMM_MC=1 selects them (N tiles must pair up: >= 2)
-  bool mc = false;
-  if (const char* env = getenv("ECHO_GEMM_MC")) mc = atoi(env) != 0 && (N + gm::kBN - 1) / gm::kBN >= 2;
+  // 256 x 512 units (two accumulators sharing A) for big products with long K loops, where the unoverlapped
+  // epilogue is cheap and A's DRAM re-reads dominate.  Interleaved A/B against cuBLAS (profiles/r2p_ab_wide.jsonl,
+  // ms): 32768 x 5120 x 151936 dhidden 40.7 wide / 49.4 not / 39.0 cuBLAS, dweight 40.7 / 50.3 / 38.4; at 8192-row
+  // chunks (<= 640 tiles, or 128-k-block K loops) the 256 x 256 tiles win: dhidden d = 5120 8.77 / 10.36 wide / 9.53
+  // cuBLAS, dweight 9.46 / 10.01 / 10.06.  ECHO_GEMM_WIDE=0/1 overrides, for A/B.
+  const int32_t n_kb = (K + gm::kBK - 1) / gm::kBK, n_nt = (N + gm::kBN - 1) / gm::kBN;
+  const int64_t n_tiles = (int64_t)((M + 255) / 256) * n_nt;
+  bool wide = n_nt >= 2 && n_kb >= 512 && n_tiles >= 1000;
+  if (const char* env = getenv("ECHO_GEMM_WIDE")) wide = atoi(env) != 0 && n_nt >= 2;
   CUtensorMap ma, mb;
-  // a K-major A is loaded in 64-row halves when multicast (one half per pair)
-  const uint32_t a_box_rows = mc ? 64 : 128;
   const bool ok_a = a_mn ? make_tensor_map_bf16(&ma, A, (uint64_t)M, (uint64_t)K, (uint64_t)a_row_bytes, 64, 64)
-                         : make_tensor_map_bf16(&ma, A, (uint64_t)K, (uint64_t)M, (uint64_t)a_row_bytes, 64, a_box_rows);
+                         : make_tensor_map_bf16(&ma, A, (uint64_t)K, (uint64_t)M, (uint64_t)a_row_bytes, 64, 128);
   const bool ok_b = b_mn ? make_tensor_map_bf16(&mb, B, (uint64_t)N, (uint64_t)K, (uint64_t)b_row_bytes, 64, 64)
                          : make_tensor_map_bf16(&mb, B, (uint64_t)K, (uint64_t)N, (uint64_t)b_row_bytes, 64, 128);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
@@ -534,8 +515,8 @@ cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void*
   const bool keep_b = !keep_a && b_bytes <= keep_max && b_bytes <= a_bytes;
   p.pol_a = keep_a ? 2 : keep_b ? 1 : 0;
   p.pol_b = keep_b ? 2 : keep_a ? 1 : 0;
-  return mc ? launch_majors<true>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms)
-            : launch_majors<false>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms);
+  return wide ? launch_majors<true>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms)
+              : launch_majors<false>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms);
 }
 
 cudaError_t tc_lmhead_grads(cudaStream_t stream, int num_sms, const void* weight, const void* hidden_chunk,

@@ -11,6 +11,8 @@
 // counter, so the warps of the whole GPU stream one compact window of rows.
 #include <cuda_bf16.h>
 
+#include <stdlib.h>
+
 #include <atomic>
 
 #include "echo_common.cuh"
@@ -20,15 +22,17 @@
 namespace echo {
 
 namespace tl {
-constexpr int kWarps = 16, kThreads = kWarps * 32, kStages = 3, kChunk = 4096;  // 4 KB = 2048 bf16 logits
+constexpr int kWarps = 16, kThreads = kWarps * 32;
+template <int kStages, int kChunk>  // default 3 x 4 KB (2048 bf16 logits) per warp: 192 KB per SM
 struct alignas(128) WarpRing {
   uint8_t buf[kStages][kChunk];
   uint64_t full[kStages];
   int64_t row[kStages];    // the (row, chunk) each slot holds (row < 0: no more work)
   int32_t chunk[kStages];
 };
+template <int kStages, int kChunk>
 struct Smem {
-  WarpRing ring[kWarps];
+  WarpRing<kStages, kChunk> ring[kWarps];
 };
 constexpr int kSlots = 256;
 }  // namespace tl
@@ -36,12 +40,13 @@ constexpr int kSlots = 256;
 __device__ unsigned long long g_logp_sched[tl::kSlots][2];  // {next row, warps done} per launch slot
 static std::atomic<uint32_t> g_logp_slot{0}, g_logp_slot_graph{0};
 
+template <int kStages, int kChunk>
 __global__ void __launch_bounds__(tl::kThreads, 1) token_logp_warp_kernel(const LossParams p) {
   using namespace tl;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  Smem<kStages, kChunk>& sm = *reinterpret_cast<Smem<kStages, kChunk>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpRing& rg = sm.ring[warp];
+  WarpRing<kStages, kChunk>& rg = sm.ring[warp];
   unsigned long long* const sched = g_logp_sched[p.sched_slot];
   const int32_t V = p.V;
   const uint32_t row_bytes = (uint32_t)V * 2u;
@@ -167,12 +172,13 @@ __global__ void __launch_bounds__(tl::kThreads, 1) token_logp_warp_kernel(const 
 
 bool token_logp_warp_supports(int32_t dtype, int32_t V) { return dtype == ECHO_BF16 && V >= 8192; }
 
-cudaError_t launch_token_logp_warp(const LossParams& p, cudaStream_t stream, int num_sms) {
-  const size_t smem = sizeof(tl::Smem);
+template <int kStages, int kChunk>
+static cudaError_t launch_ring(const LossParams& p, cudaStream_t stream, int num_sms) {
+  const size_t smem = sizeof(tl::Smem<kStages, kChunk>);
   static std::atomic<int> attr_set{0};
   if (!attr_set.load(std::memory_order_relaxed)) {
-    const cudaError_t e = cudaFuncSetAttribute(token_logp_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem);
+    const cudaError_t e = cudaFuncSetAttribute(token_logp_warp_kernel<kStages, kChunk>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set.store(1, std::memory_order_relaxed);
   }
@@ -181,8 +187,19 @@ cudaError_t launch_token_logp_warp(const LossParams& p, cudaStream_t stream, int
   int64_t grid = num_sms;
   const int64_t need = (p.n_rows + tl::kWarps - 1) / tl::kWarps;
   if (grid > need) grid = need;
-  token_logp_warp_kernel<<<(unsigned)grid, tl::kThreads, smem, stream>>>(q);
+  token_logp_warp_kernel<kStages, kChunk><<<(unsigned)grid, tl::kThreads, smem, stream>>>(q);
   return cudaGetLastError();
+}
+
+cudaError_t launch_token_logp_warp(const LossParams& p, cudaStream_t stream, int num_sms) {
+  // per-warp ring: 3 x 4 KB by default; ECHO_LOGP_RING=2 (2 x 6 KB), 4 (4 x 3 KB) or 6 (6 x 2 KB) for A/B (each
+  // 12 KB per warp, 192 KB per SM)
+  const char* env = getenv("ECHO_LOGP_RING");
+  const int ring = env ? atoi(env) : 3;
+  if (ring == 2) return launch_ring<2, 6144>(p, stream, num_sms);
+  if (ring == 4) return launch_ring<4, 3072>(p, stream, num_sms);
+  if (ring == 6) return launch_ring<6, 2048>(p, stream, num_sms);
+  return launch_ring<3, 4096>(p, stream, num_sms);
 }
 
 }  // namespace echo
