@@ -4,7 +4,7 @@
 // One WARP per row, no CTA or cluster barrier.  Read-only, the row never has to be held for a second pass, so there
 // is nothing to gain from splitting it over a cluster (the fused (3)-(5) kernel does that to keep the row in
 // registers between its read and its write): each of the 16 warps of a CTA streams its own row through a private
-// 3 x 4 KB shared-memory ring filled by 1-D TMA bulk copies (lane 0 issues them kStages chunks ahead, across row
+// 2 x 6 KB shared-memory ring filled by 1-D TMA bulk copies (lane 0 issues them kStages chunks ahead, across row
 // boundaries), and keeps an online max / sum of 2^((z - m) log2e) per lane -- one MUFU per logit, a rescale only when
 // a lane's running max grows.  At the row's end a fixed shuffle tree merges the 32 lanes (deterministic: the order
 // depends only on V), and lane 0 writes logp, lse and the non-finite flag.  Rows are taken in order from a global
@@ -23,7 +23,7 @@ namespace echo {
 
 namespace tl {
 constexpr int kWarps = 16, kThreads = kWarps * 32;
-template <int kStages, int kChunk>  // default 3 x 4 KB (2048 bf16 logits) per warp: 192 KB per SM
+template <int kStages, int kChunk>  // 2 x 6 KB (3072 bf16 logits) per warp by default: 192 KB per SM
 struct alignas(128) WarpRing {
   uint8_t buf[kStages][kChunk];
   uint64_t full[kStages];
@@ -192,14 +192,15 @@ static cudaError_t launch_ring(const LossParams& p, cudaStream_t stream, int num
 }
 
 cudaError_t launch_token_logp_warp(const LossParams& p, cudaStream_t stream, int num_sms) {
-  // per-warp ring: 3 x 4 KB by default; ECHO_LOGP_RING=2 (2 x 6 KB), 4 (4 x 3 KB) or 6 (6 x 2 KB) for A/B (each
-  // 12 KB per warp, 192 KB per SM)
+  // per-warp ring of 12 KB (192 KB per SM): 2 x 6 KB by default.  Interleaved A/B on one 32768 x 151936 micro-batch
+  // (profiles/r2q_ab_logp.jsonl): 2 x 6 KB 1.544 ms, 3 x 4 KB 1.633, 4 x 3 KB 1.711, 6 x 2 KB 1.897 -- fewer, longer
+  // bulk copies per byte; ECHO_LOGP_RING=3 / 4 / 6 selects the others
   const char* env = getenv("ECHO_LOGP_RING");
-  const int ring = env ? atoi(env) : 3;
-  if (ring == 2) return launch_ring<2, 6144>(p, stream, num_sms);
+  const int ring = env ? atoi(env) : 2;
+  if (ring == 3) return launch_ring<3, 4096>(p, stream, num_sms);
   if (ring == 4) return launch_ring<4, 3072>(p, stream, num_sms);
   if (ring == 6) return launch_ring<6, 2048>(p, stream, num_sms);
-  return launch_ring<3, 4096>(p, stream, num_sms);
+  return launch_ring<2, 6144>(p, stream, num_sms);
 }
 
 }  // namespace echo
