@@ -126,8 +126,10 @@ def main():
         src = os.path.join(a.src, f"{t}_{name}.ncu-rep")
         if not os.path.exists(src):
             continue
-        rep = os.path.join(a.dst, f"{t}_{name}.ncu-rep")
-        shutil.copy(src, rep)
+        rep = src
+        if not name.startswith("gemm"):   # the GEMM reports stay in the scratch dir (size); their metrics are kept
+            rep = os.path.join(a.dst, f"{t}_{name}.ncu-rep")
+            shutil.copy(src, rep)
         raw = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
         hdr, units, vals = raw[0], raw[1], raw[2]
         keys = METRICS + ["sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
@@ -135,6 +137,15 @@ def main():
                           "lts__t_bytes.sum", "sm__pipe_tma_cycles_active.avg.pct_of_peak_sustained_active"]
         mm = {w: [vals[hdr.index(w)], units[hdr.index(w)]] for w in keys if w in hdr}
         mm.update({h: [vals[i], units[i]] for i, h in enumerate(hdr) if "tensor" in h and "pct" in h})
+        st = {}
+        for stall in STALLS:
+            key = f"smsp__average_warps_issue_stalled_{stall}_per_issue_active.ratio"
+            if key in hdr:
+                st[stall] = float(vals[hdr.index(key)].replace(",", "") or 0)
+        if st and sum(st.values()) > 0:
+            tot = sum(st.values())
+            mm["stall_share_pct"] = {k: round(100 * v / tot, 1) for k, v in sorted(st.items(), key=lambda x: -x[1])
+                                     if 100 * v / tot >= 1.0}
         json.dump(mm, open(os.path.join(a.dst, f"{t}_ncu_{name}_metrics.json"), "w"), indent=1)
         print(name, json.dumps(mm, indent=1))
 
