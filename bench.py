@@ -500,11 +500,11 @@ def main_echo(args):
             dw = torch.empty(cfg.V, hd, dtype=torch.float32, device=dev)
             dh_u = torch.empty(M, hd, dtype=torch.bfloat16, device=dev)
             dw_u = torch.empty(cfg.V, hd, dtype=torch.bfloat16, device=dev)
-            zc = torch.empty(chunk, ldz, dtype=torch.bfloat16, device=dev)
+            zc = torch.empty(M, ldz, dtype=torch.bfloat16, device=dev)
             scratch = {}
             kl = cfg.kl_coef
 
-            def chunked_cublas_backward():
+            def chunked_cublas_backward(chunk=chunk):
                 for r0 in range(0, M, chunk):
                     rows = min(chunk, M - r0)
                     z = zc[:rows]
@@ -518,7 +518,7 @@ def main_echo(args):
                         torch.addmm(dw, D.t(), hid[r0:r0 + rows], out_dtype=torch.float32, out=dw)
 
             t2 = {"chunked": [], "chunked_16384": [], "chunked_32768": [], "recompute": [],
-                  "chunked_cublas_backward": [], "unfused_cublas": []}
+                  "chunked_cublas_backward": [], "chunked_cublas_backward_32768": [], "unfused_cublas": []}
             for r in range(5):
                 for mode in t2:
                     flush.fill_(float(r))
@@ -531,6 +531,8 @@ def main_echo(args):
                                             chunk_rows=chunk, scratch=scratch, mode=mode)
                     elif mode == "chunked_cublas_backward":
                         chunked_cublas_backward()
+                    elif mode == "chunked_cublas_backward_32768":
+                        chunked_cublas_backward(M)
                     else:
                         torch.matmul(hid, wgt.t(), out=logits[:, :cfg.V])
                         st.loss(logits, 0, kl_coef=kl, grad_scale=1.0)
@@ -560,6 +562,8 @@ def main_echo(args):
                 "chunked_cublas_backward": "comparison: the same chunked step with dhidden / dweight in cuBLAS "
                                            "(torch.mm / addmm, fp32 out, dweight accumulated)",
                 "vs_chunked_cublas_backward": ms["chunked_cublas_backward"] / t2_ms,
+                "chunked_cublas_backward_32768_ms": ms["chunked_cublas_backward_32768"],
+                "chunked_32768_vs_cublas_backward_32768": ms["chunked_cublas_backward_32768"] / ms["chunked_32768"],
                 "unfused_ms": ms["unfused_cublas"],
                 "unfused": f"comparison: cuBLAS logits ({M * cfg.V * 2 / 1e9:.1f} GB buffer) + echo_policy_loss_fwd_bwd "
                            "in place + cuBLAS dh, dW (bf16 out)",

@@ -426,6 +426,10 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, con
       }
     }
   }
+  if (const char* env = getenv("ECHO_GEMM_SPLIT")) {  // A/B knob: force S (K pieces of >= 64 k-blocks)
+    const int32_t sp = atoi(env);
+    if (sp >= 1 && sp <= kMaxSplit && p.n_kb / sp >= 64 && n_work <= kMaxSplitTiles) p.split = sp;
+  }
   if (units > n_work * p.split) units = n_work * p.split;
   // raster group: half a wave of clusters (measured better than a full wave at d = 2560: dweight at 8192 rows 5.99 ->
   // 5.24 ms), but 16 M tiles once there are >= 16 N units -- the tiles in flight then span ~16 M x 4.6 N tiles instead
