@@ -513,9 +513,9 @@ __global__ void __cluster_dims__(C::kCtas, 1, 1) __launch_bounds__(C::kThreads, 
             float t0, t1;
             f2split(fma2(z2, l2e2, nlse2), t0, t1);
             if (kEnt) {  // d = p (e (z - lse + H) - c) = p (e z + k),  k = e (H - lse) - c
-              // (the odd chunks' exponential on an FMA-pipe polynomial instead of MUFU was 17 % slower, and a tile
-              // with twice the threads per row caching both z and e (no pass-2 exponential) 21 % slower: interleaved
-              // A/B, profiles/r2j_ab_ent.jsonl, r2p_ab_ent.jsonl)
+              // (interleaved A/B, profiles/r2{j,p,t}_ab_ent.jsonl: the odd chunks' exponential on an FMA-pipe
+              // polynomial was 17 % slower; a tile with twice the threads per row caching both z and e, 21 % slower;
+              // the exps written back over the logits in the ring slots and read in pass 2, 19 % slower)
               f2split(mul2(f2(ex2(t0), ex2(t1)), fma2(z2, ee2, ek2)), d0, d1);
             }
             else
