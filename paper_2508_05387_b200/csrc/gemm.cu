@@ -519,6 +519,8 @@ cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void*
   const bool keep_b = !keep_a && b_bytes <= keep_max && b_bytes <= a_bytes;
   p.pol_a = keep_a ? 2 : keep_b ? 1 : 0;
   p.pol_b = keep_b ? 2 : keep_a ? 1 : 0;
+  if (const char* env = getenv("ECHO_GEMM_POL_A")) p.pol_a = atoi(env);  // A/B knobs: 0 normal, 1 first, 2 last
+  if (const char* env = getenv("ECHO_GEMM_POL_B")) p.pol_b = atoi(env);
   return wide ? launch_majors<true>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms)
               : launch_majors<false>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms);
 }

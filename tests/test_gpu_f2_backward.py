@@ -548,3 +548,45 @@ def test_chunked_step_deterministic_and_graph_capturable():
     for x, y, z in zip(b1, b2, b3):
         assert torch.equal(x.view(torch.uint8), y.view(torch.uint8))
         assert torch.equal(x.view(torch.uint8), z.view(torch.uint8))
+
+
+def test_dynamic_schedulers_replay_in_cuda_graphs():
+    """f1's one-warp-per-row kernel, the LM head and the backward GEMM take their row / tile counters from per-launch
+    slots; launches captured into a CUDA graph draw from a slot range of their own.  One graph holding all
+    three, replayed twice with eager launches of the same kernels in between, gives the eager results bit for bit."""
+    from paper_2508_05387_b200 import abi
+    g = torch.Generator(device="cuda").manual_seed(21)
+    n, d, V = 1024, 256, 8200
+    ld = (V + 7) // 8 * 8
+    z = (torch.randn(n, ld, generator=g, device="cuda") * 2).to(torch.bfloat16)
+    act = torch.randint(0, V, (n,), generator=g, device="cuda", dtype=torch.int32)
+    h = torch.randn(n, d, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(V, d, generator=g, device="cuda") * (2.0 / math.sqrt(d))).to(torch.bfloat16)
+    ws = torch.empty(abi.echo_lmhead_workspace_bytes(n, V) // 4 + 1, dtype=torch.float32, device="cuda")
+    outs = lambda: (torch.empty(n, device="cuda"), torch.empty(n, device="cuda"), torch.zeros(n, d, device="cuda"))
+
+    def run(o):
+        lp, lm, dh = o
+        abi.echo_token_logp(z, abi.ECHO_BF16, n, V, ld, act, lp)
+        abi.echo_lmhead_logp(h, w, n, d, V, act, lm, None, ws)
+        abi.echo_gemm_bf16(z, 0, ld, w, 1, d, n, d, V, dh, d)   # dhidden-shaped product (K = V)
+    eager = outs()
+    run(eager)
+    torch.cuda.synchronize()
+    got = outs()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run(got)                                                # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        run(got)
+    for _ in range(2):
+        for t in got:
+            t.zero_()
+        graph.replay()
+        run(outs())                                             # eager launches between replays
+        torch.cuda.synchronize()
+        for a, b in zip(got, eager):
+            assert torch.equal(a, b)

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--variants", required=True, help="';'-separated list of space-separated K=V settings")
+    ap.add_argument("--no-flush", action="store_true", help="back-to-back launches (sustained, power-capped clocks)")
     a = ap.parse_args()
     import __graft_entry__
     __graft_entry__.build()
@@ -112,7 +113,8 @@ def main():
             for r in range(a.reps + 2):
                 if regen is not None:
                     regen()
-                flush.fill_(float(r))
+                if not a.no_flush:
+                    flush.fill_(float(r))
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 run()

@@ -46,12 +46,12 @@ def cublas_grads(lib, D, W, h, dh, dw, ld, rows, d, V, beta_one):
         assert st == 0, st
 
 
-def cublas_dw(lib, D, h, dw, ld, rows, d, V):
+def cublas_dw(lib, D, h, dw, ld, rows, d, V, beta_one=True):
     handle = ctypes.c_void_p(torch.cuda.current_blas_handle())
     lib.cublasSetStream_v2(handle, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
-    one = ctypes.c_float(1.0)
+    one, zero = ctypes.c_float(1.0), ctypes.c_float(0.0)
     st = lib.cublasGemmEx(handle, 0, 1, d, V, rows, ctypes.byref(one), h.data_ptr(), 14, d, D.data_ptr(), 14, ld,
-                          ctypes.byref(one), dw.data_ptr(), 0, d, 68, -1)
+                          ctypes.byref(one if beta_one else zero), dw.data_ptr(), 0, d, 68, -1)
     assert st == 0, st
 
 
