@@ -977,3 +977,41 @@ def test_lmhead_entropy(n, d, V):
     tol = _lmhead_tol(hb, wb, np.arange(len(rows))) + 3e-5 * (1 + np.abs(lse_ref) + np.abs(ent_ref))
     assert np.all(np.abs(H - ent_ref) <= tol), np.max(np.abs(H - ent_ref) / tol)
     assert np.max(np.abs(H - ent_ref)) <= 2e-4
+
+
+def test_token_logp_fuzz_shapes():
+    """f1 (echo_token_logp) over random shapes: bf16 vocabularies from 16 to 311296 (the one-warp-per-row kernel from
+    8192 up, ragged V, rows fewer and more than the resident warps, padded ld) and fp32 ones; logp, lse and flags
+    against the oracle, the logits untouched."""
+    import dataclasses
+    from paper_2508_05387_b200 import abi
+    rng = np.random.default_rng(4242)
+    base = synth.CONFIGS["qwen3-4b"]
+    for i in range(24):
+        dtype = "f32" if i % 6 == 5 else "bf16"
+        V = int(np.exp(rng.uniform(np.log(16), np.log(311296 if dtype == "bf16" else 155648))))
+        if i % 3 == 0 and dtype == "bf16":
+            V = int(rng.integers(8192, 311297))
+        cfg = dataclasses.replace(base, V=V, dtype=dtype)
+        b = synth.make_batch(cfg, 0, cfg.G)
+        st, info = device_step(cfg, b)
+        o = oracle_step(cfg, b)
+        n = min(int(rng.integers(1, 3000)), info.n_tokens)
+        ld = (V + 7) // 8 * 8 + (8 if i % 2 else 0)
+        logits = fill(st, cfg, 0, n, ld=ld)
+        before = logits.clone()
+        lp = torch.full((n,), float("nan"), device="cuda")
+        lse = torch.full((n,), float("nan"), device="cuda")
+        flags = torch.full((n,), 7, dtype=torch.uint8, device="cuda")
+        abi.echo_token_logp(logits, abi.ECHO_BF16 if dtype == "bf16" else abi.ECHO_F32, n, V, ld, st.tok_action, lp,
+                            lse, flags)
+        torch.cuda.synchronize()
+        assert torch.equal(logits, before)
+        rows = np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, 16)]))
+        z = as_oracle_rows(logits[torch.from_numpy(rows).cuda()])[:, :V]
+        ref_lp, ref_lse, ref_flags = oracle.token_logp(z, o.pk.tok_action[rows], vocab=V)
+        g_lp = lp.cpu().numpy()[rows].astype(np.float64)
+        g_lse = lse.cpu().numpy()[rows].astype(np.float64)
+        assert np.all(np.abs(g_lp - ref_lp) <= 1e-5 + 1e-6 * np.abs(ref_lp)), (dtype, V, n, np.max(np.abs(g_lp - ref_lp)))
+        assert np.all(np.abs(g_lse - ref_lse) <= 1e-5 + 1e-6 * np.abs(ref_lse)), (dtype, V, n)
+        np.testing.assert_array_equal(flags.cpu().numpy()[rows], ref_flags)
