@@ -48,7 +48,8 @@ struct Smem {
   static constexpr int kNB = kWide ? 2 : 1;          // B tiles per stage
   uint8_t a[kSt][kOpBytes];
   uint8_t b[kSt][kNB][kOpBytes];
-  uint8_t ostage[4][32 * 128];  // epilogue staging per TMEM lane quadrant: 32 rows x 32 fp32, SWIZZLE_128B layout
+  uint8_t ostage[4][2][32 * 128];  // epilogue staging per TMEM lane quadrant, double-buffered: 32 rows x 32 fp32 each,
+                                   // SWIZZLE_128B layout
   uint64_t full[kSt], empty[kSt], tfull[2], tempty[2];
   uint64_t tid_full[kTidRing], tid_empty[kTidRing];
   uint32_t tile_id[kTidRing];
@@ -122,6 +123,7 @@ struct GemmParams {
   int64_t ldo;
   int32_t accumulate;
   int32_t tma_out;  // output 16-B aligned with ldo % 4 == 0: the epilogue writes through map_c (TMA store / L2 add)
+  uint32_t ostage_db;  // 1: alternate the two staging boxes per warp; 0: one box (A/B knob ECHO_GEMM_OSTAGE_DB)
 };
 
 template <bool kAMN, bool kBMN, bool kWide>
@@ -278,7 +280,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     uint32_t tc = 0;
     const uint32_t tempty_leader = mapa(smem_u32(&sm.tempty[0]), 0);
     const bool vec_ok = (p.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
-    const uint32_t ostage = smem_u32(sm.ostage[quad]);
+    const uint32_t ostage0 = smem_u32(sm.ostage[quad][0]);
+    uint32_t nstaged = 0;  // boxes this warp has handed to the TMA unit (picks the staging buffer)
     for (;; ++tc) {
       const int64_t u = next_tile_warp(tc);
       __syncwarp();
@@ -319,7 +322,12 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         lm::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + ch * 32, r);
         if (p.tma_out) {
           if (row0 >= p.M) continue;  // warp-uniform: the whole 32-row block is past the end
-          if (lane == 0) lm::bulk_wait_read0();  // the staging box has been read by the previous chunk's TMA
+          // the buffer's previous box (two boxes ago) has been read by its TMA; the other one may still be in flight
+          const uint32_t ostage = ostage0 + (nstaged & p.ostage_db) * (32u * 128u);
+          if (lane == 0) {
+            if (p.ostage_db) lm::bulk_wait_read1();
+            else lm::bulk_wait_read0();
+          }
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -332,6 +340,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
             else lm::tma_store_2d(&map_c, ostage, cb, (int32_t)row0);
             lm::bulk_commit();
           }
+          ++nstaged;
           continue;
         }
         if (!row_ok) continue;
@@ -437,6 +446,11 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, con
   // 11.81 -> 10.66 ms, dweight 11.28 -> 10.51 ms; profiles/r2i_ab_knobs.jsonl)
   p.group_m = (int32_t)(units / (2 * p.n_nu) > 1 ? units / (2 * p.n_nu) : 1);
   if (p.n_nu >= 16) p.group_m = 16;
+  // 256 x 512 units with 8-15 N units (d = 4096-7680): 8 M tiles per group (the chunked f2 step at d = 5120: 118.6-119.0
+  // vs 120.4-121.5 ms with the half-wave group of 3, 121.4 with 16; profiles/r3b_f2step_knobs.jsonl)
+  else if (kWide && p.n_nu >= 8) p.group_m = 8;
+  p.ostage_db = 1;
+  if (const char* env = getenv("ECHO_GEMM_OSTAGE_DB")) p.ostage_db = atoi(env) != 0;  // A/B knob
   if (const char* env = getenv("ECHO_GEMM_GROUP")) p.group_m = atoi(env) > 0 ? atoi(env) : p.group_m;  // A/B knob
   unsigned int* slots = nullptr;
   e = cudaGetSymbolAddress((void**)&slots, g_gemm_sched);
@@ -476,14 +490,15 @@ cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void*
                              int64_t b_row_bytes, int64_t M, int32_t N, int32_t K, float* out, int64_t ldo,
                              bool accumulate, cudaStream_t stream, int num_sms) {
   if (M == 0 || N == 0) return cudaSuccess;
-  // 256 x 512 units (two accumulators sharing A) for big products with long K loops, where the unoverlapped
-  // epilogue is cheap and A's DRAM re-reads dominate.  Interleaved A/B against cuBLAS (profiles/r2p_ab_wide.jsonl,
-  // ms): 32768 x 5120 x 151936 dhidden 40.7 wide / 49.4 not / 39.0 cuBLAS, dweight 40.7 / 50.3 / 38.4; at 8192-row
-  // chunks (<= 640 tiles, or 128-k-block K loops) the 256 x 256 tiles win: dhidden d = 5120 8.77 / 10.36 wide / 9.53
-  // cuBLAS, dweight 9.46 / 10.01 / 10.06.  ECHO_GEMM_WIDE=0/1 overrides, for A/B.
+  // 256 x 512 units (two accumulators sharing A) whenever there are N tiles to pair and the K loop is not short: every A
+  // k-block feeds two tiles, so A's L2 reads halve and its DRAM re-reads across N too (ncu, dhidden 8192 x 5120 x
+  // 151936: 12.7 vs 25.6 GB of DRAM reads, 2.43 vs 3.32 G L2 sectors, 1.34 vs 1.24 GHz, 8.1 vs 9.3 ms), and the
+  // power-capped clock rises.  Inside the chunked f2 step (tools/prof_f2_step.py, d = 5120, 8192-row chunks,
+  // profiles/r3a_f2step_wide.jsonl) the step's four GEMM-heavy stages take 122.0 ms instead of 134.0 (cuBLAS for
+  // the two backward products: 117.3).  Only back-to-back launches on warm, identical inputs favour 256 x 256 units
+  // (profiles/r2z_ab_wide_sus.jsonl).  ECHO_GEMM_WIDE=0/1 overrides, for A/B.
   const int32_t n_kb = (K + gm::kBK - 1) / gm::kBK, n_nt = (N + gm::kBN - 1) / gm::kBN;
-  const int64_t n_tiles = (int64_t)((M + 255) / 256) * n_nt;
-  bool wide = n_nt >= 2 && n_kb >= 512 && n_tiles >= 1000;
+  bool wide = n_nt >= 2 && n_kb >= 128;
   if (const char* env = getenv("ECHO_GEMM_WIDE")) wide = atoi(env) != 0 && n_nt >= 2;
   CUtensorMap ma, mb;
   const bool ok_a = a_mn ? make_tensor_map_bf16(&ma, A, (uint64_t)M, (uint64_t)K, (uint64_t)a_row_bytes, 64, 64)
