@@ -124,6 +124,7 @@ struct GemmParams {
   int32_t accumulate;
   int32_t tma_out;  // output 16-B aligned with ldo % 4 == 0: the epilogue writes through map_c (TMA store / L2 add)
   uint32_t ostage_db;  // 1: alternate the two staging boxes per warp; 0: one box (A/B knob ECHO_GEMM_OSTAGE_DB)
+  int32_t half_rel;    // kWide: the epilogue releases the two 256-column accumulators one by one (ECHO_GEMM_HALFREL)
 };
 
 template <bool kAMN, bool kBMN, bool kWide>
@@ -250,7 +251,43 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         const uint32_t d_tmem = tmem + buf * kBN;
         const int32_t piece = (int32_t)(u / n_units);
         const int32_t kb0 = kb_begin(piece), kb1 = kb_begin(piece + 1);
-        for (int32_t kb = kb0; kb < kb1; ++kb) {
+        int32_t kb_first = kb0;
+        if (kWide && p.half_rel) {
+          // The epilogue frees the first accumulator half-way through its read-out (tempty[0]) and the second at the
+          // end (tempty[1]): run the first ring's worth of k-blocks on accumulator 0 alone while accumulator 1 is
+          // still being drained, then the same stages again on accumulator 1, releasing them.
+          const int32_t nhead = min(S::kSt, kb1 - kb0);
+          uint32_t st = stage, ph = phase;
+          for (int32_t i = 0; i < nhead; ++i) {
+            mbar_wait_cluster(smem_u32(&sm.full[st]), ph);
+            lm::tc_fence_after();
+            const uint32_t a0 = smem_u32(sm.a[st]);
+#pragma unroll
+            for (int k = 0; k < kBK / kUmmaK; ++k)
+              lm::umma_f16<true>(d_tmem, op_desc<kAMN>(a0, k), op_desc<kBMN>(smem_u32(sm.b[st][0]), k),
+                                 idesc<kAMN, kBMN>(), (i > 0 || k > 0) ? 1u : 0u);
+            if (++st == S::kSt) {
+              st = 0;
+              ph ^= 1u;
+            }
+          }
+          mbar_wait_cluster(smem_u32(&sm.tempty[1]), aph ^ 1u);
+          lm::tc_fence_after();
+          for (int32_t i = 0; i < nhead; ++i) {
+            const uint32_t a0 = smem_u32(sm.a[stage]);
+#pragma unroll
+            for (int k = 0; k < kBK / kUmmaK; ++k)
+              lm::umma_f16<true>(d_tmem + kBN, op_desc<kAMN>(a0, k), op_desc<kBMN>(smem_u32(sm.b[stage][S::kNB - 1]), k),
+                                 idesc<kAMN, kBMN>(), (i > 0 || k > 0) ? 1u : 0u);
+            lm::umma_commit<true>(smem_u32(&sm.empty[stage]));
+            if (++stage == S::kSt) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          kb_first = kb0 + nhead;
+        }
+        for (int32_t kb = kb_first; kb < kb1; ++kb) {
           mbar_wait_cluster(smem_u32(&sm.full[stage]), phase);
           lm::tc_fence_after();
           const uint32_t a0 = smem_u32(sm.a[stage]);
@@ -314,61 +351,65 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         __syncwarp();
         __threadfence();
       }
+      // kWide with half_rel: accumulator 0 (columns 0-255) is released after its 8 chunks, accumulator 1 after the rest
+      const int n_halves = (kWide && p.half_rel) ? 2 : 1, ch_per = (kUnitN / 32) / n_halves;
+      for (int h = 0; h < n_halves; ++h) {
 #pragma unroll 1
-      for (int ch = 0; ch < kUnitN / 32; ++ch) {
-        const int32_t cb = nu * kUnitN + ch * 32;
-        if (cb >= p.N) break;  // warp-uniform
-        uint32_t r[32];
-        lm::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + ch * 32, r);
-        if (p.tma_out) {
-          if (row0 >= p.M) continue;  // warp-uniform: the whole 32-row block is past the end
-          // the buffer's previous box (two boxes ago) has been read by its TMA; the other one may still be in flight
-          const uint32_t ostage = ostage0 + (nstaged & p.ostage_db) * (32u * 128u);
-          if (lane == 0) {
-            if (p.ostage_db) lm::bulk_wait_read1();
-            else lm::bulk_wait_read0();
-          }
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            sts_v4(ostage + (uint32_t)lane * 128u + ((uint32_t)(j ^ (lane & 7)) << 4),
-                   make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
-          lm::fence_proxy_async_shared();
-          __syncwarp();
-          if (lane == 0) {
-            if (acc) lm::tma_reduce_add_2d(&map_c, ostage, cb, (int32_t)row0);
-            else lm::tma_store_2d(&map_c, ostage, cb, (int32_t)row0);
-            lm::bulk_commit();
-          }
-          ++nstaged;
-          continue;
-        }
-        if (!row_ok) continue;
-        if (vec_ok && cb + 32 <= p.N) {
-          float4* dst = reinterpret_cast<float4*>(orow + cb);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            if (acc) {
-              const float4 o = __ldcg(dst + j);
-              v.x += o.x;
-              v.y += o.y;
-              v.z += o.z;
-              v.w += o.w;
+        for (int ch = h * ch_per; ch < (h + 1) * ch_per; ++ch) {
+          const int32_t cb = nu * kUnitN + ch * 32;
+          if (cb >= p.N) break;  // warp-uniform
+          uint32_t r[32];
+          lm::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + ch * 32, r);
+          if (p.tma_out) {
+            if (row0 >= p.M) continue;  // warp-uniform: the whole 32-row block is past the end
+            // the buffer's previous box (two boxes ago) has been read by its TMA; the other one may still be in flight
+            const uint32_t ostage = ostage0 + (nstaged & p.ostage_db) * (32u * 128u);
+            if (lane == 0) {
+              if (p.ostage_db) lm::bulk_wait_read1();
+              else lm::bulk_wait_read0();
             }
-            dst[j] = v;
-          }
-        } else {
+            __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (cb + i < p.N) orow[cb + i] = __uint_as_float(r[i]) + (acc ? __ldcg(orow + cb + i) : 0.0f);
+            for (int j = 0; j < 8; ++j)
+              sts_v4(ostage + (uint32_t)lane * 128u + ((uint32_t)(j ^ (lane & 7)) << 4),
+                     make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
+            lm::fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              if (acc) lm::tma_reduce_add_2d(&map_c, ostage, cb, (int32_t)row0);
+              else lm::tma_store_2d(&map_c, ostage, cb, (int32_t)row0);
+              lm::bulk_commit();
+            }
+            ++nstaged;
+            continue;
+          }
+          if (!row_ok) continue;
+          if (vec_ok && cb + 32 <= p.N) {
+            float4* dst = reinterpret_cast<float4*>(orow + cb);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                     __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+              if (acc) {
+                const float4 o = __ldcg(dst + j);
+                v.x += o.x;
+                v.y += o.y;
+                v.z += o.z;
+                v.w += o.w;
+              }
+              dst[j] = v;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (cb + i < p.N) orow[cb + i] = __uint_as_float(r[i]) + (acc ? __ldcg(orow + cb + i) : 0.0f);
+          }
         }
+        // the accumulator (half) has been read: release it to the MMA of the tile after next (kWide: the next unit)
+        lm::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) lm::mbar_arrive_cluster(tempty_leader + (n_halves == 2 ? (uint32_t)h : buf) * 8u);
       }
-      // the accumulator has been read: release it to the MMA of the tile after next
-      lm::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) lm::mbar_arrive_cluster(tempty_leader + buf * 8u);
       if (piece + 1 < p.split) {  // publish this warp's rows of piece j (complete in global memory)
         if (p.tma_out && lane == 0) {
           lm::bulk_wait0();
@@ -449,6 +490,8 @@ static cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, con
   // 256 x 512 units with 8-15 N units (d = 4096-7680): 8 M tiles per group (the chunked f2 step at d = 5120: 118.6-119.0
   // vs 120.4-121.5 ms with the half-wave group of 3, 121.4 with 16; profiles/r3b_f2step_knobs.jsonl)
   else if (kWide && p.n_nu >= 8) p.group_m = 8;
+  p.half_rel = 1;
+  if (const char* env = getenv("ECHO_GEMM_HALFREL")) p.half_rel = atoi(env) != 0;  // A/B knob
   p.ostage_db = 1;
   if (const char* env = getenv("ECHO_GEMM_OSTAGE_DB")) p.ostage_db = atoi(env) != 0;  // A/B knob
   if (const char* env = getenv("ECHO_GEMM_GROUP")) p.group_m = atoi(env) > 0 ? atoi(env) : p.group_m;  // A/B knob
