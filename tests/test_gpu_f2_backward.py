@@ -434,14 +434,17 @@ def test_lmhead_policy_loss_edge_cases_and_errors():
 @pytest.mark.parametrize("m,n,k", [(256, 256, 64), (300, 200, 1000), (1, 72, 4096), (777, 513, 130),
                                    (300, 200, 16384), (513, 300, 9000)])   # the last two split K (4 and 2 pieces)
 @pytest.mark.parametrize("tma_out", [False, True])
-@pytest.mark.parametrize("wide", ["0", "1"])
+@pytest.mark.parametrize("wide", ["0", "1", "1-all-at-once"])
 def test_gemm_bf16_all_majors(a_mn, b_mn, m, n, k, tma_out, wide, monkeypatch):
     """echo_gemm_bf16 (the tcgen05 GEMM of the f2 backward) in every operand layout against the fp64 product, within
     the fp32-accumulation bound 4 (K/16 + 16) 2^-24 sum_k |A B|; ragged M / N / K tiles; accumulate and overwrite
     modes; an output row stride that is a multiple of 4 floats takes the TMA store / L2-add epilogue, any other the
     per-thread one.  wide = 1: 256 x 512 units, two TMEM accumulators sharing each A k-block (N tiles paired up, an
-    odd last one computed against zero-filled B and not stored)."""
-    monkeypatch.setenv("ECHO_GEMM_WIDE", wide)
+    odd last one computed against zero-filled B and not stored); the epilogue releases the two accumulators one by one
+    (the default: the next unit's first k-blocks run on accumulator 0 while accumulator 1 drains) or, with
+    1-all-at-once (ECHO_GEMM_HALFREL=0), together."""
+    monkeypatch.setenv("ECHO_GEMM_WIDE", wide[0])
+    monkeypatch.setenv("ECHO_GEMM_HALFREL", "0" if wide.endswith("once") else "1")
     from paper_2508_05387_b200 import abi
     g = torch.Generator(device="cuda").manual_seed(m + n + k + 2 * a_mn + b_mn)
     A = torch.randn(m, k, generator=g, device="cuda").to(torch.bfloat16)
