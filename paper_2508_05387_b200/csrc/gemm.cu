@@ -21,8 +21,11 @@
 // kWide: a unit is the 256 x 512 block of two N-neighbouring tiles, computed by one pair with its two TMEM
 // accumulators side by side (512 columns) instead of double-buffering: each k-block loads A once for both tiles (per CTA
 // and k-block 48 KB of L2 reads for 2 x 128 x 256 x 64 MACs instead of 2 x 32 KB), and the A operand's DRAM
-// re-reads across N halve.  The price is an epilogue that no longer overlaps the next unit's K loop, so it is chosen
-// for long K loops only.  (Round 2 also tried 4-CTA clusters multicasting A to two pairs: 7-13 % slower.)
+// re-reads across N halve.  The price: the next unit's MMAs wait for the epilogue.  The epilogue releases accumulator
+// 0 first, and the MMA warp runs the next unit's first ring's worth of k-blocks on it alone while accumulator 1 is
+// drained (half_rel).  Chosen when N has >= 2 tiles and K >= 128 k-blocks.  (Round 2 also tried 4-CTA clusters
+// multicasting A to two pairs: 7-13 % slower; round 3 eight epilogue warps reading a whole accumulator half into
+// registers before writing it out: fewer cycles, but a slower training step -- profiles/r3i_epi8_rejected.json.)
 #include <cuda.h>
 #include <cuda_bf16.h>
 
