@@ -22,7 +22,7 @@ import torch  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--op", default="dh", choices=["dh", "dw", "lm", "lmlogits", "ent", "loss", "logp"])
+    ap.add_argument("--op", default="dh", choices=["dh", "dw", "lm", "lmlogits", "zgemm", "ent", "loss", "logp"])
     ap.add_argument("--config", default="qwen3-32b", help="ent / loss: the BASELINE.json config of the micro-batch")
     ap.add_argument("--rows", type=int, default=8192)
     ap.add_argument("--d", type=int, default=2560)
@@ -90,7 +90,10 @@ def main():
         act = torch.randint(0, V, (n,), generator=g, device="cuda", dtype=torch.int32)
         z = torch.empty(n, ld, dtype=torch.bfloat16, device="cuda")
         ref_fn = lambda: torch.matmul(h, w.t(), out=z[:, :V])
-        if a.op == "lm":
+        if a.op == "zgemm":   # the logits product on echo_gemm_bf16 (fp32 out): probes its unit shapes at K = d
+            zf = torch.empty(n, ld, device="cuda")
+            fn = lambda: abi.echo_gemm_bf16(h, 0, d, w, 0, d, n, V, d, zf, ld)
+        elif a.op == "lm":
             ws = torch.empty(abi.echo_lmhead_workspace_bytes(n, V) // 4 + 1, dtype=torch.float32, device="cuda")
             lp = torch.empty(n, device="cuda")
             fn = lambda: abi.echo_lmhead_logp(h, w, n, d, V, act, lp, None, ws)
