@@ -9,6 +9,7 @@ import torch
 
 import oracle
 import synth
+from _util import coef_sens
 
 pytestmark = pytest.mark.gpu
 
@@ -512,6 +513,108 @@ def test_chunked_f4_options_equal_the_logits_path():
         outs.append((lp, loss, flags, ent))
     for a, b in zip(*outs):
         assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+
+
+def test_chunked_step_full_size_sampled_outputs():
+    """The chunked f2 step at the bench's launch configuration (f2_train_step: 32768 tokens, d = 5120 -- Qwen3-32B's
+    hidden size --, V = 151936, 8192-row chunks) against the fp64 oracle on sampled outputs it can compute one by one:
+    logp / loss / dhidden of six rows spread over the four chunks (first and last rows of chunks, the last token),
+    each row's logits computed in fp64 from the bf16 h and W and rounded like the GPU's fp32 accumulator; and sampled
+    dweight entries, sum_t D[t, v] h[t, j] over all 32768 tokens in fp64, from the D that the one-chunk run of the same
+    step leaves in its 10 GB buffer (that run's per-token results must equal the chunked run's bit for bit)."""
+    from paper_2508_05387_b200 import abi
+    n, d, V, chunk = 32768, 5120, 151936, 8192
+    h, w, act = _case(n, d, V, seed=2508)
+    rng = np.random.default_rng(2508)
+    old = (rng.normal(size=n) * 0.3 - 14.0).astype(np.float32)      # ratios around 1: both clip sides populated
+    ref = (rng.normal(size=n) * 0.3 - 14.0).astype(np.float32)
+    adv = rng.normal(size=4096).astype(np.float32)
+    slot = (np.arange(n) // 8).astype(np.int32)                      # 8 tokens per rollout slot
+    kl, gs = 0.001, float(n) / 4
+    cu = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    ng = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
+    cfg = abi.LossConfig(0.2, 0.2, 0.0, kl, gs, abi.ECHO_KL_K3, 0.0)
+    ld = abi.echo_lmhead_dlogits_ld(V)
+    runs = []
+    for ck in (chunk, n):
+        lp, loss = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+        flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+        dh, dw = torch.empty(n, d, device="cuda"), torch.empty(V, d, device="cuda")
+        ws = torch.empty(ck, ld, dtype=torch.bfloat16, device="cuda")
+        abi.echo_lmhead_policy_loss_fwd_bwd(h, w, n, d, V, act, cu(old), cu(ref), cu(slot), cu(adv), None, None, ng,
+                                            cfg, lp, loss, flags, None, dh, dw, 0, ws, ck)
+        torch.cuda.synchronize()
+        runs.append((lp, loss, flags, dh, dw, ws))
+    (lp, loss, flags, dh, dw, _), (lp1, loss1, flags1, _, _, D_all) = runs
+    assert torch.equal(lp.view(torch.int32), lp1.view(torch.int32))
+    assert torch.equal(loss.view(torch.int32), loss1.view(torch.int32))
+    assert torch.equal(flags, flags1)
+    # ---- sampled rows: fp64 logits row by row (W widened block by block), the oracle's (3)-(5), dhidden = D W
+    S = np.array([0, 1, chunk - 1, chunk, 2 * chunk + 123, n - 1])
+    hb, wb, a = _bits(h[torch.as_tensor(S, device="cuda")]), _bits(w), act.cpu().numpy()[S]
+    widen = lambda b: (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    hf = widen(hb)
+    z, tol = np.empty((len(S), V)), np.empty((len(S), V))
+    blocks = [(v0, min(v0 + 8192, V)) for v0 in range(0, V, 8192)]
+    for v0, v1 in blocks:
+        wf = widen(wb[v0:v1])
+        z[:, v0:v1] = hf @ wf.T
+        tol[:, v0:v1] = 4 * (d / 16 + 16) * 2.0 ** -24 * (np.abs(hf) @ np.abs(wf).T)
+    zb = _bf16_rne(z)
+    # an element whose z lies within the GEMM's fp32 bound of a bf16 rounding boundary may be stored one ulp away (at
+    # d = 5120 the worst-case bound makes most elements "ambiguous"; the slack below charges each of them a full ulp)
+    amb = _bf16_rne(z - 2 * tol) != _bf16_rne(z + 2 * tol)
+    o = oracle.policy_loss(zb, a, old[S], ref[S], slot[S], adv, n_global=float(n), dtype=oracle.BF16, kl_coef=kl,
+                           grad_scale=gs)
+    zf = (zb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    r = np.arange(len(S))
+    lse = zf[r, a] - o.logp
+    pz = np.exp(zf - lse[:, None])
+    u = _ulp(zf) * amb
+    dlse = (pz * u).sum(axis=1)                                      # what the ambiguous elements can move lse by
+    b_lp = 2e-5 + u[r, a] + dlse
+    g_lp, g_loss = lp.cpu().numpy()[S], loss.cpu().numpy()[S]
+    assert np.all(np.abs(g_lp - o.logp) <= b_lp), np.max(np.abs(g_lp - o.logp) / b_lp)
+    A, rho = adv[slot[S]].astype(np.float64), np.exp(o.logp - old[S])
+    lip = np.abs(A) * rho * np.exp(b_lp) + kl * (1 + np.exp(ref[S] - o.logp) * np.exp(b_lp))
+    b_loss = lip * b_lp + 1e-5 * np.maximum(np.abs(o.loss), 1)
+    assert np.all(np.abs(g_loss - o.loss) <= b_loss), np.max(np.abs(g_loss - o.loss) / b_loss)
+    # rows whose ratio sits within the logp bound of a clip boundary may legitimately flip branch: excluded
+    lr = np.log(rho)
+    far = np.minimum(np.abs(lr - math.log(0.8)), np.abs(lr - math.log(1.2))) > 2 * b_lp
+    assert far.sum() >= 4
+    assert np.array_equal(flags.cpu().numpy()[S][far], o.flags[far])
+    # dhidden rows: fp32-accumulation bound (2^-7 of sum |D||W| as in the small-size test) plus what the ambiguous
+    # elements and the logp error can move D by: |dc| |delta - p| + |c| p (e^(u + dlse + dlp) - 1)
+    sens, _ = coef_sens(o, old[S], ref[S], A, kl, gs, n_global=float(n))
+    dlp = np.abs(g_lp - o.logp)
+    dh_ref, adw, slack = np.zeros((len(S), d)), np.zeros((len(S), d)), np.zeros((len(S), d))
+    for v0, v1 in blocks:
+        wf = np.abs(widen(wb[v0:v1]))
+        wsg = widen(wb[v0:v1])
+        p_blk = pz[:, v0:v1]
+        dD = (sens * (dlp + dlse))[:, None] * np.abs((np.arange(v0, v1)[None, :] == a[:, None]) - p_blk) + \
+            np.abs(o.coef)[:, None] * p_blk * np.expm1(u[:, v0:v1] + (dlse + dlp)[:, None])
+        dh_ref += o.dlogits[:, v0:v1] @ wsg
+        adw += np.abs(o.dlogits[:, v0:v1]) @ wf
+        slack += dD @ wf
+    g_dh = dh[torch.as_tensor(S, device="cuda")].cpu().numpy().astype(np.float64)
+    bh = 2.0 ** -7 * adw + slack + 1e-6 * np.max(np.abs(dh_ref)) + 1e-12
+    err = np.abs(g_dh - dh_ref)[far]
+    assert np.all(err <= bh[far]), np.max(err / bh[far])
+    assert np.max(np.abs(dh_ref[far])) > 1e-3                        # the rows carry a real gradient
+    print(f"[f2 full size] rows {far.sum()} ambiguous logits {amb.mean():.3f} max|dh err|/bound "
+          f"{np.max(err / bh[far]):.3e} max|dh err|/max|dh| {np.max(err) / np.max(np.abs(dh_ref)):.3e}")
+    # ---- sampled dweight entries over all four chunks: sum_t D[t, v] h[t, j] in fp64 from the one-chunk run's D
+    vs = np.unique(np.concatenate([[0, V - 1, 77777], a, rng.integers(0, V, 6)]))
+    js = np.array([0, 1, 2559, d - 1, 777])
+    Dv = _bf(D_all[:, torch.as_tensor(vs, device="cuda")].contiguous())          # [n x |vs|]
+    hj = _bf(h[:, torch.as_tensor(js, device="cuda")].contiguous())              # [n x |js|]
+    dw_ref, adwj = Dv.T @ hj, np.abs(Dv).T @ np.abs(hj)
+    g_dw = dw[torch.as_tensor(vs, device="cuda")][:, torch.as_tensor(js, device="cuda")].cpu().numpy()
+    bw = 4 * (n / 16 + 16) * 2.0 ** -24 * adwj + 1e-12
+    assert np.all(np.abs(g_dw - dw_ref) <= bw), np.max(np.abs(g_dw - dw_ref) / bw)
+    assert np.max(np.abs(dw_ref)) > 0
 
 
 def test_chunked_step_deterministic_and_graph_capturable():
