@@ -639,16 +639,18 @@ def test_lmhead_logp_small(n, d, V):
     assert np.max(np.abs(lp - lp_ref)) <= 1e-4 and np.max(np.abs(lse - lse_ref)) <= 1e-4
 
 
-def test_lmhead_logp_qwen_size_sampled_rows():
-    """f2 at the Qwen3-4B LM-head shape (d = 2560, V = 151936) over 4096 tokens; sampled rows against the oracle,
-    all rows finite and deterministic across two calls."""
-    n, d, V = 4096, 2560, 151936
+@pytest.mark.parametrize("n,d", [(4096, 2560), (32768, 5120)])
+def test_lmhead_logp_qwen_size_sampled_rows(n, d):
+    """f2 at the Qwen3-4B LM-head shape (d = 2560, V = 151936) over 4096 tokens, and at the bench's f2_lmhead_logp
+    launch (32768 tokens, d = 5120: Qwen3-32B); sampled rows against the oracle, all rows finite and deterministic
+    across two calls."""
+    V = 151936
     h, w, act = _lmhead_case(n, d, V, seed=7)
     lp, lse = _lmhead_run(h, w, act)
     lp2, _ = _lmhead_run(h, w, act)
     assert np.array_equal(lp.view(np.uint64), lp2.view(np.uint64))
     assert np.all(np.isfinite(lp)) and np.all(lp <= 0)
-    rows = np.array([0, 1, 127, 128, 1000, 2047, 4095])
+    rows = np.unique(np.array([0, 1, 127, 128, 1000, 2047, n // 2 + 255, n - 256, n - 1]))
     hb = h[rows].cpu().view(torch.int16).numpy().view(np.uint16)
     wb = w.cpu().view(torch.int16).numpy().view(np.uint16)
     lp_ref, lse_ref = oracle.lmhead_logp(hb, wb, act.cpu().numpy()[rows])
