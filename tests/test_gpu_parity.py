@@ -311,6 +311,40 @@ def test_full_config_sampled_rows(name, algo_name):
 
 
 
+@pytest.mark.parametrize("name", ["qwen3-4b", "qwen3-32b"])
+def test_token_logp_full_size_sampled_rows(name):
+    """f1 at the bench's f1_token_logp launch (the AUTO bf16 kernel, token_logp_warp_kernel, on a 32768-row micro-batch
+    of the config's logits): sampled rows of the first and the last micro-batch against the oracle's logp / lse /
+    flags; the logits are left bit-for-bit unchanged."""
+    from paper_2508_05387_b200 import abi
+    cfg = synth.CONFIGS[name]
+    b = synth.make_batch(cfg)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    N, M = info.n_tokens, 32768
+    rng = np.random.default_rng(11)
+    for row0 in (0, ((N - 1) // M) * M):
+        m = min(M, N - row0)
+        logits = fill(st, cfg, row0, m)
+        before = logits[-1].clone()
+        logp = torch.empty(m, device="cuda")
+        lse = torch.empty(m, device="cuda")
+        flags = torch.empty(m, dtype=torch.uint8, device="cuda")
+        abi.echo_token_logp(logits, abi.ECHO_BF16, m, cfg.V, cfg.V, st.tok_action[row0:], logp, lse, flags)
+        torch.cuda.synchronize()
+        assert torch.equal(before.view(torch.int16), logits[-1].view(torch.int16))
+        sample = np.unique(np.concatenate([[0, m - 1], rng.integers(0, m, 30)]))
+        gl = row0 + sample
+        z = host_rows(cfg, o.keys[gl], o.pk.tok_action[gl])
+        ref_logp, ref_lse, ref_flags = oracle.token_logp(z, o.pk.tok_action[gl], vocab=cfg.V, dtype=oracle.BF16)
+        g = torch.from_numpy(sample).cuda()
+        assert np.all(np.abs(logp[g].cpu().numpy() - ref_logp) <= 1e-5 + 1e-6 * np.abs(ref_logp))
+        assert np.all(np.abs(lse[g].cpu().numpy() - ref_lse) <= 1e-5 + 1e-6 * np.abs(ref_lse))
+        np.testing.assert_array_equal(flags[g].cpu().numpy(), ref_flags)
+        del logits
+    torch.cuda.empty_cache()
+
+
 def test_check_rows_rejects_dropped_small_gradients():
     """Mutation test of the dlogits bar: the AUTO kernel's output on sampled Qwen3-4B rows passes check_rows; the same
     output with every entry whose p_v < 1e-5 zeroed (the bulk of a 152k-column row) must fail it, and so must an
