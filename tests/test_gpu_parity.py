@@ -345,6 +345,61 @@ def test_token_logp_full_size_sampled_rows(name):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("leg", ["entropy", "weights_adv"])
+def test_f4_legs_full_size_sampled_rows(leg):
+    """The bench's two f4 legs at their launch (AUTO kernel, the Qwen3-32B-shaped batch's first 32768-row micro-batch):
+    the entropy bonus (eta = 0.01, tok_entropy written) and per-token advantages + sequence-mean weights; sampled rows
+    (first, last, 30 random) against the oracle with the same bars as the small-size variant tests."""
+    cfg = synth.CONFIGS["qwen3-32b"]
+    b = synth.make_batch(cfg)
+    st, info = device_step(cfg, b)
+    o = oracle_step(cfg, b)
+    N, m = info.n_tokens, 32768
+    logits = fill(st, cfg, 0, m)
+    rng = np.random.default_rng(5)
+    sample = np.unique(np.concatenate([[0, m - 1], rng.integers(0, m, 30)]))
+    z = host_rows(cfg, o.keys[sample], o.pk.tok_action[sample])
+    args = (o.pk.tok_action[sample], o.pk.tok_old[sample], o.pk.tok_ref[sample], o.pk.tok_slot[sample], o.adv)
+    kl, eta = cfg.kl_coef, 0.01
+    idx = torch.from_numpy(sample).cuda()
+    if leg == "entropy":
+        kw = dict(n_global=N, kl_coef=kl, entropy_coef=eta)
+        probe = oracle.policy_loss(z, *args, **kw)
+        s = pow2_scale_for(np.abs(probe.dlogits).max())
+        ref = oracle.policy_loss(z, *args, grad_scale=s, **kw)
+        ent = torch.full((m,), float("nan"), device="cuda")
+        st.loss(logits, 0, kl_coef=kl, grad_scale=s, entropy_coef=eta, tok_entropy=ent)
+        H = ent[idx].cpu().numpy().astype(np.float64)
+        _, lse, _ = oracle.token_logp(z, o.pk.tok_action[sample], vocab=cfg.V)
+        hbar = 3e-5 * (1 + np.abs(lse) + np.abs(ref.entropy))
+        assert np.all(np.abs(H - ref.entropy) <= hbar), np.max(np.abs(H - ref.entropy) / hbar)
+        zf = (z.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        p = np.exp(zf - lse[:, None])
+        e = s * eta / N
+        es = e * p * (np.abs(zf) + np.abs(lse)[:, None] + np.abs(ref.entropy)[:, None] + 1) * 3e-5
+        sens = coef_sens(ref, o.pk.tok_old[sample], o.pk.tok_ref[sample], o.adv[o.pk.tok_slot[sample]], kl, s, N)
+        extra = dict(eslack=es, loss_atol=1e-6 + eta * hbar, p=p, action=o.pk.tok_action[sample])
+    else:
+        gen = np.random.default_rng(6)
+        tok_adv = (gen.normal(size=N) * 1.5).astype(np.float32)
+        L = np.diff(o.pk.kept_offset)
+        w = (1.0 / (o.pk.n_rollouts_kept * L[o.pk.tok_slot])).astype(np.float32)
+        kw = dict(n_global=N, kl_coef=kl, tok_adv=tok_adv[sample], tok_weight=w[sample])
+        probe = oracle.policy_loss(z, *args, **kw)
+        s = pow2_scale_for(np.abs(probe.dlogits).max())
+        ref = oracle.policy_loss(z, *args, grad_scale=s, **kw)
+        st.loss(logits, 0, kl_coef=kl, grad_scale=s, tok_adv=torch.from_numpy(tok_adv).cuda(),
+                tok_weight=torch.from_numpy(w).cuda())
+        sens = coef_sens(ref, o.pk.tok_old[sample], o.pk.tok_ref[sample], tok_adv[sample], kl, s,
+                         tok_weight=w[sample])
+        extra = {}
+    check_rows(d_gpu=logits[idx].float().cpu().numpy(), logp_gpu=st.tok_logp[idx].cpu().numpy(),
+               loss_gpu=st.tok_loss[idx].cpu().numpy(), flags_gpu=st.tok_flags[idx].cpu().numpy(), ref=ref,
+               dtype=cfg.dtype, old=o.pk.tok_old[sample], sens=sens, label=f"f4 {leg} full size", **extra)
+    del logits
+    torch.cuda.empty_cache()
+
+
 def test_check_rows_rejects_dropped_small_gradients():
     """Mutation test of the dlogits bar: the AUTO kernel's output on sampled Qwen3-4B rows passes check_rows; the same
     output with every entry whose p_v < 1e-5 zeroed (the bulk of a 152k-column row) must fail it, and so must an
