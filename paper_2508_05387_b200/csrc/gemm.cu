@@ -570,16 +570,15 @@ cudaError_t gemm_bf16(const void* A, bool a_mn, int64_t a_row_bytes, const void*
                make_tensor_map_f32(&mc_map, out, (uint64_t)N, (uint64_t)M, (uint64_t)ldo * 4, 32, 32))
                   ? 1
                   : 0;
-  // an operand small enough to stay in L2 (<= 48 MB, e.g. h of an 8192-row chunk for dweight) is kept there while the
-  // large one streams through with evict_first; with both large, both load with evict_normal (grouped tiles share
-  // k-blocks)
+  // L2 policy: the smaller operand loads with evict_last, the other with evict_normal.  Both are re-read by the units
+  // in flight (A by the N units of its M tile, B by the M tiles of the group), so neither is streamed with
+  // evict_first.  Sustained at the 1000 W power cap (tools/power_probe.py, profiles/r3t_power_pol.jsonl,
+  // r3u_power_pol.jsonl): dweight at d = 2560 5.00 instead of 5.28 ms (the former rule: h evict_last, D
+  // evict_first), at d = 5120 10.04 instead of 10.20 (former: both normal), dhidden at d = 5120 9.83 instead of 10.00;
+  // evict_first on D costs 10 %.
   const int64_t a_bytes = M * (int64_t)K * 2, b_bytes = (int64_t)N * K * 2;
-  int64_t keep_max = 48ll << 20;
-  if (const char* env = getenv("ECHO_GEMM_KEEP_MB")) keep_max = (int64_t)atoi(env) << 20;  // A/B knob
-  const bool keep_a = a_bytes <= keep_max && a_bytes < b_bytes;
-  const bool keep_b = !keep_a && b_bytes <= keep_max && b_bytes <= a_bytes;
-  p.pol_a = keep_a ? 2 : keep_b ? 1 : 0;
-  p.pol_b = keep_b ? 2 : keep_a ? 1 : 0;
+  p.pol_a = a_bytes < b_bytes ? 2 : 0;
+  p.pol_b = a_bytes < b_bytes ? 0 : 2;
   if (const char* env = getenv("ECHO_GEMM_POL_A")) p.pol_a = atoi(env);  // A/B knobs: 0 normal, 1 first, 2 last
   if (const char* env = getenv("ECHO_GEMM_POL_B")) p.pol_b = atoi(env);
   return wide ? launch_majors<true>(a_mn, b_mn, ma, mb, mc_map, p, stream, num_sms)

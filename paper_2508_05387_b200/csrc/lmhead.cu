@@ -99,6 +99,7 @@ struct LmParams {
   int64_t n_rows;
   int32_t d, V, n_tt, n_vt, n_kb;
   int32_t group_m;  // token tiles per rasterisation group (launch_tile)
+  int32_t pol;      // L2 hints on the operand loads (pair tile): 0 none, 1 h evict_last + W evict_normal (ECHO_LM_POL)
   unsigned int* sched;  // this launch's {tile counter, finished CTAs} (in-order dynamic scheduler; reset by the last CTA)
   const int32_t* __restrict__ tok_action;
   float* __restrict__ part_m;  // [n_vt][n_rows]
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
     // ---------------------------------------------------------------- TMA producer (the leader's is the scheduler)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      const uint64_t pol_h = policy_evict_last(), pol_w = policy_evict_normal();
       for (uint32_t use = 0;; ++use) {
         int64_t u;
         if (leader) {
@@ -216,8 +218,15 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
           // both CTAs' bytes complete on the leader's full barrier; only the leader arms it (with both halves)
           const uint32_t bar = kPair ? mapa(smem_u32(&sm.full[stage]), 0) : smem_u32(&sm.full[stage]);
           if (leader) mbar_arrive_expect_tx(smem_u32(&sm.full[stage]), C::kStageBytes * C::kCtas);
-          tma_load_2d<kPair>(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * C::kTileRows + (int32_t)rank * kBM, bar);
-          tma_load_2d<kPair>(smem_u32(sm.b[stage]), &map_w, kb * kBK, vt * kBN + (int32_t)rank * C::kBRows, bar);
+          if (kPair && p.pol) {
+            tma_load_2d_pair_hint(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * C::kTileRows + (int32_t)rank * kBM, bar,
+                                  pol_h);
+            tma_load_2d_pair_hint(smem_u32(sm.b[stage]), &map_w, kb * kBK, vt * kBN + (int32_t)rank * C::kBRows, bar,
+                                  pol_w);
+          } else {
+            tma_load_2d<kPair>(smem_u32(sm.a[stage]), &map_h, kb * kBK, tt * C::kTileRows + (int32_t)rank * kBM, bar);
+            tma_load_2d<kPair>(smem_u32(sm.b[stage]), &map_w, kb * kBK, vt * kBN + (int32_t)rank * C::kBRows, bar);
+          }
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1u;
@@ -528,6 +537,8 @@ static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams&
   p.group_m = (int32_t)((42ll << 20) / ((int64_t)C::kTileRows * p.d * 2));
   if (const char* env = getenv("ECHO_LM_GROUP")) p.group_m = atoi(env);
   p.group_m = p.group_m < 2 ? 2 : p.group_m > 128 ? 128 : p.group_m;
+  p.pol = 0;
+  if (const char* env = getenv("ECHO_LM_POL")) p.pol = atoi(env) != 0;  // A/B knob
   const void* fn = (const void*)lmhead_tile_kernel<kLmPair, kMode>;
   const size_t smem = lm::smem_bytes<kLmPair>();
   // per device, once: the shared-memory opt-in and the resident-cluster count

@@ -41,24 +41,6 @@ ECHO_DEVINL void tma_load_2d_pair_hint(uint32_t dst, const CUtensorMap* map, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
       : "memory");
 }
-// Pair form with TMA multicast: the box lands at the same offset in every CTA of `mask` (a 4-CTA cluster of two
-// pairs), and each destination signals its own pair leader's barrier at bar's offset (bar: this CTA's pair leader's
-// barrier, i.e. peer bit 0).
-ECHO_DEVINL void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int32_t x, int32_t y, uint32_t bar,
-                                     uint16_t mask, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "h"(mask), "l"(policy)
-      : "memory");
-}
-// Arrive on `bar` (same offset) in every CTA of `mask` when the MMAs issued so far have completed (pair MMA).
-ECHO_DEVINL void umma_commit_mask(uint32_t bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-      "h"(mask)
-      : "memory");
-}
 // Arrive on `bar` when the MMAs issued so far have completed: this CTA's barrier, or (pair) the barrier at the
 // same offset in both CTAs of the pair.
 template <bool kPair>

@@ -53,9 +53,23 @@ def main():
         "dh_cublas": lambda: prof_gemm.cublas_grads(lib, D, W, h, dh, None, ld, n, d, V, False),
         "dw_cublas": lambda: prof_gemm.cublas_dw(lib, D, h, dw, ld, n, d, V),
     }
-    flops = 2.0 * n * d * V
+    # the LM head's two launches of the f2 paths: logits store (chunked step, 8192 rows) and the fused log-prob
+    # (32768 rows), and cuBLAS's bf16 GEMM into the logits buffer for comparison
+    w_lm = (torch.randn(V, d, generator=g, device="cuda") * (2.0 / d ** 0.5)).to(torch.bfloat16)
+    zc = D  # [n x ld] bf16 buffer
+    arms["lm_logits"] = lambda: abi.echo_lmhead_logits(h, w_lm, n, d, V, zc, ld)
+    arms["lm_logits_cublas"] = lambda: torch.matmul(h, w_lm.t(), out=zc[:, :V])
+    if any(x.startswith("lm_logp") for x in a.arms.split(",")):
+        n4 = 4 * n
+        h4 = torch.randn(n4, d, generator=g, device="cuda").to(torch.bfloat16)
+        act4 = torch.randint(0, V, (n4,), generator=g, device="cuda", dtype=torch.int32)
+        ws4 = torch.empty(abi.echo_lmhead_workspace_bytes(n4, V) // 4 + 1, dtype=torch.float32, device="cuda")
+        lp4 = torch.empty(n4, device="cuda")
+        arms["lm_logp"] = lambda: abi.echo_lmhead_logp(h4, w_lm, n4, d, V, act4, lp4, None, ws4)
+    flops_of = {"lm_logp": 2.0 * 4 * n * d * V}
     for name in a.arms.split(","):
         fn = arms[name]
+        flops = flops_of.get(name, 2.0 * n * d * V)
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
