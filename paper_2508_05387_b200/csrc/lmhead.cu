@@ -1,6 +1,8 @@
 // lmhead.cu -- f2: the LM head fused with the log-softmax-and-gather of (3), and the two epilogues of
 // the training step through the LM head (lmhead_bwd.cu, abi.cu): D = dL/dz recomputed from h and W (kMode 2,
-// echo_lmhead_dlogits) and the logits themselves stored as bf16 (kMode 3, echo_lmhead_logits).
+// echo_lmhead_dlogits) and the logits themselves stored as bf16 (kMode 3, echo_lmhead_logits).  The store modes
+// write through a per-warp 32 x 64 shared-memory box and a TMA store when V % 8 == 0 (sustained at the power cap,
+// 8192 x 151936 x 5120 logits: 9.81 instead of 9.95 ms with per-thread 16-byte stores, profiles/r3y_lmtma.jsonl).
 //
 // logp_t = z[t, a_t] - logsumexp_v z[t, v],  z = h W^T  (h: [N x d] bf16 hidden states, W: [V x d] bf16 LM-head
 // weight).  The [N x V] logits are never written to HBM: the GEMM runs on the 5th-generation tensor cores with
@@ -33,6 +35,7 @@
 #include <cuda_bf16.h>
 
 #include <stdlib.h>
+#include <string.h>
 
 #include <atomic>
 #include <mutex>
@@ -66,6 +69,7 @@ struct Smem {
   uint64_t tid_full[kTidRing], tid_empty[kTidRing];
   uint32_t tile_id[kTidRing];
   uint32_t tmem_base;
+  alignas(1024) uint8_t zstage[4][32 * 128];  // store modes: per-warp staging box, 32 rows x 64 bf16 (SWIZZLE_128B)
 };
 // consumers of a tile id: the leader's MMA thread, 4 epilogue warps per CTA, the peer's producer thread
 template <bool kPair>
@@ -99,7 +103,8 @@ struct LmParams {
   int64_t n_rows;
   int32_t d, V, n_tt, n_vt, n_kb;
   int32_t group_m;  // token tiles per rasterisation group (launch_tile)
-  int32_t pol;      // L2 hints on the operand loads (pair tile): 0 none, 1 h evict_last + W evict_normal (ECHO_LM_POL)
+  int32_t pol;      // L2 hints on the operand loads (pair tile): 0 none, 1 h evict_last, 2 W evict_last (ECHO_LM_POL)
+  int32_t tma_z;    // store modes: the bf16 output goes through map_z (TMA stores of 32 x 64 boxes)
   unsigned int* sched;  // this launch's {tile counter, finished CTAs} (in-order dynamic scheduler; reset by the last CTA)
   const int32_t* __restrict__ tok_action;
   float* __restrict__ part_m;  // [n_vt][n_rows]
@@ -123,7 +128,7 @@ struct LmParams {
 template <bool kPair, int kMode>
 __global__ void __launch_bounds__(lm::kThreads, 1)
     lmhead_tile_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w,
-                       const LmParams p) {
+                       const __grid_constant__ CUtensorMap map_z, const LmParams p) {
   using namespace lm;
   constexpr bool kEnt = kMode == 1, kStore = kMode >= 2;  // 2: D, 3: the logits z themselves (bf16)
   using C = Cfg<kPair>;
@@ -191,7 +196,8 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
     // ---------------------------------------------------------------- TMA producer (the leader's is the scheduler)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      const uint64_t pol_h = policy_evict_last(), pol_w = policy_evict_normal();
+      const uint64_t pol_h = p.pol == 1 ? policy_evict_last() : policy_evict_normal();
+      const uint64_t pol_w = p.pol == 2 ? policy_evict_last() : policy_evict_normal();
       for (uint32_t use = 0;; ++use) {
         int64_t u;
         if (leader) {
@@ -289,15 +295,8 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
         const float k = fmaf(e, H - lse, -c);
         const uint64_t l2e2 = f2(kLog2e, kLog2e), nl2 = f2(-lse * kLog2e, -lse * kLog2e), e2 = f2(e, e), k2 = f2(k, k);
         uint16_t* drow = p.dz + (row_ok ? row : 0) * p.ld;
-        mbar_wait_cluster_warp(smem_u32(&sm.tfull[buf]), aph, lane);
-        tc_fence_after();
-#pragma unroll 1
-        for (int ch = 0; ch < kBN / 32; ++ch) {
-          const int32_t cb = col0 + ch * 32;
-          if (cb >= p.V) break;  // warp-uniform: nothing left of the vocabulary in this tile
-          uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + ch * 32, r);
-          uint32_t o[16];
+        // one 32-column TMEM chunk -> 16 packed bf16 pairs (the logits, or D)
+        auto convert = [&](const uint32_t (&r)[32], uint32_t (&o)[16], int32_t cb) {
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             if constexpr (kMode == 3) {
@@ -313,6 +312,46 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
             if (cb + i + 1 == a) d1 += c;
             o[i >> 1] = pack_bf16x2(d0, d1);
           }
+        };
+        mbar_wait_cluster_warp(smem_u32(&sm.tfull[buf]), aph, lane);
+        tc_fence_after();
+        if (p.tma_z) {
+          // two chunks per 32 x 64 box in the warp's staging buffer (16-byte granule j of row r at j ^ (r & 7):
+          // SWIZZLE_128B), written by one TMA store; the tensor map clips rows >= n_rows and columns >= V
+          const int64_t row0 = row - lane;
+          const uint32_t zst = smem_u32(sm.zstage[quad]);
+#pragma unroll 1
+          for (int c2 = 0; c2 < kBN / 64; ++c2) {
+            const int32_t cbb = col0 + c2 * 64;
+            if (cbb >= p.V || row0 >= p.n_rows) break;  // warp-uniform
+            if (lane == 0) bulk_wait_read0();              // the box's previous contents have been read by the TMA
+            __syncwarp();
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t r[32], o[16];
+              tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + c2 * 64 + hf * 32, r);
+              convert(r, o, cbb + hf * 32);
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                sts_v4(zst + (uint32_t)lane * 128u + ((uint32_t)((hf * 4 + j) ^ (lane & 7)) << 4),
+                       make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]));
+            }
+            fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&map_z, zst, cbb, (int32_t)row0);
+              bulk_commit();
+            }
+          }
+        }
+#pragma unroll 1
+        for (int ch = 0; ch < (p.tma_z ? 0 : kBN / 32); ++ch) {
+          const int32_t cb = col0 + ch * 32;
+          if (cb >= p.V) break;  // warp-uniform: nothing left of the vocabulary in this tile
+          uint32_t r[32];
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * kBN + ch * 32, r);
+          uint32_t o[16];
+          convert(r, o, cb);
           if (row_ok) {
             if (cb + 32 <= p.V) {
               uint4* dst = reinterpret_cast<uint4*>(drow + cb);
@@ -400,6 +439,9 @@ __global__ void __launch_bounds__(lm::kThreads, 1)
     }
   }
 
+  if constexpr (kStore) {
+    if (warp >= 2 && p.tma_z && lane == 0) bulk_wait0();  // staging boxes read and stores done before the CTA retires
+  }
   __syncwarp();
   tc_fence_before();
   if constexpr (kPair) cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
@@ -538,7 +580,7 @@ static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams&
   if (const char* env = getenv("ECHO_LM_GROUP")) p.group_m = atoi(env);
   p.group_m = p.group_m < 2 ? 2 : p.group_m > 128 ? 128 : p.group_m;
   p.pol = 0;
-  if (const char* env = getenv("ECHO_LM_POL")) p.pol = atoi(env) != 0;  // A/B knob
+  if (const char* env = getenv("ECHO_LM_POL")) p.pol = atoi(env);  // A/B knob: 1 h evict_last, 2 W evict_last
   const void* fn = (const void*)lmhead_tile_kernel<kLmPair, kMode>;
   const size_t smem = lm::smem_bytes<kLmPair>();
   // per device, once: the shared-memory opt-in and the resident-cluster count
@@ -571,7 +613,15 @@ static cudaError_t launch_tile(const void* hidden, const void* weight, LmParams&
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kLmPair, kMode>, mh, mw, p);
+  // store modes: the bf16 output [n_rows x V] (row stride ld) through a tensor map when its base is 16-B aligned and
+  // V % 8 == 0 (a tensor-map store writes whole 16-byte granules: a ragged last one would spill into columns >= V)
+  CUtensorMap mz;
+  memset(&mz, 0, sizeof(mz));
+  p.tma_z = 0;
+  if (kMode >= 2 && (reinterpret_cast<uintptr_t>(p.dz) & 15) == 0 && p.ld % 8 == 0 && p.V % 8 == 0)
+    p.tma_z = make_tensor_map_bf16(&mz, p.dz, (uint64_t)p.V, (uint64_t)p.n_rows, (uint64_t)p.ld * 2, 64, 32) ? 1 : 0;
+  if (const char* env = getenv("ECHO_LM_TMA_OUT")) p.tma_z = p.tma_z && atoi(env) != 0;  // A/B knob
+  return cudaLaunchKernelEx(&cfg, lmhead_tile_kernel<kLmPair, kMode>, mh, mw, mz, p);
 }
 
 cudaError_t launch_lmhead_logp(const void* hidden, const void* weight, int64_t n_rows, int32_t d, int32_t V,
