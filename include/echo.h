@@ -36,6 +36,11 @@
  *   - Results are deterministic: no floating-point atomics; every reduction has a fixed order that
  *     depends only on the sizes (vocab, n_tokens), never on grid size, micro-batch split or rank.
  *   - Requires an sm_100 (B200) device; there is no fallback path.
+ *
+ * Environment: the GEMM, LM-head and f1 kernels read a few ECHO_* variables at launch (unit shapes, raster groups, L2
+ * policies, ring shapes; DESIGN.md §7 "A/B knobs") so that the measurement tools can compare designs in one
+ * process.  They are not part of this ABI and change no result beyond fp32 summation order of the GEMMs; unset,
+ * each takes its measured-best default.
  */
 #ifndef ECHO_H
 #define ECHO_H
