@@ -39,7 +39,7 @@
  *
  * Environment: the GEMM, LM-head and f1 kernels read a few ECHO_* variables at launch (unit shapes, raster groups, L2
  * policies, ring shapes; DESIGN.md §7 "A/B knobs") so that the measurement tools can compare designs in one
- * process.  They are not part of this ABI and change no result beyond fp32 summation order of the GEMMs; unset,
+ * process.  They are not part of this ABI and change results only within fp32 rounding (summation order); unset,
  * each takes its measured-best default.
  */
 #ifndef ECHO_H
